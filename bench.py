@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""TVSpecNET K-band decomposition throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+One step = one forward of the config's whole batch through the drop-in
+``TVSpecNet`` (conv0 -> 15 tcgen05 hidden convs -> head + closure), inputs
+resident in HBM.  Default workload: BASELINE.json configs[1] = config 2,
+64 x 1 x 256 x 256, fast (fp16 tcgen05) mode; the fp32-accurate mode is
+measured on the same workload and reported alongside.  Multi-GPU (torchrun):
+every rank processes its own config-2 batch (weak scaling, no collective on
+the data path); value = all ranks' megapixels / max-over-ranks time.
+
+``--impl reference`` times the reference's CPU forward (the oracle port of
+/root/reference/pkg/trainer/src/tvsurrogate/model.py, identical torch CPU ops)
+on the host cores, rank 0 only, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2006_10004_b200.workloads import CONFIGS, flop_per_px, make_image  # noqa: E402
+
+METRIC = "TVSpecNET megapixels/sec (K-band decomposition)"
+UNIT = "MP/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["bf16_tflops"], d.get("bf16_tflops_sustained"), d["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock/throttle sampling (NVML) during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x20: "sync_boost", 0x40: "sw_thermal_slowdown", 0x80: "hw_thermal_slowdown",
+        0x100: "hw_power_brake_slowdown", 0x200: "display_clock_setting",
+    }
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                mask = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        if self.nvml:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nvml:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _batch(spec, count=None):
+    n = spec.batch if count is None else count
+    return np.stack([make_image(spec, i) for i in range(n)])[:, None]
+
+
+def _seeded_state(depth, channels):
+    from oracle.tvspecnet_oracle import build_seeded_state  # checker-side weight recipe only
+
+    return build_seeded_state(depth, channels, 5)
+
+
+def cpu_reference(spec, steps, warmup, sample_images, threads):
+    """The reference CPU forward (oracle port) on `sample_images` images per step."""
+    from oracle.tvspecnet_oracle import oracle_from_state
+
+    torch.set_num_threads(threads)
+    model = oracle_from_state(_seeded_state(spec.depth, spec.channels), spec.depth, spec.channels, 5)
+    x = torch.from_numpy(_batch(spec, sample_images))
+    times = []
+    with torch.no_grad():
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            for j in range(sample_images):  # per image, as predict_bands does (inference.py:25-32)
+                model(x[j : j + 1])
+            dt = time.perf_counter() - t0
+            if i >= warmup:
+                times.append(dt)
+    px = sample_images * spec.height * spec.width
+    return px / 1e6 / statistics.median(times), statistics.median(times), times
+
+
+def run_reference(args, spec):
+    world, rank, _ = _dist()
+    if world > 1 and rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample = args.cpu_sample
+    mp_s, sec, _ = cpu_reference(spec, args.steps, args.warmup, sample, threads)
+    line = {
+        "metric": METRIC, "value": round(mp_s, 5), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (SURVEY §8(d) generator)",
+        "impl": "reference",
+        "config": {"workload": spec.name, "batch": spec.batch, "height": spec.height, "width": spec.width,
+                   "depth": spec.depth, "channels": spec.channels, "sample_images_per_step": sample},
+        "cpu_baseline": {"value": round(mp_s, 5), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} of {spec.batch} images per step, torch CPU (oneDNN) fp32, "
+                                   f"{threads} threads"},
+        "e2e": {"value": round(mp_s, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _flush_l2(buf):
+    buf.add_(1.0)
+
+
+def time_steps(fn, steps, warmup, flush):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in evs:
+        _flush_l2(flush)
+        a.record(st)
+        fn()
+        b.record(st)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def run_ours(args, spec):
+    world, rank, local = _dist()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2006_10004_b200 import TVSpecNet
+
+    state = _seeded_state(spec.depth, spec.channels)
+    x_host = torch.from_numpy(_batch(spec)).pin_memory()
+    x = x_host.to(dev)
+    B, _, H, W = x.shape
+    px = B * H * W
+    flush = torch.empty(256 << 20 >> 2, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+
+    results = {}
+    for prec in ("fast", "fp32"):
+        model = TVSpecNet(spec.depth, spec.channels, 5, precision=prec).eval()
+        model.load_state_dict(state)
+        bands = torch.empty((B, 5, H, W), device=dev)
+        clos = torch.empty((B, 1, H, W), device=dev)
+        plan = model._plan_for(dev)
+
+        def step():
+            plan.forward(x.data_ptr(), bands.data_ptr(), clos.data_ptr(), B, H, W, 0, H,
+                         torch.cuda.current_stream().cuda_stream)
+
+        steps = args.steps if prec == "fast" else max(1, min(args.steps, args.fp32_steps))
+        warm = args.warmup if prec == "fast" else max(1, min(args.warmup, 3))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            ms = time_steps(step, steps, warm, flush)
+        launches = plan.last_launch_count()
+        tot_ms = sum(ms)
+        if world > 1:
+            t = torch.tensor([tot_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot_ms = float(t.item())
+        value = world * px * steps / 1e6 / (tot_ms / 1e3)
+
+        # live per-kernel timing of the dominant kernel (hidden conv), separate pass
+        plan.profile_enable(True)
+        for _ in range(max(1, min(steps, 3))):
+            _flush_l2(flush)
+            step()
+        torch.cuda.synchronize()
+        hid_ms, hid_n, hid_flops = plan.profile_read(1)
+        c0_ms, _, _ = plan.profile_read(0)
+        hd_ms, _, _ = plan.profile_read(2)
+        plan.profile_enable(False)
+
+        # end to end through the public API with host buffers (H2D + D2H inside)
+        e2e_steps = max(1, min(steps, args.e2e_steps))
+        for _ in range(2):
+            model(x_host)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            _flush_l2(flush)
+            out_host = model(x_host)  # pinned (B,1,H,W) -> CPU (B,5,H,W)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        results[prec] = dict(value=value, ms=tot_ms / steps, ms_list=ms, launches=launches, steps=steps,
+                             warmup=warm, clocks=clk.summary(), hid_ms=hid_ms, hid_n=hid_n, hid_flops=hid_flops,
+                             c0_ms=c0_ms, hd_ms=hd_ms, e2e=world * px / 1e6 / e2e_s,
+                             e2e_bytes=(x_host.numel() * 4, out_host.numel() * 4))
+        del model, plan, bands, clos
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak_tf, peak_sus, hbm, peak_kind = _peaks()
+    f = results["fast"]
+    fpx = flop_per_px(spec.depth, spec.channels)
+    hid_avg_ms = f["hid_ms"] / max(1, f["hid_n"])
+    hid_tflops = f["hid_flops"] / max(1, f["hid_n"]) / (hid_avg_ms / 1e3) / 1e12
+    step_ms = f["ms"]
+    line = {
+        "metric": METRIC, "value": round(f["value"], 3), "unit": UNIT, "n_gpus": world, "steps": f["steps"],
+        "warmup": f["warmup"], "ms_per_step": round(step_ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16 operands / f32 accumulate (tcgen05 kind::f16); conv0+head f32",
+        "data": "synthetic (SURVEY §8(d) piecewise-constant generator, seed 2)",
+        "config": {"workload": spec.name, "batch_per_gpu": B, "height": H, "width": W, "depth": spec.depth,
+                   "channels": spec.channels, "out_bands": 5, "precision": "fast", "parallelism": f"batch x{world}",
+                   "l2": "256 MiB buffer written between timed steps", "inputs_resident": "HBM"},
+        "tflops_algorithmic": round(f["value"] * 1e6 * fpx / 1e12 / world, 2),
+        "frac_of_bf16_peak": round(f["value"] * 1e6 * fpx / 1e12 / world / peak_tf, 4),
+        "roofline": {"bound": "tensor", "kernel": "conv3x3_hidden_f16_kernel",
+                     "achieved": round(hid_tflops, 2), "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": round(hid_tflops / peak_tf, 4), "peak_kind": f"{peak_kind} bf16 burst",
+                     "frac_of_sustained": round(hid_tflops / peak_sus, 4) if peak_sus else None,
+                     "avg_launch_ms": round(hid_avg_ms, 5), "launches_timed": f["hid_n"],
+                     "flop_per_launch": f["hid_flops"] / max(1, f["hid_n"]),
+                     "share_of_step": round(f["hid_ms"] / max(1e-9, f["hid_ms"] + f["c0_ms"] + f["hd_ms"]), 4),
+                     "traffic": None},
+        "gpu_launches": f["launches"] * f["steps"],
+        "e2e": {"value": round(f["e2e"], 3), "unit": UNIT, "h2d_bytes_per_step": f["e2e_bytes"][0],
+                "d2h_bytes_per_step": f["e2e_bytes"][1]},
+        "clocks": f["clocks"],
+        "fp32_mode": {"value": round(results["fp32"]["value"], 3), "unit": UNIT,
+                      "ms_per_step": round(results["fp32"]["ms"], 3), "steps": results["fp32"]["steps"],
+                      "e2e": round(results["fp32"]["e2e"], 3)},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        mp_s, sec, _ = cpu_reference(spec, 1, 1, args.cpu_sample, threads)
+        line["cpu_baseline"] = {"value": round(mp_s, 5), "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"{args.cpu_sample} of {spec.batch} images, per-image forward, "
+                                          f"torch CPU fp32 oracle port, {threads} threads, median of 1 after 1 warm-up"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="2")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-sample", type=int, default=8, help="images per CPU baseline step")
+    ap.add_argument("--fp32-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    key = args.config if args.config == "5w" else int(args.config)
+    spec = CONFIGS[key]
+    if args.impl == "reference":
+        run_reference(args, spec)
+    else:
+        run_ours(args, spec)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,94 @@
+/* tvs_b200.h — C ABI of the B200-native TVSpecNET forward (libtvsb200.so).
+ *
+ * This is the drop-in boundary for the reference's model module
+ * /root/reference/pkg/trainer/src/tvsurrogate/model.py:29-56.  The reference
+ * has no FFI (pure PyTorch CPU); every entry point below replaces a piece of
+ * the in-process call the reference makes:
+ *
+ *   tvs_plan_create       <- TVSpecNet.__init__(depth, channels, out_bands)   model.py:32-47
+ *   tvs_plan_set_weights  <- load_state_dict + eval() (BN running stats)       training.py:163-172
+ *   tvs_forward           <- TVSpecNet.forward(x) -> (B, out_bands, H, W)      model.py:49-52
+ *                            (+ optional closure plane image - sum(bands),     inference.py:34-42)
+ *   tvs_forward_host      <- predict_bands(model, image) with CPU in/out       inference.py:25-32
+ *   tvs_plan_destroy      <- module teardown
+ *
+ * Conventions: every function returns 0 on success or a negative TVS_E_*
+ * code; no C++ exception crosses the boundary; tvs_last_error() returns the
+ * calling thread's last message.  All device pointers are caller-owned; the
+ * plan owns packed weights, TMA descriptors and activation scratch.  Calls
+ * on one plan must be serialised by the caller (one plan per device; plans on
+ * different devices are independent).  `stream` is a cudaStream_t (NULL =
+ * legacy default stream).
+ */
+#ifndef TVS_B200_H_
+#define TVS_B200_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TVS_ABI_VERSION 1
+
+/* status codes */
+#define TVS_OK 0
+#define TVS_E_INVALID (-1)     /* bad argument (shape, depth, null pointer) -> ValueError */
+#define TVS_E_UNSUPPORTED (-2) /* valid model, configuration not built (e.g. channels != 64) */
+#define TVS_E_CUDA (-3)        /* CUDA runtime/driver failure */
+#define TVS_E_STATE (-4)       /* forward before set_weights, etc. */
+
+/* numerics modes */
+#define TVS_MODE_FP32 0 /* fp32-accurate: fp32 activations + fp32 FFMA hidden layers   */
+#define TVS_MODE_FAST 1 /* fp16 tcgen05 hidden layers, exact fp32 conv0 + head          */
+
+typedef struct tvs_plan tvs_plan;
+
+int tvs_abi_version(void);
+const char* tvs_last_error(void);
+
+/* depth >= 3 (model.py:34-35), channels == 64 in this build, 1 <= out_bands <= 8 */
+int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode, tvs_plan** out_plan);
+
+/* n_layers == depth.  Layer i computes  y[co] = scale[co] * conv(W_i, a)[co] + shift[co]
+ * (then ReLU for all but the head).  w_dev[i]: DEVICE pointer to the conv
+ * weights [cout][cin][3][3] fp32; scale_dev[i]: DEVICE pointer to [cout]
+ * fp32, or NULL for 1 (scale_dev itself may be NULL); shift_dev[i]: DEVICE
+ * pointer to [cout] fp32.  For the reference module: conv0/head have scale
+ * NULL and shift = conv bias; hidden layer j has the eval-BatchNorm fold
+ * scale = gamma/sqrt(var+eps), shift = beta - mean*scale (model.py:40-43).
+ * The plan repacks on `stream` (FAST: W*scale rounded to fp16 with tap-sum
+ * compensation); the sources may be freed once the stream passes this call. */
+int tvs_plan_set_weights(tvs_plan* plan, const float* const* w_dev, const float* const* scale_dev,
+                         const float* const* shift_dev, int n_layers, void* stream);
+
+/* x: (B,1,H,W) fp32 NCHW; bands: (B,out_bands,valid_rows,W) fp32 receiving
+ * rows [valid_row0, valid_row0+valid_rows) of the full forward; closure (may
+ * be NULL): (B,1,valid_rows,W) = x - sum_k bands_k.  valid_rows < 0 means all
+ * H rows.  All device pointers, 16-byte aligned. */
+int tvs_forward(tvs_plan* plan, const float* x, float* bands, float* closure_or_null, int B, int H, int W,
+                int valid_row0, int valid_rows, void* stream);
+
+/* Same contract with HOST buffers: copies in, runs, copies out, and
+ * synchronises `stream` before returning. */
+int tvs_forward_host(tvs_plan* plan, const float* x_host, float* bands_host, float* closure_host_or_null, int B,
+                     int H, int W, void* stream);
+
+/* Number of kernels the last tvs_forward launched (for launch accounting). */
+int tvs_last_launch_count(const tvs_plan* plan);
+
+/* Per-kernel CUDA-event timing on the forward's stream (off by default).
+ * kind: 0 = conv0 (K1), 1 = hidden conv (K2), 2 = head + closure (K3).
+ * tvs_profile_read synchronises the recorded events and returns, since the
+ * last enable/reset, the summed device milliseconds, the launch count and the
+ * algorithmic FLOPs of those launches. */
+#define TVS_KIND_CONV0 0
+#define TVS_KIND_HIDDEN 1
+#define TVS_KIND_HEAD 2
+int tvs_profile_enable(tvs_plan* plan, int on);
+int tvs_profile_read(tvs_plan* plan, int kind, double* total_ms, long long* launches, double* flops);
+
+int tvs_plan_destroy(tvs_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TVS_B200_H_ */

@@ -1,0 +1,149 @@
+"""ctypes binding of libtvsb200.so (include/tvs_b200.h).
+
+The library is the product: there is no Python or CPU fallback.  Loading it
+fails loudly if the .so is missing (run ``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libtvsb200.so"
+
+TVS_OK = 0
+TVS_E_INVALID = -1
+TVS_E_UNSUPPORTED = -2
+TVS_E_CUDA = -3
+TVS_E_STATE = -4
+
+MODE_FP32 = 0
+MODE_FAST = 1
+
+EXPORTS = (
+    "tvs_abi_version",
+    "tvs_last_error",
+    "tvs_plan_create",
+    "tvs_plan_set_weights",
+    "tvs_forward",
+    "tvs_forward_host",
+    "tvs_last_launch_count",
+    "tvs_profile_enable",
+    "tvs_profile_read",
+    "tvs_plan_destroy",
+)
+
+_lock = threading.Lock()
+_lib = None
+
+
+class TVSError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libtvsb200 error {code}: {msg}")
+        self.code = code
+
+
+def load() -> ctypes.CDLL:
+    """Load (once) and type the C ABI.  Raises if the library is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: the TVSpecNET B200 path has no CPU fallback; "
+                "build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        lib = ctypes.CDLL(str(LIB_PATH))
+        P = ctypes.c_void_p
+        i = ctypes.c_int
+        lib.tvs_abi_version.restype = i
+        lib.tvs_abi_version.argtypes = []
+        lib.tvs_last_error.restype = ctypes.c_char_p
+        lib.tvs_last_error.argtypes = []
+        lib.tvs_plan_create.restype = i
+        lib.tvs_plan_create.argtypes = [i, i, i, i, i, ctypes.POINTER(P)]
+        lib.tvs_plan_set_weights.restype = i
+        lib.tvs_plan_set_weights.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), i, P]
+        lib.tvs_forward.restype = i
+        lib.tvs_forward.argtypes = [P, P, P, P, i, i, i, i, i, P]
+        lib.tvs_forward_host.restype = i
+        lib.tvs_forward_host.argtypes = [P, P, P, P, i, i, i, P]
+        lib.tvs_last_launch_count.restype = i
+        lib.tvs_last_launch_count.argtypes = [P]
+        lib.tvs_profile_enable.restype = i
+        lib.tvs_profile_enable.argtypes = [P, i]
+        lib.tvs_profile_read.restype = i
+        lib.tvs_profile_read.argtypes = [P, i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong),
+                                         ctypes.POINTER(ctypes.c_double)]
+        lib.tvs_plan_destroy.restype = i
+        lib.tvs_plan_destroy.argtypes = [P]
+        _lib = lib
+        return lib
+
+
+def check(code: int) -> None:
+    if code != TVS_OK:
+        msg = load().tvs_last_error().decode(errors="replace")
+        if code == TVS_E_INVALID:
+            raise ValueError(msg)
+        raise TVSError(code, msg)
+
+
+class Plan:
+    """RAII owner of one ``tvs_plan`` (one device, one architecture, one mode)."""
+
+    def __init__(self, device: int, depth: int, channels: int, out_bands: int, mode: int):
+        self.lib = load()
+        self.handle = ctypes.c_void_p()
+        check(self.lib.tvs_plan_create(device, depth, channels, out_bands, mode, ctypes.byref(self.handle)))
+        self.device, self.depth, self.channels, self.out_bands, self.mode = device, depth, channels, out_bands, mode
+
+    def set_weights(self, w_ptrs, scale_ptrs, shift_ptrs, stream: int) -> None:
+        """Device pointers per layer; scale_ptrs entries may be 0 (= no BatchNorm)."""
+        n = len(w_ptrs)
+        W = (ctypes.c_void_p * n)(*w_ptrs)
+        S = (ctypes.c_void_p * n)(*[p or None for p in scale_ptrs])
+        Bv = (ctypes.c_void_p * n)(*shift_ptrs)
+        check(self.lib.tvs_plan_set_weights(self.handle, W, S, Bv, n, ctypes.c_void_p(stream)))
+
+    def forward(self, x_ptr, bands_ptr, closure_ptr, B, H, W, row0, rows, stream: int) -> None:
+        check(
+            self.lib.tvs_forward(
+                self.handle, ctypes.c_void_p(x_ptr), ctypes.c_void_p(bands_ptr),
+                ctypes.c_void_p(closure_ptr) if closure_ptr else None,
+                B, H, W, row0, rows, ctypes.c_void_p(stream),
+            )
+        )
+
+    def forward_host(self, x_ptr, bands_ptr, closure_ptr, B, H, W, stream: int) -> None:
+        check(
+            self.lib.tvs_forward_host(
+                self.handle, ctypes.c_void_p(x_ptr), ctypes.c_void_p(bands_ptr),
+                ctypes.c_void_p(closure_ptr) if closure_ptr else None, B, H, W, ctypes.c_void_p(stream),
+            )
+        )
+
+    def last_launch_count(self) -> int:
+        return int(self.lib.tvs_last_launch_count(self.handle))
+
+    def profile_enable(self, on: bool) -> None:
+        check(self.lib.tvs_profile_enable(self.handle, 1 if on else 0))
+
+    def profile_read(self, kind: int) -> tuple[float, int, float]:
+        """(device ms, launches, algorithmic FLOPs) for kind 0 conv0, 1 hidden, 2 head."""
+        ms, n, fl = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_double()
+        check(self.lib.tvs_profile_read(self.handle, kind, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(fl)))
+        return ms.value, n.value, fl.value
+
+    def close(self) -> None:
+        if self.handle and self.handle.value:
+            self.lib.tvs_plan_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

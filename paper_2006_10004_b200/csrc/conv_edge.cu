@@ -1,0 +1,279 @@
+// conv_edge.cu — the two thin ends of the TVSpecNET stack and the fp32
+// hidden layer used by the fp32-accurate mode.
+//
+//   K1 conv0_kernel : Conv2d(1,64,3,p=1,bias) + ReLU  (model.py:37-38)
+//       fp32 NCHW plane -> activation NHWC (fp16 or fp32).  K = 9, so it runs
+//       on CUDA cores (0.10% of the FLOPs).
+//   K3 head_kernel  : Conv2d(64,K,3,p=1,bias)          (model.py:44)
+//       + closure plane image - sum(bands)              (inference.py:34-42)
+//       activation NHWC -> bands fp32 NCHW, exact fp32 arithmetic in every
+//       mode; optional row window so row-band shards store only valid rows.
+//   hidden_f32_kernel : Conv2d(64,64)+BN+ReLU on fp32 NHWC (fp32-accurate
+//       mode).  Products of fp32 operands are accumulated in fp64 (DFMA) and
+//       the BatchNorm scale/shift applied after the sum, so each layer's
+//       output is the correctly-rounded fp32 of the exact conv+BN: the
+//       remaining distance to the reference is the reference's own fp32
+//       rounding (an fp32 re-computation alone is 7-9e-6 away
+//       from the oracle, too close to the 1e-5 gate).
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace tvs {
+
+// ------------------------------------------------------------------ K1 ----
+template <typename T>
+__device__ __forceinline__ void store_act8(T* dst, const float* v);
+template <>
+__device__ __forceinline__ void store_act8<__half>(__half* dst, const float* v) {
+  uint4 o;
+  __half2 h0 = __floats2half2_rn(v[0], v[1]), h1 = __floats2half2_rn(v[2], v[3]);
+  __half2 h2 = __floats2half2_rn(v[4], v[5]), h3 = __floats2half2_rn(v[6], v[7]);
+  o.x = *reinterpret_cast<uint32_t*>(&h0); o.y = *reinterpret_cast<uint32_t*>(&h1);
+  o.z = *reinterpret_cast<uint32_t*>(&h2); o.w = *reinterpret_cast<uint32_t*>(&h3);
+  *reinterpret_cast<uint4*>(dst) = o;
+}
+template <>
+__device__ __forceinline__ void store_act8<float>(float* dst, const float* v) {
+  reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+// one thread per pixel; 128 pixels per block are contiguous in NHWC, so the
+// block's output is staged through shared memory and written coalesced.
+template <typename T>
+__global__ void __launch_bounds__(128)
+conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const float* __restrict__ w0,
+             const float* __restrict__ b0, int B, int H, int W) {
+  __shared__ float sw[kC * 9];
+  __shared__ float sb[kC];
+  __shared__ __align__(16) T stage[128 * kC];
+  for (int i = threadIdx.x; i < kC * 9; i += blockDim.x) sw[i] = w0[i];
+  if (threadIdx.x < kC) sb[threadIdx.x] = b0[threadIdx.x];
+  __syncthreads();
+  const long long npx = (long long)B * H * W;
+  const long long p0 = (long long)blockIdx.x * 128;
+  const long long p = p0 + threadIdx.x;
+  if (p < npx) {
+    const int xw = (int)(p % W);
+    const long long t = p / W;
+    const int y = (int)(t % H);
+    const long long b = t / H;
+    const float* img = x + b * (long long)H * W;
+    float in[9];
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        const int yy = y + ky - 1, xx = xw + kx - 1;
+        in[ky * 3 + kx] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(img + (long long)yy * W + xx) : 0.0f;
+      }
+    T* dst = stage + threadIdx.x * kC;
+#pragma unroll
+    for (int c8 = 0; c8 < kC / 8; ++c8) {
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int co = c8 * 8 + e;
+        using Acc = std::conditional_t<std::is_same_v<T, float>, double, float>;  // fp64 in fp32 mode
+        Acc acc = 0;
+#pragma unroll
+        for (int t9 = 0; t9 < 9; ++t9) acc = fma((Acc)sw[co * 9 + t9], (Acc)in[t9], acc);
+        v[e] = fmaxf((float)(acc + (Acc)sb[co]), 0.0f);
+      }
+      store_act8<T>(dst + c8 * 8, v);
+    }
+  }
+  __syncthreads();
+  // coalesced copy of the staged block (valid pixels only)
+  const long long nvalid = min((long long)128, npx - p0);
+  const int n16 = (int)(nvalid * kC * sizeof(T) / 16);
+  const uint4* src = reinterpret_cast<const uint4*>(stage);
+  uint4* out = reinterpret_cast<uint4*>(act + p0 * kC);
+  for (int i = threadIdx.x; i < n16; i += blockDim.x) out[i] = src[i];
+}
+
+// ------------------------------------------------------------------ K3 ----
+template <typename T>
+__device__ __forceinline__ void load_act8(const T* src, float* v);
+template <>
+__device__ __forceinline__ void load_act8<__half>(const __half* src, float* v) {
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(src));
+  const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { float2 f = __half22float2(h[i]); v[2 * i] = f.x; v[2 * i + 1] = f.y; }
+}
+template <>
+__device__ __forceinline__ void load_act8<float>(const float* src, float* v) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(src));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(src) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+// wh: [K][64][3][3] fp32 ; output rows [row0, row0+rows) of each image go to
+// bands[b][k][r-row0][x] and closure[b][0][r-row0][x].
+template <typename T>
+__global__ void __launch_bounds__(128)
+head_kernel(const T* __restrict__ act, const float* __restrict__ x, const float* __restrict__ wh,
+            const float* __restrict__ bh, float* __restrict__ bands, float* __restrict__ closure, int B,
+            int H, int W, int K, int row0, int rows) {
+  extern __shared__ float swh[];  // [9][64][K]
+  for (int i = threadIdx.x; i < 9 * kC * K; i += blockDim.x) {
+    const int k = i % K, ci = (i / K) % kC, t = i / (K * kC);
+    swh[i] = wh[(k * kC + ci) * 9 + t];
+  }
+  __syncthreads();
+  const long long nout = (long long)B * rows * W;
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nout) return;
+  const int xw = (int)(p % W);
+  const long long t = p / W;
+  const int rr = (int)(t % rows);
+  const long long b = t / rows;
+  const int y = row0 + rr;
+  using Acc = std::conditional_t<std::is_same_v<T, float>, double, float>;  // fp64 in fp32 mode
+  Acc acc[kMaxBands];
+#pragma unroll
+  for (int k = 0; k < kMaxBands; ++k) acc[k] = 0;
+  const T* base = act + b * (long long)H * W * kC;
+  for (int ky = 0; ky < 3; ++ky) {
+    const int yy = y + ky - 1;
+    if (yy < 0 || yy >= H) continue;
+    for (int kx = 0; kx < 3; ++kx) {
+      const int xx = xw + kx - 1;
+      if (xx < 0 || xx >= W) continue;
+      const T* src = base + ((long long)yy * W + xx) * kC;
+      const float* wt = swh + (ky * 3 + kx) * kC * K;
+#pragma unroll 2
+      for (int c8 = 0; c8 < kC / 8; ++c8) {
+        float v[8];
+        load_act8<T>(src + c8 * 8, v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float* wr = wt + (c8 * 8 + e) * K;
+#pragma unroll
+          for (int k = 0; k < kMaxBands; ++k)
+            if (k < K) acc[k] = fma((Acc)wr[k], (Acc)v[e], acc[k]);
+        }
+      }
+    }
+  }
+  float sum = 0.0f;
+  const long long plane = (long long)rows * W;
+  float* ob = bands + b * K * plane + (long long)rr * W + xw;
+#pragma unroll
+  for (int k = 0; k < kMaxBands; ++k)
+    if (k < K) {
+      const float o = (float)(acc[k] + (Acc)bh[k]);
+      ob[k * plane] = o;
+      sum += o;
+    }
+  if (closure != nullptr) closure[b * plane + (long long)rr * W + xw] = x[(b * H + y) * (long long)W + xw] - sum;
+}
+
+// --------------------------------------------------- fp32 hidden layer ----
+// Output tile 4 rows x 32 px x 64 co per 256-thread block; thread = (co
+// group of 8, px column); input channels streamed in chunks of 16.
+__global__ void __launch_bounds__(256)
+hidden_f32_kernel(const float* __restrict__ in, float* __restrict__ out, const float* __restrict__ w /*[co][ci][9]*/,
+                  const float* __restrict__ scale, const float* __restrict__ shift, int B, int H, int W) {
+  extern __shared__ float sm[];
+  float* sIn = sm;                                        // [rows][px][ci]
+  float* sWt = sm + kF32InRows * kF32InPx * kF32CiChunk;  // [ci][tap][co]
+  const int tx = threadIdx.x & 31;  // px column
+  const int g = threadIdx.x >> 5;   // co group (8 channels)
+  const int tiles_x = (W + kF32TilePx - 1) / kF32TilePx;
+  const int tiles_y = (H + kF32TileRows - 1) / kF32TileRows;
+  const int tile = blockIdx.x;
+  const int b = tile / (tiles_x * tiles_y);
+  const int ty0 = ((tile / tiles_x) % tiles_y) * kF32TileRows;
+  const int tx0 = (tile % tiles_x) * kF32TilePx;
+  double acc[kF32TileRows][8];
+#pragma unroll
+  for (int r = 0; r < kF32TileRows; ++r)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[r][e] = 0.0;
+  const float* ib = in + (long long)b * H * W * kC;
+  for (int c0 = 0; c0 < kC; c0 += kF32CiChunk) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < kF32InRows * kF32InPx * kF32CiChunk; i += blockDim.x) {
+      const int ci = i % kF32CiChunk, px = (i / kF32CiChunk) % kF32InPx, r = i / (kF32CiChunk * kF32InPx);
+      const int yy = ty0 + r - 1, xx = tx0 + px - 1;
+      sIn[i] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? ib[((long long)yy * W + xx) * kC + c0 + ci] : 0.0f;
+    }
+    for (int i = threadIdx.x; i < kF32CiChunk * 9 * kC; i += blockDim.x) {
+      const int co = i % kC, t = (i / kC) % 9, ci = i / (kC * 9);
+      sWt[i] = w[((long long)co * kC + c0 + ci) * 9 + t];
+    }
+    __syncthreads();
+    for (int ci = 0; ci < kF32CiChunk; ++ci) {
+#pragma unroll
+      for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+          const float4 w0 = *reinterpret_cast<const float4*>(sWt + (ci * 9 + ky * 3 + kx) * kC + g * 8);
+          const float4 w1 = *reinterpret_cast<const float4*>(sWt + (ci * 9 + ky * 3 + kx) * kC + g * 8 + 4);
+          const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+          for (int r = 0; r < kF32TileRows; ++r) {
+            const float a = sIn[((r + ky) * kF32InPx + tx + kx) * kF32CiChunk + ci];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[r][e] = fma((double)wv[e], (double)a, acc[r][e]);
+          }
+        }
+    }
+  }
+  const int xw = tx0 + tx;
+  if (xw >= W) return;
+#pragma unroll
+  for (int r = 0; r < kF32TileRows; ++r) {
+    const int y = ty0 + r;
+    if (y >= H) break;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      v[e] = fmaxf((float)fma(acc[r][e], (double)scale[g * 8 + e], (double)shift[g * 8 + e]), 0.0f);
+    float* dst = out + (((long long)b * H + y) * W + xw) * kC + g * 8;
+    reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
+cudaError_t launch_conv0(bool fp16_act, const float* x, void* act, const float* w0, const float* b0, int B, int H,
+                         int W, cudaStream_t st) {
+  const long long npx = (long long)B * H * W;
+  const unsigned grid = (unsigned)((npx + 127) / 128);
+  if (fp16_act)
+    conv0_kernel<__half><<<grid, 128, 0, st>>>(x, static_cast<__half*>(act), w0, b0, B, H, W);
+  else
+    conv0_kernel<float><<<grid, 128, 0, st>>>(x, static_cast<float*>(act), w0, b0, B, H, W);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_head(bool fp16_act, const void* act, const float* x, const float* wh, const float* bh,
+                        float* bands, float* closure, int B, int H, int W, int K, int row0, int rows,
+                        cudaStream_t st) {
+  const long long nout = (long long)B * rows * W;
+  const unsigned grid = (unsigned)((nout + 127) / 128);
+  const size_t smem = (size_t)9 * kC * K * sizeof(float);
+  if (fp16_act)
+    head_kernel<__half><<<grid, 128, smem, st>>>(static_cast<const __half*>(act), x, wh, bh, bands, closure, B, H, W,
+                                                 K, row0, rows);
+  else
+    head_kernel<float><<<grid, 128, smem, st>>>(static_cast<const float*>(act), x, wh, bh, bands, closure, B, H, W, K,
+                                                row0, rows);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hidden_f32(const float* in, float* out, const float* w, const float* scale, const float* shift,
+                              int B, int H, int W, cudaStream_t st) {
+  const long long tiles = (long long)B * ((H + kF32TileRows - 1) / kF32TileRows) * ((W + kF32TilePx - 1) / kF32TilePx);
+  hidden_f32_kernel<<<(unsigned)tiles, 256, kF32Smem, st>>>(in, out, w, scale, shift, B, H, W);
+  return cudaGetLastError();
+}
+
+cudaError_t configure_edge_kernels() {
+  return cudaFuncSetAttribute(hidden_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem);
+}
+
+}  // namespace tvs

@@ -1,0 +1,413 @@
+// tvs_api.cu — host runtime behind include/tvs_b200.h: plans, packed
+// weights, TMA descriptors, activation scratch and the per-layer launch
+// sequence.  See DESIGN.md for the data layout.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tvs_b200.h"
+#include "common.cuh"
+
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct TvsError : std::runtime_error {
+  int code;
+  TvsError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define TVS_CUDA(call)                                                                                     \
+  do {                                                                                                     \
+    cudaError_t e_ = (call);                                                                               \
+    if (e_ != cudaSuccess)                                                                                 \
+      throw TvsError(TVS_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + " (" __FILE__ ":" + \
+                                     std::to_string(__LINE__) + ")");                                      \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    TVS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw TvsError(TVS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// fp16 NHWC activation [B][H][W][64] as a 4-D tensor map, SW128, box (64, box_px, 1, 1)
+CUtensorMap make_act_map(void* base, int B, int H, int W, int box_px) {
+  CUtensorMap m;
+  cuuint64_t dims[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {128, (cuuint64_t)W * 128, (cuuint64_t)H * W * 128};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_px, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw TvsError(TVS_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+}  // namespace
+
+struct tvs_plan {
+  int device = 0, depth = 17, channels = 64, out_bands = 5, mode = TVS_MODE_FAST;
+  int num_sms = 148;
+  bool weights_ready = false;
+  // conv0 [64][1][3][3] + bias, head [K][64][3][3] + bias (fp32, folded)
+  float* w0 = nullptr;
+  float* b0 = nullptr;
+  float* wh = nullptr;
+  float* bh = nullptr;
+  // hidden: fast -> packed fp16 (n_hidden * kWBytes) ; fp32 -> [co][ci][9] fp32
+  uint8_t* wpack = nullptr;
+  float* whid = nullptr;
+  float* bhid = nullptr;  // per hidden layer: shift (beta - mu*s)
+  float* shid = nullptr;  // per hidden layer: BatchNorm scale s (fp32 mode epilogue; folded in FAST)
+  // activation ping-pong scratch
+  void* act[2] = {nullptr, nullptr};
+  size_t act_bytes = 0;
+  // host-API staging
+  float* dx = nullptr;  // [x | bands | closure] staging for tvs_forward_host
+  size_t io_bytes = 0;
+  int last_launches = 0;
+  // optional per-kernel event timing
+  struct Rec { cudaEvent_t a, b; int kind; double flops; };
+  bool profiling = false;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> event_pool;
+  double prof_ms[3] = {0, 0, 0};
+  long long prof_n[3] = {0, 0, 0};
+  double prof_flops[3] = {0, 0, 0};
+  size_t chunk_budget = 48ull << 20;
+
+  int n_hidden() const { return depth - 2; }
+  size_t act_px_bytes() const { return mode == TVS_MODE_FAST ? 128 : 256; }
+};
+
+namespace {
+
+void ensure_device(const tvs_plan* p) { TVS_CUDA(cudaSetDevice(p->device)); }
+
+void free_all(tvs_plan* p) {
+  for (auto& r : p->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : p->event_pool) cudaEventDestroy(e);
+  p->recs.clear();
+  p->event_pool.clear();
+  void* ptrs[] = {p->w0, p->b0, p->wh, p->bh, p->wpack, p->whid, p->bhid, p->shid, p->act[0], p->act[1], p->dx};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+}
+
+void ensure_act(tvs_plan* p, size_t bytes) {
+  if (bytes <= p->act_bytes) return;
+  for (int i = 0; i < 2; ++i) {
+    if (p->act[i]) TVS_CUDA(cudaFree(p->act[i]));
+    p->act[i] = nullptr;
+  }
+  p->act_bytes = 0;
+  for (int i = 0; i < 2; ++i) TVS_CUDA(cudaMalloc(&p->act[i], bytes));
+  p->act_bytes = bytes;
+}
+
+int pick_band_rows(long long strip_rows_total, int H, int num_sms) {
+  // aim for >= 4 work units per SM, bands between 4 and 64 rows
+  long long target = (strip_rows_total + 4LL * num_sms - 1) / (4LL * num_sms);
+  int hb = (int)std::max(4LL, std::min(64LL, target));
+  return std::min(hb, H);
+}
+
+cudaEvent_t pool_event(tvs_plan* p) {
+  if (!p->event_pool.empty()) {
+    cudaEvent_t e = p->event_pool.back();
+    p->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  TVS_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+// Launch `f` bracketed by events when profiling is on.
+template <typename F>
+void timed_launch(tvs_plan* p, cudaStream_t st, int kind, double flops, F&& f) {
+  if (!p->profiling) {
+    TVS_CUDA(f());
+    p->last_launches++;
+    return;
+  }
+  tvs_plan::Rec r{pool_event(p), pool_event(p), kind, flops};
+  TVS_CUDA(cudaEventRecord(r.a, st));
+  TVS_CUDA(f());
+  TVS_CUDA(cudaEventRecord(r.b, st));
+  p->recs.push_back(r);
+  p->last_launches++;
+}
+
+void drain_profile(tvs_plan* p) {
+  for (auto& r : p->recs) {
+    TVS_CUDA(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    TVS_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    p->prof_ms[r.kind] += ms;
+    p->prof_n[r.kind] += 1;
+    p->prof_flops[r.kind] += r.flops;
+    p->event_pool.push_back(r.a);
+    p->event_pool.push_back(r.b);
+  }
+  p->recs.clear();
+}
+
+void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B, int H, int W, int row0, int rows,
+               cudaStream_t st) {
+  const bool fast = p->mode == TVS_MODE_FAST;
+  const double px = (double)B * H * W;
+  // K1
+  timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * 64,
+               [&] { return tvs::launch_conv0(fast, x, p->act[0], p->w0, p->b0, B, H, W, st); });
+  // K2 x (depth-2)
+  int cur = 0;
+  if (fast) {
+    tvs::HiddenArgs a;
+    a.B = B; a.H = H; a.W = W;
+    a.strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
+    a.band_rows = pick_band_rows((long long)B * a.strips * H, H, p->num_sms);
+    a.bands = (H + a.band_rows - 1) / a.band_rows;
+    a.units = B * a.bands * a.strips;
+    const unsigned grid = (unsigned)std::min(a.units, p->num_sms);
+    CUtensorMap in_map[2], out_map[2];
+    for (int i = 0; i < 2; ++i) {
+      in_map[i] = make_act_map(p->act[i], B, H, W, tvs::kHaloPx);
+      out_map[i] = make_act_map(p->act[i], B, H, W, tvs::kStripPx);
+    }
+    for (int l = 0; l < p->n_hidden(); ++l) {
+      a.wpack = p->wpack + (size_t)l * tvs::kWBytes;
+      a.bias = p->bhid + (size_t)l * tvs::kC;
+      timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64,
+                   [&] { return tvs::launch_hidden_f16(in_map[cur], out_map[cur ^ 1], a, (int)grid, st); });
+      cur ^= 1;
+    }
+  } else {
+    for (int l = 0; l < p->n_hidden(); ++l) {
+      timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64, [&] {
+        return tvs::launch_hidden_f32((const float*)p->act[cur], (float*)p->act[cur ^ 1],
+                                      p->whid + (size_t)l * 64 * 64 * 9, p->shid + (size_t)l * 64,
+                                      p->bhid + (size_t)l * 64, B, H, W, st);
+      });
+      cur ^= 1;
+    }
+  }
+  // K3
+  timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands, [&] {
+    return tvs::launch_head(fast, p->act[cur], x, p->wh, p->bh, bands, closure, B, H, W, p->out_bands, row0, rows,
+                            st);
+  });
+}
+
+void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int B, int H, int W, int row0, int rows,
+                  cudaStream_t st) {
+  if (!p->weights_ready) throw TvsError(TVS_E_STATE, "tvs_forward before tvs_plan_set_weights");
+  if (!x || !bands) throw TvsError(TVS_E_INVALID, "null x/bands pointer");
+  if (B < 0 || H < 1 || W < 1) throw TvsError(TVS_E_INVALID, "bad shape B/H/W");
+  if (rows < 0) { row0 = 0; rows = H; }
+  if (row0 < 0 || rows < 1 || row0 + rows > H) throw TvsError(TVS_E_INVALID, "bad valid row window");
+  p->last_launches = 0;
+  if (B == 0) return;
+  ensure_device(p);
+  const size_t per_img = (size_t)H * W * p->act_px_bytes();
+  int cb = (int)std::max<size_t>(1, p->chunk_budget / std::max<size_t>(per_img, 1));
+  cb = std::min(cb, B);
+  ensure_act(p, per_img * cb);
+  const size_t in_img = (size_t)H * W, out_img = (size_t)rows * W;
+  for (int b0 = 0; b0 < B; b0 += cb) {
+    const int nb = std::min(cb, B - b0);
+    run_chunk(p, x + b0 * in_img, bands + (size_t)b0 * p->out_bands * out_img,
+              closure ? closure + b0 * out_img : nullptr, nb, H, W, row0, rows, st);
+  }
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TVS_OK;
+  } catch (const TvsError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TVS_E_CUDA;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return TVS_E_CUDA;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int tvs_abi_version(void) { return TVS_ABI_VERSION; }
+
+const char* tvs_last_error(void) { return g_last_error.c_str(); }
+
+int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode, tvs_plan** out_plan) {
+  return guarded([&] {
+    if (!out_plan) throw TvsError(TVS_E_INVALID, "out_plan is null");
+    *out_plan = nullptr;
+    if (depth < 3) throw TvsError(TVS_E_INVALID, "depth must be at least 3 (first, hidden, last)");
+    if (channels != 64) throw TvsError(TVS_E_UNSUPPORTED, "this build supports channels == 64 only");
+    if (out_bands < 1 || out_bands > 8) throw TvsError(TVS_E_UNSUPPORTED, "out_bands must be in [1, 8]");
+    if (mode != TVS_MODE_FP32 && mode != TVS_MODE_FAST) throw TvsError(TVS_E_INVALID, "unknown mode");
+    int ndev = 0;
+    TVS_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw TvsError(TVS_E_INVALID, "bad device ordinal");
+    TVS_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    TVS_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+      throw TvsError(TVS_E_UNSUPPORTED, "libtvsb200 is built for sm_100a (B200) only");
+    auto* p = new tvs_plan();
+    p->device = device; p->depth = depth; p->channels = channels; p->out_bands = out_bands; p->mode = mode;
+    p->num_sms = prop.multiProcessorCount;
+    if (const char* e = std::getenv("TVS_CHUNK_MB")) p->chunk_budget = (size_t)std::atoll(e) << 20;
+    try {
+      TVS_CUDA(tvs::configure_kernels());
+      const int nh = depth - 2;
+      TVS_CUDA(cudaMalloc(&p->w0, 64 * 9 * 4));
+      TVS_CUDA(cudaMalloc(&p->b0, 64 * 4));
+      TVS_CUDA(cudaMalloc(&p->wh, (size_t)out_bands * 64 * 9 * 4));
+      TVS_CUDA(cudaMalloc(&p->bh, (size_t)out_bands * 4));
+      TVS_CUDA(cudaMalloc(&p->bhid, (size_t)nh * 64 * 4));
+      TVS_CUDA(cudaMalloc(&p->shid, (size_t)nh * 64 * 4));
+      if (mode == TVS_MODE_FAST)
+        TVS_CUDA(cudaMalloc(&p->wpack, (size_t)nh * tvs::kWBytes));
+      else
+        TVS_CUDA(cudaMalloc(&p->whid, (size_t)nh * 64 * 64 * 9 * 4));
+    } catch (...) {
+      free_all(p);
+      delete p;
+      throw;
+    }
+    *out_plan = p;
+  });
+}
+
+int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* const* scale_dev,
+                         const float* const* shift_dev, int n_layers, void* stream) {
+  return guarded([&] {
+    if (!p || !w_dev || !shift_dev) throw TvsError(TVS_E_INVALID, "null argument");
+    if (n_layers != p->depth) throw TvsError(TVS_E_INVALID, "n_layers must equal depth");
+    for (int i = 0; i < n_layers; ++i)
+      if (!w_dev[i] || !shift_dev[i]) throw TvsError(TVS_E_INVALID, "null weight/shift pointer");
+    ensure_device(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nh = p->n_hidden();
+    auto scale_of = [&](int i) -> const float* { return scale_dev ? scale_dev[i] : nullptr; };
+    if (scale_of(0) || scale_of(p->depth - 1))
+      throw TvsError(TVS_E_UNSUPPORTED, "conv0/head take no BatchNorm scale (model.py:37,44)");
+    TVS_CUDA(cudaMemcpyAsync(p->w0, w_dev[0], 64 * 9 * 4, cudaMemcpyDeviceToDevice, st));
+    TVS_CUDA(cudaMemcpyAsync(p->b0, shift_dev[0], 64 * 4, cudaMemcpyDeviceToDevice, st));
+    TVS_CUDA(cudaMemcpyAsync(p->wh, w_dev[p->depth - 1], (size_t)p->out_bands * 64 * 9 * 4,
+                             cudaMemcpyDeviceToDevice, st));
+    TVS_CUDA(cudaMemcpyAsync(p->bh, shift_dev[p->depth - 1], (size_t)p->out_bands * 4, cudaMemcpyDeviceToDevice,
+                             st));
+    for (int l = 0; l < nh; ++l) {
+      const float* sc = scale_of(l + 1);
+      float* dst_scale = p->shid + l * 64;
+      if (sc)
+        TVS_CUDA(cudaMemcpyAsync(dst_scale, sc, 64 * 4, cudaMemcpyDeviceToDevice, st));
+      else
+        TVS_CUDA(tvs::launch_fill(dst_scale, 1.0f, 64, st));
+      TVS_CUDA(cudaMemcpyAsync(p->bhid + l * 64, shift_dev[l + 1], 64 * 4, cudaMemcpyDeviceToDevice, st));
+      if (p->mode == TVS_MODE_FAST) {
+        TVS_CUDA(cudaMemsetAsync(p->wpack + (size_t)l * tvs::kWBytes, 0, tvs::kWBytes, st));
+        TVS_CUDA(tvs::launch_pack_hidden_f16(w_dev[l + 1], dst_scale, p->wpack + (size_t)l * tvs::kWBytes, st));
+      } else {
+        TVS_CUDA(cudaMemcpyAsync(p->whid + (size_t)l * 64 * 64 * 9, w_dev[l + 1], 64 * 64 * 9 * 4,
+                                 cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    p->weights_ready = true;
+  });
+}
+
+int tvs_forward(tvs_plan* p, const float* x, float* bands, float* closure_or_null, int B, int H, int W,
+                int valid_row0, int valid_rows, void* stream) {
+  return guarded([&] {
+    if (!p) throw TvsError(TVS_E_INVALID, "null plan");
+    forward_impl(p, x, bands, closure_or_null, B, H, W, valid_row0, valid_rows, (cudaStream_t)stream);
+  });
+}
+
+int tvs_forward_host(tvs_plan* p, const float* x_host, float* bands_host, float* closure_host_or_null, int B, int H,
+                     int W, void* stream) {
+  return guarded([&] {
+    if (!p || !x_host || !bands_host) throw TvsError(TVS_E_INVALID, "null argument");
+    if (B < 0 || H < 1 || W < 1) throw TvsError(TVS_E_INVALID, "bad shape B/H/W");
+    ensure_device(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t nx = (size_t)B * H * W, nb = nx * p->out_bands;
+    const size_t need = (nx + nb + nx) * 4;
+    if (need > p->io_bytes) {
+      if (p->dx) cudaFree(p->dx);
+      p->dx = nullptr; p->io_bytes = 0;
+      TVS_CUDA(cudaMalloc(&p->dx, need));
+      p->io_bytes = need;
+    }
+    float* dbands = p->dx + nx;
+    float* dclos = dbands + nb;
+    TVS_CUDA(cudaMemcpyAsync(p->dx, x_host, nx * 4, cudaMemcpyHostToDevice, st));
+    forward_impl(p, p->dx, dbands, closure_host_or_null ? dclos : nullptr, B, H, W, 0, H, st);
+    TVS_CUDA(cudaMemcpyAsync(bands_host, dbands, nb * 4, cudaMemcpyDeviceToHost, st));
+    if (closure_host_or_null)
+      TVS_CUDA(cudaMemcpyAsync(closure_host_or_null, dclos, nx * 4, cudaMemcpyDeviceToHost, st));
+    TVS_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int tvs_last_launch_count(const tvs_plan* p) { return p ? p->last_launches : 0; }
+
+int tvs_profile_enable(tvs_plan* p, int on) {
+  return guarded([&] {
+    if (!p) throw TvsError(TVS_E_INVALID, "null plan");
+    ensure_device(p);
+    drain_profile(p);
+    for (int k = 0; k < 3; ++k) { p->prof_ms[k] = 0; p->prof_n[k] = 0; p->prof_flops[k] = 0; }
+    p->profiling = on != 0;
+  });
+}
+
+int tvs_profile_read(tvs_plan* p, int kind, double* total_ms, long long* launches, double* flops) {
+  return guarded([&] {
+    if (!p || kind < 0 || kind > 2) throw TvsError(TVS_E_INVALID, "bad plan/kind");
+    ensure_device(p);
+    drain_profile(p);
+    if (total_ms) *total_ms = p->prof_ms[kind];
+    if (launches) *launches = p->prof_n[kind];
+    if (flops) *flops = p->prof_flops[kind];
+  });
+}
+
+int tvs_plan_destroy(tvs_plan* p) {
+  return guarded([&] {
+    if (!p) return;
+    cudaSetDevice(p->device);
+    free_all(p);
+    delete p;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,199 @@
+"""Drop-in TVSpecNet whose forward runs on hand-written sm_100a kernels.
+
+Mirrors /root/reference/pkg/trainer/src/tvsurrogate/model.py:
+
+* ``ARCH_SPEC``            — model.py:19-26 (unchanged constants)
+* ``TVSpecNet(depth=17, channels=64, out_bands=5)`` — model.py:29-47: the
+  same ``nn.Sequential`` body, so ``state_dict`` keys/shapes, ``depth`` and
+  ``out_bands`` attributes, module counts and ``load_state_dict`` (strict)
+  behave exactly like the reference (training.py:163-172 loads into it).
+* ``forward(x)``           — model.py:49-52: ValueError unless x is
+  (B, 1, H, W); returns (B, out_bands, H, W) float32 on x's device.
+* ``receptive_field``      — model.py:55-56.
+
+What differs is where the arithmetic happens: ``forward`` turns eval-mode
+BatchNorm into per-channel scale/shift (fp64 on the host side, cached by
+parameter versions), hands them to a per-device C-ABI plan (libtvsb200.so), and runs
+conv0 -> 15 tcgen05 hidden convs -> head on the GPU.  CPU tensors are copied
+to the execution device and the result copied back, so the reference's CPU
+callers (``predict_bands``, inference.py:25-32) work unchanged.  There is no
+CPU fallback and no train-mode path: ``forward`` raises in ``train()`` mode
+(batch statistics are out of scope) and when no CUDA device is present.
+
+``precision`` selects the numerics: ``"fast"`` (default; fp16 tcgen05 hidden
+layers, exact fp32 conv0/head; <= 1e-2 relative L2 per band vs the fp32
+reference) or ``"fp32"`` (fp32 activations and arithmetic; <= 1e-5).
+"""
+
+from __future__ import annotations
+
+import torch
+from torch import nn
+
+from . import _native
+
+__all__ = ["ARCH_SPEC", "TVSpecNet", "receptive_field"]
+
+ARCH_SPEC = {
+    "depth": 17,
+    "channels": 64,
+    "kernel": 3,
+    "out_bands": 5,
+    "batch_norm": True,
+    "receptive_field": 35,
+}
+
+_PRECISIONS = {"fp32": _native.MODE_FP32, "fast": _native.MODE_FAST}
+
+
+class TVSpecNet(nn.Module):
+    """DnCNN-shaped regressor from an image to its first ``out_bands`` bands."""
+
+    def __init__(self, depth: int = 17, channels: int = 64, out_bands: int = 5, *, precision: str = "fast"):
+        super().__init__()
+        if depth < 3:
+            raise ValueError("depth must be at least 3 (first, hidden, last)")
+        layers: list[nn.Module] = [nn.Conv2d(1, channels, 3, padding=1, bias=True), nn.ReLU(inplace=True)]
+        for _ in range(depth - 2):
+            layers.append(nn.Conv2d(channels, channels, 3, padding=1, bias=False))
+            layers.append(nn.BatchNorm2d(channels))
+            layers.append(nn.ReLU(inplace=True))
+        layers.append(nn.Conv2d(channels, out_bands, 3, padding=1, bias=True))
+        self.body = nn.Sequential(*layers)
+        self.depth = depth
+        self.out_bands = out_bands
+        self.channels = channels
+        if precision not in _PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(_PRECISIONS)}")
+        self._precision = precision
+        self._plans: dict[int, tuple[_native.Plan, tuple]] = {}
+
+    # ------------------------------------------------------------ config ----
+    @property
+    def precision(self) -> str:
+        return self._precision
+
+    @precision.setter
+    def precision(self, value: str) -> None:
+        if value not in _PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(_PRECISIONS)}")
+        if value != self._precision:
+            self._precision = value
+            self._drop_plans()
+
+    def _drop_plans(self) -> None:
+        for plan, _ in self._plans.values():
+            plan.close()
+        self._plans.clear()
+
+    def __getstate__(self):
+        state = self.__dict__.copy()
+        state["_plans"] = {}
+        return state
+
+    # ------------------------------------------------------ weight folding ----
+    def _weight_key(self, device: torch.device) -> tuple:
+        key = [str(device), self._precision]
+        for t in list(self.parameters()) + list(self.buffers()):
+            key.append((t.data_ptr(), t._version))
+        return tuple(key)
+
+    @torch.no_grad()
+    def layer_params(self) -> list[tuple[torch.Tensor, torch.Tensor | None, torch.Tensor]]:
+        """Per conv: (W, scale-or-None, shift) in fp64 with y = scale*conv(W, a) + shift.
+        Eval BatchNorm2d (model.py:41): scale = gamma/sqrt(var+eps),
+        shift = beta + (bias - mean)*scale; convs without BN: scale None, shift = bias."""
+        mods = list(self.body)
+        out = []
+        for i, m in enumerate(mods):
+            if not isinstance(m, nn.Conv2d):
+                continue
+            w = m.weight.detach().double()
+            b = (m.bias.detach().double() if m.bias is not None
+                 else torch.zeros(w.shape[0], dtype=torch.float64, device=w.device))
+            nxt = mods[i + 1] if i + 1 < len(mods) else None
+            if isinstance(nxt, nn.BatchNorm2d):
+                s = nxt.weight.detach().double() / torch.sqrt(nxt.running_var.detach().double() + nxt.eps)
+                out.append((w, s, nxt.bias.detach().double() + (b - nxt.running_mean.detach().double()) * s))
+            else:
+                out.append((w, None, b))
+        return out
+
+    def _plan_for(self, device: torch.device) -> _native.Plan:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        key = self._weight_key(torch.device("cuda", idx))
+        entry = self._plans.get(idx)
+        if entry is not None and entry[1] == key:
+            return entry[0]
+        plan = entry[0] if entry is not None else _native.Plan(
+            idx, self.depth, self.channels, self.out_bands, _PRECISIONS[self._precision]
+        )
+        with torch.cuda.device(idx):
+            stream = torch.cuda.current_stream(idx)
+            dev = torch.device("cuda", idx)
+            staged = []
+            for w, s, b in self.layer_params():
+                staged.append((w.to(dev, torch.float32).contiguous(),
+                               None if s is None else s.to(dev, torch.float32).contiguous(),
+                               b.to(dev, torch.float32).contiguous()))
+            plan.set_weights([w.data_ptr() for w, _, _ in staged],
+                             [0 if s is None else s.data_ptr() for _, s, _ in staged],
+                             [b.data_ptr() for _, _, b in staged], stream.cuda_stream)
+            # keep the fp32 staging alive until the repack kernels have consumed it
+            stream.synchronize()
+        self._plans[idx] = (plan, key)
+        return plan
+
+    # ------------------------------------------------------------- forward ----
+    def _exec_device(self, x: torch.Tensor) -> torch.device:
+        if x.is_cuda:
+            return x.device
+        if not torch.cuda.is_available():
+            raise RuntimeError("TVSpecNet (B200) needs a CUDA device; there is no CPU fallback")
+        p = next(self.parameters())
+        if p.is_cuda:
+            return p.device
+        return torch.device("cuda", torch.cuda.current_device())
+
+    def _check_input(self, x: torch.Tensor) -> None:
+        if x.ndim != 4 or x.shape[1] != 1:
+            raise ValueError(f"expected (batch, 1, h, w) input, got {tuple(x.shape)}")
+        if x.dtype != torch.float32:
+            raise RuntimeError(f"Input type ({x.dtype}) and weight type (torch.float32) should be the same")
+        if self.training:
+            raise RuntimeError("TVSpecNet (B200) implements the eval-mode forward only; call .eval() first")
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        return self.forward_planes(x)[0]
+
+    def forward_planes(self, x: torch.Tensor, closure: bool = False, rows: tuple[int, int] | None = None):
+        """(bands, closure-or-None).  ``closure`` adds the band-sum
+        reconstruction plane image - sum(bands) (inference.py:34-42) from the
+        head kernel's epilogue; ``rows=(row0, nrows)`` returns only that row
+        window of the full-image forward (row-band sharding)."""
+        self._check_input(x)
+        dev = self._exec_device(x)
+        plan = self._plan_for(dev)
+        B, _, H, W = x.shape
+        row0, nrows = (0, H) if rows is None else rows
+        if not (0 <= row0 and nrows >= 1 and row0 + nrows <= H):
+            raise ValueError(f"bad row window {rows} for height {H}")
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev)
+            xd = x.to(dev, non_blocking=True).contiguous()
+            bands = torch.empty((B, self.out_bands, nrows, W), device=dev, dtype=torch.float32)
+            clos = torch.empty((B, 1, nrows, W), device=dev, dtype=torch.float32) if closure else None
+            plan.forward(xd.data_ptr(), bands.data_ptr(), clos.data_ptr() if closure else 0, B, H, W, row0, nrows,
+                         stream.cuda_stream)
+        if not x.is_cuda:
+            bands = bands.cpu()
+            clos = clos.cpu() if clos is not None else None
+        return bands, clos
+
+    def last_launch_count(self, device: int | None = None) -> int:
+        idx = torch.cuda.current_device() if device is None else device
+        return self._plans[idx][0].last_launch_count() if idx in self._plans else 0
+
+
+def receptive_field(depth: int = 17, kernel: int = 3) -> int:
+    return depth * (kernel - 1) + 1

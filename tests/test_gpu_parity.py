@@ -1,0 +1,210 @@
+"""GPU parity of the B200 path against the CPU oracle / reference fixtures.
+
+Tolerances (BASELINE.json north_star), relative L2 per image per band:
+  * precision="fp32": <= 1e-5
+  * precision="fast": <= 1e-2, closure (band-sum reconstruction) <= 1e-2
+All calls go through the C ABI (libtvsb200.so) via the drop-in module.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.tvspecnet_oracle import band_rel_l2, build_seeded_state, oracle_from_state
+from paper_2006_10004_b200 import TVSpecNet, predict_bands, predict_planes
+from paper_2006_10004_b200 import _native
+from paper_2006_10004_b200.shard import forward_shard
+from paper_2006_10004_b200.workloads import CONFIGS, make_image
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-5, "fast": 1e-2}
+CLOSURE_TOL = {"fp32": 1e-5, "fast": 1e-2}
+
+
+@pytest.fixture(scope="module")
+def oracle(seeded_state):
+    torch.set_num_threads(max(1, min(32, torch.get_num_threads())))
+    return oracle_from_state(seeded_state)
+
+
+@pytest.fixture(scope="module", params=["fast", "fp32"])
+def model(request, seeded_state):
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    m = TVSpecNet(precision=request.param).eval()
+    m.load_state_dict(seeded_state)
+    return m
+
+
+def _run(m, x):
+    bands, clos = m.forward_planes(torch.from_numpy(x).cuda(), closure=True)
+    torch.cuda.synchronize()
+    return bands.cpu().numpy(), clos.cpu().numpy()
+
+
+def _check(m, x, ref):
+    out, clos = _run(m, x)
+    assert out.shape == ref.shape
+    assert np.isfinite(out).all()
+    err = band_rel_l2(out, ref)
+    assert err.max() <= TOL[m.precision], f"worst band rel-L2 {err.max():.3e}"
+    cref = x[:, 0:1] - ref.sum(1, keepdims=True)
+    cerr = band_rel_l2(clos, cref)
+    assert cerr.max() <= CLOSURE_TOL[m.precision], f"closure rel-L2 {cerr.max():.3e}"
+    # the closure plane closes the decomposition exactly (inference.py:34-42)
+    np.testing.assert_allclose(out.sum(1, keepdims=True) + clos, x[:, 0:1], atol=1e-5)
+    return err.max()
+
+
+@pytest.mark.parametrize("case", ["small", "nonsq", "tiny", "tiny2", "cfg1"])
+def test_golden_fixtures(model, golden, case):
+    _check(model, golden[f"{case}_x"], golden[f"{case}_y"])
+
+
+def test_depth3_fixture(golden):
+    for prec in ("fast", "fp32"):
+        m = TVSpecNet(depth=3, precision=prec).eval()
+        m.load_state_dict(build_seeded_state(3, 64, 5))
+        _check(m, golden["d3_x"], golden["d3_y"])
+
+
+@pytest.mark.parametrize("cfg,count", [(2, 4), (3, 1), (5, 2)])
+def test_configs_vs_oracle(model, oracle, cfg, count):
+    spec = CONFIGS[cfg]
+    x = np.stack([make_image(spec, i) for i in range(count)])[:, None]
+    with torch.no_grad():
+        ref = oracle(torch.from_numpy(x)).numpy()
+    _check(model, x, ref)
+
+
+def test_config4_plane0_vs_oracle(model, oracle):
+    x = make_image(CONFIGS[4], 0)[None, None]
+    with torch.no_grad():
+        ref = oracle(torch.from_numpy(x)).numpy()
+    _check(model, x, ref)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 5, 300), (2, 1, 129, 131), (1, 1, 300, 1), (1, 1, 1, 257), (3, 1, 33, 255)])
+def test_ragged_shapes(model, oracle, shape):
+    x = np.random.default_rng(sum(shape)).random(shape).astype(np.float32)
+    with torch.no_grad():
+        ref = oracle(torch.from_numpy(x)).numpy()
+    _check(model, x, ref)
+
+
+def test_translation_equivariance_interior(model):  # test_model.py:42-59
+    rng = np.random.default_rng(3)
+    x = torch.from_numpy(rng.standard_normal((48, 48)).astype(np.float32))
+    shifted = torch.zeros_like(x)
+    shifted[4:, :] = x[:-4, :]
+    y = model(x[None, None].cuda())[0]
+    y2 = model(shifted[None, None].cuda())[0]
+    half = 35 // 2
+    lo, hi = half + 4, 48 - half
+    torch.testing.assert_close(y2[:, lo:hi, :], y[:, lo - 4 : hi - 4, :], atol=1e-5, rtol=1e-5)
+
+
+def test_eval_is_deterministic(model):  # test_model.py:62-70
+    x = torch.randn(2, 1, 64, 200, device="cuda")
+    a, b = model(x), model(x)
+    assert torch.equal(a, b)
+
+
+def test_row_window_equals_full_rows(model):
+    x = torch.rand(2, 1, 96, 140, device="cuda")
+    full = model(x)
+    bands, clos = model.forward_planes(x, closure=True, rows=(30, 17))
+    assert torch.equal(bands, full[:, :, 30:47])
+    torch.testing.assert_close(clos, x[:, :, 30:47] - full[:, :, 30:47].sum(1, keepdim=True))
+
+
+def test_row_band_shards_equal_unsharded(model):
+    """halo = depth rows makes every band bitwise equal to the full forward."""
+    x = torch.from_numpy(make_image(CONFIGS[3], 0)[None, None]).cuda()
+    full = model(x)
+    for world in (2, 4, 8):
+        parts = [forward_shard(model, x, r, world, "rows")[0] for r in range(world)]
+        assert torch.equal(torch.cat(parts, dim=2), full), world
+
+
+def test_batch_shards_equal_unsharded(model):
+    x = torch.rand(5, 1, 64, 64, device="cuda")
+    full = model(x)
+    parts = [forward_shard(model, x, r, 4, "batch")[0] for r in range(4)]
+    assert torch.equal(torch.cat(parts, dim=0), full)
+
+
+def test_cpu_tensors_in_and_out(model, golden):
+    x = torch.from_numpy(golden["nonsq_x"])
+    y = model(x)
+    assert y.device.type == "cpu" and y.shape == (1, 5, 32, 40)
+    img = golden["small_x"][0, 0].astype(np.float64)
+    out = predict_bands(model, img)  # inference.py:25-32 calling convention
+    assert out.shape == (5, 16, 20) and np.isfinite(out).all()
+
+
+def test_predict_planes_stack(model):
+    x = torch.rand(2, 1, 20, 30, device="cuda")
+    planes = predict_planes(model, x)
+    assert planes.shape == (2, 7, 20, 30)
+    torch.testing.assert_close(planes[:, 1:].sum(1), planes[:, 0], atol=1e-5, rtol=0)
+
+
+def test_host_buffer_abi_matches_device_path(model, golden):
+    x = np.ascontiguousarray(golden["small_x"])
+    plan = model._plan_for(torch.device("cuda", 0))
+    bands = np.empty((2, 5, 16, 20), np.float32)
+    clos = np.empty((2, 1, 16, 20), np.float32)
+    plan.forward_host(x.ctypes.data, bands.ctypes.data, clos.ctypes.data, 2, 16, 20, 0)
+    dev_b, dev_c = _run(model, x)
+    np.testing.assert_array_equal(bands, dev_b)
+    np.testing.assert_array_equal(clos, dev_c)
+
+
+def test_weight_reload_invalidates_pack(seeded_state):
+    m = TVSpecNet().eval()
+    m.load_state_dict(seeded_state)
+    x = torch.rand(1, 1, 32, 32, device="cuda")
+    a = m(x)
+    other = build_seeded_state(seed=1)
+    m.load_state_dict(other)
+    b = m(x)
+    ref = oracle_from_state(other)(x.cpu()).detach().numpy()
+    assert not torch.equal(a, b)
+    assert band_rel_l2(b.cpu().numpy(), ref).max() < 1e-2
+
+
+def test_nontrivial_batchnorm_stats(oracle):
+    """Trained-looking BN stats (not the identity init) fold correctly."""
+    torch.manual_seed(5)
+    ref = oracle_from_state(build_seeded_state(seed=2))
+    with torch.no_grad():
+        for mod in ref.modules():
+            if isinstance(mod, torch.nn.BatchNorm2d):
+                mod.running_mean.uniform_(0.0, 0.3)
+                mod.running_var.uniform_(0.5, 2.0)
+                mod.weight.uniform_(0.7, 1.3)
+                mod.bias.uniform_(-0.1, 0.1)
+    x = np.random.default_rng(9).random((2, 1, 40, 70)).astype(np.float32)
+    with torch.no_grad():
+        y = ref(torch.from_numpy(x)).numpy()
+    for prec in ("fast", "fp32"):
+        m = TVSpecNet(precision=prec).eval()
+        m.load_state_dict(ref.state_dict())
+        _check(m, x, y)
+
+
+def test_launch_accounting(model):
+    x = torch.rand(1, 1, 64, 64, device="cuda")
+    model(x)
+    assert model.last_launch_count() == model.depth  # conv0 + (depth-2) hidden + head
+
+
+def test_abi_errors_on_gpu(model):
+    plan = model._plan_for(torch.device("cuda", 0))
+    with pytest.raises(ValueError):
+        plan.forward(0, 0, 0, 1, 8, 8, 0, -1, 0)
+    x = torch.rand(1, 1, 8, 8, device="cuda")
+    y = torch.empty(1, 5, 8, 8, device="cuda")
+    with pytest.raises(ValueError):
+        plan.forward(x.data_ptr(), y.data_ptr(), 0, 1, 8, 8, 6, 5, 0)  # window past H
+    assert _native.load().tvs_abi_version() == 1

@@ -1,0 +1,89 @@
+"""API contract of the drop-in (no GPU needed): the reference's
+test_model.py structure/validation checks plus state_dict identity."""
+import pytest
+import torch
+
+from oracle.tvspecnet_oracle import TVSpecNetOracle, build_seeded_state
+from paper_2006_10004_b200 import ARCH_SPEC, TVSpecNet, receptive_field
+
+
+def test_arch_spec_unchanged():
+    assert ARCH_SPEC == {"depth": 17, "channels": 64, "kernel": 3, "out_bands": 5, "batch_norm": True,
+                         "receptive_field": 35}
+
+
+def test_layer_counts():  # test_model.py:16-23
+    model = TVSpecNet()
+    convs = [m for m in model.modules() if isinstance(m, torch.nn.Conv2d)]
+    bns = [m for m in model.modules() if isinstance(m, torch.nn.BatchNorm2d)]
+    assert len(convs) == ARCH_SPEC["depth"]
+    assert len(bns) == ARCH_SPEC["depth"] - 2
+    assert all(c.kernel_size == (3, 3) for c in convs)
+    assert convs[-1].out_channels == ARCH_SPEC["out_bands"]
+
+
+def test_receptive_field():  # test_model.py:26-28
+    assert receptive_field(17, 3) == 35
+
+
+def test_rejects_bad_input_shape():  # test_model.py:31-34 (raised before any device work)
+    model = TVSpecNet().eval()
+    with pytest.raises(ValueError):
+        model(torch.zeros(2, 3, 16, 16))
+    with pytest.raises(ValueError):
+        model(torch.zeros(16, 16))
+
+
+def test_rejects_shallow_depth():  # test_model.py:37-39
+    with pytest.raises(ValueError):
+        TVSpecNet(depth=2)
+
+
+@pytest.mark.parametrize("arch", [(17, 64, 5), (26, 128, 5), (3, 64, 2)])
+def test_state_dict_identical_to_reference_layout(arch):
+    ours = TVSpecNet(*arch).state_dict()
+    ref = TVSpecNetOracle(*arch).state_dict()
+    assert list(ours) == list(ref)
+    assert all(ours[k].shape == ref[k].shape and ours[k].dtype == ref[k].dtype for k in ref)
+
+
+def test_load_state_dict_strict_and_cache_key():
+    m = TVSpecNet().eval()
+    k0 = m._weight_key(torch.device("cuda", 0))
+    m.load_state_dict(build_seeded_state(), strict=True)
+    assert m._weight_key(torch.device("cuda", 0)) != k0  # load bumps tensor versions -> repack
+
+
+def test_layer_params_fold_matches_eval_bn():
+    torch.manual_seed(1)
+    m = TVSpecNet(depth=4).eval()
+    with torch.no_grad():
+        for mod in m.modules():
+            if isinstance(mod, torch.nn.BatchNorm2d):
+                mod.running_mean.uniform_(-0.5, 0.5)
+                mod.running_var.uniform_(0.5, 2.0)
+                mod.weight.uniform_(0.5, 1.5)
+                mod.bias.uniform_(-0.2, 0.2)
+    x = torch.randn(1, 64, 8, 8, dtype=torch.float64)
+    conv, bn = m.body[2].double(), m.body[3].double()
+    ref = bn(conv(x))
+    w, s, b = m.layer_params()[1]
+    y = torch.nn.functional.conv2d(x, w, padding=1) * s[None, :, None, None] + b[None, :, None, None]
+    torch.testing.assert_close(y, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_train_mode_and_dtype_rejected():
+    m = TVSpecNet()
+    with pytest.raises(RuntimeError):
+        m(torch.zeros(1, 1, 8, 8))  # train mode: no batch-statistics path
+    m.eval()
+    with pytest.raises(RuntimeError):
+        m(torch.zeros(1, 1, 8, 8, dtype=torch.float64))
+
+
+def test_precision_validation():
+    with pytest.raises(ValueError):
+        TVSpecNet(precision="bf16")
+    m = TVSpecNet()
+    m.precision = "fp32"
+    assert m.precision == "fp32"
