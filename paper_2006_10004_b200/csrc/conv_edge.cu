@@ -4,10 +4,10 @@
 //   K1 conv0_kernel : Conv2d(1,64,3,p=1,bias) + ReLU  (model.py:37-38)
 //       fp32 NCHW plane -> activation NHWC (fp16 or fp32).  K = 9, so it runs
 //       on CUDA cores (0.10% of the FLOPs).
-//   K3 head_kernel  : Conv2d(64,K,3,p=1,bias)          (model.py:44)
-//       + closure plane image - sum(bands)              (inference.py:34-42)
-//       activation NHWC -> bands fp32 NCHW, exact fp32 arithmetic in every
-//       mode; optional row window so row-band shards store only valid rows.
+//   head_kernel<float> : Conv2d(64,K,3,p=1,bias) (model.py:44) + closure
+//       plane (inference.py:34-42) for the fp32-accurate mode (fp32 NHWC
+//       activations, fp64 accumulation).  The fast mode's head runs on
+//       tcgen05 (conv_tc.cu).
 //   hidden_f32_kernel : Conv2d(64,64)+BN+ReLU on fp32 NHWC (fp32-accurate
 //       mode).  Products of fp32 operands are accumulated in fp64 (DFMA) and
 //       the BatchNorm scale/shift applied after the sum, so each layer's
@@ -250,18 +250,12 @@ cudaError_t launch_conv0(bool fp16_act, const float* x, void* act, const float* 
   return cudaGetLastError();
 }
 
-cudaError_t launch_head(bool fp16_act, const void* act, const float* x, const float* wh, const float* bh,
-                        float* bands, float* closure, int B, int H, int W, int K, int row0, int rows,
-                        cudaStream_t st) {
+cudaError_t launch_head_f32(const float* act, const float* x, const float* wh, const float* bh, float* bands,
+                            float* closure, int B, int H, int W, int K, int row0, int rows, cudaStream_t st) {
   const long long nout = (long long)B * rows * W;
   const unsigned grid = (unsigned)((nout + 127) / 128);
   const size_t smem = (size_t)9 * kC * K * sizeof(float);
-  if (fp16_act)
-    head_kernel<__half><<<grid, 128, smem, st>>>(static_cast<const __half*>(act), x, wh, bh, bands, closure, B, H, W,
-                                                 K, row0, rows);
-  else
-    head_kernel<float><<<grid, 128, smem, st>>>(static_cast<const float*>(act), x, wh, bh, bands, closure, B, H, W, K,
-                                                row0, rows);
+  head_kernel<float><<<grid, 128, smem, st>>>(act, x, wh, bh, bands, closure, B, H, W, K, row0, rows);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,434 @@
+// conv_tc.cu — tcgen05 implicit-GEMM 3x3 convolutions over fp16 NHWC
+// activations (sm_100a).  One kernel template, two epilogues:
+//
+//  K2 hidden layer  (Conv2d(64,64,3,p=1,no bias) -> BatchNorm2d(eval) -> ReLU,
+//     /root/reference/pkg/trainer/src/tvsurrogate/model.py:40-43)
+//     N block = 64 output channels, epilogue +shift, ReLU, fp16 -> TMA store.
+//  K3 head          (Conv2d(64,K,3,p=1,bias), model.py:44, + closure plane
+//     image - sum(bands), inference.py:34-42)
+//     N block = 32 = [16 cols W_hi | 16 cols W_lo] with W = W_hi + W_lo both
+//     fp16 (exact split of the fp32 weight to ~2^-22), so the head stays
+//     fp32-accurate on fp16 activations; epilogue sums hi+lo+bias and writes
+//     fp32 NCHW bands (+ closure) for a row window.
+//
+// GEMM mapping (persistent CTAs, each owning an equal contiguous range of
+// 128-px strip-rows, see SegIter):
+//   * M = 128 output pixels of one row (TMEM lanes);
+//   * the three dy taps are stacked along N: B = [W(dy=+1) | W(0) | W(-1)],
+//     so one input row r updates the accumulators of output rows r-1, r, r+1,
+//     which live in consecutive TMEM slots (slot = output-row sequence mod 8);
+//     N = 3*NB >= 96 keeps the MMA off the shared-memory operand limit
+//     (N=64 SS MMAs run at 2/3 rate on B200: tools/ubench_tcgen05.cu);
+//   * K = 64 input channels x 3 dx taps; a dx tap is a 128 B shift of the A
+//     descriptor start inside the SW128 input-row buffer (one 130-px halo
+//     row loaded by TMA; OOB zero fill = Conv2d zero padding).
+//   * The slot an input row touches for the first time is written with
+//     accumulate=0 in that row's first K step (split into its own MMA), so
+//     slots never need zeroing.
+//
+// Warp roles: w0 TMA producer, w1 TMEM alloc + single-thread MMA issuer,
+// w2..w9 epilogue in two groups (even / odd output rows); every epilogue warp
+// owns one TMEM lane quarter (32 pixels) and stores independently.
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace tvs {
+
+// Work partition: the output is a list of strip-rows ordered (image, strip,
+// row) with rows restricted to the window [row0, row0+rows).  CTA i owns the
+// contiguous range [i*T/G, (i+1)*T/G) of the T = B*strips*rows strip-rows, so
+// every CTA gets the same number of output rows (+-1).  A range is walked as
+// segments: maximal runs of consecutive rows inside one (image, strip) column.
+struct Segment {
+  int b, x0, ya, yb;
+};
+struct SegIter {
+  long long cur, end;
+  TVS_DEV SegIter(const ConvArgs& a) {
+    const long long T = (long long)a.B * a.strips * a.rows;
+    cur = T * blockIdx.x / gridDim.x;
+    end = T * (blockIdx.x + 1) / gridDim.x;
+  }
+  TVS_DEV bool next(const ConvArgs& a, Segment& g) {
+    if (cur >= end) return false;
+    const long long col = cur / a.rows;
+    const int y0 = (int)(cur - col * a.rows);
+    const int n = (int)min((long long)(a.rows - y0), end - cur);
+    g.b = (int)(col / a.strips);
+    g.x0 = (int)(col % a.strips) * kStripPx;
+    g.ya = a.row0 + y0;
+    g.yb = g.ya + n;
+    cur += n;
+    return true;
+  }
+};
+
+template <bool kHead>
+struct ConvCfg {
+  static constexpr int NB = kHead ? 32 : 64;          // TMEM columns per output row (slot)
+  static constexpr int kWdx = 3 * NB * 128;           // B bytes per dx (3 dy blocks x NB rows x 128 B)
+  static constexpr int kW = 3 * kWdx;
+  static constexpr int kTmemCols = kSlots * NB;       // 512 / 256
+  static constexpr int kStageOut = kHead ? 0 : 32 * 128;  // per-warp staging (hidden only)
+  static constexpr size_t kSmem = 1024 + kW + kStages * kInRowStride + 8 * kStageOut + 1024;
+};
+
+template <bool kHead>
+__global__ void __launch_bounds__(kConvThreads, 1)
+conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
+                  const ConvArgs a) {
+  using Cfg = ConvCfg<kHead>;
+  constexpr int NB = Cfg::NB;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ uint64_t full[kStages], empty[kStages], slot_full[kSlots], slot_empty[kSlots], wbar;
+  __shared__ uint32_t tmem_base_smem;
+  __shared__ float sShift[kC];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = smem;
+  uint8_t* sIn = sW + Cfg::kW;
+  uint8_t* sOut = sIn + kStages * kInRowStride;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < kSlots; ++i) { mbar_init(&slot_full[i], 1); mbar_init(&slot_empty[i], 4); }
+    mbar_init(&wbar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < kC) sShift[threadIdx.x] = (threadIdx.x < a.nshift) ? a.shift[threadIdx.x] : 0.0f;
+  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(&tmem_base_smem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_smem;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer ----
+    if (elect_one()) {
+      prefetch_tmap(&tm_in);
+      mbar_arrive_expect_tx(&wbar, Cfg::kW);
+      for (int i = 0; i < 3; ++i) bulk_load(sW + i * Cfg::kWdx, a.wpack + i * Cfg::kWdx, Cfg::kWdx, &wbar);
+      int stage = 0;
+      uint32_t phase = 0;
+      SegIter it(a);
+      Segment g;
+      while (it.next(a, g)) {
+        const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
+        for (int r = r0; r <= r1; ++r) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], kInRowBytes);
+          tma_load_4d(sIn + stage * kInRowStride, &tm_in, &full[stage], 0, g.x0 - 1, r, g.b);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer ----
+    // The whole warp walks the schedule (warp-uniform values stay in uniform
+    // registers); one elected lane issues.  Per input row the MMA budget is
+    // ~12 x 96 cycles, so the issue path is kept to a few instructions per MMA:
+    // descriptors are a per-row base plus compile-time offsets.
+    const uint32_t idesc1 = make_idesc(128, NB, kFmtF16, kFmtF16);
+    const uint32_t idesc2 = make_idesc(128, 2 * NB, kFmtF16, kFmtF16);
+    const uint32_t idesc3 = make_idesc(128, 3 * NB, kFmtF16, kFmtF16);
+    const uint64_t adesc0 = make_smem_desc(smem_u32(sIn), 0, 1024, kLayoutSW128);
+    const uint64_t bdesc0 = make_smem_desc(smem_u32(sW), 0, 1024, kLayoutSW128);
+    const bool leader = elect_one();
+    mbar_wait(&wbar, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t seq = 0;  // output-row sequence number: slot = seq & 7, use = seq >> 3
+    SegIter it(a);
+    Segment g;
+    while (it.next(a, g)) {
+      const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
+      for (int r = r0; r <= r1; ++r) {
+        const int q_lo = max(r - 1, g.ya), q_hi = min(r + 1, g.yb - 1);
+        // output rows whose first contributing input row is r: first(q) = max(q-1, 0)
+        const int q_new = (r == 0) ? q_lo : r + 1;
+        for (int q = max(q_new, q_lo); q <= q_hi; ++q) {
+          const uint32_t sq = seq + (uint32_t)(q - g.ya);
+          mbar_wait(&slot_empty[sq & 7], ((sq >> 3) & 1) ^ 1);
+        }
+        // Target rows [q_lo, q_hi] -> consecutive slots, split at the ring wrap
+        // (regular ops R0, R1); the first K step also splits off the
+        // newly-entered suffix [q_new, q_hi] with accumulate = 0 (ops F0..F2).
+        // An op = (TMEM column, B row offset in 16-byte units, idesc, acc).
+        const uint32_t s_lo = (seq + (uint32_t)(q_lo - g.ya)) & 7;
+        const int cnt = q_hi - q_lo + 1;
+        const int c0 = min(cnt, 8 - (int)s_lo), c1 = cnt - c0;
+        auto idesc_of = [&](int c) { return c == 3 ? idesc3 : (c == 2 ? idesc2 : idesc1); };
+        auto brow16 = [&](int q) { return (uint32_t)(q - (r - 1)) * (uint32_t)(NB * 128 / 16); };
+        const uint32_t R0t = tmem + s_lo * NB, R0b = brow16(q_lo), R0i = idesc_of(c0);
+        const uint32_t R1t = tmem, R1b = brow16(q_lo + c0), R1i = idesc_of(c1);
+        // first-K-step ops: old / new part of segment 0 and of segment 1
+        const int s0e = q_lo + c0 - 1, s1b = q_lo + c0;
+        const int A_e = min(s0e, q_new - 1), B_b = max(q_lo, q_new);
+        const int C_e = min(q_hi, q_new - 1), D_b = max(s1b, q_new);
+        const bool vA = q_lo <= A_e, vB = B_b <= s0e, vC = c1 > 0 && s1b <= C_e, vD = c1 > 0 && D_b <= q_hi;
+        const uint32_t At = R0t, Ab = R0b, Ai = idesc_of(A_e - q_lo + 1);
+        const uint32_t Bt = R0t + (uint32_t)(B_b - q_lo) * NB, Bb = brow16(B_b), Bi = idesc_of(s0e - B_b + 1);
+        const uint32_t Ct = R1t, Cb = R1b, Ci = idesc_of(C_e - s1b + 1);
+        const uint32_t Dt = R1t + (uint32_t)(D_b - s1b) * NB, Db = brow16(D_b), Di = idesc_of(q_hi - D_b + 1);
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (leader) {
+          const uint64_t ad_row = adesc0 + (uint64_t)((stage * kInRowStride) >> 4);
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
+              const uint64_t bd = bdesc0 + (uint64_t)((dx * Cfg::kWdx + k * 32) >> 4);
+              if (dx == 0 && k == 0) {
+                if (vA) mma_f16_ss(At, ad, bd + Ab, Ai, 1u);
+                if (vB) mma_f16_ss(Bt, ad, bd + Bb, Bi, 0u);
+                if (vC) mma_f16_ss(Ct, ad, bd + Cb, Ci, 1u);
+                if (vD) mma_f16_ss(Dt, ad, bd + Db, Di, 0u);
+              } else {
+                mma_f16_ss(R0t, ad, bd + R0b, R0i, 1u);
+                if (c1 > 0) mma_f16_ss(R1t, ad, bd + R1b, R1i, 1u);
+              }
+            }
+          }
+          mma_commit(&empty[stage]);
+          for (int q = q_lo; q <= q_hi; ++q)
+            if (min(q + 1, a.H - 1) == r) mma_commit(&slot_full[(seq + (uint32_t)(q - g.ya)) & 7]);
+        }
+        __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+      seq += (uint32_t)(g.yb - g.ya);
+    }
+  } else {
+    // ------------------------------------------------ epilogue (w2..w9) ----
+    const int ew = warp - 2;                  // 0..7
+    const uint32_t grp = (uint32_t)(ew >> 2); // row parity handled by this warp
+    const int quarter = warp & 3;             // TMEM lane quarter this warp may access
+    const int px = quarter * 32 + lane;       // pixel within the strip == TMEM lane
+    const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+    uint8_t* stage_out = sOut + ew * Cfg::kStageOut;
+    if (!kHead && lane == 0) prefetch_tmap(&tm_out);
+    uint32_t seq = 0;
+    SegIter it(a);
+    Segment g;
+    while (it.next(a, g)) {
+      for (int q = g.ya; q < g.yb; ++q, ++seq) {
+        if ((seq & 1) != grp) continue;
+        const uint32_t slot = seq & 7;
+        mbar_wait(&slot_full[slot], (seq >> 3) & 1);
+        tc_fence_after();
+        const int xg = g.x0 + px;
+        if constexpr (!kHead) {
+          uint32_t v[4][16];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tmem_ld16(tmem + lane_addr + slot * NB + j * 16, v[j]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 4; ++j) reg_fence16(v[j]);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&slot_empty[slot]);
+          // this warp's staging buffer: previous store (2 rows ago) must have read it
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+          uint8_t* rowp = stage_out + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              uint32_t packed[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int c = j * 16 + h * 8 + e * 2;
+                const float f0 = fmaxf(__uint_as_float(v[j][h * 8 + e * 2]) + sShift[c], 0.0f);
+                const float f1 = fmaxf(__uint_as_float(v[j][h * 8 + e * 2 + 1]) + sShift[c + 1], 0.0f);
+                __half2 hv = __floats2half2_rn(f0, f1);
+                packed[e] = *reinterpret_cast<uint32_t*>(&hv);
+              }
+              const int chunk = j * 2 + h;  // 16-byte chunk = 8 channels
+              *reinterpret_cast<uint4*>(rowp + ((chunk ^ (lane & 7)) << 4)) =
+                  make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            }
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(&tm_out, stage_out, 0, g.x0 + quarter * 32, q, g.b);
+            bulk_commit();
+          }
+        } else {
+          uint32_t v[2][16];
+          tmem_ld16(tmem + lane_addr + slot * NB, v[0]);
+          tmem_ld16(tmem + lane_addr + slot * NB + 16, v[1]);
+          tmem_ld_wait();
+          reg_fence16(v[0]);
+          reg_fence16(v[1]);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&slot_empty[slot]);
+          if (xg < a.W) {
+            const long long plane = (long long)a.rows * a.W;
+            const long long pix = (long long)(q - a.row0) * a.W + xg;
+            float* ob = a.bands + (long long)g.b * a.K * plane + pix;
+            float sum = 0.0f;
+#pragma unroll
+            for (int k = 0; k < kMaxBands; ++k) {
+              if (k < a.K) {
+                const float o = (__uint_as_float(v[0][k]) + __uint_as_float(v[1][k])) + sShift[k];
+                ob[k * plane] = o;
+                sum += o;
+              }
+            }
+            if (a.closure) a.closure[(long long)g.b * plane + pix] = a.x[((long long)g.b * a.H + q) * a.W + xg] - sum;
+          }
+        }
+      }
+    }
+    if (!kHead && lane == 0) bulk_wait<0>();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::kTmemCols>(tmem);
+  }
+}
+
+// --------------------------------------------------------------------------
+// Weight packs.
+//
+// Hidden: BN-folded W*s rounded to fp16 with tap-sum compensation: round to
+// nearest, then per (co, ci) flip the rounding direction of individual taps
+// (cheapest first) while that brings the sum of rounding residuals over the 9
+// taps closer to zero.  Each filter's response to locally-constant input (the
+// DC term that dominates with non-negative ReLU activations) is then exact to
+// fp32 precision; this halves the fp16 error of the 17-layer stack
+// (tools/emulate_precision.py: 1.04e-2 -> 6.1e-3 worst band on config 1).
+//
+// Head: W = W_hi + W_lo, both fp16 round-to-nearest (exact split to ~2^-22).
+// --------------------------------------------------------------------------
+__device__ __forceinline__ float half_other_side(float w, __half rn) {
+  const float r = __half2float(rn);
+  if (r == w) return r;
+  unsigned short bits = __half_as_ushort(rn);
+  const bool toward_up = (r < w);
+  const bool neg = (bits & 0x8000u) != 0;
+  if (r == 0.0f) {
+    bits = toward_up ? 0x0001u : 0x8001u;
+  } else {
+    const bool grow = (toward_up != neg);  // magnitude grows when moving away from zero
+    bits = grow ? (unsigned short)(bits + 1) : (unsigned short)(bits - 1);
+  }
+  return __half2float(__ushort_as_half(bits));
+}
+
+// B row n (0..3*NB) of dx block kx: 128 B = 64 ci fp16, SW128 chunk swizzle
+__device__ __forceinline__ void put_b(uint8_t* out, int wdx, int kx, int n, int ci, __half v) {
+  const uint32_t off = (uint32_t)kx * wdx + (uint32_t)n * 128u + (uint32_t)(((ci >> 3) ^ (n & 7)) << 4) +
+                       (uint32_t)((ci & 7) << 1);
+  *reinterpret_cast<__half*>(out + off) = v;
+}
+
+__global__ void pack_hidden_f16_kernel(const float* __restrict__ w, const float* __restrict__ scale,
+                                       uint8_t* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*64 + ci
+  if (idx >= kC * kC) return;
+  const int co = idx / kC, ci = idx % kC;
+  float wv[9], rn[9], alt[9], cost[9];
+  float s = 0.0f;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    wv[t] = w[idx * 9 + t] * scale[co];  // BatchNorm fold W' = W*s (fp32)
+    const __half h = __float2half_rn(wv[t]);
+    rn[t] = __half2float(h);
+    alt[t] = half_other_side(wv[t], h);
+    cost[t] = fabsf(alt[t] - wv[t]) - fabsf(rn[t] - wv[t]);
+    s += rn[t] - wv[t];
+  }
+  uint32_t used = 0;
+  for (int it = 0; it < 9; ++it) {
+    int best = 0;
+    float bc = 3.4e38f;
+#pragma unroll
+    for (int t = 0; t < 9; ++t)
+      if (!(used >> t & 1u) && cost[t] < bc) { bc = cost[t]; best = t; }
+    used |= 1u << best;
+    const float d = (alt[best] - wv[best]) - (rn[best] - wv[best]);
+    if (fabsf(s + d) < fabsf(s)) { s += d; rn[best] = alt[best]; }
+  }
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int ky = t / 3, kx = t % 3;
+    put_b(out, ConvCfg<false>::kWdx, kx, (2 - ky) * 64 + co, ci, __float2half_rn(rn[t]));
+  }
+}
+
+__global__ void pack_head_f16_kernel(const float* __restrict__ w, int K, uint8_t* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // k*64 + ci
+  if (idx >= K * kC) return;
+  const int k = idx / kC, ci = idx % kC;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int ky = t / 3, kx = t % 3;
+    const float wf = w[idx * 9 + t];
+    const __half hi = __float2half_rn(wf);
+    const __half lo = __float2half_rn(wf - __half2float(hi));
+    const int nb = (2 - ky) * 32;
+    put_b(out, ConvCfg<true>::kWdx, kx, nb + k, ci, hi);
+    put_b(out, ConvCfg<true>::kWdx, kx, nb + 16 + k, ci, lo);
+  }
+}
+
+__global__ void fill_kernel(float* dst, float v, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = v;
+}
+
+// ------------------------------------------------------------ launchers ----
+size_t conv_smem_bytes(bool head) { return head ? ConvCfg<true>::kSmem : ConvCfg<false>::kSmem; }
+size_t conv_wpack_bytes(bool head) { return head ? ConvCfg<true>::kW : ConvCfg<false>::kW; }
+
+cudaError_t launch_conv_tc(bool head, const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a,
+                           int grid, cudaStream_t st) {
+  if (head)
+    conv3x3_tc_kernel<true><<<grid, kConvThreads, ConvCfg<true>::kSmem, st>>>(tm_in, tm_out, a);
+  else
+    conv3x3_tc_kernel<false><<<grid, kConvThreads, ConvCfg<false>::kSmem, st>>>(tm_in, tm_out, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<false>::kW, st);
+  if (e != cudaSuccess) return e;
+  pack_hidden_f16_kernel<<<(kC * kC + 127) / 128, 128, 0, st>>>(w, scale, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_head_f16(const float* w, int K, uint8_t* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<true>::kW, st);
+  if (e != cudaSuccess) return e;
+  pack_head_f16_kernel<<<(K * kC + 127) / 128, 128, 0, st>>>(w, K, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(float* dst, float v, int n, cudaStream_t st) {
+  fill_kernel<<<(n + 255) / 256, 256, 0, st>>>(dst, v, n);
+  return cudaGetLastError();
+}
+
+cudaError_t configure_edge_kernels();
+cudaError_t configure_kernels() {
+  cudaError_t e = cudaFuncSetAttribute(conv3x3_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)ConvCfg<false>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<true>::kSmem);
+  if (e != cudaSuccess) return e;
+  return configure_edge_kernels();
+}
+
+}  // namespace tvs

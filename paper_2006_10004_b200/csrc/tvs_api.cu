@@ -71,8 +71,9 @@ struct tvs_plan {
   float* b0 = nullptr;
   float* wh = nullptr;
   float* bh = nullptr;
-  // hidden: fast -> packed fp16 (n_hidden * kWBytes) ; fp32 -> [co][ci][9] fp32
+  // hidden: fast -> packed fp16 (n_hidden * conv_wpack_bytes(false)) ; fp32 -> [co][ci][9] fp32
   uint8_t* wpack = nullptr;
+  uint8_t* hpack = nullptr;  // fast-mode head: fp16 hi/lo pack
   float* whid = nullptr;
   float* bhid = nullptr;  // per hidden layer: shift (beta - mu*s)
   float* shid = nullptr;  // per hidden layer: BatchNorm scale s (fp32 mode epilogue; folded in FAST)
@@ -91,7 +92,7 @@ struct tvs_plan {
   double prof_ms[3] = {0, 0, 0};
   long long prof_n[3] = {0, 0, 0};
   double prof_flops[3] = {0, 0, 0};
-  size_t chunk_budget = 48ull << 20;
+  size_t chunk_budget = 2048ull << 20;  // activation bytes per chunk (TVS_CHUNK_MB)
 
   int n_hidden() const { return depth - 2; }
   size_t act_px_bytes() const { return mode == TVS_MODE_FAST ? 128 : 256; }
@@ -106,7 +107,7 @@ void free_all(tvs_plan* p) {
   for (auto e : p->event_pool) cudaEventDestroy(e);
   p->recs.clear();
   p->event_pool.clear();
-  void* ptrs[] = {p->w0, p->b0, p->wh, p->bh, p->wpack, p->whid, p->bhid, p->shid, p->act[0], p->act[1], p->dx};
+  void* ptrs[] = {p->w0, p->b0, p->wh, p->bh, p->wpack, p->hpack, p->whid, p->bhid, p->shid, p->act[0], p->act[1], p->dx};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -122,11 +123,11 @@ void ensure_act(tvs_plan* p, size_t bytes) {
   p->act_bytes = bytes;
 }
 
-int pick_band_rows(long long strip_rows_total, int H, int num_sms) {
-  // aim for >= 4 work units per SM, bands between 4 and 64 rows
-  long long target = (strip_rows_total + 4LL * num_sms - 1) / (4LL * num_sms);
-  int hb = (int)std::max(4LL, std::min(64LL, target));
-  return std::min(hb, H);
+// one CTA per SM, but never fewer than ~3 output rows per CTA (short
+// segments pay two extra input rows each)
+int conv_grid(const tvs_plan* p, const tvs::ConvArgs& a) {
+  const long long total = (long long)a.B * a.strips * a.rows;
+  return (int)std::max(1LL, std::min<long long>(p->num_sms, (total + 2) / 3));
 }
 
 cudaEvent_t pool_event(tvs_plan* p) {
@@ -177,28 +178,39 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
   // K1
   timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * 64,
                [&] { return tvs::launch_conv0(fast, x, p->act[0], p->w0, p->b0, B, H, W, st); });
-  // K2 x (depth-2)
+  // K2 x (depth-2), K3
   int cur = 0;
   if (fast) {
-    tvs::HiddenArgs a;
-    a.B = B; a.H = H; a.W = W;
-    a.strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
-    a.band_rows = pick_band_rows((long long)B * a.strips * H, H, p->num_sms);
-    a.bands = (H + a.band_rows - 1) / a.band_rows;
-    a.units = B * a.bands * a.strips;
-    const unsigned grid = (unsigned)std::min(a.units, p->num_sms);
+    const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
     CUtensorMap in_map[2], out_map[2];
     for (int i = 0; i < 2; ++i) {
       in_map[i] = make_act_map(p->act[i], B, H, W, tvs::kHaloPx);
-      out_map[i] = make_act_map(p->act[i], B, H, W, tvs::kStripPx);
+      out_map[i] = make_act_map(p->act[i], B, H, W, 32);
     }
+    auto geom = [&](int r0, int nrows) {
+      tvs::ConvArgs a{};
+      a.B = B; a.H = H; a.W = W; a.strips = strips;
+      a.row0 = r0; a.rows = nrows;
+      return a;
+    };
     for (int l = 0; l < p->n_hidden(); ++l) {
-      a.wpack = p->wpack + (size_t)l * tvs::kWBytes;
-      a.bias = p->bhid + (size_t)l * tvs::kC;
+      tvs::ConvArgs a = geom(0, H);
+      a.wpack = p->wpack + (size_t)l * tvs::conv_wpack_bytes(false);
+      a.shift = p->bhid + (size_t)l * tvs::kC;
+      a.nshift = tvs::kC;
+      const int grid = conv_grid(p, a);
       timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64,
-                   [&] { return tvs::launch_hidden_f16(in_map[cur], out_map[cur ^ 1], a, (int)grid, st); });
+                   [&] { return tvs::launch_conv_tc(false, in_map[cur], out_map[cur ^ 1], a, grid, st); });
       cur ^= 1;
     }
+    tvs::ConvArgs a = geom(row0, rows);
+    a.wpack = p->hpack;
+    a.shift = p->bh;
+    a.nshift = p->out_bands;
+    a.x = x; a.bands = bands; a.closure = closure; a.K = p->out_bands;
+    const int grid = conv_grid(p, a);
+    timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands,
+                 [&] { return tvs::launch_conv_tc(true, in_map[cur], in_map[cur], a, grid, st); });
   } else {
     for (int l = 0; l < p->n_hidden(); ++l) {
       timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64, [&] {
@@ -208,12 +220,11 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       });
       cur ^= 1;
     }
+    timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands, [&] {
+      return tvs::launch_head_f32((const float*)p->act[cur], x, p->wh, p->bh, bands, closure, B, H, W, p->out_bands,
+                                  row0, rows, st);
+    });
   }
-  // K3
-  timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands, [&] {
-    return tvs::launch_head(fast, p->act[cur], x, p->wh, p->bh, bands, closure, B, H, W, p->out_bands, row0, rows,
-                            st);
-  });
 }
 
 void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int B, int H, int W, int row0, int rows,
@@ -292,9 +303,10 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
       TVS_CUDA(cudaMalloc(&p->bh, (size_t)out_bands * 4));
       TVS_CUDA(cudaMalloc(&p->bhid, (size_t)nh * 64 * 4));
       TVS_CUDA(cudaMalloc(&p->shid, (size_t)nh * 64 * 4));
-      if (mode == TVS_MODE_FAST)
-        TVS_CUDA(cudaMalloc(&p->wpack, (size_t)nh * tvs::kWBytes));
-      else
+      if (mode == TVS_MODE_FAST) {
+        TVS_CUDA(cudaMalloc(&p->wpack, (size_t)nh * tvs::conv_wpack_bytes(false)));
+        TVS_CUDA(cudaMalloc(&p->hpack, tvs::conv_wpack_bytes(true)));
+      } else
         TVS_CUDA(cudaMalloc(&p->whid, (size_t)nh * 64 * 64 * 9 * 4));
     } catch (...) {
       free_all(p);
@@ -333,13 +345,14 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
         TVS_CUDA(tvs::launch_fill(dst_scale, 1.0f, 64, st));
       TVS_CUDA(cudaMemcpyAsync(p->bhid + l * 64, shift_dev[l + 1], 64 * 4, cudaMemcpyDeviceToDevice, st));
       if (p->mode == TVS_MODE_FAST) {
-        TVS_CUDA(cudaMemsetAsync(p->wpack + (size_t)l * tvs::kWBytes, 0, tvs::kWBytes, st));
-        TVS_CUDA(tvs::launch_pack_hidden_f16(w_dev[l + 1], dst_scale, p->wpack + (size_t)l * tvs::kWBytes, st));
+        TVS_CUDA(tvs::launch_pack_hidden_f16(w_dev[l + 1], dst_scale,
+                                             p->wpack + (size_t)l * tvs::conv_wpack_bytes(false), st));
       } else {
         TVS_CUDA(cudaMemcpyAsync(p->whid + (size_t)l * 64 * 64 * 9, w_dev[l + 1], 64 * 64 * 9 * 4,
                                  cudaMemcpyDeviceToDevice, st));
       }
     }
+    if (p->mode == TVS_MODE_FAST) TVS_CUDA(tvs::launch_pack_head_f16(w_dev[p->depth - 1], p->out_bands, p->hpack, st));
     p->weights_ready = true;
   });
 }
