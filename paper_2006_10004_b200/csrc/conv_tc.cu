@@ -145,6 +145,65 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     while (it.next(a, g)) {
       const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
       for (int r = r0; r <= r1; ++r) {
+        // ---- fast path: interior input row (targets r-1, r, r+1 all inside the
+        // segment; r+1 is the only new slot; r-1 completes after this row)
+        if (r >= 1 && r - 1 >= g.ya && r + 1 <= g.yb - 1) {
+          const uint32_t sq = seq + (uint32_t)(r - 1 - g.ya);  // sequence of output row r-1
+          const uint32_t s = sq & 7, sn = (sq + 2) & 7;
+          mbar_wait2(&slot_empty[sn], (((sq + 2) >> 3) & 1) ^ 1, &full[stage], phase);
+          tc_fence_after();
+          if (leader) {
+            const uint64_t ad_row = adesc0 + (uint64_t)((stage * kInRowStride) >> 4);
+            const uint32_t t0 = tmem + s * NB;
+            constexpr uint32_t b1 = NB * 128 / 16, b2 = 2 * NB * 128 / 16;  // W(dy=0), W(dy=-1) blocks
+            if (s <= 5) {
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
+                  const uint64_t bd = bdesc0 + (uint64_t)((dx * Cfg::kWdx + k * 32) >> 4);
+                  if (dx == 0 && k == 0) {
+                    mma_f16_ss(t0, ad, bd, idesc2, 1u);
+                    mma_f16_ss(t0 + 2 * NB, ad, bd + b2, idesc1, 0u);
+                  } else {
+                    mma_f16_ss(t0, ad, bd, idesc3, 1u);
+                  }
+                }
+            } else if (s == 6) {
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
+                  const uint64_t bd = bdesc0 + (uint64_t)((dx * Cfg::kWdx + k * 32) >> 4);
+                  mma_f16_ss(t0, ad, bd, idesc2, 1u);
+                  mma_f16_ss(tmem, ad, bd + b2, idesc1, (dx == 0 && k == 0) ? 0u : 1u);
+                }
+            } else {
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
+                  const uint64_t bd = bdesc0 + (uint64_t)((dx * Cfg::kWdx + k * 32) >> 4);
+                  mma_f16_ss(t0, ad, bd, idesc1, 1u);
+                  if (dx == 0 && k == 0) {
+                    mma_f16_ss(tmem, ad, bd + b1, idesc1, 1u);
+                    mma_f16_ss(tmem + NB, ad, bd + b2, idesc1, 0u);
+                  } else {
+                    mma_f16_ss(tmem, ad, bd + b1, idesc2, 1u);
+                  }
+                }
+            }
+            mma_commit(&empty[stage]);
+            mma_commit(&slot_full[s]);
+          }
+          __syncwarp();
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          continue;
+        }
+        // ---- general path (segment edges, image top/bottom)
         const int q_lo = max(r - 1, g.ya), q_hi = min(r + 1, g.yb - 1);
         // output rows whose first contributing input row is r: first(q) = max(q-1, 0)
         const int q_new = (r == 0) ? q_lo : r + 1;

@@ -61,6 +61,20 @@ TVS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(a, parity)) {
   }
 }
+// Wait on two barriers at once (both try_waits in flight together).
+TVS_DEV void mbar_wait2(uint64_t* b0, uint32_t p0, uint64_t* b1, uint32_t p1) {
+  const uint32_t a0 = smem_u32(b0), a1 = smem_u32(b1);
+  uint32_t ok0, ok1;
+  asm volatile(
+      "{\n\t.reg .pred P0, P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P0, [%2], %3;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%4], %5;\n\t"
+      "selp.b32 %0, 1, 0, P0;\n\t"
+      "selp.b32 %1, 1, 0, P1;\n\t}"
+      : "=r"(ok0), "=r"(ok1) : "r"(a0), "r"(p0), "r"(a1), "r"(p1) : "memory");
+  if (!ok0) while (!mbar_try_wait(a0, p0)) {}
+  if (!ok1) while (!mbar_try_wait(a1, p1)) {}
+}
 // Bounded variant for bring-up/microbenchmarks: gives up after `limit`
 // polls and returns false instead of hanging the GPU.
 TVS_DEV bool mbar_wait_bounded(uint64_t* bar, uint32_t parity, uint64_t limit) {

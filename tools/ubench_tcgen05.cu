@@ -102,7 +102,7 @@ k_rate(int iters, long long* cycles, int* err) {
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid / 32;
-  for (int i = tid; i < (96 * 1024) / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < (112 * 1024) / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
   fence_async_smem();
   if (warp == 0) tmem_alloc<256>(&tbase);
   if (tid == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
@@ -136,6 +136,18 @@ k_rate(int iters, long long* cycles, int* err) {
                        ::"r"(tmem + 64), "l"(ad), "l"(bd1), "r"(idesc) : "memory");
           asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::lastuse [%0], %1, %2, %3, 1;"
                        ::"r"(tmem + 128), "l"(ad), "l"(bd2), "r"(idesc) : "memory");
+        } else if constexpr (V == 8 || V == 9 || V == 11 || V == 12) {
+          // conv row pattern: A shifted by dx*128 B (V=8) or aligned (V=9), B = N192 block of dx
+          const int dx = it % 3;
+          const uint32_t ash = (V == 9) ? 0u : (uint32_t)dx * 128u;
+          uint64_t ad8 = make_smem_desc(a0 + ash + k * 32, 0, 1024, kLayoutSW128);
+          uint64_t bd8 = make_smem_desc(b0 + dx * 24576 + k * 32, 0, 1024, kLayoutSW128);
+          mma_f16_ss(tmem, ad8, bd8, make_idesc(128, 192, kFmtF16, kFmtF16), 1);
+        } else if constexpr (V == 10) {
+          // split step: N128 + N64 into different columns
+          uint64_t bd1 = make_smem_desc(b0 + 16384 + k * 32, 0, 1024, kLayoutSW128);
+          mma_f16_ss(tmem, ad, bd, make_idesc(128, 128, kFmtF16, kFmtF16), 1);
+          mma_f16_ss(tmem + 128, ad, bd1, make_idesc(128, 64, kFmtF16, kFmtF16), 1);
         } else if constexpr (V == 7) {
           uint64_t adn = make_smem_desc(a0 + (it & 15) * 16 + k * 2 * 2304, 2304, 128, kLayoutNone);
           uint64_t bdn = make_smem_desc(b0 + k * 2 * 1024, 1024, 128, kLayoutNone);
@@ -148,6 +160,19 @@ k_rate(int iters, long long* cycles, int* err) {
     long long t1 = clock64();
     if (!ok) atomicAdd(err, 1);
     cycles[blockIdx.x] = t1 - t0;
+    if constexpr (V == 11 || V == 12) *reinterpret_cast<volatile uint32_t*>(smem + 110 * 1024) = 1;
+  }
+  if constexpr (V == 11 || V == 12) {
+    if (warp != 0) {
+      volatile uint32_t* flag = reinterpret_cast<volatile uint32_t*>(smem + 110 * 1024);
+      uint4* region = reinterpret_cast<uint4*>(smem + 104 * 1024) + (warp - 1) * 32 * 4;
+      const uint4 v = make_uint4(tid, 1, 2, 3);
+      while (*flag == 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) region[j * 32 + (tid & 31)] = v;
+        if constexpr (V == 12) __nanosleep(200);
+      }
+    }
   }
   __syncwarp();
   if (warp != 0) mbar_wait_bounded(&bar, 0, 1ull << 26);
@@ -197,7 +222,7 @@ template <int V>
 static void run_rate(const char* name, int ctas, double macs_per_iter) {
   long long* dC; int* dErr;
   CK(cudaMalloc(&dC, ctas * sizeof(long long))); CK(cudaMalloc(&dErr, 4)); CK(cudaMemset(dErr, 0, 4));
-  const int smem = 96 * 1024 + 1024;
+  const int smem = 112 * 1024 + 1024;
   CK(cudaFuncSetAttribute(k_rate<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int iters = 4096;
   k_rate<V><<<ctas, 128, smem>>>(64, dC, dErr);  // warm
@@ -219,11 +244,11 @@ static void run_rate(const char* name, int ctas, double macs_per_iter) {
   cudaFree(dC); cudaFree(dErr);
 }
 
-int main() {
+int main(int argc, char** argv) {
   int dev = 0; cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, dev));
   printf("device %s sm_%d%d SMs=%d smemOptin=%zu\n", p.name, p.major, p.minor, p.multiProcessorCount,
          p.sharedMemPerBlockOptin);
-  run_layout_tests();
+  if (argc < 2) run_layout_tests();
   const int sms = p.multiProcessorCount;
   for (int ctas : {1, sms}) {
     run_rate<0>("f16 M128 N64 K64", ctas, 128.0 * 64 * 64);
@@ -234,6 +259,11 @@ int main() {
     run_rate<5>("e4m3 M128 N64 K128", ctas, 128.0 * 64 * 128);
     run_rate<6>("f16 N64 x3 collector::a", ctas, 3 * 128.0 * 64 * 64);
     run_rate<7>("f16 N64 noswz shifted A", ctas, 128.0 * 64 * 64);
+    run_rate<8>("f16 N192 conv dx-shifted A", ctas, 128.0 * 192 * 64);
+    run_rate<9>("f16 N192 conv aligned A", ctas, 128.0 * 192 * 64);
+    run_rate<10>("f16 N128+N64 split", ctas, 128.0 * 192 * 64);
+    run_rate<11>("N192 conv + STS flood", ctas, 128.0 * 192 * 64);
+    run_rate<12>("N192 conv + STS throttled", ctas, 128.0 * 192 * 64);
   }
   printf("DONE\n");
   return 0;
