@@ -19,7 +19,8 @@ constexpr int kSlots = 8;                              // TMEM accumulator slots
 
 // tcgen05 conv kernels (conv_tc.cu)
 constexpr int kStages = 6;             // input-row ring depth
-constexpr int kConvThreads = 320;      // w0 TMA, w1 MMA, w2..w9 epilogue (2 row-parity groups)
+constexpr int kEpiGroups = 3;          // epilogue row groups (output row seq % 3)
+constexpr int kConvThreads = 64 + kEpiGroups * 128;  // w0 TMA, w1 MMA, 4 epilogue warps per group
 
 struct ConvArgs {
   int B, H, W;

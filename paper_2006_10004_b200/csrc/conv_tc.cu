@@ -27,8 +27,9 @@
 //     slots never need zeroing.
 //
 // Warp roles: w0 TMA producer, w1 TMEM alloc + single-thread MMA issuer,
-// w2..w9 epilogue in two groups (even / odd output rows); every epilogue warp
-// owns one TMEM lane quarter (32 pixels) and stores independently.
+// then kEpiGroups groups of 4 epilogue warps (output rows round-robin over the
+// groups); every epilogue warp owns one TMEM lane quarter (32 pixels) and
+// stores independently.
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -70,7 +71,7 @@ struct ConvCfg {
   static constexpr int kW = 3 * kWdx;
   static constexpr int kTmemCols = kSlots * NB;       // 512 / 256
   static constexpr int kStageOut = kHead ? 0 : 32 * 128;  // per-warp staging (hidden only)
-  static constexpr size_t kSmem = 1024 + kW + kStages * kInRowStride + 8 * kStageOut + 1024;
+  static constexpr size_t kSmem = 1024 + kW + kStages * kInRowStride + 4 * kEpiGroups * kStageOut + 1024;
 };
 
 template <bool kHead>
@@ -82,7 +83,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t full[kStages], empty[kStages], slot_full[kSlots], slot_empty[kSlots], wbar;
   __shared__ uint32_t tmem_base_smem;
-  __shared__ float sShift[kC];
+  __shared__ __align__(16) float sShift[kC];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
   uint8_t* sIn = sW + Cfg::kW;
@@ -262,20 +263,21 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
       seq += (uint32_t)(g.yb - g.ya);
     }
   } else {
-    // ------------------------------------------------ epilogue (w2..w9) ----
-    const int ew = warp - 2;                  // 0..7
-    const uint32_t grp = (uint32_t)(ew >> 2); // row parity handled by this warp
+    // ------------------------------------------------ epilogue ----
+    const int ew = warp - 2;                  // 0 .. 4*kEpiGroups-1
+    const uint32_t grp = (uint32_t)(ew >> 2); // output rows with seq % kEpiGroups == grp
     const int quarter = warp & 3;             // TMEM lane quarter this warp may access
     const int px = quarter * 32 + lane;       // pixel within the strip == TMEM lane
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-    uint8_t* stage_out = sOut + ew * Cfg::kStageOut;
+    const uint32_t stage_out = smem_u32(sOut + ew * Cfg::kStageOut);
+    const uint32_t shift_u = smem_u32(sShift);
     if (!kHead && lane == 0) prefetch_tmap(&tm_out);
-    uint32_t seq = 0;
+    uint32_t seq = 0, gsel = 0;  // gsel = seq % kEpiGroups
     SegIter it(a);
     Segment g;
     while (it.next(a, g)) {
-      for (int q = g.ya; q < g.yb; ++q, ++seq) {
-        if ((seq & 1) != grp) continue;
+      for (int q = g.ya; q < g.yb; ++q, ++seq, gsel = (gsel + 1 == kEpiGroups) ? 0 : gsel + 1) {
+        if (gsel != grp) continue;
         const uint32_t slot = seq & 7;
         mbar_wait(&slot_full[slot], (seq >> 3) & 1);
         tc_fence_after();
@@ -290,32 +292,30 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
-          // this warp's staging buffer: previous store (2 rows ago) must have read it
+          // this warp's staging buffer: its previous TMA store must have read it
           if (lane == 0) bulk_wait_read<0>();
           __syncwarp();
-          uint8_t* rowp = stage_out + lane * 128;
+          const uint32_t rowp = stage_out + lane * 128;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int chunk = 0; chunk < 8; ++chunk) {  // 16-byte chunk = 8 channels
+            const float4 s0 = ld_shared_f4(shift_u + chunk * 32);
+            const float4 s1 = ld_shared_f4(shift_u + chunk * 32 + 16);
+            const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            uint32_t packed[4];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              uint32_t packed[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int c = j * 16 + h * 8 + e * 2;
-                const float f0 = fmaxf(__uint_as_float(v[j][h * 8 + e * 2]) + sShift[c], 0.0f);
-                const float f1 = fmaxf(__uint_as_float(v[j][h * 8 + e * 2 + 1]) + sShift[c + 1], 0.0f);
-                __half2 hv = __floats2half2_rn(f0, f1);
-                packed[e] = *reinterpret_cast<uint32_t*>(&hv);
-              }
-              const int chunk = j * 2 + h;  // 16-byte chunk = 8 channels
-              *reinterpret_cast<uint4*>(rowp + ((chunk ^ (lane & 7)) << 4)) =
-                  make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            for (int e = 0; e < 4; ++e) {
+              const int c = chunk * 8 + e * 2;
+              const float f0 = fmaxf(__uint_as_float(v[c >> 4][c & 15]) + sh[2 * e], 0.0f);
+              const float f1 = fmaxf(__uint_as_float(v[c >> 4][(c & 15) + 1]) + sh[2 * e + 1], 0.0f);
+              __half2 hv = __floats2half2_rn(f0, f1);
+              packed[e] = *reinterpret_cast<uint32_t*>(&hv);
             }
+            st_shared_v4(rowp + ((chunk ^ (lane & 7)) << 4), packed[0], packed[1], packed[2], packed[3]);
           }
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_4d(&tm_out, stage_out, 0, g.x0 + quarter * 32, q, g.b);
+            tma_store_4d(&tm_out, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b);
             bulk_commit();
           }
         } else {
