@@ -99,6 +99,18 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def _traffic(spec):
+    """dram read+write bytes per launch of the hidden conv from the committed
+    ncu capture (profiles/traffic.json), when it was taken on this workload."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text()).get("conv3x3_tc_kernel<0>", {})
+    if d.get("config") != spec.name:
+        return None
+    return d["dram_bytes_read"] + d["dram_bytes_write"]
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -284,7 +296,8 @@ def run_ours(args, spec):
                      "avg_launch_ms": round(hid_avg_ms, 5), "launches_timed": f["hid_n"],
                      "flop_per_launch": f["hid_flops"] / max(1, f["hid_n"]),
                      "share_of_step": round(f["hid_ms"] / max(1e-9, f["hid_ms"] + f["c0_ms"] + f["hd_ms"]), 4),
-                     "traffic": None},
+                     "traffic": _traffic(spec), "traffic_unit": "bytes per launch (ncu dram read+write)",
+                     "algorithmic_bytes_per_launch": 2 * B * H * W * 128},
         "gpu_launches": f["launches"] * f["steps"],
         "e2e": {"value": round(f["e2e"], 3), "unit": UNIT, "h2d_bytes_per_step": f["e2e_bytes"][0],
                 "d2h_bytes_per_step": f["e2e_bytes"][1]},

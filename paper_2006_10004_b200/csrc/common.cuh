@@ -50,8 +50,12 @@ cudaError_t launch_conv_tc(bool head, const CUtensorMap& tm_in, const CUtensorMa
 cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
 cudaError_t launch_pack_head_f16(const float* w, int K, uint8_t* out, cudaStream_t st);
 cudaError_t launch_fill(float* dst, float v, int n, cudaStream_t st);
-cudaError_t launch_conv0(bool fp16_act, const float* x, void* act, const float* w0, const float* b0, int B, int H,
-                         int W, cudaStream_t st);
+struct Conv0Params {  // passed by value: lives in the kernel's constant bank
+  float w[kC * 9];     // [co][ky*3+kx]
+  float b[kC];
+};
+cudaError_t launch_conv0(bool fp16_act, const float* x, void* act, const Conv0Params& p, int B, int H, int W,
+                         cudaStream_t st);
 cudaError_t launch_head_f32(const float* act, const float* x, const float* wh, const float* bh, float* bands,
                             float* closure, int B, int H, int W, int K, int row0, int rows, cudaStream_t st);
 cudaError_t launch_hidden_f32(const float* in, float* out, const float* w, const float* scale, const float* shift,

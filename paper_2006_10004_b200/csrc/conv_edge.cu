@@ -39,24 +39,21 @@ __device__ __forceinline__ void store_act8<float>(float* dst, const float* v) {
   reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
 }
 
-// one thread per pixel; 128 pixels per block are contiguous in NHWC, so the
-// block's output is staged through shared memory and written coalesced.
+// One thread per pixel; the conv0 weights/bias arrive BY VALUE in the kernel
+// parameter block (constant bank), so every FFMA takes its weight operand
+// straight from the constant cache (no shared-memory loads).  128 pixels per
+// block are contiguous in NHWC, so the block's output is staged through shared
+// memory and written coalesced.
 template <typename T>
 __global__ void __launch_bounds__(128)
-conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const float* __restrict__ w0,
-             const float* __restrict__ b0, int B, int H, int W) {
-  __shared__ float sw[kC * 9];
-  __shared__ float sb[kC];
+conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params p, int B, int H, int W) {
   __shared__ __align__(16) T stage[128 * kC];
-  for (int i = threadIdx.x; i < kC * 9; i += blockDim.x) sw[i] = w0[i];
-  if (threadIdx.x < kC) sb[threadIdx.x] = b0[threadIdx.x];
-  __syncthreads();
   const long long npx = (long long)B * H * W;
   const long long p0 = (long long)blockIdx.x * 128;
-  const long long p = p0 + threadIdx.x;
-  if (p < npx) {
-    const int xw = (int)(p % W);
-    const long long t = p / W;
+  const long long pix = p0 + threadIdx.x;
+  if (pix < npx) {
+    const int xw = (int)(pix % W);
+    const long long t = pix / W;
     const int y = (int)(t % H);
     const long long b = t / H;
     const float* img = x + b * (long long)H * W;
@@ -78,8 +75,8 @@ conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const float* __re
         using Acc = std::conditional_t<std::is_same_v<T, float>, double, float>;  // fp64 in fp32 mode
         Acc acc = 0;
 #pragma unroll
-        for (int t9 = 0; t9 < 9; ++t9) acc = fma((Acc)sw[co * 9 + t9], (Acc)in[t9], acc);
-        v[e] = fmaxf((float)(acc + (Acc)sb[co]), 0.0f);
+        for (int t9 = 0; t9 < 9; ++t9) acc = fma((Acc)p.w[co * 9 + t9], (Acc)in[t9], acc);
+        v[e] = fmaxf((float)(acc + (Acc)p.b[co]), 0.0f);
       }
       store_act8<T>(dst + c8 * 8, v);
     }
@@ -239,14 +236,14 @@ hidden_f32_kernel(const float* __restrict__ in, float* __restrict__ out, const f
   }
 }
 
-cudaError_t launch_conv0(bool fp16_act, const float* x, void* act, const float* w0, const float* b0, int B, int H,
-                         int W, cudaStream_t st) {
+cudaError_t launch_conv0(bool fp16_act, const float* x, void* act, const Conv0Params& p, int B, int H, int W,
+                         cudaStream_t st) {
   const long long npx = (long long)B * H * W;
   const unsigned grid = (unsigned)((npx + 127) / 128);
   if (fp16_act)
-    conv0_kernel<__half><<<grid, 128, 0, st>>>(x, static_cast<__half*>(act), w0, b0, B, H, W);
+    conv0_kernel<__half><<<grid, 128, 0, st>>>(x, static_cast<__half*>(act), p, B, H, W);
   else
-    conv0_kernel<float><<<grid, 128, 0, st>>>(x, static_cast<float*>(act), w0, b0, B, H, W);
+    conv0_kernel<float><<<grid, 128, 0, st>>>(x, static_cast<float*>(act), p, B, H, W);
   return cudaGetLastError();
 }
 

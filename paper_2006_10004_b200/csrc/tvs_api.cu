@@ -67,8 +67,7 @@ struct tvs_plan {
   int num_sms = 148;
   bool weights_ready = false;
   // conv0 [64][1][3][3] + bias, head [K][64][3][3] + bias (fp32, folded)
-  float* w0 = nullptr;
-  float* b0 = nullptr;
+  tvs::Conv0Params conv0{};  // host copy, passed by value to K1
   float* wh = nullptr;
   float* bh = nullptr;
   // hidden: fast -> packed fp16 (n_hidden * conv_wpack_bytes(false)) ; fp32 -> [co][ci][9] fp32
@@ -107,7 +106,7 @@ void free_all(tvs_plan* p) {
   for (auto e : p->event_pool) cudaEventDestroy(e);
   p->recs.clear();
   p->event_pool.clear();
-  void* ptrs[] = {p->w0, p->b0, p->wh, p->bh, p->wpack, p->hpack, p->whid, p->bhid, p->shid, p->act[0], p->act[1], p->dx};
+  void* ptrs[] = {p->wh, p->bh, p->wpack, p->hpack, p->whid, p->bhid, p->shid, p->act[0], p->act[1], p->dx};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -177,7 +176,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
   const double px = (double)B * H * W;
   // K1
   timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * 64,
-               [&] { return tvs::launch_conv0(fast, x, p->act[0], p->w0, p->b0, B, H, W, st); });
+               [&] { return tvs::launch_conv0(fast, x, p->act[0], p->conv0, B, H, W, st); });
   // K2 x (depth-2), K3
   int cur = 0;
   if (fast) {
@@ -297,8 +296,6 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
     try {
       TVS_CUDA(tvs::configure_kernels());
       const int nh = depth - 2;
-      TVS_CUDA(cudaMalloc(&p->w0, 64 * 9 * 4));
-      TVS_CUDA(cudaMalloc(&p->b0, 64 * 4));
       TVS_CUDA(cudaMalloc(&p->wh, (size_t)out_bands * 64 * 9 * 4));
       TVS_CUDA(cudaMalloc(&p->bh, (size_t)out_bands * 4));
       TVS_CUDA(cudaMalloc(&p->bhid, (size_t)nh * 64 * 4));
@@ -330,8 +327,9 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
     auto scale_of = [&](int i) -> const float* { return scale_dev ? scale_dev[i] : nullptr; };
     if (scale_of(0) || scale_of(p->depth - 1))
       throw TvsError(TVS_E_UNSUPPORTED, "conv0/head take no BatchNorm scale (model.py:37,44)");
-    TVS_CUDA(cudaMemcpyAsync(p->w0, w_dev[0], 64 * 9 * 4, cudaMemcpyDeviceToDevice, st));
-    TVS_CUDA(cudaMemcpyAsync(p->b0, shift_dev[0], 64 * 4, cudaMemcpyDeviceToDevice, st));
+    TVS_CUDA(cudaMemcpyAsync(p->conv0.w, w_dev[0], sizeof(p->conv0.w), cudaMemcpyDeviceToHost, st));
+    TVS_CUDA(cudaMemcpyAsync(p->conv0.b, shift_dev[0], sizeof(p->conv0.b), cudaMemcpyDeviceToHost, st));
+    TVS_CUDA(cudaStreamSynchronize(st));  // conv0 weights are kernel parameters (host side)
     TVS_CUDA(cudaMemcpyAsync(p->wh, w_dev[p->depth - 1], (size_t)p->out_bands * 64 * 9 * 4,
                              cudaMemcpyDeviceToDevice, st));
     TVS_CUDA(cudaMemcpyAsync(p->bh, shift_dev[p->depth - 1], (size_t)p->out_bands * 4, cudaMemcpyDeviceToDevice,
