@@ -157,6 +157,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             const uint64_t ad_row = adesc0 + (uint64_t)((stage * kInRowStride) >> 4);
             const uint32_t t0 = tmem + s * NB;
             constexpr uint32_t b1 = NB * 128 / 16, b2 = 2 * NB * 128 / 16;  // W(dy=0), W(dy=-1) blocks
+            // Split pieces share A through the collector: the N=NB piece is
+            // issued first (fill), the N=2NB piece second (lastuse) -> full rate.
             if (s <= 5) {
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx)
@@ -164,36 +166,36 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                 for (int k = 0; k < 4; ++k) {
                   const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
                   const uint64_t bd = bdesc0 + (uint64_t)((dx * Cfg::kWdx + k * 32) >> 4);
-                  if (dx == 0 && k == 0) {
-                    mma_f16_ss(t0, ad, bd, idesc2, 1u);
-                    mma_f16_ss(t0 + 2 * NB, ad, bd + b2, idesc1, 0u);
+                  if (dx == 0 && k == 0) {  // enter row r+1 (acc=0), keep r-1, r
+                    mma_f16_ss_fill(t0 + 2 * NB, ad, bd + b2, idesc1, 0u);
+                    mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
                   } else {
                     mma_f16_ss(t0, ad, bd, idesc3, 1u);
                   }
                 }
-            } else if (s == 6) {
+            } else if (s == 6) {  // slots 6,7 | wrap | 0
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                   const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
                   const uint64_t bd = bdesc0 + (uint64_t)((dx * Cfg::kWdx + k * 32) >> 4);
-                  mma_f16_ss(t0, ad, bd, idesc2, 1u);
-                  mma_f16_ss(tmem, ad, bd + b2, idesc1, (dx == 0 && k == 0) ? 0u : 1u);
+                  mma_f16_ss_fill(tmem, ad, bd + b2, idesc1, (dx == 0 && k == 0) ? 0u : 1u);
+                  mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
                 }
-            } else {
+            } else {  // s == 7: slot 7 | wrap | 0,1
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                   const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
                   const uint64_t bd = bdesc0 + (uint64_t)((dx * Cfg::kWdx + k * 32) >> 4);
-                  mma_f16_ss(t0, ad, bd, idesc1, 1u);
+                  mma_f16_ss_fill(t0, ad, bd, idesc1, 1u);
                   if (dx == 0 && k == 0) {
-                    mma_f16_ss(tmem, ad, bd + b1, idesc1, 1u);
-                    mma_f16_ss(tmem + NB, ad, bd + b2, idesc1, 0u);
+                    mma_f16_ss_use(tmem, ad, bd + b1, idesc1, 1u);
+                    mma_f16_ss_lastuse(tmem + NB, ad, bd + b2, idesc1, 0u);
                   } else {
-                    mma_f16_ss(tmem, ad, bd + b1, idesc2, 1u);
+                    mma_f16_ss_lastuse(tmem, ad, bd + b1, idesc2, 1u);
                   }
                 }
             }

@@ -148,6 +148,32 @@ k_rate(int iters, long long* cycles, int* err) {
           uint64_t bd1 = make_smem_desc(b0 + 16384 + k * 32, 0, 1024, kLayoutSW128);
           mma_f16_ss(tmem, ad, bd, make_idesc(128, 128, kFmtF16, kFmtF16), 1);
           mma_f16_ss(tmem + 128, ad, bd1, make_idesc(128, 64, kFmtF16, kFmtF16), 1);
+        } else if constexpr (V == 13 || V == 14) {
+          // split step with A reuse: N128 (collector::a::fill) + N64 (collector::a::lastuse)
+          uint64_t bd1 = make_smem_desc(b0 + 16384 + k * 32, 0, 1024, kLayoutSW128);
+          const uint32_t i128 = make_idesc(128, 128, kFmtF16, kFmtF16), i64 = make_idesc(128, 64, kFmtF16, kFmtF16);
+          if constexpr (V == 13) {
+            asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::fill [%0], %1, %2, %3, 1;"
+                         ::"r"(tmem), "l"(ad), "l"(bd), "r"(i128) : "memory");
+            asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::lastuse [%0], %1, %2, %3, 1;"
+                         ::"r"(tmem + 128), "l"(ad), "l"(bd1), "r"(i64) : "memory");
+          } else {  // N64 first then N128
+            asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::fill [%0], %1, %2, %3, 1;"
+                         ::"r"(tmem + 128), "l"(ad), "l"(bd1), "r"(i64) : "memory");
+            asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::lastuse [%0], %1, %2, %3, 1;"
+                         ::"r"(tmem), "l"(ad), "l"(bd), "r"(i128) : "memory");
+          }
+        } else if constexpr (V == 15) {
+          // three N64 pieces sharing A (s=7 first step pattern)
+          uint64_t bd1 = make_smem_desc(b0 + 8192 + k * 32, 0, 1024, kLayoutSW128);
+          uint64_t bd2 = make_smem_desc(b0 + 16384 + k * 32, 0, 1024, kLayoutSW128);
+          const uint32_t i64 = make_idesc(128, 64, kFmtF16, kFmtF16);
+          asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::fill [%0], %1, %2, %3, 1;"
+                       ::"r"(tmem), "l"(ad), "l"(bd), "r"(i64) : "memory");
+          asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::use [%0], %1, %2, %3, 1;"
+                       ::"r"(tmem + 64), "l"(ad), "l"(bd1), "r"(i64) : "memory");
+          asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::lastuse [%0], %1, %2, %3, 1;"
+                       ::"r"(tmem + 128), "l"(ad), "l"(bd2), "r"(i64) : "memory");
         } else if constexpr (V == 7) {
           uint64_t adn = make_smem_desc(a0 + (it & 15) * 16 + k * 2 * 2304, 2304, 128, kLayoutNone);
           uint64_t bdn = make_smem_desc(b0 + k * 2 * 1024, 1024, 128, kLayoutNone);
@@ -237,7 +263,7 @@ static void run_rate(const char* name, int ctas, double macs_per_iter) {
   CK(cudaMemcpy(c.data(), dC, ctas * sizeof(long long), cudaMemcpyDeviceToHost));
   int herr; CK(cudaMemcpy(&herr, dErr, 4, cudaMemcpyDeviceToHost));
   double avg = 0; for (auto v : c) avg += v; avg /= ctas;
-  double n_mma = (double)iters * (V == 6 ? 12 : 4);
+  double n_mma = (double)iters * (V == 6 || V == 15 ? 12 : (V == 10 || V == 13 || V == 14 ? 8 : 4));
   double tflops = 2.0 * macs_per_iter * iters * ctas / (ms * 1e-3) / 1e12;
   printf("RATE %-26s ctas=%3d cyc/mma=%7.2f  cyc/iter=%8.2f  MAC/clk/SM=%7.1f  %.1f TFLOP/s  timeout=%d\n",
          name, ctas, avg / n_mma, avg / iters, macs_per_iter * iters / avg, tflops, herr);
@@ -262,6 +288,9 @@ int main(int argc, char** argv) {
     run_rate<8>("f16 N192 conv dx-shifted A", ctas, 128.0 * 192 * 64);
     run_rate<9>("f16 N192 conv aligned A", ctas, 128.0 * 192 * 64);
     run_rate<10>("f16 N128+N64 split", ctas, 128.0 * 192 * 64);
+    run_rate<13>("N128 fill + N64 lastuse", ctas, 128.0 * 192 * 64);
+    run_rate<14>("N64 fill + N128 lastuse", ctas, 128.0 * 192 * 64);
+    run_rate<15>("3x N64 fill/use/lastuse", ctas, 128.0 * 192 * 64);
     run_rate<11>("N192 conv + STS flood", ctas, 128.0 * 192 * 64);
     run_rate<12>("N192 conv + STS throttled", ctas, 128.0 * 192 * 64);
   }
