@@ -141,22 +141,34 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     int stage = 0;
     uint32_t phase = 0;
     uint32_t seq = 0;  // output-row sequence number: slot = seq & 7, use = seq >> 3
+    bool prewaited = false;  // this row's barriers were already awaited by the previous row
     SegIter it(a);
     Segment g;
     while (it.next(a, g)) {
       const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
       for (int r = r0; r <= r1; ++r) {
-        // ---- fast path: interior input row (targets r-1, r, r+1 all inside the
-        // segment; r+1 is the only new slot; r-1 completes after this row)
+        // ---- fast path: interior input row (targets r-1, r, r+1 inside the
+        // segment; r+1 is the only new slot; r-1 completes after this row).
+        // The barriers of the NEXT row are awaited (by the issuing lane) in
+        // the middle of this row's MMA stream, while the tensor-core queue
+        // (~5 MMAs deep) still holds work, so row transitions do not drain it.
         if (r >= 1 && r - 1 >= g.ya && r + 1 <= g.yb - 1) {
           const uint32_t sq = seq + (uint32_t)(r - 1 - g.ya);  // sequence of output row r-1
-          const uint32_t s = sq & 7, sn = (sq + 2) & 7;
-          mbar_wait2(&slot_empty[sn], (((sq + 2) >> 3) & 1) ^ 1, &full[stage], phase);
-          tc_fence_after();
+          const uint32_t s = sq & 7;
+          const bool next_fast = (r + 2 <= g.yb - 1);  // row r+1 is interior too
+          const int nstage = (stage + 1 == kStages) ? 0 : stage + 1;
+          const uint32_t nphase = (stage + 1 == kStages) ? (phase ^ 1) : phase;
+          const uint32_t sq2 = sq + 3;  // output row r+2, entered by input row r+1
           if (leader) {
+            if (!prewaited) mbar_wait2(&slot_empty[(sq + 2) & 7], (((sq + 2) >> 3) & 1) ^ 1, &full[stage], phase);
+            tc_fence_after();
             const uint64_t ad_row = adesc0 + (uint64_t)((stage * kInRowStride) >> 4);
             const uint32_t t0 = tmem + s * NB;
             constexpr uint32_t b1 = NB * 128 / 16, b2 = 2 * NB * 128 / 16;  // W(dy=0), W(dy=-1) blocks
+            auto prewait = [&](int dx, int k) {
+              if (dx == 1 && k == 1 && next_fast)
+                mbar_wait2(&slot_empty[sq2 & 7], ((sq2 >> 3) & 1) ^ 1, &full[nstage], nphase);
+            };
             // Split pieces share A through the collector: the N=NB piece is
             // issued first (fill), the N=2NB piece second (lastuse) -> full rate.
             if (s <= 5) {
@@ -172,6 +184,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                   } else {
                     mma_f16_ss(t0, ad, bd, idesc3, 1u);
                   }
+                  prewait(dx, k);
                 }
             } else if (s == 6) {  // slots 6,7 | wrap | 0
 #pragma unroll
@@ -182,6 +195,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                   const uint64_t bd = bdesc0 + (uint64_t)((dx * Cfg::kWdx + k * 32) >> 4);
                   mma_f16_ss_fill(tmem, ad, bd + b2, idesc1, (dx == 0 && k == 0) ? 0u : 1u);
                   mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
+                  prewait(dx, k);
                 }
             } else {  // s == 7: slot 7 | wrap | 0,1
 #pragma unroll
@@ -197,15 +211,19 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                   } else {
                     mma_f16_ss_lastuse(tmem, ad, bd + b1, idesc2, 1u);
                   }
+                  prewait(dx, k);
                 }
             }
             mma_commit(&empty[stage]);
             mma_commit(&slot_full[s]);
           }
           __syncwarp();
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          prewaited = next_fast;
+          stage = nstage;
+          phase = nphase;
           continue;
         }
+        prewaited = false;
         // ---- general path (segment edges, image top/bottom)
         const int q_lo = max(r - 1, g.ya), q_hi = min(r + 1, g.yb - 1);
         // output rows whose first contributing input row is r: first(q) = max(q-1, 0)

@@ -220,6 +220,34 @@ TVS_DEV void mma_f8_ss(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t
       "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
       ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
 }
+// Warp-converged issue: every lane executes these, elect.sync picks the one
+// lane that issues (no divergent branch around the MMA sequence).
+#define TVS_MMA_ELECT(QUAL)                                                                              \
+  asm volatile(                                                                                          \
+      "{\n\t.reg .pred p, e;\n\t"                                                                     \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                                 \
+      "setp.ne.b32 p, %4, 0;\n\t"                                                                       \
+      "@e tcgen05.mma.cta_group::1.kind::f16" QUAL " [%0], %1, %2, %3, p;\n\t}"                         \
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory")
+TVS_DEV void wmma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  TVS_MMA_ELECT("");
+}
+TVS_DEV void wmma_f16_fill(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  TVS_MMA_ELECT(".collector::a::fill");
+}
+TVS_DEV void wmma_f16_use(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  TVS_MMA_ELECT(".collector::a::use");
+}
+TVS_DEV void wmma_f16_lastuse(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  TVS_MMA_ELECT(".collector::a::lastuse");
+}
+TVS_DEV void wmma_commit(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+      ::"r"(smem_u32(bar)) : "memory");
+}
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread
 // complete (implies tcgen05.fence::before_thread_sync).
 TVS_DEV void mma_commit(uint64_t* bar) {

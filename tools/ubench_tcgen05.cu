@@ -207,6 +207,60 @@ k_rate(int iters, long long* cycles, int* err) {
   if (warp == 0) tmem_dealloc<256>(tmem);
 }
 
+// issue-queue probe: clock after each of 24 back-to-back N=192 MMAs (96 cyc each)
+__global__ void __launch_bounds__(128, 1) k_queue(long long* out, int gap) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int i = tid; i < (64 * 1024) / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  fence_async_smem();
+  if (warp == 0) tmem_alloc<256>(&tbase);
+  if (tid == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 32768);
+    const uint32_t idesc = make_idesc(128, 192, kFmtF16, kFmtF16);
+    long long t[25];
+    t[0] = clock64();
+    for (int i = 0; i < 24; ++i) {
+      uint64_t ad = make_smem_desc(a0 + (i & 3) * 32, 0, 1024, kLayoutSW128);
+      uint64_t bd = make_smem_desc(b0 + (i & 3) * 32, 0, 1024, kLayoutSW128);
+      mma_f16_ss(tmem, ad, bd, idesc, 1);
+      t[i + 1] = clock64();
+      if (gap) { long long w = clock64(); while (clock64() - w < gap) {} }
+    }
+    mma_commit(&bar);
+    mbar_wait_bounded(&bar, 0, 1ull << 26);
+    long long tend = clock64();
+    for (int i = 0; i <= 24; ++i) out[i] = t[i] - t[0];
+    out[25] = tend - t[0];
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<256>(tmem);
+}
+
+static void run_queue_probe() {
+  long long* d; CK(cudaMalloc(&d, 26 * 8));
+  const int smem = 64 * 1024 + 1024;
+  CK(cudaFuncSetAttribute(k_queue, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  for (int gap : {0, 0, 200}) {
+    k_queue<<<1, 128, smem>>>(d, gap);
+    CK(cudaDeviceSynchronize());
+    long long h[26]; CK(cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost));
+    printf("QUEUE gap=%d issue-clock after MMA i:", gap);
+    for (int i = 1; i <= 24; ++i) printf(" %lld", h[i]);
+    printf(" | all done %lld\n", h[25]);
+  }
+  cudaFree(d);
+}
+
 static void run_layout_tests() {
   std::vector<__half> A(kRowsA * 64), B(64 * 64);
   std::vector<float> Af(kRowsA * 64), Bf(64 * 64);
@@ -275,6 +329,8 @@ int main(int argc, char** argv) {
   printf("device %s sm_%d%d SMs=%d smemOptin=%zu\n", p.name, p.major, p.minor, p.multiProcessorCount,
          p.sharedMemPerBlockOptin);
   if (argc < 2) run_layout_tests();
+  run_queue_probe();
+  if (argc > 1 && argv[1][0] == 'q') return 0;
   const int sms = p.multiProcessorCount;
   for (int ctas : {1, sms}) {
     run_rate<0>("f16 M128 N64 K64", ctas, 128.0 * 64 * 64);
