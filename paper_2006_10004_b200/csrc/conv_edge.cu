@@ -48,6 +48,8 @@ template <typename T>
 __global__ void __launch_bounds__(128)
 conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params p, int B, int H, int W) {
   __shared__ __align__(16) T stage[128 * kC];
+  // PDL: the first hidden layer may start its prologue (it waits for this grid's completion)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long npx = (long long)B * H * W;
   const long long p0 = (long long)blockIdx.x * 128;
   const long long pix = p0 + threadIdx.x;

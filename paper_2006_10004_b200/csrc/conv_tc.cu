@@ -100,17 +100,23 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   }
   if (threadIdx.x < kC) sShift[threadIdx.x] = (threadIdx.x < a.nshift) ? a.shift[threadIdx.x] : 0.0f;
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(&tmem_base_smem);
+  // weights do not depend on the previous layer: start their load before the
+  // PDL wait so it overlaps the previous kernel's tail
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&wbar, Cfg::kW);
+    for (int i = 0; i < 3; ++i) bulk_load(sW + i * Cfg::kWdx, a.wpack + i * Cfg::kWdx, Cfg::kWdx, &wbar);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_smem;
+  pdl_launch_dependents();  // the next layer may start its prologue on free SMs
+  pdl_wait();               // previous layer's activations are complete and visible
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer ----
     if (elect_one()) {
       prefetch_tmap(&tm_in);
-      mbar_arrive_expect_tx(&wbar, Cfg::kW);
-      for (int i = 0; i < 3; ++i) bulk_load(sW + i * Cfg::kWdx, a.wpack + i * Cfg::kWdx, Cfg::kWdx, &wbar);
       int stage = 0;
       uint32_t phase = 0;
       SegIter it(a);
@@ -471,13 +477,23 @@ __global__ void fill_kernel(float* dst, float v, int n) {
 size_t conv_smem_bytes(bool head) { return head ? ConvCfg<true>::kSmem : ConvCfg<false>::kSmem; }
 size_t conv_wpack_bytes(bool head) { return head ? ConvCfg<true>::kW : ConvCfg<false>::kW; }
 
+// Launched with programmatic stream serialization (PDL): the kernel's
+// prologue overlaps the previous kernel; griddepcontrol.wait guards all
+// activation reads and writes.
 cudaError_t launch_conv_tc(bool head, const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a,
                            int grid, cudaStream_t st) {
-  if (head)
-    conv3x3_tc_kernel<true><<<grid, kConvThreads, ConvCfg<true>::kSmem, st>>>(tm_in, tm_out, a);
-  else
-    conv3x3_tc_kernel<false><<<grid, kConvThreads, ConvCfg<false>::kSmem, st>>>(tm_in, tm_out, a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kConvThreads);
+  cfg.dynamicSmemBytes = head ? ConvCfg<true>::kSmem : ConvCfg<false>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (head) return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<true>, tm_in, tm_out, a);
+  return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<false>, tm_in, tm_out, a);
 }
 
 cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* out, cudaStream_t st) {

@@ -298,6 +298,10 @@ TVS_DEV float4 ld_shared_f4(uint32_t addr) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
+// Programmatic dependent launch: let the next grid in the stream start its
+// prologue now / wait until the previous grid's memory is visible.
+TVS_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+TVS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // Named barrier over a subset of warps (id 1..15; id 0 is __syncthreads).
 TVS_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
