@@ -248,8 +248,9 @@ def run_ours(args, spec):
 
         # end to end through the public API with host buffers (H2D + D2H inside)
         e2e_steps = max(1, min(steps, args.e2e_steps))
-        for _ in range(2):
-            model(x_host)
+        out_host = None
+        for _ in range(3):  # same pattern as timed: keeps two pinned result blocks cached
+            out_host = model(x_host)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):

@@ -178,17 +178,68 @@ class TVSpecNet(nn.Module):
         row0, nrows = (0, H) if rows is None else rows
         if not (0 <= row0 and nrows >= 1 and row0 + nrows <= H):
             raise ValueError(f"bad row window {rows} for height {H}")
+        if not x.is_cuda:
+            return self._forward_host(plan, x, dev, closure, row0, nrows)
         with torch.cuda.device(dev):
             stream = torch.cuda.current_stream(dev)
-            xd = x.to(dev, non_blocking=True).contiguous()
+            xd = x.contiguous()
             bands = torch.empty((B, self.out_bands, nrows, W), device=dev, dtype=torch.float32)
             clos = torch.empty((B, 1, nrows, W), device=dev, dtype=torch.float32) if closure else None
             plan.forward(xd.data_ptr(), bands.data_ptr(), clos.data_ptr() if closure else 0, B, H, W, row0, nrows,
                          stream.cuda_stream)
-        if not x.is_cuda:
-            bands = bands.cpu()
-            clos = clos.cpu() if clos is not None else None
         return bands, clos
+
+    # host tensors: pipelined H2D -> forward -> D2H over sub-batches
+    host_chunks = 4
+
+    def _forward_host(self, plan, x: torch.Tensor, dev: torch.device, closure: bool, row0: int, nrows: int):
+        """CPU in / CPU out (the reference calling convention, inference.py:25-32).
+        Sub-batches flow through three streams so the PCIe copies of one
+        sub-batch overlap the forward of another; results land in pinned
+        host memory."""
+        B, _, H, W = x.shape
+        K = self.out_bands
+        x_pin = x.contiguous()
+        if not x_pin.is_pinned():
+            x_pin = x_pin.pin_memory()
+        out = torch.empty((B, K, nrows, W), dtype=torch.float32, pin_memory=True)
+        cout = torch.empty((B, 1, nrows, W), dtype=torch.float32, pin_memory=True) if closure else None
+        n = max(1, min(self.host_chunks, B))
+        bounds = [(B * i // n, B * (i + 1) // n) for i in range(n)]
+        per = max(e - s for s, e in bounds)
+        with torch.cuda.device(dev):
+            comp = torch.cuda.current_stream(dev)
+            h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+            xbuf = [torch.empty((per, 1, H, W), device=dev) for _ in range(2)]
+            bbuf = [torch.empty((per, K, nrows, W), device=dev) for _ in range(2)]
+            cbuf = [torch.empty((per, 1, nrows, W), device=dev) if closure else None for _ in range(2)]
+            x_free = [torch.cuda.Event() for _ in range(2)]
+            b_free = [torch.cuda.Event() for _ in range(2)]
+            for ev in x_free + b_free:
+                ev.record(comp)
+            for i, (s, e) in enumerate(bounds):
+                j, nb = i % 2, e - s
+                h2d.wait_event(x_free[j])
+                with torch.cuda.stream(h2d):
+                    xbuf[j][:nb].copy_(x_pin[s:e], non_blocking=True)
+                landed = torch.cuda.Event()
+                landed.record(h2d)
+                comp.wait_event(landed)
+                comp.wait_event(b_free[j])
+                plan.forward(xbuf[j].data_ptr(), bbuf[j].data_ptr(), cbuf[j].data_ptr() if closure else 0,
+                             nb, H, W, row0, nrows, comp.cuda_stream)
+                done = torch.cuda.Event()
+                done.record(comp)
+                x_free[j].record(comp)
+                d2h.wait_event(done)
+                with torch.cuda.stream(d2h):
+                    out[s:e].copy_(bbuf[j][:nb], non_blocking=True)
+                    if closure:
+                        cout[s:e].copy_(cbuf[j][:nb], non_blocking=True)
+                b_free[j].record(d2h)
+            d2h.synchronize()
+            comp.synchronize()
+        return out, cout
 
     def last_launch_count(self, device: int | None = None) -> int:
         idx = torch.cuda.current_device() if device is None else device
