@@ -45,7 +45,8 @@ typedef struct tvs_plan tvs_plan;
 int tvs_abi_version(void);
 const char* tvs_last_error(void);
 
-/* depth >= 3 (model.py:34-35), channels == 64 in this build, 1 <= out_bands <= 8 */
+/* depth >= 3 (model.py:34-35); channels 64 (FAST: tcgen05) or 128 (both modes run the fp32
+ * CUDA-core path in this build); 1 <= out_bands <= 8 */
 int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode, tvs_plan** out_plan);
 
 /* n_layers == depth.  Layer i computes  y[co] = scale[co] * conv(W_i, a)[co] + shift[co]

@@ -39,7 +39,8 @@ struct ConvArgs {
 // fp32 hidden layer (conv_edge.cu)
 constexpr int kF32TileRows = 4, kF32TilePx = 32, kF32CiChunk = 16;
 constexpr int kF32InRows = kF32TileRows + 2, kF32InPx = kF32TilePx + 2;
-constexpr size_t kF32Smem = (size_t)(kF32InRows * kF32InPx * kF32CiChunk + kF32CiChunk * 9 * kC) * 4;
+constexpr size_t f32_smem(int C) { return (size_t)(kF32InRows * kF32InPx * kF32CiChunk + kF32CiChunk * 9 * C) * 4; }
+constexpr int kMaxC = 128;  // channels supported by the CUDA-core (fp32) path
 constexpr int kMaxBands = 8;
 
 // host-side launchers (defined next to their kernels)
@@ -51,15 +52,15 @@ cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* 
 cudaError_t launch_pack_head_f16(const float* w, int K, uint8_t* out, cudaStream_t st);
 cudaError_t launch_fill(float* dst, float v, int n, cudaStream_t st);
 struct Conv0Params {  // passed by value: lives in the kernel's constant bank
-  float w[kC * 9];     // [co][ky*3+kx]
-  float b[kC];
+  float w[kMaxC * 9];  // [co][ky*3+kx]
+  float b[kMaxC];
 };
-cudaError_t launch_conv0(bool fp16_act, const float* x, void* act, const Conv0Params& p, int B, int H, int W,
-                         cudaStream_t st);
-cudaError_t launch_head_f32(const float* act, const float* x, const float* wh, const float* bh, float* bands,
+cudaError_t launch_conv0(bool fp16_act, int C, const float* x, void* act, const Conv0Params& p, int B, int H,
+                         int W, cudaStream_t st);
+cudaError_t launch_head_f32(int C, const float* act, const float* x, const float* wh, const float* bh, float* bands,
                             float* closure, int B, int H, int W, int K, int row0, int rows, cudaStream_t st);
-cudaError_t launch_hidden_f32(const float* in, float* out, const float* w, const float* scale, const float* shift,
-                              int B, int H, int W, cudaStream_t st);
+cudaError_t launch_hidden_f32(int C, const float* in, float* out, const float* w, const float* scale,
+                              const float* shift, int B, int H, int W, cudaStream_t st);
 cudaError_t configure_kernels();  // one-time smem opt-ins
 
 }  // namespace tvs

@@ -44,14 +44,15 @@ __device__ __forceinline__ void store_act8<float>(float* dst, const float* v) {
 // straight from the constant cache (no shared-memory loads).  128 pixels per
 // block are contiguous in NHWC, so the block's output is staged through shared
 // memory and written coalesced.
-template <typename T>
+template <typename T, int C>
 __global__ void __launch_bounds__(128)
 conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params p, int B, int H, int W) {
-  __shared__ __align__(16) T stage[128 * kC];
+  constexpr int P = (C == 64) ? 128 : 64;  // pixels per block (static smem <= 32 KB)
+  __shared__ __align__(16) T stage[P * C];
   // PDL: the first hidden layer may start its prologue (it waits for this grid's completion)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long npx = (long long)B * H * W;
-  const long long p0 = (long long)blockIdx.x * 128;
+  const long long p0 = (long long)blockIdx.x * P;
   const long long pix = p0 + threadIdx.x;
   if (pix < npx) {
     const int xw = (int)(pix % W);
@@ -67,9 +68,9 @@ conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params
         const int yy = y + ky - 1, xx = xw + kx - 1;
         in[ky * 3 + kx] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(img + (long long)yy * W + xx) : 0.0f;
       }
-    T* dst = stage + threadIdx.x * kC;
+    T* dst = stage + threadIdx.x * C;
 #pragma unroll
-    for (int c8 = 0; c8 < kC / 8; ++c8) {
+    for (int c8 = 0; c8 < C / 8; ++c8) {
       float v[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -85,10 +86,10 @@ conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params
   }
   __syncthreads();
   // coalesced copy of the staged block (valid pixels only)
-  const long long nvalid = min((long long)128, npx - p0);
-  const int n16 = (int)(nvalid * kC * sizeof(T) / 16);
+  const long long nvalid = min((long long)P, npx - p0);
+  const int n16 = (int)(nvalid * C * sizeof(T) / 16);
   const uint4* src = reinterpret_cast<const uint4*>(stage);
-  uint4* out = reinterpret_cast<uint4*>(act + p0 * kC);
+  uint4* out = reinterpret_cast<uint4*>(act + p0 * C);
   for (int i = threadIdx.x; i < n16; i += blockDim.x) out[i] = src[i];
 }
 
@@ -111,15 +112,15 @@ __device__ __forceinline__ void load_act8<float>(const float* src, float* v) {
 
 // wh: [K][64][3][3] fp32 ; output rows [row0, row0+rows) of each image go to
 // bands[b][k][r-row0][x] and closure[b][0][r-row0][x].
-template <typename T>
+template <typename T, int C>
 __global__ void __launch_bounds__(128)
 head_kernel(const T* __restrict__ act, const float* __restrict__ x, const float* __restrict__ wh,
             const float* __restrict__ bh, float* __restrict__ bands, float* __restrict__ closure, int B,
             int H, int W, int K, int row0, int rows) {
   extern __shared__ float swh[];  // [9][64][K]
-  for (int i = threadIdx.x; i < 9 * kC * K; i += blockDim.x) {
-    const int k = i % K, ci = (i / K) % kC, t = i / (K * kC);
-    swh[i] = wh[(k * kC + ci) * 9 + t];
+  for (int i = threadIdx.x; i < 9 * C * K; i += blockDim.x) {
+    const int k = i % K, ci = (i / K) % C, t = i / (K * C);
+    swh[i] = wh[(k * C + ci) * 9 + t];
   }
   __syncthreads();
   const long long nout = (long long)B * rows * W;
@@ -134,17 +135,17 @@ head_kernel(const T* __restrict__ act, const float* __restrict__ x, const float*
   Acc acc[kMaxBands];
 #pragma unroll
   for (int k = 0; k < kMaxBands; ++k) acc[k] = 0;
-  const T* base = act + b * (long long)H * W * kC;
+  const T* base = act + b * (long long)H * W * C;
   for (int ky = 0; ky < 3; ++ky) {
     const int yy = y + ky - 1;
     if (yy < 0 || yy >= H) continue;
     for (int kx = 0; kx < 3; ++kx) {
       const int xx = xw + kx - 1;
       if (xx < 0 || xx >= W) continue;
-      const T* src = base + ((long long)yy * W + xx) * kC;
-      const float* wt = swh + (ky * 3 + kx) * kC * K;
+      const T* src = base + ((long long)yy * W + xx) * C;
+      const float* wt = swh + (ky * 3 + kx) * C * K;
 #pragma unroll 2
-      for (int c8 = 0; c8 < kC / 8; ++c8) {
+      for (int c8 = 0; c8 < C / 8; ++c8) {
         float v[8];
         load_act8<T>(src + c8 * 8, v);
 #pragma unroll
@@ -173,7 +174,8 @@ head_kernel(const T* __restrict__ act, const float* __restrict__ x, const float*
 // --------------------------------------------------- fp32 hidden layer ----
 // Output tile 4 rows x 32 px x 64 co per 256-thread block; thread = (co
 // group of 8, px column); input channels streamed in chunks of 16.
-__global__ void __launch_bounds__(256)
+template <int C>
+__global__ void __launch_bounds__(32 * (C / 8))
 hidden_f32_kernel(const float* __restrict__ in, float* __restrict__ out, const float* __restrict__ w /*[co][ci][9]*/,
                   const float* __restrict__ scale, const float* __restrict__ shift, int B, int H, int W) {
   extern __shared__ float sm[];
@@ -192,17 +194,17 @@ hidden_f32_kernel(const float* __restrict__ in, float* __restrict__ out, const f
   for (int r = 0; r < kF32TileRows; ++r)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[r][e] = 0.0;
-  const float* ib = in + (long long)b * H * W * kC;
-  for (int c0 = 0; c0 < kC; c0 += kF32CiChunk) {
+  const float* ib = in + (long long)b * H * W * C;
+  for (int c0 = 0; c0 < C; c0 += kF32CiChunk) {
     __syncthreads();
     for (int i = threadIdx.x; i < kF32InRows * kF32InPx * kF32CiChunk; i += blockDim.x) {
       const int ci = i % kF32CiChunk, px = (i / kF32CiChunk) % kF32InPx, r = i / (kF32CiChunk * kF32InPx);
       const int yy = ty0 + r - 1, xx = tx0 + px - 1;
-      sIn[i] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? ib[((long long)yy * W + xx) * kC + c0 + ci] : 0.0f;
+      sIn[i] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? ib[((long long)yy * W + xx) * C + c0 + ci] : 0.0f;
     }
-    for (int i = threadIdx.x; i < kF32CiChunk * 9 * kC; i += blockDim.x) {
-      const int co = i % kC, t = (i / kC) % 9, ci = i / (kC * 9);
-      sWt[i] = w[((long long)co * kC + c0 + ci) * 9 + t];
+    for (int i = threadIdx.x; i < kF32CiChunk * 9 * C; i += blockDim.x) {
+      const int co = i % C, t = (i / C) % 9, ci = i / (C * 9);
+      sWt[i] = w[((long long)co * C + c0 + ci) * 9 + t];
     }
     __syncthreads();
     for (int ci = 0; ci < kF32CiChunk; ++ci) {
@@ -210,8 +212,8 @@ hidden_f32_kernel(const float* __restrict__ in, float* __restrict__ out, const f
       for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
         for (int kx = 0; kx < 3; ++kx) {
-          const float4 w0 = *reinterpret_cast<const float4*>(sWt + (ci * 9 + ky * 3 + kx) * kC + g * 8);
-          const float4 w1 = *reinterpret_cast<const float4*>(sWt + (ci * 9 + ky * 3 + kx) * kC + g * 8 + 4);
+          const float4 w0 = *reinterpret_cast<const float4*>(sWt + (ci * 9 + ky * 3 + kx) * C + g * 8);
+          const float4 w1 = *reinterpret_cast<const float4*>(sWt + (ci * 9 + ky * 3 + kx) * C + g * 8 + 4);
           const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
           for (int r = 0; r < kF32TileRows; ++r) {
@@ -232,41 +234,64 @@ hidden_f32_kernel(const float* __restrict__ in, float* __restrict__ out, const f
 #pragma unroll
     for (int e = 0; e < 8; ++e)
       v[e] = fmaxf((float)fma(acc[r][e], (double)scale[g * 8 + e], (double)shift[g * 8 + e]), 0.0f);
-    float* dst = out + (((long long)b * H + y) * W + xw) * kC + g * 8;
+    float* dst = out + (((long long)b * H + y) * W + xw) * C + g * 8;
     reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
     reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
   }
 }
 
-cudaError_t launch_conv0(bool fp16_act, const float* x, void* act, const Conv0Params& p, int B, int H, int W,
-                         cudaStream_t st) {
+cudaError_t launch_conv0(bool fp16_act, int C, const float* x, void* act, const Conv0Params& p, int B, int H,
+                         int W, cudaStream_t st) {
   const long long npx = (long long)B * H * W;
-  const unsigned grid = (unsigned)((npx + 127) / 128);
-  if (fp16_act)
-    conv0_kernel<__half><<<grid, 128, 0, st>>>(x, static_cast<__half*>(act), p, B, H, W);
-  else
-    conv0_kernel<float><<<grid, 128, 0, st>>>(x, static_cast<float*>(act), p, B, H, W);
+  if (C == 64) {
+    const unsigned grid = (unsigned)((npx + 127) / 128);
+    if (fp16_act)
+      conv0_kernel<__half, 64><<<grid, 128, 0, st>>>(x, static_cast<__half*>(act), p, B, H, W);
+    else
+      conv0_kernel<float, 64><<<grid, 128, 0, st>>>(x, static_cast<float*>(act), p, B, H, W);
+  } else if (C == 128 && !fp16_act) {
+    const unsigned grid = (unsigned)((npx + 63) / 64);
+    conv0_kernel<float, 128><<<grid, 64, 0, st>>>(x, static_cast<float*>(act), p, B, H, W);
+  } else {
+    return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
-cudaError_t launch_head_f32(const float* act, const float* x, const float* wh, const float* bh, float* bands,
+cudaError_t launch_head_f32(int C, const float* act, const float* x, const float* wh, const float* bh, float* bands,
                             float* closure, int B, int H, int W, int K, int row0, int rows, cudaStream_t st) {
   const long long nout = (long long)B * rows * W;
   const unsigned grid = (unsigned)((nout + 127) / 128);
-  const size_t smem = (size_t)9 * kC * K * sizeof(float);
-  head_kernel<float><<<grid, 128, smem, st>>>(act, x, wh, bh, bands, closure, B, H, W, K, row0, rows);
+  const size_t smem = (size_t)9 * C * K * sizeof(float);
+  if (C == 64)
+    head_kernel<float, 64><<<grid, 128, smem, st>>>(act, x, wh, bh, bands, closure, B, H, W, K, row0, rows);
+  else if (C == 128)
+    head_kernel<float, 128><<<grid, 128, smem, st>>>(act, x, wh, bh, bands, closure, B, H, W, K, row0, rows);
+  else
+    return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
-cudaError_t launch_hidden_f32(const float* in, float* out, const float* w, const float* scale, const float* shift,
-                              int B, int H, int W, cudaStream_t st) {
+cudaError_t launch_hidden_f32(int C, const float* in, float* out, const float* w, const float* scale,
+                              const float* shift, int B, int H, int W, cudaStream_t st) {
   const long long tiles = (long long)B * ((H + kF32TileRows - 1) / kF32TileRows) * ((W + kF32TilePx - 1) / kF32TilePx);
-  hidden_f32_kernel<<<(unsigned)tiles, 256, kF32Smem, st>>>(in, out, w, scale, shift, B, H, W);
+  if (C == 64)
+    hidden_f32_kernel<64><<<(unsigned)tiles, 256, f32_smem(64), st>>>(in, out, w, scale, shift, B, H, W);
+  else if (C == 128)
+    hidden_f32_kernel<128><<<(unsigned)tiles, 512, f32_smem(128), st>>>(in, out, w, scale, shift, B, H, W);
+  else
+    return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
 cudaError_t configure_edge_kernels() {
-  return cudaFuncSetAttribute(hidden_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF32Smem);
+  cudaError_t e = cudaFuncSetAttribute(hidden_f32_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)f32_smem(64));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(hidden_f32_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f32_smem(128));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(head_kernel<float, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              9 * 128 * kMaxBands * 4);
 }
 
 }  // namespace tvs

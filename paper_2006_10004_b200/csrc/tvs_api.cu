@@ -94,7 +94,10 @@ struct tvs_plan {
   size_t chunk_budget = 2048ull << 20;  // activation bytes per chunk (TVS_CHUNK_MB)
 
   int n_hidden() const { return depth - 2; }
-  size_t act_px_bytes() const { return mode == TVS_MODE_FAST ? 128 : 256; }
+  // tcgen05 fp16 path: FAST mode with 64 channels; everything else runs the
+  // CUDA-core fp32 path (fp32-accurate mode, and the 128-channel wide variant)
+  bool tc_path() const { return mode == TVS_MODE_FAST && channels == 64; }
+  size_t act_px_bytes() const { return tc_path() ? 128 : (size_t)channels * 4; }
 };
 
 namespace {
@@ -172,11 +175,12 @@ void drain_profile(tvs_plan* p) {
 
 void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B, int H, int W, int row0, int rows,
                cudaStream_t st) {
-  const bool fast = p->mode == TVS_MODE_FAST;
+  const bool fast = p->tc_path();
+  const int C = p->channels;
   const double px = (double)B * H * W;
   // K1
-  timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * 64,
-               [&] { return tvs::launch_conv0(fast, x, p->act[0], p->conv0, B, H, W, st); });
+  timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
+               [&] { return tvs::launch_conv0(fast, C, x, p->act[0], p->conv0, B, H, W, st); });
   // K2 x (depth-2), K3
   int cur = 0;
   if (fast) {
@@ -212,15 +216,15 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
                  [&] { return tvs::launch_conv_tc(true, in_map[cur], in_map[cur], a, grid, st); });
   } else {
     for (int l = 0; l < p->n_hidden(); ++l) {
-      timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64, [&] {
-        return tvs::launch_hidden_f32((const float*)p->act[cur], (float*)p->act[cur ^ 1],
-                                      p->whid + (size_t)l * 64 * 64 * 9, p->shid + (size_t)l * 64,
-                                      p->bhid + (size_t)l * 64, B, H, W, st);
+      timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * C * C, [&] {
+        return tvs::launch_hidden_f32(C, (const float*)p->act[cur], (float*)p->act[cur ^ 1],
+                                      p->whid + (size_t)l * C * C * 9, p->shid + (size_t)l * C,
+                                      p->bhid + (size_t)l * C, B, H, W, st);
       });
       cur ^= 1;
     }
-    timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands, [&] {
-      return tvs::launch_head_f32((const float*)p->act[cur], x, p->wh, p->bh, bands, closure, B, H, W, p->out_bands,
+    timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * C * p->out_bands, [&] {
+      return tvs::launch_head_f32(C, (const float*)p->act[cur], x, p->wh, p->bh, bands, closure, B, H, W, p->out_bands,
                                   row0, rows, st);
     });
   }
@@ -278,7 +282,8 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
     if (!out_plan) throw TvsError(TVS_E_INVALID, "out_plan is null");
     *out_plan = nullptr;
     if (depth < 3) throw TvsError(TVS_E_INVALID, "depth must be at least 3 (first, hidden, last)");
-    if (channels != 64) throw TvsError(TVS_E_UNSUPPORTED, "this build supports channels == 64 only");
+    if (channels != 64 && channels != 128)
+      throw TvsError(TVS_E_UNSUPPORTED, "this build supports channels 64 (tcgen05 + CUDA-core paths) and 128 (CUDA-core path)");
     if (out_bands < 1 || out_bands > 8) throw TvsError(TVS_E_UNSUPPORTED, "out_bands must be in [1, 8]");
     if (mode != TVS_MODE_FP32 && mode != TVS_MODE_FAST) throw TvsError(TVS_E_INVALID, "unknown mode");
     int ndev = 0;
@@ -296,15 +301,15 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
     try {
       TVS_CUDA(tvs::configure_kernels());
       const int nh = depth - 2;
-      TVS_CUDA(cudaMalloc(&p->wh, (size_t)out_bands * 64 * 9 * 4));
+      TVS_CUDA(cudaMalloc(&p->wh, (size_t)out_bands * channels * 9 * 4));
       TVS_CUDA(cudaMalloc(&p->bh, (size_t)out_bands * 4));
-      TVS_CUDA(cudaMalloc(&p->bhid, (size_t)nh * 64 * 4));
-      TVS_CUDA(cudaMalloc(&p->shid, (size_t)nh * 64 * 4));
-      if (mode == TVS_MODE_FAST) {
+      TVS_CUDA(cudaMalloc(&p->bhid, (size_t)nh * channels * 4));
+      TVS_CUDA(cudaMalloc(&p->shid, (size_t)nh * channels * 4));
+      if (p->tc_path()) {
         TVS_CUDA(cudaMalloc(&p->wpack, (size_t)nh * tvs::conv_wpack_bytes(false)));
         TVS_CUDA(cudaMalloc(&p->hpack, tvs::conv_wpack_bytes(true)));
       } else
-        TVS_CUDA(cudaMalloc(&p->whid, (size_t)nh * 64 * 64 * 9 * 4));
+        TVS_CUDA(cudaMalloc(&p->whid, (size_t)nh * channels * channels * 9 * 4));
     } catch (...) {
       free_all(p);
       delete p;
@@ -327,30 +332,31 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
     auto scale_of = [&](int i) -> const float* { return scale_dev ? scale_dev[i] : nullptr; };
     if (scale_of(0) || scale_of(p->depth - 1))
       throw TvsError(TVS_E_UNSUPPORTED, "conv0/head take no BatchNorm scale (model.py:37,44)");
-    TVS_CUDA(cudaMemcpyAsync(p->conv0.w, w_dev[0], sizeof(p->conv0.w), cudaMemcpyDeviceToHost, st));
-    TVS_CUDA(cudaMemcpyAsync(p->conv0.b, shift_dev[0], sizeof(p->conv0.b), cudaMemcpyDeviceToHost, st));
+    const int C = p->channels;
+    TVS_CUDA(cudaMemcpyAsync(p->conv0.w, w_dev[0], (size_t)C * 9 * 4, cudaMemcpyDeviceToHost, st));
+    TVS_CUDA(cudaMemcpyAsync(p->conv0.b, shift_dev[0], (size_t)C * 4, cudaMemcpyDeviceToHost, st));
     TVS_CUDA(cudaStreamSynchronize(st));  // conv0 weights are kernel parameters (host side)
-    TVS_CUDA(cudaMemcpyAsync(p->wh, w_dev[p->depth - 1], (size_t)p->out_bands * 64 * 9 * 4,
+    TVS_CUDA(cudaMemcpyAsync(p->wh, w_dev[p->depth - 1], (size_t)p->out_bands * C * 9 * 4,
                              cudaMemcpyDeviceToDevice, st));
     TVS_CUDA(cudaMemcpyAsync(p->bh, shift_dev[p->depth - 1], (size_t)p->out_bands * 4, cudaMemcpyDeviceToDevice,
                              st));
     for (int l = 0; l < nh; ++l) {
       const float* sc = scale_of(l + 1);
-      float* dst_scale = p->shid + l * 64;
+      float* dst_scale = p->shid + l * C;
       if (sc)
-        TVS_CUDA(cudaMemcpyAsync(dst_scale, sc, 64 * 4, cudaMemcpyDeviceToDevice, st));
+        TVS_CUDA(cudaMemcpyAsync(dst_scale, sc, C * 4, cudaMemcpyDeviceToDevice, st));
       else
-        TVS_CUDA(tvs::launch_fill(dst_scale, 1.0f, 64, st));
-      TVS_CUDA(cudaMemcpyAsync(p->bhid + l * 64, shift_dev[l + 1], 64 * 4, cudaMemcpyDeviceToDevice, st));
-      if (p->mode == TVS_MODE_FAST) {
+        TVS_CUDA(tvs::launch_fill(dst_scale, 1.0f, C, st));
+      TVS_CUDA(cudaMemcpyAsync(p->bhid + l * C, shift_dev[l + 1], C * 4, cudaMemcpyDeviceToDevice, st));
+      if (p->tc_path()) {
         TVS_CUDA(tvs::launch_pack_hidden_f16(w_dev[l + 1], dst_scale,
                                              p->wpack + (size_t)l * tvs::conv_wpack_bytes(false), st));
       } else {
-        TVS_CUDA(cudaMemcpyAsync(p->whid + (size_t)l * 64 * 64 * 9, w_dev[l + 1], 64 * 64 * 9 * 4,
+        TVS_CUDA(cudaMemcpyAsync(p->whid + (size_t)l * C * C * 9, w_dev[l + 1], (size_t)C * C * 9 * 4,
                                  cudaMemcpyDeviceToDevice, st));
       }
     }
-    if (p->mode == TVS_MODE_FAST) TVS_CUDA(tvs::launch_pack_head_f16(w_dev[p->depth - 1], p->out_bands, p->hpack, st));
+    if (p->tc_path()) TVS_CUDA(tvs::launch_pack_head_f16(w_dev[p->depth - 1], p->out_bands, p->hpack, st));
     p->weights_ready = true;
   });
 }

@@ -29,7 +29,7 @@ def test_invalid_arguments_report_errors_without_gpu_work():
     plan = ctypes.c_void_p()
     assert lib.tvs_plan_create(0, 2, 64, 5, 1, ctypes.byref(plan)) == _native.TVS_E_INVALID
     assert b"depth" in lib.tvs_last_error()
-    assert lib.tvs_plan_create(0, 17, 128, 5, 1, ctypes.byref(plan)) == _native.TVS_E_UNSUPPORTED
+    assert lib.tvs_plan_create(0, 17, 96, 5, 1, ctypes.byref(plan)) == _native.TVS_E_UNSUPPORTED
     assert lib.tvs_plan_create(0, 17, 64, 5, 1, None) == _native.TVS_E_INVALID
     assert lib.tvs_forward(None, None, None, None, 1, 1, 1, 0, -1, None) == _native.TVS_E_INVALID
     assert lib.tvs_plan_destroy(None) == 0
