@@ -20,7 +20,6 @@ constexpr int kSlots = 8;                              // TMEM accumulator slots
 // tcgen05 conv kernels (conv_tc.cu)
 constexpr int kStages = 6;             // input-row ring depth
 constexpr int kEpiGroups = 3;          // epilogue row groups (output row seq % 3)
-constexpr int kConvThreads = 64 + kEpiGroups * 128;  // w0 TMA, w1 MMA, 4 epilogue warps per group
 
 struct ConvArgs {
   int B, H, W;
@@ -44,10 +43,10 @@ constexpr int kMaxC = 128;  // channels supported by the CUDA-core (fp32) path
 constexpr int kMaxBands = 8;
 
 // host-side launchers (defined next to their kernels)
-size_t conv_smem_bytes(bool head);
 size_t conv_wpack_bytes(bool head);
-cudaError_t launch_conv_tc(bool head, const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a,
-                           int grid, cudaStream_t st);
+struct Conv0Params;
+cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a,
+                           const Conv0Params* c0, int grid, cudaStream_t st);
 cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
 cudaError_t launch_pack_head_f16(const float* w, int K, uint8_t* out, cudaStream_t st);
 cudaError_t launch_fill(float* dst, float v, int n, cudaStream_t st);

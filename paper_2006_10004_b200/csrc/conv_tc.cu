@@ -64,21 +64,34 @@ struct SegIter {
   }
 };
 
-template <bool kHead>
+// kMode: 0 = hidden layer (TMA producer), 1 = head, 2 = first hidden layer
+// with conv0 fused into its producer (4 warps compute Conv2d(1,64)+ReLU of
+// each input row from the fp32 image straight into the smem ring).
+template <int kMode>
 struct ConvCfg {
+  static constexpr bool kHead = kMode == 1;
+  static constexpr bool kFirst = kMode == 2;
+  static constexpr int kProdWarps = kFirst ? 4 : 1;
+  static constexpr int kMmaWarp = kProdWarps;
+  static constexpr int kEpiWarp0 = kProdWarps + 1;
+  // 4 more producer warps in mode 2 -> two epilogue groups keep <= 4 warps per
+  // SM sub-partition (register file: 16K regs per SMSP, so 128 regs/thread)
+  static constexpr int kGroups = kFirst ? 2 : kEpiGroups;
+  static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kGroups);
   static constexpr int NB = kHead ? 32 : 64;          // TMEM columns per output row (slot)
   static constexpr int kWdx = 3 * NB * 128;           // B bytes per dx (3 dy blocks x NB rows x 128 B)
   static constexpr int kW = 3 * kWdx;
   static constexpr int kTmemCols = kSlots * NB;       // 512 / 256
   static constexpr int kStageOut = kHead ? 0 : 32 * 128;  // per-warp staging (hidden only)
-  static constexpr size_t kSmem = 1024 + kW + kStages * kInRowStride + 4 * kEpiGroups * kStageOut + 1024;
+  static constexpr size_t kSmem = 1024 + kW + kStages * kInRowStride + 4 * kGroups * kStageOut + 1024;
 };
 
-template <bool kHead>
-__global__ void __launch_bounds__(kConvThreads, 1)
+template <int kMode>
+__global__ void __launch_bounds__(ConvCfg<kMode>::kThreads, 1)
 conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
-                  const ConvArgs a) {
-  using Cfg = ConvCfg<kHead>;
+                  const ConvArgs a, const __grid_constant__ Conv0Params c0) {
+  using Cfg = ConvCfg<kMode>;
+  constexpr bool kHead = Cfg::kHead;
   constexpr int NB = Cfg::NB;
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t full[kStages], empty[kStages], slot_full[kSlots], slot_empty[kSlots], wbar;
@@ -93,13 +106,13 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < kStages; ++i) { mbar_init(&full[i], Cfg::kProdWarps); mbar_init(&empty[i], 1); }
     for (int i = 0; i < kSlots; ++i) { mbar_init(&slot_full[i], 1); mbar_init(&slot_empty[i], 4); }
     mbar_init(&wbar, 1);
     fence_barrier_init();
   }
   if (threadIdx.x < kC) sShift[threadIdx.x] = (threadIdx.x < a.nshift) ? a.shift[threadIdx.x] : 0.0f;
-  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(&tmem_base_smem);
+  if (warp == Cfg::kMmaWarp) tmem_alloc<Cfg::kTmemCols>(&tmem_base_smem);
   // weights do not depend on the previous layer: start their load before the
   // PDL wait so it overlaps the previous kernel's tail
   if (threadIdx.x == 0) {
@@ -113,7 +126,83 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   pdl_launch_dependents();  // the next layer may start its prologue on free SMs
   pdl_wait();               // previous layer's activations are complete and visible
 
-  if (warp == 0) {
+  if (Cfg::kFirst && warp < Cfg::kProdWarps) {
+    // ------------------------------------------- conv0 producer (K1 fused) ----
+    // Input row r of this layer = ReLU(Conv2d(1,64)(x))[row r] at pixels
+    // x0-1 .. x0+128, written as fp16 into the SW128 ring stage; pixels outside
+    // the image are zero (this layer's Conv2d padding).  Thread t (128 threads)
+    // owns strip pixel 1+t (all 64 channels) and keeps its 3x3 input window in
+    // registers, loading one new x row per input row, one row ahead.  The two
+    // halo pixels (0 and 129) are split over all threads: thread t computes
+    // channel t%64 of halo pixel t/64.  Weights come from the parameter block.
+    const int pt = warp * 32 + lane;                 // 0..127
+    const int sp = 1 + pt;                           // strip pixel (ring row)
+    const int hp = (pt >> 6) ? 129 : 0;              // halo pixel of this thread
+    const int hco = pt & 63;                         // its channel
+    int stage = 0;
+    uint32_t phase = 0;
+    SegIter it(a);
+    Segment g;
+    while (it.next(a, g)) {
+      const float* img = a.x + (long long)g.b * a.H * a.W;
+      const int xg = g.x0 - 1 + sp, xh = g.x0 - 1 + hp;
+      auto ld3 = [&](int yy, int xc, float* v) {  // x[yy][xc-1..xc+1], zero outside the image
+        const bool rowok = yy >= 0 && yy < a.H;
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+          const int xx = xc + kx - 1;
+          v[kx] = (rowok && xx >= 0 && xx < a.W) ? __ldg(img + (long long)yy * a.W + xx) : 0.0f;
+        }
+      };
+      const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
+      float win[9], hwin[9], nxt[3], hnxt[3];
+      ld3(r0 - 1, xg, win); ld3(r0, xg, win + 3); ld3(r0 + 1, xg, win + 6);
+      ld3(r0 - 1, xh, hwin); ld3(r0, xh, hwin + 3); ld3(r0 + 1, xh, hwin + 6);
+      for (int r = r0; r <= r1; ++r) {
+        ld3(r + 2, xg, nxt);  // next row's window, in flight during this row's math
+        ld3(r + 2, xh, hnxt);
+        mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t row_u = smem_u32(sIn + stage * kInRowStride);
+        const bool inside = xg >= 0 && xg < a.W;
+#pragma unroll
+        for (int chunk = 0; chunk < 8; ++chunk) {
+          uint32_t packed[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float v2[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int co = chunk * 8 + e * 2 + h;
+              float acc = 0.0f;
+#pragma unroll
+              for (int t9 = 0; t9 < 9; ++t9) acc = fmaf(c0.w[co * 9 + t9], win[t9], acc);
+              v2[h] = inside ? fmaxf(acc + c0.b[co], 0.0f) : 0.0f;
+            }
+            __half2 hv = __floats2half2_rn(v2[0], v2[1]);
+            packed[e] = *reinterpret_cast<uint32_t*>(&hv);
+          }
+          st_shared_v4(row_u + sp * 128 + ((chunk ^ (sp & 7)) << 4), packed[0], packed[1], packed[2], packed[3]);
+        }
+        {  // one channel of one halo pixel
+          float acc = 0.0f;
+#pragma unroll
+          for (int t9 = 0; t9 < 9; ++t9) acc = fmaf(c0.w[hco * 9 + t9], hwin[t9], acc);
+          const bool hin = xh >= 0 && xh < a.W;
+          const __half hv = __float2half_rn(hin ? fmaxf(acc + c0.b[hco], 0.0f) : 0.0f);
+          const uint32_t addr = row_u + hp * 128 + (((hco >> 3) ^ (hp & 7)) << 4) + ((hco & 7) << 1);
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(addr), "h"(__half_as_ushort(hv)) : "memory");
+        }
+        fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+#pragma unroll
+        for (int i = 0; i < 6; ++i) { win[i] = win[i + 3]; hwin[i] = hwin[i + 3]; }
+#pragma unroll
+        for (int i = 0; i < 3; ++i) { win[6 + i] = nxt[i]; hwin[6 + i] = hnxt[i]; }
+      }
+    }
+  } else if (!Cfg::kFirst && warp == 0) {
     // ------------------------------------------------ TMA producer ----
     if (elect_one()) {
       prefetch_tmap(&tm_in);
@@ -131,7 +220,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == Cfg::kMmaWarp) {
     // ------------------------------------------------ MMA issuer ----
     // The whole warp walks the schedule (warp-uniform values stay in uniform
     // registers); one elected lane issues.  Per input row the MMA budget is
@@ -290,19 +379,19 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     }
   } else {
     // ------------------------------------------------ epilogue ----
-    const int ew = warp - 2;                  // 0 .. 4*kEpiGroups-1
-    const uint32_t grp = (uint32_t)(ew >> 2); // output rows with seq % kEpiGroups == grp
+    const int ew = warp - Cfg::kEpiWarp0;     // 0 .. 4*kEpiGroups-1
+    const uint32_t grp = (uint32_t)(ew >> 2); // output rows with seq % kGroups == grp
     const int quarter = warp & 3;             // TMEM lane quarter this warp may access
     const int px = quarter * 32 + lane;       // pixel within the strip == TMEM lane
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
     const uint32_t stage_out = smem_u32(sOut + ew * Cfg::kStageOut);
     const uint32_t shift_u = smem_u32(sShift);
     if (!kHead && lane == 0) prefetch_tmap(&tm_out);
-    uint32_t seq = 0, gsel = 0;  // gsel = seq % kEpiGroups
+    uint32_t seq = 0, gsel = 0;  // gsel = seq % kGroups
     SegIter it(a);
     Segment g;
     while (it.next(a, g)) {
-      for (int q = g.ya; q < g.yb; ++q, ++seq, gsel = (gsel + 1 == kEpiGroups) ? 0 : gsel + 1) {
+      for (int q = g.ya; q < g.yb; ++q, ++seq, gsel = (gsel + 1 == Cfg::kGroups) ? 0 : gsel + 1) {
         if (gsel != grp) continue;
         const uint32_t slot = seq & 7;
         mbar_wait(&slot_full[slot], (seq >> 3) & 1);
@@ -377,7 +466,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == Cfg::kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<Cfg::kTmemCols>(tmem);
   }
@@ -448,7 +537,7 @@ __global__ void pack_hidden_f16_kernel(const float* __restrict__ w, const float*
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
     const int ky = t / 3, kx = t % 3;
-    put_b(out, ConvCfg<false>::kWdx, kx, (2 - ky) * 64 + co, ci, __float2half_rn(rn[t]));
+    put_b(out, ConvCfg<0>::kWdx, kx, (2 - ky) * 64 + co, ci, __float2half_rn(rn[t]));
   }
 }
 
@@ -463,8 +552,8 @@ __global__ void pack_head_f16_kernel(const float* __restrict__ w, int K, uint8_t
     const __half hi = __float2half_rn(wf);
     const __half lo = __float2half_rn(wf - __half2float(hi));
     const int nb = (2 - ky) * 32;
-    put_b(out, ConvCfg<true>::kWdx, kx, nb + k, ci, hi);
-    put_b(out, ConvCfg<true>::kWdx, kx, nb + 16 + k, ci, lo);
+    put_b(out, ConvCfg<1>::kWdx, kx, nb + k, ci, hi);
+    put_b(out, ConvCfg<1>::kWdx, kx, nb + 16 + k, ci, lo);
   }
 }
 
@@ -474,37 +563,50 @@ __global__ void fill_kernel(float* dst, float v, int n) {
 }
 
 // ------------------------------------------------------------ launchers ----
-size_t conv_smem_bytes(bool head) { return head ? ConvCfg<true>::kSmem : ConvCfg<false>::kSmem; }
-size_t conv_wpack_bytes(bool head) { return head ? ConvCfg<true>::kW : ConvCfg<false>::kW; }
+
+size_t conv_wpack_bytes(bool head) { return head ? ConvCfg<1>::kW : ConvCfg<0>::kW; }
 
 // Launched with programmatic stream serialization (PDL): the kernel's
 // prologue overlaps the previous kernel; griddepcontrol.wait guards all
 // activation reads and writes.
-cudaError_t launch_conv_tc(bool head, const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a,
-                           int grid, cudaStream_t st) {
+cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a,
+                           const Conv0Params* c0, int grid, cudaStream_t st) {
+  static const Conv0Params zero{};
+  const Conv0Params& p0 = c0 ? *c0 : zero;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kConvThreads);
-  cfg.dynamicSmemBytes = head ? ConvCfg<true>::kSmem : ConvCfg<false>::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (head) return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<true>, tm_in, tm_out, a);
-  return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<false>, tm_in, tm_out, a);
+  switch (mode) {
+    case 0:
+      cfg.blockDim = dim3(ConvCfg<0>::kThreads);
+      cfg.dynamicSmemBytes = ConvCfg<0>::kSmem;
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<0>, tm_in, tm_out, a, p0);
+    case 1:
+      cfg.blockDim = dim3(ConvCfg<1>::kThreads);
+      cfg.dynamicSmemBytes = ConvCfg<1>::kSmem;
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<1>, tm_in, tm_out, a, p0);
+    case 2:
+      cfg.blockDim = dim3(ConvCfg<2>::kThreads);
+      cfg.dynamicSmemBytes = ConvCfg<2>::kSmem;
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<2>, tm_in, tm_out, a, p0);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* out, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<false>::kW, st);
+  cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<0>::kW, st);
   if (e != cudaSuccess) return e;
   pack_hidden_f16_kernel<<<(kC * kC + 127) / 128, 128, 0, st>>>(w, scale, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pack_head_f16(const float* w, int K, uint8_t* out, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<true>::kW, st);
+  cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<1>::kW, st);
   if (e != cudaSuccess) return e;
   pack_head_f16_kernel<<<(K * kC + 127) / 128, 128, 0, st>>>(w, K, out);
   return cudaGetLastError();
@@ -517,11 +619,14 @@ cudaError_t launch_fill(float* dst, float v, int n, cudaStream_t st) {
 
 cudaError_t configure_edge_kernels();
 cudaError_t configure_kernels() {
-  cudaError_t e = cudaFuncSetAttribute(conv3x3_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)ConvCfg<false>::kSmem);
+  cudaError_t e = cudaFuncSetAttribute(conv3x3_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)ConvCfg<0>::kSmem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(conv3x3_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)ConvCfg<true>::kSmem);
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<1>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<2>::kSmem);
   if (e != cudaSuccess) return e;
   return configure_edge_kernels();
 }

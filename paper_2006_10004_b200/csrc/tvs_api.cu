@@ -91,7 +91,11 @@ struct tvs_plan {
   double prof_ms[3] = {0, 0, 0};
   long long prof_n[3] = {0, 0, 0};
   double prof_flops[3] = {0, 0, 0};
-  size_t chunk_budget = 2048ull << 20;  // activation bytes per chunk (TVS_CHUNK_MB)
+  size_t chunk_budget = 2048ull << 20;
+  // TVS_FUSE_CONV0=1: compute conv0 in the first hidden layer's producer warps
+  // (saves the K1 kernel and 2x128 B/px of HBM traffic, but on B200 the
+  // producer's ~600 FFMA/px-row currently cost more than they save)
+  bool unfused_conv0 = true;  // activation bytes per chunk (TVS_CHUNK_MB)
 
   int n_hidden() const { return depth - 2; }
   // tcgen05 fp16 path: FAST mode with 64 channels; everything else runs the
@@ -178,9 +182,10 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
   const bool fast = p->tc_path();
   const int C = p->channels;
   const double px = (double)B * H * W;
-  // K1
-  timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
-               [&] { return tvs::launch_conv0(fast, C, x, p->act[0], p->conv0, B, H, W, st); });
+  // K1 (the FAST path fuses it into the first hidden layer's producer)
+  if (!fast || p->unfused_conv0)
+    timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
+                 [&] { return tvs::launch_conv0(fast, C, x, p->act[0], p->conv0, B, H, W, st); });
   // K2 x (depth-2), K3
   int cur = 0;
   if (fast) {
@@ -196,14 +201,20 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.row0 = r0; a.rows = nrows;
       return a;
     };
+    const bool fuse0 = !p->unfused_conv0;
+    if (fuse0) cur = 1;  // the first hidden layer reads x and writes act[0]
     for (int l = 0; l < p->n_hidden(); ++l) {
       tvs::ConvArgs a = geom(0, H);
       a.wpack = p->wpack + (size_t)l * tvs::conv_wpack_bytes(false);
       a.shift = p->bhid + (size_t)l * tvs::kC;
       a.nshift = tvs::kC;
+      a.x = x;
       const int grid = conv_grid(p, a);
-      timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64,
-                   [&] { return tvs::launch_conv_tc(false, in_map[cur], out_map[cur ^ 1], a, grid, st); });
+      const bool first = fuse0 && l == 0;
+      timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64 + (first ? px * 2.0 * 9 * 64 : 0.0), [&] {
+        return tvs::launch_conv_tc(first ? 2 : 0, in_map[cur], out_map[cur ^ 1], a, first ? &p->conv0 : nullptr,
+                                   grid, st);
+      });
       cur ^= 1;
     }
     tvs::ConvArgs a = geom(row0, rows);
@@ -213,7 +224,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     a.x = x; a.bands = bands; a.closure = closure; a.K = p->out_bands;
     const int grid = conv_grid(p, a);
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands,
-                 [&] { return tvs::launch_conv_tc(true, in_map[cur], in_map[cur], a, grid, st); });
+                 [&] { return tvs::launch_conv_tc(1, in_map[cur], in_map[cur], a, nullptr, grid, st); });
   } else {
     for (int l = 0; l < p->n_hidden(); ++l) {
       timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * C * C, [&] {
@@ -298,6 +309,7 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
     p->device = device; p->depth = depth; p->channels = channels; p->out_bands = out_bands; p->mode = mode;
     p->num_sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("TVS_CHUNK_MB")) p->chunk_budget = (size_t)std::atoll(e) << 20;
+    if (const char* e = std::getenv("TVS_FUSE_CONV0")) p->unfused_conv0 = std::atoi(e) == 0;
     try {
       TVS_CUDA(tvs::configure_kernels());
       const int nh = depth - 2;

@@ -232,6 +232,25 @@ def test_launch_accounting(model):
     assert model.last_launch_count() == model.depth  # conv0 + (depth-2) hidden + head
 
 
+def test_fused_conv0_path(seeded_state, oracle, monkeypatch):
+    """Opt-in K1 fusion (TVS_FUSE_CONV0=1): conv0 computed by the first hidden
+    layer's producer warps; identical numerics contract, one launch fewer."""
+    monkeypatch.setenv("TVS_FUSE_CONV0", "1")
+    m = TVSpecNet().eval()
+    m.load_state_dict(seeded_state)
+    x = np.stack([make_image(CONFIGS[2], i) for i in range(2)])[:, None]
+    with torch.no_grad():
+        ref = oracle(torch.from_numpy(x)).numpy()
+    _check(m, x, ref)
+    assert m.last_launch_count() == m.depth - 1
+    # bitwise equal to the unfused path (same fp32 conv0 arithmetic, fp16 rounding)
+    monkeypatch.setenv("TVS_FUSE_CONV0", "0")
+    m2 = TVSpecNet().eval()
+    m2.load_state_dict(seeded_state)
+    xd = torch.from_numpy(x).cuda()
+    assert torch.equal(m(xd), m2(xd))
+
+
 def test_abi_errors_on_gpu(model):
     plan = model._plan_for(torch.device("cuda", 0))
     with pytest.raises(ValueError):
