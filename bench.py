@@ -129,24 +129,31 @@ def _seeded_state(depth, channels):
     return build_seeded_state(depth, channels, 5)
 
 
-def cpu_reference(spec, steps, warmup, sample_images, threads):
-    """The reference CPU forward (oracle port) on `sample_images` images per step."""
+def cpu_reference(spec, steps, warmup, sample_images, threads, budget_s=None):
+    """The reference CPU forward (oracle port), per image as predict_bands does
+    (inference.py:25-32).  Each step runs `sample_images` images, or - with
+    `budget_s` - as many images (>= 1) as fit in that many seconds."""
     from oracle.tvspecnet_oracle import oracle_from_state
 
     torch.set_num_threads(threads)
     model = oracle_from_state(_seeded_state(spec.depth, spec.channels), spec.depth, spec.channels, 5)
-    x = torch.from_numpy(_batch(spec, sample_images))
-    times = []
+    n_max = min(spec.batch, sample_images)
+    imgs = [torch.from_numpy(make_image(spec, j)[None, None]) for j in range(n_max)]
+    rates, secs = [], []
     with torch.no_grad():
         for i in range(warmup + steps):
             t0 = time.perf_counter()
-            for j in range(sample_images):  # per image, as predict_bands does (inference.py:25-32)
-                model(x[j : j + 1])
+            n = 0
+            while n < n_max:
+                model(imgs[n])
+                n += 1
+                if budget_s is not None and time.perf_counter() - t0 >= budget_s:
+                    break
             dt = time.perf_counter() - t0
             if i >= warmup:
-                times.append(dt)
-    px = sample_images * spec.height * spec.width
-    return px / 1e6 / statistics.median(times), statistics.median(times), times
+                rates.append(n * spec.height * spec.width / 1e6 / dt)
+                secs.append((n, dt))
+    return statistics.median(rates), secs
 
 
 def run_reference(args, spec):
@@ -154,21 +161,29 @@ def run_reference(args, spec):
     if world > 1 and rank != 0:
         return
     threads = os.cpu_count() or 1
-    sample = args.cpu_sample
-    mp_s, sec, _ = cpu_reference(spec, args.steps, args.warmup, sample, threads)
+    budget = args.ref_step_seconds
+    mp_s, secs = cpu_reference(spec, args.steps, args.warmup, spec.batch, threads, budget_s=budget)
+    n_img = statistics.median([n for n, _ in secs])
     line = {
         "metric": METRIC, "value": round(mp_s, 5), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (SURVEY §8(d) generator)",
-        "impl": "reference",
+        "warmup": args.warmup, "ms_per_step": round(statistics.median([d for _, d in secs]) * 1e3, 3),
+        "higher_is_better": True, "scaling": _scaling(spec), "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (SURVEY §8(d) generator)", "impl": "reference",
         "config": {"workload": spec.name, "batch": spec.batch, "height": spec.height, "width": spec.width,
-                   "depth": spec.depth, "channels": spec.channels, "sample_images_per_step": sample},
+                   "depth": spec.depth, "channels": spec.channels},
         "cpu_baseline": {"value": round(mp_s, 5), "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample} of {spec.batch} images per step, torch CPU (oneDNN) fp32, "
-                                   f"{threads} threads"},
+                         "sample": f"per step: images of this workload, one forward each (predict_bands style), "
+                                   f"until {budget:g} s elapse (median {n_img:g} images), torch CPU (oneDNN) "
+                                   f"fp32, {threads} threads"},
         "e2e": {"value": round(mp_s, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _scaling(spec):
+    # config 2: every rank its own batch (weak); single images are row-banded and
+    # configs 4/5 batch-sharded across ranks (strong, fixed total work)
+    return "weak" if spec.name.startswith("cfg2") else "strong"
 
 
 def _flush_l2(buf):
@@ -190,6 +205,18 @@ def time_steps(fn, steps, warmup, flush):
     return [a.elapsed_time(b) for a, b in evs]
 
 
+def _rank_work(spec, world, rank):
+    """This rank's images / rows.  Returns (image indices, row band or None)."""
+    from paper_2006_10004_b200.shard import batch_shards, row_bands
+
+    if spec.name.startswith("cfg2"):
+        return list(range(spec.batch)), None  # weak scaling: each rank a full config-2 batch
+    if spec.batch == 1:
+        return [0], (row_bands(spec.height, world, spec.depth)[rank] if world > 1 else None)
+    s, n = batch_shards(spec.batch, world)[rank]
+    return list(range(s, s + n)), None
+
+
 def run_ours(args, spec):
     world, rank, local = _dist()
     if world > 1:
@@ -202,22 +229,31 @@ def run_ours(args, spec):
     from paper_2006_10004_b200 import TVSpecNet
 
     state = _seeded_state(spec.depth, spec.channels)
-    x_host = torch.from_numpy(_batch(spec)).pin_memory()
+    idx, band = _rank_work(spec, world, rank)
+    x_np = np.stack([make_image(spec, i) for i in idx])[:, None]
+    if band is not None:  # row band with receptive-field halo (shard.row_bands)
+        x_np = np.ascontiguousarray(x_np[:, :, band.src0 : band.src1])
+        row0, nrows = band.valid_row0, band.rows
+    else:
+        row0, nrows = 0, x_np.shape[2]
+    x_host = torch.from_numpy(x_np).pin_memory()
     x = x_host.to(dev)
     B, _, H, W = x.shape
-    px = B * H * W
+    px_out = B * nrows * W  # output pixels this rank produces
+    total_px = (spec.batch * spec.height * spec.width) if _scaling(spec) == "strong" else world * px_out
     flush = torch.empty(256 << 20 >> 2, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
+    precs = ["fast"] + (["fp32"] if args.fp32_steps > 0 else [])
     results = {}
-    for prec in ("fast", "fp32"):
+    for prec in precs:
         model = TVSpecNet(spec.depth, spec.channels, 5, precision=prec).eval()
         model.load_state_dict(state)
-        bands = torch.empty((B, 5, H, W), device=dev)
-        clos = torch.empty((B, 1, H, W), device=dev)
+        bands = torch.empty((B, 5, nrows, W), device=dev)
+        clos = torch.empty((B, 1, nrows, W), device=dev)
         plan = model._plan_for(dev)
 
         def step():
-            plan.forward(x.data_ptr(), bands.data_ptr(), clos.data_ptr(), B, H, W, 0, H,
+            plan.forward(x.data_ptr(), bands.data_ptr(), clos.data_ptr(), B, H, W, row0, nrows,
                          torch.cuda.current_stream().cuda_stream)
 
         steps = args.steps if prec == "fast" else max(1, min(args.steps, args.fp32_steps))
@@ -233,7 +269,7 @@ def run_ours(args, spec):
             t = torch.tensor([tot_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tot_ms = float(t.item())
-        value = world * px * steps / 1e6 / (tot_ms / 1e3)
+        value = total_px * steps / 1e6 / (tot_ms / 1e3)
 
         # live per-kernel timing of the dominant kernel (hidden conv), separate pass
         plan.profile_enable(True)
@@ -246,26 +282,31 @@ def run_ours(args, spec):
         hd_ms, _, _ = plan.profile_read(2)
         plan.profile_enable(False)
 
-        # end to end through the public API with host buffers (H2D + D2H inside)
+        # end to end through the public API with host buffers (pinned input ->
+        # CPU result: H2D + forward + D2H inside the timed region), on at most
+        # `e2e_max_images` images of this rank's work
+        ne = max(1, min(B, args.e2e_max_images, (1 << 30) // (5 * 4 * nrows * W)))  # <= 1 GiB of pinned results
+        xe = x_host[:ne]
         e2e_steps = max(1, min(steps, args.e2e_steps))
         out_host = None
         for _ in range(3):  # same pattern as timed: keeps two pinned result blocks cached
-            out_host = model(x_host)
+            out_host = model.forward_planes(xe, rows=(row0, nrows))[0]
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             _flush_l2(flush)
-            out_host = model(x_host)  # pinned (B,1,H,W) -> CPU (B,5,H,W)
+            out_host = model.forward_planes(xe, rows=(row0, nrows))[0]
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / e2e_steps
         if world > 1:
             t = torch.tensor([e2e_s], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
+        e2e_px = ne * nrows * W * (world if _scaling(spec) == "weak" or band is not None else world)
         results[prec] = dict(value=value, ms=tot_ms / steps, ms_list=ms, launches=launches, steps=steps,
                              warmup=warm, clocks=clk.summary(), hid_ms=hid_ms, hid_n=hid_n, hid_flops=hid_flops,
-                             c0_ms=c0_ms, hd_ms=hd_ms, e2e=world * px / 1e6 / e2e_s,
-                             e2e_bytes=(x_host.numel() * 4, out_host.numel() * 4))
+                             c0_ms=c0_ms, hd_ms=hd_ms, e2e=e2e_px / 1e6 / e2e_s,
+                             e2e_bytes=(xe.numel() * 4, out_host.numel() * 4), e2e_images=ne)
         del model, plan, bands, clos
 
     if rank != 0:
@@ -280,17 +321,24 @@ def run_ours(args, spec):
     hid_avg_ms = f["hid_ms"] / max(1, f["hid_n"])
     hid_tflops = f["hid_flops"] / max(1, f["hid_n"]) / (hid_avg_ms / 1e3) / 1e12
     step_ms = f["ms"]
+    tc = spec.channels == 64
+    parallelism = (f"row-bands x{world} (halo {spec.depth})" if band is not None else
+                   ("batch per rank" if _scaling(spec) == "weak" else f"batch-shard x{world}"))
     line = {
         "metric": METRIC, "value": round(f["value"], 3), "unit": UNIT, "n_gpus": world, "steps": f["steps"],
-        "warmup": f["warmup"], "ms_per_step": round(step_ms, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f16 operands / f32 accumulate (tcgen05 kind::f16); conv0+head f32",
-        "data": "synthetic (SURVEY §8(d) piecewise-constant generator, seed 2)",
-        "config": {"workload": spec.name, "batch_per_gpu": B, "height": H, "width": W, "depth": spec.depth,
-                   "channels": spec.channels, "out_bands": 5, "precision": "fast", "parallelism": f"batch x{world}",
+        "warmup": f["warmup"], "ms_per_step": round(step_ms, 4), "higher_is_better": True,
+        "scaling": _scaling(spec), "vs_baseline": None,
+        "dtype": ("f16 operands / f32 accumulate (tcgen05 kind::f16); conv0+head f32" if tc
+                  else "f32 (CUDA-core path, fp64 accumulation)"),
+        "data": f"synthetic (SURVEY §8(d) piecewise-constant generator, seed {spec.seed})",
+        "config": {"workload": spec.name, "batch": spec.batch, "rank_images": B, "height": spec.height,
+                   "width": spec.width, "depth": spec.depth, "channels": spec.channels, "out_bands": 5,
+                   "precision": "fast", "parallelism": parallelism,
                    "l2": "256 MiB buffer written between timed steps", "inputs_resident": "HBM"},
+        "latency_ms": round(step_ms, 4) if spec.batch == 1 else None,
         "tflops_algorithmic": round(f["value"] * 1e6 * fpx / 1e12 / world, 2),
         "frac_of_bf16_peak": round(f["value"] * 1e6 * fpx / 1e12 / world / peak_tf, 4),
-        "roofline": {"bound": "tensor", "kernel": "conv3x3_hidden_f16_kernel",
+        "roofline": {"bound": "tensor", "kernel": "conv3x3_tc_kernel<0> (hidden layer)" if tc else "hidden_f32_kernel",
                      "achieved": round(hid_tflops, 2), "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": round(hid_tflops / peak_tf, 4), "peak_kind": f"{peak_kind} bf16 burst",
                      "frac_of_sustained": round(hid_tflops / peak_sus, 4) if peak_sus else None,
@@ -301,18 +349,20 @@ def run_ours(args, spec):
                      "algorithmic_bytes_per_launch": 2 * B * H * W * 128},
         "gpu_launches": f["launches"] * f["steps"],
         "e2e": {"value": round(f["e2e"], 3), "unit": UNIT, "h2d_bytes_per_step": f["e2e_bytes"][0],
-                "d2h_bytes_per_step": f["e2e_bytes"][1]},
+                "d2h_bytes_per_step": f["e2e_bytes"][1], "images_per_rank": f["e2e_images"]},
         "clocks": f["clocks"],
-        "fp32_mode": {"value": round(results["fp32"]["value"], 3), "unit": UNIT,
-                      "ms_per_step": round(results["fp32"]["ms"], 3), "steps": results["fp32"]["steps"],
-                      "e2e": round(results["fp32"]["e2e"], 3)},
     }
+    if "fp32" in results:
+        r32 = results["fp32"]
+        line["fp32_mode"] = {"value": round(r32["value"], 3), "unit": UNIT, "ms_per_step": round(r32["ms"], 3),
+                             "steps": r32["steps"], "e2e": round(r32["e2e"], 3)}
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        mp_s, sec, _ = cpu_reference(spec, 1, 1, args.cpu_sample, threads)
+        mp_s, secs = cpu_reference(spec, 1, 0, spec.batch, threads, budget_s=args.cpu_seconds)
+        n, dt = secs[0]
         line["cpu_baseline"] = {"value": round(mp_s, 5), "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": f"{args.cpu_sample} of {spec.batch} images, per-image forward, "
-                                          f"torch CPU fp32 oracle port, {threads} threads, median of 1 after 1 warm-up"}
+                                "sample": f"{n} of {spec.batch} images ({dt:.1f} s), one forward per image, "
+                                          f"torch CPU fp32 oracle port, {threads} threads"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -326,15 +376,19 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="2")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-sample", type=int, default=8, help="images per CPU baseline step")
-    ap.add_argument("--fp32-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample budget (s)")
+    ap.add_argument("--ref-step-seconds", type=float, default=4.0, help="--impl reference: seconds per step")
+    ap.add_argument("--fp32-steps", type=int, default=None, help="fp32-accurate mode steps (0 = skip)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-max-images", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps
     key = args.config if args.config == "5w" else int(args.config)
     spec = CONFIGS[key]
+    if args.fp32_steps is None:  # the CUDA-core fp32 mode takes ~0.1 s/MP: only on the small configs
+        args.fp32_steps = 3 if spec.batch * spec.height * spec.width <= (1 << 23) else 0
     if args.impl == "reference":
         run_reference(args, spec)
     else:
