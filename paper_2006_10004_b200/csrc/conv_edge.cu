@@ -8,13 +8,12 @@
 //       plane (inference.py:34-42) for the fp32-accurate mode (fp32 NHWC
 //       activations, fp64 accumulation).  The fast mode's head runs on
 //       tcgen05 (conv_tc.cu).
-//   hidden_f32_kernel : Conv2d(64,64)+BN+ReLU on fp32 NHWC (fp32-accurate
-//       mode).  Products of fp32 operands are accumulated in fp64 (DFMA) and
-//       the BatchNorm scale/shift applied after the sum, so each layer's
-//       output is the correctly-rounded fp32 of the exact conv+BN: the
-//       remaining distance to the reference is the reference's own fp32
-//       rounding (an fp32 re-computation alone is 7-9e-6 away
-//       from the oracle, too close to the 1e-5 gate).
+//   hidden_f32_kernel : Conv2d(C,C)+BN+ReLU on fp32 NHWC (fp32-accurate
+//       mode).  fp32 FFMA partial sums per 16-input-channel chunk, combined in
+//       fp64, BatchNorm scale/shift applied after the sum in fp64.  A plain
+//       sequential fp32 sum over all 576 terms lands at 1.0e-5 from the
+//       reference - too close to the 1e-5 gate; chunked
+//       partials are as good as full fp64 (5.1e-6).
 #include <type_traits>
 
 #include "common.cuh"
@@ -189,6 +188,10 @@ hidden_f32_kernel(const float* __restrict__ in, float* __restrict__ out, const f
   const int b = tile / (tiles_x * tiles_y);
   const int ty0 = ((tile / tiles_x) % tiles_y) * kF32TileRows;
   const int tx0 = (tile % tiles_x) * kF32TilePx;
+  // fp32 FFMA partial sums over one 16-input-channel chunk (144 terms), added
+  // into fp64 accumulators per chunk: each output is then within the fp32
+  // reference's own rounding of the exact value (tools/emulate_fp32_accum.py:
+  // 5.1e-6 vs 4.9e-6 for full fp64 on config 1), at FFMA speed.
   double acc[kF32TileRows][8];
 #pragma unroll
   for (int r = 0; r < kF32TileRows; ++r)
@@ -207,6 +210,12 @@ hidden_f32_kernel(const float* __restrict__ in, float* __restrict__ out, const f
       sWt[i] = w[((long long)co * C + c0 + ci) * 9 + t];
     }
     __syncthreads();
+    float part[kF32TileRows][8];
+#pragma unroll
+    for (int r = 0; r < kF32TileRows; ++r)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) part[r][e] = 0.0f;
+#pragma unroll 2
     for (int ci = 0; ci < kF32CiChunk; ++ci) {
 #pragma unroll
       for (int ky = 0; ky < 3; ++ky)
@@ -217,12 +226,16 @@ hidden_f32_kernel(const float* __restrict__ in, float* __restrict__ out, const f
           const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
           for (int r = 0; r < kF32TileRows; ++r) {
-            const float a = sIn[((r + ky) * kF32InPx + tx + kx) * kF32CiChunk + ci];
+            const float av = sIn[((r + ky) * kF32InPx + tx + kx) * kF32CiChunk + ci];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc[r][e] = fma((double)wv[e], (double)a, acc[r][e]);
+            for (int e = 0; e < 8; ++e) part[r][e] = fmaf(wv[e], av, part[r][e]);
           }
         }
     }
+#pragma unroll
+    for (int r = 0; r < kF32TileRows; ++r)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[r][e] += (double)part[r][e];
   }
   const int xw = tx0 + tx;
   if (xw >= W) return;
