@@ -79,6 +79,15 @@ struct tvs_plan {
   // activation ping-pong scratch
   void* act[2] = {nullptr, nullptr};
   size_t act_bytes = 0;
+  // concurrent L2-sized chunks (FAST path): stream s runs whole layer
+  // sequences of its chunks on its own ping-pong buffers, grids of num_sms/S
+  int n_streams = 1;                   // TVS_STREAMS (measured: >1 does not help on B200)
+  size_t l2_chunk_bytes = 16ull << 20; // TVS_L2_CHUNK_MB: activation bytes per chunk
+  std::vector<cudaStream_t> streams;
+  std::vector<void*> sact;             // 2 per stream
+  size_t sact_bytes = 0;
+  cudaEvent_t fork_ev = nullptr;
+  std::vector<cudaEvent_t> join_ev;
   // host-API staging
   float* dx = nullptr;  // [x | bands | closure] staging for tvs_forward_host
   size_t io_bytes = 0;
@@ -109,6 +118,15 @@ namespace {
 void ensure_device(const tvs_plan* p) { TVS_CUDA(cudaSetDevice(p->device)); }
 
 void free_all(tvs_plan* p) {
+  for (void* q : p->sact)
+    if (q) cudaFree(q);
+  p->sact.clear();
+  for (auto st : p->streams) cudaStreamDestroy(st);
+  p->streams.clear();
+  for (auto e : p->join_ev) cudaEventDestroy(e);
+  p->join_ev.clear();
+  if (p->fork_ev) cudaEventDestroy(p->fork_ev);
+  p->fork_ev = nullptr;
   for (auto& r : p->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : p->event_pool) cudaEventDestroy(e);
   p->recs.clear();
@@ -131,9 +149,30 @@ void ensure_act(tvs_plan* p, size_t bytes) {
 
 // one CTA per SM, but never fewer than ~3 output rows per CTA (short
 // segments pay two extra input rows each)
-int conv_grid(const tvs_plan* p, const tvs::ConvArgs& a) {
+void ensure_streams(tvs_plan* p, int ns, size_t bytes) {
+  if (!p->fork_ev) TVS_CUDA(cudaEventCreateWithFlags(&p->fork_ev, cudaEventDisableTiming));
+  while ((int)p->streams.size() < ns) {
+    cudaStream_t st;
+    TVS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    p->streams.push_back(st);
+    cudaEvent_t e;
+    TVS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->join_ev.push_back(e);
+  }
+  if (bytes > p->sact_bytes || (int)p->sact.size() < 2 * ns) {
+    TVS_CUDA(cudaDeviceSynchronize());  // buffers may be in use by earlier forwards
+    for (void* q : p->sact)
+      if (q) TVS_CUDA(cudaFree(q));
+    p->sact.assign(2 * p->streams.size(), nullptr);
+    const size_t nbytes = std::max(bytes, p->sact_bytes);
+    for (auto& q : p->sact) TVS_CUDA(cudaMalloc(&q, nbytes));
+    p->sact_bytes = nbytes;
+  }
+}
+
+int conv_grid(int max_ctas, const tvs::ConvArgs& a) {
   const long long total = (long long)a.B * a.strips * a.rows;
-  return (int)std::max(1LL, std::min<long long>(p->num_sms, (total + 2) / 3));
+  return (int)std::max(1LL, std::min<long long>(max_ctas, (total + 2) / 3));
 }
 
 cudaEvent_t pool_event(tvs_plan* p) {
@@ -178,22 +217,22 @@ void drain_profile(tvs_plan* p) {
 }
 
 void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B, int H, int W, int row0, int rows,
-               cudaStream_t st) {
+               cudaStream_t st, void* const* act, int max_ctas) {
   const bool fast = p->tc_path();
   const int C = p->channels;
   const double px = (double)B * H * W;
   // K1 (the FAST path fuses it into the first hidden layer's producer)
   if (!fast || p->unfused_conv0)
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
-                 [&] { return tvs::launch_conv0(fast, C, x, p->act[0], p->conv0, B, H, W, st); });
+                 [&] { return tvs::launch_conv0(fast, C, x, act[0], p->conv0, B, H, W, st); });
   // K2 x (depth-2), K3
   int cur = 0;
   if (fast) {
     const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
     CUtensorMap in_map[2], out_map[2];
     for (int i = 0; i < 2; ++i) {
-      in_map[i] = make_act_map(p->act[i], B, H, W, tvs::kHaloPx);
-      out_map[i] = make_act_map(p->act[i], B, H, W, 32);
+      in_map[i] = make_act_map(act[i], B, H, W, tvs::kHaloPx);
+      out_map[i] = make_act_map(act[i], B, H, W, 32);
     }
     auto geom = [&](int r0, int nrows) {
       tvs::ConvArgs a{};
@@ -209,7 +248,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.shift = p->bhid + (size_t)l * tvs::kC;
       a.nshift = tvs::kC;
       a.x = x;
-      const int grid = conv_grid(p, a);
+      const int grid = conv_grid(max_ctas, a);
       const bool first = fuse0 && l == 0;
       timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64 + (first ? px * 2.0 * 9 * 64 : 0.0), [&] {
         return tvs::launch_conv_tc(first ? 2 : 0, in_map[cur], out_map[cur ^ 1], a, first ? &p->conv0 : nullptr,
@@ -222,20 +261,20 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     a.shift = p->bh;
     a.nshift = p->out_bands;
     a.x = x; a.bands = bands; a.closure = closure; a.K = p->out_bands;
-    const int grid = conv_grid(p, a);
+    const int grid = conv_grid(max_ctas, a);
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands,
                  [&] { return tvs::launch_conv_tc(1, in_map[cur], in_map[cur], a, nullptr, grid, st); });
   } else {
     for (int l = 0; l < p->n_hidden(); ++l) {
       timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * C * C, [&] {
-        return tvs::launch_hidden_f32(C, (const float*)p->act[cur], (float*)p->act[cur ^ 1],
+        return tvs::launch_hidden_f32(C, (const float*)act[cur], (float*)act[cur ^ 1],
                                       p->whid + (size_t)l * C * C * 9, p->shid + (size_t)l * C,
                                       p->bhid + (size_t)l * C, B, H, W, st);
       });
       cur ^= 1;
     }
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * C * p->out_bands, [&] {
-      return tvs::launch_head_f32(C, (const float*)p->act[cur], x, p->wh, p->bh, bands, closure, B, H, W, p->out_bands,
+      return tvs::launch_head_f32(C, (const float*)act[cur], x, p->wh, p->bh, bands, closure, B, H, W, p->out_bands,
                                   row0, rows, st);
     });
   }
@@ -252,14 +291,36 @@ void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int
   if (B == 0) return;
   ensure_device(p);
   const size_t per_img = (size_t)H * W * p->act_px_bytes();
+  const size_t in_img = (size_t)H * W, out_img = (size_t)rows * W;
+  // concurrent L2-resident chunks: only when an image fits the chunk budget
+  const int S = p->tc_path() ? std::min(p->n_streams, B) : 1;
+  if (S > 1 && per_img <= p->l2_chunk_bytes) {
+    const int cb = (int)std::min<size_t>((size_t)B, std::max<size_t>(1, p->l2_chunk_bytes / per_img));
+    const int nchunks = (B + cb - 1) / cb;
+    const int ns = std::min(S, nchunks);
+    ensure_streams(p, ns, per_img * cb);
+    TVS_CUDA(cudaEventRecord(p->fork_ev, st));
+    for (int s = 0; s < ns; ++s) TVS_CUDA(cudaStreamWaitEvent(p->streams[s], p->fork_ev, 0));
+    const int max_ctas = std::max(1, p->num_sms / ns);
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % ns, b0 = c * cb, nb = std::min(cb, B - b0);
+      run_chunk(p, x + b0 * in_img, bands + (size_t)b0 * p->out_bands * out_img,
+                closure ? closure + b0 * out_img : nullptr, nb, H, W, row0, rows, p->streams[s], &p->sact[2 * s],
+                max_ctas);
+    }
+    for (int s = 0; s < ns; ++s) {
+      TVS_CUDA(cudaEventRecord(p->join_ev[s], p->streams[s]));
+      TVS_CUDA(cudaStreamWaitEvent(st, p->join_ev[s], 0));
+    }
+    return;
+  }
   int cb = (int)std::max<size_t>(1, p->chunk_budget / std::max<size_t>(per_img, 1));
   cb = std::min(cb, B);
   ensure_act(p, per_img * cb);
-  const size_t in_img = (size_t)H * W, out_img = (size_t)rows * W;
   for (int b0 = 0; b0 < B; b0 += cb) {
     const int nb = std::min(cb, B - b0);
     run_chunk(p, x + b0 * in_img, bands + (size_t)b0 * p->out_bands * out_img,
-              closure ? closure + b0 * out_img : nullptr, nb, H, W, row0, rows, st);
+              closure ? closure + b0 * out_img : nullptr, nb, H, W, row0, rows, st, p->act, p->num_sms);
   }
 }
 
@@ -309,6 +370,8 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
     p->device = device; p->depth = depth; p->channels = channels; p->out_bands = out_bands; p->mode = mode;
     p->num_sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("TVS_CHUNK_MB")) p->chunk_budget = (size_t)std::atoll(e) << 20;
+    if (const char* e = std::getenv("TVS_STREAMS")) p->n_streams = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("TVS_L2_CHUNK_MB")) p->l2_chunk_bytes = (size_t)std::atoll(e) << 20;
     if (const char* e = std::getenv("TVS_FUSE_CONV0")) p->unfused_conv0 = std::atoi(e) == 0;
     try {
       TVS_CUDA(tvs::configure_kernels());
