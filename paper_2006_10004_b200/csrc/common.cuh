@@ -25,6 +25,7 @@ struct ConvArgs {
   int B, H, W;
   int strips;            // ceil(W / 128)
   int row0, rows;        // output rows computed: [row0, row0 + rows)
+  int reverse, nsub;     // visit each CTA's range as nsub sub-ranges, last first
   const uint8_t* wpack;  // packed fp16 B operand (SW128)
   const float* shift;    // per output channel (hidden: beta - mu*s; head: conv bias)
   int nshift;

@@ -44,14 +44,29 @@ struct Segment {
   int b, x0, ya, yb;
 };
 struct SegIter {
-  long long cur, end;
+  // [cur, end) of the current sub-range; sub-ranges are visited last-first
+  // when a.reverse is set, so a layer first reads the rows the previous layer
+  // wrote last (those are still L2-resident).
+  long long lo, hi, cur, end;
+  int sub, nsub;
   TVS_DEV SegIter(const ConvArgs& a) {
     const long long T = (long long)a.B * a.strips * a.rows;
-    cur = T * blockIdx.x / gridDim.x;
-    end = T * (blockIdx.x + 1) / gridDim.x;
+    lo = T * blockIdx.x / gridDim.x;
+    hi = T * (blockIdx.x + 1) / gridDim.x;
+    nsub = a.reverse ? a.nsub : 1;
+    sub = 0;
+    set_sub();
+  }
+  TVS_DEV void set_sub() {
+    const int k = nsub - 1 - sub;  // reverse order
+    cur = lo + (hi - lo) * k / nsub;
+    end = lo + (hi - lo) * (k + 1) / nsub;
   }
   TVS_DEV bool next(const ConvArgs& a, Segment& g) {
-    if (cur >= end) return false;
+    while (cur >= end) {
+      if (++sub >= nsub) return false;
+      set_sub();
+    }
     const long long col = cur / a.rows;
     const int y0 = (int)(cur - col * a.rows);
     const int n = (int)min((long long)(a.rows - y0), end - cur);

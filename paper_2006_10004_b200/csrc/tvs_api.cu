@@ -81,6 +81,7 @@ struct tvs_plan {
   size_t act_bytes = 0;
   // concurrent L2-sized chunks (FAST path): stream s runs whole layer
   // sequences of its chunks on its own ping-pong buffers, grids of num_sms/S
+  int l2_reverse_sub = 1;              // TVS_REVERSE_SUB: odd layers visit sub-ranges last-first (measured: no gain)
   int n_streams = 1;                   // TVS_STREAMS (measured: >1 does not help on B200)
   size_t l2_chunk_bytes = 16ull << 20; // TVS_L2_CHUNK_MB: activation bytes per chunk
   std::vector<cudaStream_t> streams;
@@ -250,6 +251,8 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.x = x;
       const int grid = conv_grid(max_ctas, a);
       const bool first = fuse0 && l == 0;
+      a.reverse = (p->l2_reverse_sub > 1) && (l & 1);
+      a.nsub = p->l2_reverse_sub;
       timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64 + (first ? px * 2.0 * 9 * 64 : 0.0), [&] {
         return tvs::launch_conv_tc(first ? 2 : 0, in_map[cur], out_map[cur ^ 1], a, first ? &p->conv0 : nullptr,
                                    grid, st);
@@ -261,6 +264,8 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     a.shift = p->bh;
     a.nshift = p->out_bands;
     a.x = x; a.bands = bands; a.closure = closure; a.K = p->out_bands;
+    a.reverse = (p->l2_reverse_sub > 1) && (p->n_hidden() & 1);
+    a.nsub = p->l2_reverse_sub;
     const int grid = conv_grid(max_ctas, a);
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands,
                  [&] { return tvs::launch_conv_tc(1, in_map[cur], in_map[cur], a, nullptr, grid, st); });
@@ -371,6 +376,7 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
     p->num_sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("TVS_CHUNK_MB")) p->chunk_budget = (size_t)std::atoll(e) << 20;
     if (const char* e = std::getenv("TVS_STREAMS")) p->n_streams = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("TVS_REVERSE_SUB")) p->l2_reverse_sub = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("TVS_L2_CHUNK_MB")) p->l2_chunk_bytes = (size_t)std::atoll(e) << 20;
     if (const char* e = std::getenv("TVS_FUSE_CONV0")) p->unfused_conv0 = std::atoi(e) == 0;
     try {

@@ -89,6 +89,17 @@ def main():
     x = rng.standard_normal((1, 1, 9, 11)).astype(np.float32)
     out["d3_x"], out["d3_y"] = x, d3(torch.from_numpy(x)).numpy()
 
+    # a BTF file written by the reference writer (tensorfile.py:51-59), byte for byte
+    import tempfile
+
+    from tvsurrogate.tensorfile import write_tensor as ref_write
+
+    with tempfile.TemporaryDirectory() as td:
+        arr = np.random.default_rng(11).standard_normal((3, 5, 7))
+        ref_write(Path(td) / "t.btf", arr)
+        out["btf_array"] = arr
+        out["btf_bytes"] = np.frombuffer((Path(td) / "t.btf").read_bytes(), dtype=np.uint8)
+
     out["torch_version"] = np.array(torch.__version__)
     np.savez_compressed(HERE / "golden.npz", **out)
     print("wrote", HERE / "golden.npz", sorted(out))
