@@ -89,6 +89,22 @@ int tvs_profile_read(tvs_plan* plan, int kind, double* total_ms, long long* laun
 
 int tvs_plan_destroy(tvs_plan* plan);
 
+/* Band scoring statistics (spectv metrics.py:28-237), fp64.
+ * gt, pred: DEVICE (planes, H, W) fp32.  stats: DEVICE planes x 8 doubles:
+ *   [0] sum (gt - pred)^2           -> PSNR / MSE   (metrics.py:28-37)
+ *   [1] sLMSE numerator, [2] denominator: sums over 16x16 patches at stride 8
+ *       (+ clipped tail patch) of (gt-pred)^2 and pred^2   (metrics.py:126-150)
+ *   [3] gt max, [4] gt min           -> data range      (metrics.py:222-225)
+ *   [5] sum of the 11x11 Gaussian SSIM map over the interior, [6] interior
+ *       pixel count                  -> windowed SSIM   (metrics.py:61-112)
+ *   [7] unused
+ * range_or_null: DEVICE planes doubles = SSIM data range per plane (ssim(...,
+ * data_range), metrics.py:61); NULL = each gt plane's own floored range
+ * (band_metrics convention).  Replaces the per-plane numpy loop of
+ * band_metrics (metrics.py:211-237). */
+int tvs_band_stats(const float* gt, const float* pred, int planes, int H, int W, const double* range_or_null,
+                   double* stats, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

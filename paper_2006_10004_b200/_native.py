@@ -32,6 +32,7 @@ EXPORTS = (
     "tvs_profile_enable",
     "tvs_profile_read",
     "tvs_plan_destroy",
+    "tvs_band_stats",
 )
 
 _lock = threading.Lock()
@@ -77,6 +78,8 @@ def load() -> ctypes.CDLL:
         lib.tvs_profile_read.restype = i
         lib.tvs_profile_read.argtypes = [P, i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong),
                                          ctypes.POINTER(ctypes.c_double)]
+        lib.tvs_band_stats.restype = i
+        lib.tvs_band_stats.argtypes = [P, P, i, i, i, P, P, P]
         lib.tvs_plan_destroy.restype = i
         lib.tvs_plan_destroy.argtypes = [P]
         _lib = lib

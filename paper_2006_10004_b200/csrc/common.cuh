@@ -62,5 +62,8 @@ cudaError_t launch_head_f32(int C, const float* act, const float* x, const float
 cudaError_t launch_hidden_f32(int C, const float* in, float* out, const float* w, const float* scale,
                               const float* shift, int B, int H, int W, cudaStream_t st);
 cudaError_t configure_kernels();  // one-time smem opt-ins
+// metrics.cu: per-plane scoring statistics (8 doubles per plane)
+cudaError_t launch_band_stats(const float* gt, const float* pred, int planes, int H, int W,
+                              const double* range_override, double* stats, cudaStream_t st);
 
 }  // namespace tvs

@@ -499,6 +499,16 @@ int tvs_profile_read(tvs_plan* p, int kind, double* total_ms, long long* launche
   });
 }
 
+int tvs_band_stats(const float* gt, const float* pred, int planes, int H, int W, const double* range_or_null,
+                   double* stats, void* stream) {
+  return guarded([&] {
+    if (!gt || !pred || !stats) throw TvsError(TVS_E_INVALID, "null pointer");
+    if (planes < 0 || H < 1 || W < 1) throw TvsError(TVS_E_INVALID, "bad shape");
+    if (planes == 0) return;
+    TVS_CUDA(tvs::launch_band_stats(gt, pred, planes, H, W, range_or_null, stats, (cudaStream_t)stream));
+  });
+}
+
 int tvs_plan_destroy(tvs_plan* p) {
   return guarded([&] {
     if (!p) return;

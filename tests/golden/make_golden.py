@@ -100,6 +100,25 @@ def main():
         out["btf_array"] = arr
         out["btf_bytes"] = np.frombuffer((Path(td) / "t.btf").read_bytes(), dtype=np.uint8)
 
+    # band scoring cases from the REFERENCE producer metrics (spectv/metrics.py:211-237)
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from spectv.metrics import band_metrics as ref_band_metrics
+
+    mrng = np.random.default_rng(5)
+    gt = mrng.standard_normal((5, 40, 57)).astype(np.float32)
+    cases = {
+        "noisy": (gt, (gt + 0.1 * mrng.standard_normal(gt.shape)).astype(np.float32)),
+        "exact": (gt, gt.copy()),
+        "zero_pred": (gt, np.zeros_like(gt)),
+        "const_gt": (np.full((2, 24, 24), 0.5, np.float32), mrng.random((2, 24, 24)).astype(np.float32)),
+        "square_aligned": (mrng.random((3, 64, 64)).astype(np.float32), mrng.random((3, 64, 64)).astype(np.float32)),
+    }
+    for name, (g, p) in cases.items():
+        rep = ref_band_metrics(g, p)
+        out[f"metrics_{name}_gt"], out[f"metrics_{name}_pred"] = g, p
+        out[f"metrics_{name}_per_band"] = np.array(rep.per_band, dtype=np.float64)
+        out[f"metrics_{name}_max_i"] = np.array(rep.max_i, dtype=np.float64)
+
     out["torch_version"] = np.array(torch.__version__)
     np.savez_compressed(HERE / "golden.npz", **out)
     print("wrote", HERE / "golden.npz", sorted(out))
