@@ -105,6 +105,29 @@ int tvs_plan_destroy(tvs_plan* plan);
 int tvs_band_stats(const float* gt, const float* pred, int planes, int H, int W, const double* range_or_null,
                    double* stats, void* stream);
 
+/* Model-driven TV-flow decomposition: the ground-truth producer (SURVEY §8(f)
+ * row 3).  Replaces ModelDrivenDecomposer.analyze (spectv pipeline.py:105-145)
+ * with rof_prox's accelerated primal-dual solver (solver.py:242-372): fp64,
+ * reference operation order, one persistent CTA per image.
+ *   f          DEVICE (N, H, W) fp64 finite images, W <= 2048
+ *   schedule   HOST n_bands (<= 16) inclusive band end indices on the fine grid
+ *              1..n_steps-1, strictly increasing, last == n_steps-1
+ *              (transform.py:131-144, dyadic_schedule :186-207)
+ *   solver     max_iters >= 1, gap_tol > 0, pd_tau*pd_sigma*8 <= 1, pd_accel
+ *              0/1 (SolverConfig, solver.py:54-90; method primal-dual only)
+ *   workspace  DEVICE, >= tvs_tvflow_workspace_bytes(N, H, W)
+ *   bands      DEVICE (N, n_bands, H, W) fp64, last band includes the residual
+ *   spectrum   DEVICE (N, n_steps-1) fp64: S(t_i) = sum |phi_i|
+ *   residual   DEVICE (N, H, W) fp64: f_r = u_N - N (u_N - u_{N-1})
+ *   iters      DEVICE (N, n_steps) int32: prox iterations of each flow step,
+ *              stored as -(iters+1) when the gap tolerance was not certified
+ *              (the reference's `warnings` list, pipeline.py:116-127). */
+size_t tvs_tvflow_workspace_bytes(int N, int H, int W);
+int tvs_tvflow_analyze(const double* f, int N, int H, int W, double dt, int n_steps, const int* schedule,
+                       int n_bands, int max_iters, double gap_tol, double pd_tau, double pd_sigma, int pd_accel,
+                       void* workspace, double* bands, double* spectrum, double* residual, int* iters,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,6 +33,8 @@ EXPORTS = (
     "tvs_profile_read",
     "tvs_plan_destroy",
     "tvs_band_stats",
+    "tvs_tvflow_workspace_bytes",
+    "tvs_tvflow_analyze",
 )
 
 _lock = threading.Lock()
@@ -80,6 +82,11 @@ def load() -> ctypes.CDLL:
                                          ctypes.POINTER(ctypes.c_double)]
         lib.tvs_band_stats.restype = i
         lib.tvs_band_stats.argtypes = [P, P, i, i, i, P, P, P]
+        lib.tvs_tvflow_workspace_bytes.restype = ctypes.c_size_t
+        lib.tvs_tvflow_workspace_bytes.argtypes = [i, i, i]
+        d = ctypes.c_double
+        lib.tvs_tvflow_analyze.restype = i
+        lib.tvs_tvflow_analyze.argtypes = [P, i, i, i, d, i, P, i, i, d, d, d, i, P, P, P, P, P, P]
         lib.tvs_plan_destroy.restype = i
         lib.tvs_plan_destroy.argtypes = [P]
         _lib = lib

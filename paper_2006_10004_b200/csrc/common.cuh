@@ -65,5 +65,23 @@ cudaError_t configure_kernels();  // one-time smem opt-ins
 // metrics.cu: per-plane scoring statistics (8 doubles per plane)
 cudaError_t launch_band_stats(const float* gt, const float* pred, int planes, int H, int W,
                               const double* range_override, double* stats, cudaStream_t st);
+// tvflow.cu: model-driven TV-flow decomposition (ground-truth producer)
+constexpr int kTvMaxW = 2048;
+constexpr int kTvMaxBands = 16;
+struct TvFlowArgs {
+  int N, H, W;
+  double dt;
+  int n_steps, n_bands;
+  int schedule[kTvMaxBands];  // inclusive band end indices on the fine grid 1..n_steps-1
+  int max_iters, accel;
+  double gap_tol, tau0, sigma0;
+  const double* f;   // (N, H, W)
+  double* work;      // (N, 6, H, W): three rotating flow states, vbar, qx, qy
+  double* bands;     // (N, n_bands, H, W)
+  double* spectrum;  // (N, n_steps-1)
+  double* residual;  // (N, H, W)
+  int* iters;        // (N, n_steps), -(iters+1) when not certified
+};
+cudaError_t launch_tvflow(const TvFlowArgs& a, cudaStream_t st);
 
 }  // namespace tvs

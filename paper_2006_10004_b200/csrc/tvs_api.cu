@@ -509,6 +509,57 @@ int tvs_band_stats(const float* gt, const float* pred, int planes, int H, int W,
   });
 }
 
+size_t tvs_tvflow_workspace_bytes(int N, int H, int W) {
+  if (N < 0 || H < 1 || W < 1) return 0;
+  return (size_t)N * 6 * (size_t)H * (size_t)W * sizeof(double);
+}
+
+int tvs_tvflow_analyze(const double* f, int N, int H, int W, double dt, int n_steps, const int* schedule,
+                       int n_bands, int max_iters, double gap_tol, double pd_tau, double pd_sigma, int pd_accel,
+                       void* workspace, double* bands, double* spectrum, double* residual, int* iters,
+                       void* stream) {
+  return guarded([&] {
+    if (!f || !schedule || !workspace || !bands || !spectrum || !residual || !iters)
+      throw TvsError(TVS_E_INVALID, "null pointer");
+    if (N < 0 || H < 1 || W < 1) throw TvsError(TVS_E_INVALID, "bad shape");
+    if (W > tvs::kTvMaxW) throw TvsError(TVS_E_INVALID, "image width exceeds 2048");
+    if (!(dt > 0)) throw TvsError(TVS_E_INVALID, "dt must be positive");
+    if (n_steps < 2) throw TvsError(TVS_E_INVALID, "n_steps must be >= 2");
+    if (n_bands < 1 || n_bands > tvs::kTvMaxBands) throw TvsError(TVS_E_INVALID, "n_bands must lie in [1, 16]");
+    int prev = 0;
+    for (int b = 0; b < n_bands; ++b) {
+      if (schedule[b] <= prev) throw TvsError(TVS_E_INVALID, "schedule indices must be strictly increasing");
+      prev = schedule[b];
+    }
+    if (prev != n_steps - 1) throw TvsError(TVS_E_INVALID, "schedule must end at n_steps - 1");
+    if (max_iters < 1) throw TvsError(TVS_E_INVALID, "max_iters must be >= 1");
+    if (!(gap_tol > 0)) throw TvsError(TVS_E_INVALID, "gap_tol must be positive");
+    if (!(pd_tau > 0) || !(pd_sigma > 0)) throw TvsError(TVS_E_INVALID, "primal-dual steps must be positive");
+    if (pd_tau * pd_sigma * 8.0 > 1.0 + 1e-12) throw TvsError(TVS_E_INVALID, "pd_step_tau * pd_step_sigma * 8 must be <= 1");
+    if (N == 0) return;
+    tvs::TvFlowArgs a{};
+    a.N = N;
+    a.H = H;
+    a.W = W;
+    a.dt = dt;
+    a.n_steps = n_steps;
+    a.n_bands = n_bands;
+    for (int b = 0; b < n_bands; ++b) a.schedule[b] = schedule[b];
+    a.max_iters = max_iters;
+    a.accel = pd_accel ? 1 : 0;
+    a.gap_tol = gap_tol;
+    a.tau0 = pd_tau;
+    a.sigma0 = pd_sigma;
+    a.f = f;
+    a.work = (double*)workspace;
+    a.bands = bands;
+    a.spectrum = spectrum;
+    a.residual = residual;
+    a.iters = iters;
+    TVS_CUDA(tvs::launch_tvflow(a, (cudaStream_t)stream));
+  });
+}
+
 int tvs_plan_destroy(tvs_plan* p) {
   return guarded([&] {
     if (!p) return;

@@ -1,0 +1,146 @@
+"""GPU parity of the ground-truth producer (csrc/tvflow.cu via
+tvs_tvflow_analyze) against outputs of the REFERENCE decomposer
+(tests/golden/golden_tvflow.npz, spectv pipeline.py:105-145) and the oracle.
+
+The kernel replays the reference's fp64 iterate sequence operation by
+operation; only the gap-certificate sums are reduced in another order, so a
+stop/restart decision may in rare cases move by one 10-iteration check.
+Tolerances below are therefore stated against the solver's own certificate:
+gap_tol = 1e-6 relative bounds ||v - v*|| per prox, and the parity gate is a
+relative max error of 1e-6 on bands/spectrum (observed: bitwise or ~1e-13).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["gauss", "disk", "const", "row", "col", "cap", "noaccel", "wide", "tol"]
+TOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def golden_tv():
+    from pathlib import Path
+
+    return np.load(Path(__file__).parent / "golden" / "golden_tvflow.npz")
+
+
+def _cfg(g, name):
+    from paper_2006_10004_b200.producer import DecompositionConfig, SolverConfig
+
+    dt, n = g[f"{name}_meta"]
+    mi, tol, acc = g[f"{name}_solver"]
+    return DecompositionConfig(dt=float(dt), n_steps=int(n), schedule=tuple(int(e) for e in g[f"{name}_schedule"]),
+                               solver=SolverConfig(max_iters=int(mi), gap_tol=float(tol), pd_accel=bool(acc)))
+
+
+def _rel(a, b, atol=1e-12):
+    """max |a-b| / max|b|, with an absolute floor for all-but-zero fixtures
+    (a constant image's mean differs from numpy's pairwise mean by an ulp)."""
+    d = float(np.abs(a - b).max()) if a.size else 0.0
+    s = float(np.abs(b).max()) if b.size else 0.0
+    return 0.0 if d <= atol else d / max(s, 1e-300)
+
+
+@pytest.fixture(params=["cluster", "global"])
+def kernel(request, monkeypatch):
+    """Both device kernels: shared-memory/cluster resident and the global row sweep."""
+    if request.param == "global":
+        monkeypatch.setenv("TVS_TVFLOW_KERNEL", "global")
+    else:
+        monkeypatch.delenv("TVS_TVFLOW_KERNEL", raising=False)
+    return request.param
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_producer_matches_reference(golden_tv, name, kernel):
+    from paper_2006_10004_b200.producer import ModelDrivenDecomposer
+
+    cfg = _cfg(golden_tv, name)
+    r = ModelDrivenDecomposer(cfg).analyze(golden_tv[f"{name}_f"])
+    assert r.bands.bands.shape == golden_tv[f"{name}_bands"].shape
+    assert _rel(r.bands.bands, golden_tv[f"{name}_bands"]) <= TOL
+    assert _rel(r.spectrum.values, golden_tv[f"{name}_spectrum"]) <= TOL
+    assert _rel(r.residual, golden_tv[f"{name}_residual"]) <= TOL
+    ref_it = golden_tv[f"{name}_iterations"]
+    # iteration counts: identical except where a gap check lands within rounding
+    # of gap_tol (the sums are reduced in another order); the flow states then
+    # still agree to the certified tolerance (asserted above)
+    assert np.mean(r.iterations == ref_it) >= 0.8, (r.iterations, ref_it)
+    if np.array_equal(r.iterations, ref_it):
+        assert r.warnings == [int(w) for w in golden_tv[f"{name}_warnings"]]
+    np.testing.assert_allclose(r.spectrum.scales, cfg.dt * np.arange(1, cfg.n_steps))
+
+
+def test_batch_equals_single(golden_tv, kernel):
+    """One launch over a stack == per-image launches, bitwise (images are independent CTAs)."""
+    from paper_2006_10004_b200.producer import DecompositionConfig, ModelDrivenDecomposer
+
+    rng = np.random.default_rng(3)
+    f = rng.standard_normal((5, 18, 22))
+    dec = ModelDrivenDecomposer(DecompositionConfig(dt=0.2, n_steps=14, schedule=(2, 6, 13)))
+    batch = dec.analyze_batch(f)
+    for n in range(5):
+        single = dec.analyze(f[n])
+        assert np.array_equal(batch[n].bands.bands, single.bands.bands)
+        assert np.array_equal(batch[n].spectrum.values, single.spectrum.values)
+
+
+def test_reconstruction_and_mean_large(kernel):
+    """Size-independent properties at a production size (256x256, 20 steps):
+    bands telescope to the input (transform.py:1-14, Abel summation) and every
+    prox preserves the mean."""
+    from paper_2006_10004_b200.producer import DecompositionConfig, ModelDrivenDecomposer, SolverConfig
+
+    rng = np.random.default_rng(4)
+    f = rng.standard_normal((2, 256, 256))
+    dec = ModelDrivenDecomposer(DecompositionConfig(dt=0.2, n_steps=20, schedule=(2, 4, 8, 19),
+                                                    solver=SolverConfig(max_iters=300)))
+    out = dec.analyze_batch_device(torch.from_numpy(f))
+    recon = out.bands.sum(dim=1).cpu().numpy()
+    assert np.abs(recon - f).max() <= 1e-9 * np.abs(f).max()
+    assert torch.all(out.iterations != 0)
+    assert torch.isfinite(out.spectrum).all() and (out.spectrum >= 0).all()
+
+
+def test_oracle_agrees_off_golden():
+    """A seeded case outside the fixtures, GPU vs the oracle restatement."""
+    import oracle.tvflow_oracle as O
+    from paper_2006_10004_b200.producer import DecompositionConfig, ModelDrivenDecomposer
+
+    rng = np.random.default_rng(8)
+    f = np.cumsum(rng.standard_normal((14, 19)), axis=1) * 0.3
+    ref = O.analyze(f, dt=0.2, n_steps=15, schedule=(2, 4, 8, 14))
+    r = ModelDrivenDecomposer(DecompositionConfig(dt=0.2, n_steps=15, schedule=(2, 4, 8, 14))).analyze(f)
+    assert _rel(r.bands.bands, ref["bands"]) <= TOL
+    assert np.mean(r.iterations == ref["iterations"]) >= 0.8
+
+
+def test_rejects_bad_input():
+    from paper_2006_10004_b200.producer import ModelDrivenDecomposer
+
+    dec = ModelDrivenDecomposer()
+    with pytest.raises(ValueError):
+        dec.analyze(np.full((4, 4), np.nan))
+    with pytest.raises(ValueError):
+        dec.analyze(np.zeros((2, 3, 4)))
+    with pytest.raises(ValueError):
+        dec.analyze(np.zeros((4, 2049)))
+
+
+@pytest.mark.parametrize("shape", [(40, 40), (64, 100), (160, 160), (256, 200), (300, 64)])
+def test_cluster_partitions_vs_oracle(shape):
+    """Shapes that need 1, 2, 8 and 16 CTAs per image in the shared-memory
+    kernel (rows split across the cluster, halos over DSMEM), vs the oracle."""
+    import oracle.tvflow_oracle as O
+    from paper_2006_10004_b200.producer import DecompositionConfig, ModelDrivenDecomposer, SolverConfig
+
+    rng = np.random.default_rng(shape[0] * 1000 + shape[1])
+    f = rng.standard_normal(shape)
+    kw = dict(dt=0.2, n_steps=3, schedule=(1, 2))
+    ref = O.analyze(f, max_iters=150, **kw)
+    r = ModelDrivenDecomposer(DecompositionConfig(**kw, solver=SolverConfig(max_iters=150))).analyze(f)
+    assert _rel(r.bands.bands, ref["bands"]) <= TOL
+    assert _rel(r.spectrum.values, ref["spectrum"]) <= TOL
