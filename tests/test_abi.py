@@ -10,7 +10,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def _declared():
     text = (ROOT / "include" / "tvs_b200.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(tvs_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(tvs_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_declares_expected_api():
