@@ -56,6 +56,30 @@ __device__ __forceinline__ double block_sum_d(double v, double* red) {
   return t;  // valid in every lane of every warp
 }
 
+// a / b for b > 0 with rb = RN(1/b): q = RN(a rb) is within 1 ulp of a/b and
+// one FMA correction makes it the correctly rounded quotient (Markstein's
+// theorem; no over/underflow in this range), i.e. bitwise equal to a / b.
+__device__ __forceinline__ double div_recip(double a, double b, double rb) {
+  const double q = __dmul_rn(a, rb);
+  const double r = __fma_rn(-q, b, a);
+  return __fma_rn(r, rb, q);
+}
+
+// Dual projection of solver.py:278-282: scale = max(|q|/dt, 1); q /= scale.
+// |q| is evaluated as the correctly rounded sqrt of RN(qx^2 + qy^2) (within
+// an ulp of libm's hypot); pairs provably inside the ball keep scale == 1
+// exactly and skip the (then exact) unit division.
+__device__ __forceinline__ void project_ball(double& px, double& py, double dt, double rdt, double dt2_lo) {
+  const double s2 = __dadd_rn(__dmul_rn(px, px), __dmul_rn(py, py));
+  if (s2 < dt2_lo) return;
+  const double sc = fmax(div_recip(__dsqrt_rn(s2), dt, rdt), 1.0);
+  if (sc != 1.0) {
+    const double r = __drcp_rn(sc);
+    px = div_recip(px, sc, r);
+    py = div_recip(py, sc, r);
+  }
+}
+
 __device__ __forceinline__ double relative_gap(double primal, double dual, double floor_) {
   return __ddiv_rn(__dsub_rn(primal, dual), fmax(fmax(fabs(primal), fabs(dual)), floor_));
 }
@@ -73,6 +97,8 @@ __global__ void __launch_bounds__(kTvThreads) tvflow_kernel(const TvFlowArgs a) 
   double* qy = wk + 5 * plane;
   double* bands = a.bands + (long long)img * a.n_bands * plane;
   const double dt = a.dt;
+  const double rdt = __drcp_rn(dt);
+  const double dt2_lo = dt * dt * (1.0 - 1e-12);
   const int tid = threadIdx.x;
 
   // u_prev = f ; zero bands ; dual = 0
@@ -131,6 +157,8 @@ __global__ void __launch_bounds__(kTvThreads) tvflow_kernel(const TvFlowArgs a) 
         const int n_inner = min(10, a.max_iters - iters);
         for (int it = 0; it < n_inner; ++it) {
           const double th = a.accel ? 1.0 / sqrt(__dadd_rn(1.0, __dmul_rn(2.0, tau))) : theta;
+          const double opt = __dadd_rn(1.0, tau);
+          const double ropt = __drcp_rn(opt);
           double qy_prev[kTvMaxCols];
           for (int y = 0; y < H; ++y) {
             const long long ro = (long long)y * W;
@@ -144,9 +172,7 @@ __global__ void __launch_bounds__(kTvThreads) tvflow_kernel(const TvFlowArgs a) 
               if (x < W - 1) gx = __dmul_rn(__dsub_rn(vbar[ro + x + 1], vb), sigma);
               if (y < H - 1) gy = __dmul_rn(__dsub_rn(vbar[ro + W + x], vb), sigma);
               double px = __dadd_rn(qx[ro + x], gx), py = __dadd_rn(qy[ro + x], gy);
-              const double sc = fmax(__ddiv_rn(hypot(px, py), dt), 1.0);
-              px = __ddiv_rn(px, sc);
-              py = __ddiv_rn(py, sc);
+              project_ball(px, py, dt, rdt, dt2_lo);
               qxn[k] = px;
               qyn[k] = py;
               s_row[x] = px;
@@ -171,7 +197,7 @@ __global__ void __launch_bounds__(kTvThreads) tvflow_kernel(const TvFlowArgs a) 
                 else dq = __dsub_rn(__dadd_rn(dq, qyn[k]), qy_prev[k]);
               }
               const double vo = v[ro + x];
-              const double vn = __ddiv_rn(__dadd_rn(__dmul_rn(dq, tau), vo), __dadd_rn(1.0, tau));
+              const double vn = div_recip(__dadd_rn(__dmul_rn(dq, tau), vo), opt, ropt);
               const double vbn = __dadd_rn(__dmul_rn(__dsub_rn(vn, vo), th), vn);
               qx[ro + x] = qxn[k];
               qy[ro + x] = qyn[k];
@@ -238,8 +264,8 @@ __global__ void __launch_bounds__(kTvThreads) tvflow_kernel(const TvFlowArgs a) 
       // warm start for the next prox: dual_field = c*q/dt (solver.py:320), which
       // rof_prox multiplies back by dt (:369-371) — rounded exactly that way
       for (long long i = tid; i < plane; i += blockDim.x) {
-        qx[i] = __dmul_rn(__ddiv_rn(__dmul_rn(c, qx[i]), dt), dt);
-        qy[i] = __dmul_rn(__ddiv_rn(__dmul_rn(c, qy[i]), dt), dt);
+        qx[i] = __dmul_rn(div_recip(__dmul_rn(c, qx[i]), dt, rdt), dt);
+        qy[i] = __dmul_rn(div_recip(__dmul_rn(c, qy[i]), dt, rdt), dt);
       }
       __syncthreads();
     }
@@ -253,7 +279,7 @@ __global__ void __launch_bounds__(kTvThreads) tvflow_kernel(const TvFlowArgs a) 
       double s_abs = 0.0;
       for (long long k = tid; k < plane; k += blockDim.x) {
         const double t = __dadd_rn(__dsub_rn(v[k], __dmul_rn(2.0, u[k])), up[k]);
-        const double phi = __ddiv_rn(__dmul_rn((double)i, t), dt);
+        const double phi = div_recip(__dmul_rn((double)i, t), dt, rdt);
         band[k] = __dadd_rn(band[k], phi);
         s_abs = __dadd_rn(s_abs, fabs(phi));
       }
@@ -320,20 +346,15 @@ __device__ __forceinline__ void cluster_sum(double (&v)[K], double* red, double*
   for (int k = 0; k < K; ++k) v[k] = bcast[k];
 }
 
-// x / max(hypot(x, y)/dt, 1) for both components, skipping the (exact) unit
-// division when the pair is provably inside the ball of radius dt.
-__device__ __forceinline__ void project_ball(double& px, double& py, double dt, double dt2_lo) {
-  const double s2 = __dadd_rn(__dmul_rn(px, px), __dmul_rn(py, py));
-  if (s2 < dt2_lo) return;
-  const double sc = fmax(__ddiv_rn(hypot(px, py), dt), 1.0);
-  if (sc != 1.0) {
-    px = __ddiv_rn(px, sc);
-    py = __ddiv_rn(py, sc);
-  }
-}
+// Per-thread pixel geometry, fixed for the whole launch.
+constexpr int kTcPix = 4;  // pixels per thread: a CTA holds at most kTcPix * kTcThreads pixels
+constexpr int kTcMaxPx = kTcPix * kTcThreads;  // plane stride in shared memory (5 fp64 planes = 160 KB)
+constexpr int kPU = 0, kPV = kTcMaxPx, kPVB = 2 * kTcMaxPx, kPQX = 3 * kTcMaxPx, kPQY = 4 * kTcMaxPx;
+constexpr unsigned kFx0 = 1u << 16, kFxL = 1u << 17, kFyN = 1u << 18, kFyR = 1u << 19, kFy0 = 1u << 20,
+                   kFyL = 1u << 21, kFlp = 1u << 22;
 
 __global__ void __launch_bounds__(kTcThreads, 1) tvflow_cluster_kernel(const TvFlowArgs a, int rows_per) {
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(16) double sm[];  // planes u | v | vbar | qx | qy, stride kTcMaxPx
   __shared__ double red[4 * 32];
   __shared__ double slot[4];
   __shared__ double bcast[4];
@@ -345,30 +366,59 @@ __global__ void __launch_bounds__(kTcThreads, 1) tvflow_cluster_kernel(const TvF
   const int row0 = min(H, rank * rows_per);
   const int nrows = min(H, row0 + rows_per) - row0;
   const int nloc = nrows * W;
-  const int cap = rows_per * W;
   const bool has_next = row0 + nrows < H;  // rows below live on rank+1
   const bool has_prev = row0 > 0;          // rows above live on rank-1
-  double* U = sm;
-  double* V = sm + cap;
-  double* VB = sm + 2 * cap;
-  double* QX = sm + 3 * cap;
-  double* QY = sm + 4 * cap;
   const long long plane = (long long)H * W;
   const long long goff = (long long)row0 * W;
   double* uprev = a.work + (long long)img * 6 * plane + goff;  // global: u_{i-1}, own rows
   double* bands = a.bands + (long long)img * a.n_bands * plane + goff;
   const double dt = a.dt;
   const double dt2_lo = dt * dt * (1.0 - 1e-12);
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const double rdt = __drcp_rn(dt);
+  const int tid = threadIdx.x;
+  constexpr int nt = kTcThreads;
   const double npx = (double)plane;
+  const bool wide = W > 1, tall = H > 1;
+  auto bar = [&]() {
+    if (G == 1) __syncthreads();
+    else cl.sync();
+  };
+  // remote halo rows (DSMEM): row 0 of rank+1, last row of rank-1
+  const double* vb_next0 = has_next ? cl.map_shared_rank(sm + kPVB, rank + 1) : nullptr;
+  const double* v_next0 = has_next ? cl.map_shared_rank(sm + kPV, rank + 1) : nullptr;
+  const double* qy_prev0 = has_prev ? cl.map_shared_rank(sm + kPQY, rank - 1) + (rows_per - 1) * W : nullptr;
+  // Halo addresses are used by boundary-row pixels only: re-derive them inside
+  // each sweep (opaque copy) instead of letting the compiler hoist one 64-bit
+  // address per pixel into registers.
+  auto opaque = [](const double* q) {
+    asm volatile("" : "+l"(q));
+    return q;
+  };
+
+  // pixel k of this thread is p = tid + k * nt (valid while p < nloc)
+  unsigned pfl[kTcPix];
+#pragma unroll
+  for (int k = 0; k < kTcPix; ++k) {
+    const int p = tid + k * nt;
+    pfl[k] = 0;
+    if (p < nloc) {
+      const int ly = p / W, x = p - ly * W, y = row0 + ly;
+      pfl[k] = (unsigned)x | (x == 0 ? kFx0 : 0) | (x == W - 1 ? kFxL : 0) | (ly + 1 < nrows ? kFyN : 0) |
+               (ly + 1 == nrows && has_next ? kFyR : 0) | (y == 0 ? kFy0 : 0) | (y == H - 1 ? kFyL : 0) |
+               (ly > 0 ? kFlp : 0);
+    }
+  }
 
   const double* fimg = a.f + (long long)img * plane + goff;
-  for (int p = tid; p < nloc; p += nt) {
+#pragma unroll
+  for (int k = 0; k < kTcPix; ++k) {
+    const int p = tid + k * nt;
+    if (p >= nloc) continue;
     const double x = fimg[p];
-    U[p] = x;
+    sm[kPU + p] = x;
     uprev[p] = x;
-    QX[p] = 0.0;
-    QY[p] = 0.0;
+    sm[kPQX + p] = 0.0;
+    sm[kPQY + p] = 0.0;
   }
   for (int p = tid; p < a.n_bands * nloc; p += nt) {
     const int b = p / nloc, q = p - b * nloc;
@@ -376,12 +426,37 @@ __global__ void __launch_bounds__(kTcThreads, 1) tvflow_cluster_kernel(const TvF
   }
   __syncthreads();
 
+  // div(q) (+ u when with_u) at one pixel, the reference's boundary folding
+  auto divq = [&](int p, unsigned fl, const double* qy_prevc, double base, bool with_u) -> double {
+    double d;
+    if (wide) {
+      const double qx = sm[kPQX + p];
+      if (fl & kFx0) d = with_u ? __dadd_rn(qx, base) : qx;
+      else if (fl & kFxL) d = with_u ? __dsub_rn(base, sm[kPQX + p - 1]) : -sm[kPQX + p - 1];
+      else d = with_u ? __dadd_rn(__dsub_rn(qx, sm[kPQX + p - 1]), base) : __dsub_rn(qx, sm[kPQX + p - 1]);
+    } else {
+      d = with_u ? base : 0.0;
+    }
+    if (tall) {
+      if (fl & kFy0) {
+        d = __dadd_rn(d, sm[kPQY + p]);
+      } else {
+        const double qyp = (fl & kFlp) ? sm[kPQY + p - W] : qy_prevc[fl & 0xffff];
+        d = (fl & kFyL) ? __dsub_rn(d, qyp) : __dsub_rn(__dadd_rn(d, sm[kPQY + p]), qyp);
+      }
+    }
+    return d;
+  };
+
   int band_idx = 0;
   for (int step = 0; step < a.n_steps; ++step) {
     // ---- rof_prox flat shortcut (solver.py:358-366) -------------------------
     double s2v[2] = {0.0, 0.0};
-    for (int p = tid; p < nloc; p += nt) {
-      const double x = U[p];
+#pragma unroll
+    for (int k = 0; k < kTcPix; ++k) {
+      const int p = tid + k * nt;
+      if (p >= nloc) continue;
+      const double x = sm[kPU + p];
       s2v[0] += x;
       s2v[1] = __dadd_rn(s2v[1], __dmul_rn(x, x));
     }
@@ -389,72 +464,72 @@ __global__ void __launch_bounds__(kTcThreads, 1) tvflow_cluster_kernel(const TvF
     const double mean = s2v[0] / npx;
     const double floor_ = 1e-12 * (1.0 + s2v[1]);
     double s1v[1] = {0.0};
-    for (int p = tid; p < nloc; p += nt) {
-      const double d = __dsub_rn(U[p], mean);
+#pragma unroll
+    for (int k = 0; k < kTcPix; ++k) {
+      const int p = tid + k * nt;
+      if (p >= nloc) continue;
+      const double d = __dsub_rn(sm[kPU + p], mean);
       s1v[0] = __dadd_rn(s1v[0], __dmul_rn(d, d));
     }
     cluster_sum<1>(s1v, red, slot, bcast, cl);
     int iters = 0;
     bool converged = true;
     if (0.5 * s1v[0] <= a.gap_tol * floor_) {
-      for (int p = tid; p < nloc; p += nt) {
-        V[p] = mean;
-        QX[p] = 0.0;
-        QY[p] = 0.0;
+#pragma unroll
+      for (int k = 0; k < kTcPix; ++k) {
+        const int p = tid + k * nt;
+        if (p >= nloc) continue;
+        sm[kPV + p] = mean;
+        sm[kPQX + p] = 0.0;
+        sm[kPQY + p] = 0.0;
       }
     } else {
       double tau = a.tau0, sigma = a.sigma0, theta = 1.0, prev_rel = INFINITY, c = 1.0;
-      for (int p = tid; p < nloc; p += nt) {
-        V[p] = U[p];
-        VB[p] = U[p];
+#pragma unroll
+      for (int k = 0; k < kTcPix; ++k) {
+        const int p = tid + k * nt;
+        if (p >= nloc) continue;
+        sm[kPV + p] = sm[kPU + p];
+        sm[kPVB + p] = sm[kPU + p];
       }
-      cl.sync();
-      const double* vb_next = has_next ? cl.map_shared_rank(VB, rank + 1) : nullptr;  // its row 0
-      const double* qy_prevc = has_prev ? cl.map_shared_rank(QY, rank - 1) + (rows_per - 1) * W : nullptr;
+      bar();
       while (true) {
         const int n_inner = min(10, a.max_iters - iters);
         for (int it = 0; it < n_inner; ++it) {
           const double th = a.accel ? 1.0 / sqrt(__dadd_rn(1.0, __dmul_rn(2.0, tau))) : theta;
+          const double* vb_next = opaque(vb_next0);
           // phase A: q += sigma grad(vbar); project onto the ball of radius dt
-          for (int p = tid; p < nloc; p += nt) {
-            const int ly = p / W, x = p - ly * W;
-            const double vb = VB[p];
-            double gx = 0.0, gy = 0.0;
-            if (x < W - 1) gx = __dmul_rn(__dsub_rn(VB[p + 1], vb), sigma);
-            if (ly + 1 < nrows) gy = __dmul_rn(__dsub_rn(VB[p + W], vb), sigma);
-            else if (has_next) gy = __dmul_rn(__dsub_rn(vb_next[x], vb), sigma);
-            double px = __dadd_rn(QX[p], gx), py = __dadd_rn(QY[p], gy);
-            project_ball(px, py, dt, dt2_lo);
-            QX[p] = px;
-            QY[p] = py;
+#pragma unroll
+          for (int k = 0; k < kTcPix; ++k) {
+            const int p = tid + k * nt;
+            if (p >= nloc) continue;
+            const unsigned fl = pfl[k];
+            const double vb = sm[kPVB + p];
+            const double gx = (fl & kFxL) ? 0.0 : __dmul_rn(__dsub_rn(sm[kPVB + p + 1], vb), sigma);
+            double gy = 0.0;
+            if (fl & kFyN) gy = __dmul_rn(__dsub_rn(sm[kPVB + p + W], vb), sigma);
+            else if (fl & kFyR) gy = __dmul_rn(__dsub_rn(vb_next[fl & 0xffff], vb), sigma);
+            double px = __dadd_rn(sm[kPQX + p], gx), py = __dadd_rn(sm[kPQY + p], gy);
+            project_ball(px, py, dt, rdt, dt2_lo);
+            sm[kPQX + p] = px;
+            sm[kPQY + p] = py;
           }
-          cl.sync();
+          bar();
           // phase B: v = (v + tau (div q + u)) / (1 + tau); vbar = v + theta (v - v_old)
           const double opt = __dadd_rn(1.0, tau);
-          for (int p = tid; p < nloc; p += nt) {
-            const int ly = p / W, x = p - ly * W;
-            const double uu = U[p];
-            double dq;
-            if (W > 1) {
-              if (x == 0) dq = __dadd_rn(QX[p], uu);
-              else if (x == W - 1) dq = __dsub_rn(uu, QX[p - 1]);
-              else dq = __dadd_rn(__dsub_rn(QX[p], QX[p - 1]), uu);
-            } else {
-              dq = uu;
-            }
-            if (H > 1) {
-              const int y = row0 + ly;
-              const double qyp = (y == 0) ? 0.0 : (ly > 0 ? QY[p - W] : qy_prevc[x]);
-              if (y == 0) dq = __dadd_rn(dq, QY[p]);
-              else if (y == H - 1) dq = __dsub_rn(dq, qyp);
-              else dq = __dsub_rn(__dadd_rn(dq, QY[p]), qyp);
-            }
-            const double vo = V[p];
-            const double vn = __ddiv_rn(__dadd_rn(__dmul_rn(dq, tau), vo), opt);
-            V[p] = vn;
-            VB[p] = __dadd_rn(__dmul_rn(__dsub_rn(vn, vo), th), vn);
+          const double ropt = __drcp_rn(opt);
+          const double* qy_prevc = opaque(qy_prev0);
+#pragma unroll
+          for (int k = 0; k < kTcPix; ++k) {
+            const int p = tid + k * nt;
+            if (p >= nloc) continue;
+            const double dq = divq(p, pfl[k], qy_prevc, sm[kPU + p], true);
+            const double vo = sm[kPV + p];
+            const double vn = div_recip(__dadd_rn(__dmul_rn(dq, tau), vo), opt, ropt);
+            sm[kPV + p] = vn;
+            sm[kPVB + p] = __dadd_rn(__dmul_rn(__dsub_rn(vn, vo), th), vn);
           }
-          cl.sync();
+          bar();
           if (a.accel) {
             theta = th;
             tau = __dmul_rn(tau, th);
@@ -463,29 +538,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) tvflow_cluster_kernel(const TvF
           ++iters;
         }
         // certificate (_certified_pair with w = div(q), solver.py:134-150)
-        const double* v_next = has_next ? cl.map_shared_rank(V, rank + 1) : nullptr;
         double cs[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int p = tid; p < nloc; p += nt) {
-          const int ly = p / W, x = p - ly * W;
-          const int y = row0 + ly;
-          const double vv = V[p], uu = U[p];
+        const double* v_next = opaque(v_next0);
+        const double* qy_prevc = opaque(qy_prev0);
+#pragma unroll
+        for (int k = 0; k < kTcPix; ++k) {
+          const int p = tid + k * nt;
+          if (p >= nloc) continue;
+          const unsigned fl = pfl[k];
+          const double vv = sm[kPV + p], uu = sm[kPU + p];
           const double d = __dsub_rn(uu, vv);
           cs[0] = __dadd_rn(cs[0], __dmul_rn(d, d));
-          const double gx = (x < W - 1) ? __dsub_rn(V[p + 1], vv) : 0.0;
-          const double gy = (ly + 1 < nrows) ? __dsub_rn(V[p + W], vv) : (has_next ? __dsub_rn(v_next[x], vv) : 0.0);
+          const double gx = (fl & kFxL) ? 0.0 : __dsub_rn(sm[kPV + p + 1], vv);
+          const double gy = (fl & kFyN) ? __dsub_rn(sm[kPV + p + W], vv)
+                                        : ((fl & kFyR) ? __dsub_rn(v_next[fl & 0xffff], vv) : 0.0);
           cs[1] = __dadd_rn(cs[1], __dsqrt_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy))));
-          double w = 0.0;
-          if (W > 1) {
-            if (x == 0) w = QX[p];
-            else if (x == W - 1) w = -QX[p - 1];
-            else w = __dsub_rn(QX[p], QX[p - 1]);
-          }
-          if (H > 1) {
-            const double qyp = (y == 0) ? 0.0 : (ly > 0 ? QY[p - W] : qy_prevc[x]);
-            if (y == 0) w = __dadd_rn(w, QY[p]);
-            else if (y == H - 1) w = __dsub_rn(w, qyp);
-            else w = __dsub_rn(__dadd_rn(w, QY[p]), qyp);
-          }
+          const double w = divq(p, fl, qy_prevc, 0.0, false);
           cs[2] = __dadd_rn(cs[2], __dmul_rn(uu, w));
           cs[3] = __dadd_rn(cs[3], __dmul_rn(w, w));
         }
@@ -502,43 +570,60 @@ __global__ void __launch_bounds__(kTcThreads, 1) tvflow_cluster_kernel(const TvF
           tau = a.tau0;
           sigma = a.sigma0;
           theta = 1.0;
-          for (int p = tid; p < nloc; p += nt) VB[p] = V[p];
-          cl.sync();
+#pragma unroll
+          for (int k = 0; k < kTcPix; ++k) {
+            const int p = tid + k * nt;
+            if (p < nloc) sm[kPVB + p] = sm[kPV + p];
+          }
+          bar();
         }
         prev_rel = rel;
       }
-      for (int p = tid; p < nloc; p += nt) {
-        QX[p] = __dmul_rn(__ddiv_rn(__dmul_rn(c, QX[p]), dt), dt);
-        QY[p] = __dmul_rn(__ddiv_rn(__dmul_rn(c, QY[p]), dt), dt);
+#pragma unroll
+      for (int k = 0; k < kTcPix; ++k) {
+        const int p = tid + k * nt;
+        if (p >= nloc) continue;
+        sm[kPQX + p] = __dmul_rn(div_recip(__dmul_rn(c, sm[kPQX + p]), dt, rdt), dt);
+        sm[kPQY + p] = __dmul_rn(div_recip(__dmul_rn(c, sm[kPQY + p]), dt, rdt), dt);
       }
     }
     if (rank == 0 && tid == 0) a.iters[(long long)img * a.n_steps + step] = converged ? iters : -(iters + 1);
-    // ---- band accumulation (pipeline.py:120-137); u_prev <- u --------------
+    // ---- band accumulation (pipeline.py:120-137); u_prev <- u; u <- v -------
     double sa[1] = {0.0};
-    if (step >= 1) {
-      const int i = step;
+    const int i = step;
+    double* band = nullptr;
+    if (i >= 1) {
       while (i > a.schedule[band_idx]) ++band_idx;
-      double* band = bands + (long long)band_idx * plane;
-      for (int p = tid; p < nloc; p += nt) {
-        const double t = __dadd_rn(__dsub_rn(V[p], __dmul_rn(2.0, U[p])), uprev[p]);
-        const double phi = __ddiv_rn(__dmul_rn((double)i, t), dt);
+      band = bands + (long long)band_idx * plane;
+    }
+#pragma unroll
+    for (int k = 0; k < kTcPix; ++k) {
+      const int p = tid + k * nt;
+      if (p >= nloc) continue;
+      const double uc = sm[kPU + p], un = sm[kPV + p];
+      if (i >= 1) {
+        const double t = __dadd_rn(__dsub_rn(un, __dmul_rn(2.0, uc)), uprev[p]);
+        const double phi = div_recip(__dmul_rn((double)i, t), dt, rdt);
         band[p] = __dadd_rn(band[p], phi);
         sa[0] = __dadd_rn(sa[0], fabs(phi));
-        uprev[p] = U[p];
       }
+      uprev[p] = uc;
+      sm[kPU + p] = un;
+    }
+    if (i >= 1) {
       cluster_sum<1>(sa, red, slot, bcast, cl);
       if (rank == 0 && tid == 0) a.spectrum[(long long)img * (a.n_steps - 1) + (i - 1)] = sa[0];
     } else {
       cl.sync();
     }
-    double* t = U;  // u <- v
-    U = V;
-    V = t;
   }
   const double n = (double)a.n_steps;
   double* res = a.residual + (long long)img * plane + goff;
-  for (int p = tid; p < nloc; p += nt) {
-    const double uc = U[p];
+#pragma unroll
+  for (int k = 0; k < kTcPix; ++k) {
+    const int p = tid + k * nt;
+    if (p >= nloc) continue;
+    const double uc = sm[kPU + p];
     const double fr = __dsub_rn(uc, __dmul_rn(n, __dsub_rn(uc, uprev[p])));
     res[p] = fr;
     for (int b = 0; b < a.n_bands; ++b) {
@@ -552,6 +637,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tvflow_cluster_kernel(const TvF
 
 namespace {
 constexpr int kTvSmemMax = 224 * 1024;  // dynamic; static (~1 KB) + dynamic <= 227 KB opt-in
+static_assert(kTcMaxPx * 5 * 8 <= kTvSmemMax, "cluster kernel state exceeds shared memory");
 int g_max_cluster = 0;  // largest usable cluster size, probed once
 
 int usable_cluster_max() {
@@ -580,18 +666,30 @@ int usable_cluster_max() {
 }
 }  // namespace
 
-int tvflow_cluster_size(int H, int W) {
+// Smallest cluster whose shared memory holds the image, then widened (more
+// CTAs per image, fewer pixels per CTA) while the whole batch still fits in
+// one wave of SMs: small batches get more SMs per image.
+int tvflow_cluster_size(int N, int H, int W) {
   const int gmax = usable_cluster_max();
-  for (int g = 1; g <= gmax; g *= 2) {
-    const long long rows = (H + g - 1) / g;
-    if (rows * W * 5 * (long long)sizeof(double) <= kTvSmemMax) return g;
+  int g = 0;
+  for (int c = 1; c <= gmax; c *= 2) {
+    const long long rows = (H + c - 1) / c;
+    if (rows * W <= kTcMaxPx) {
+      g = c;
+      break;
+    }
   }
-  return 0;
+  if (g == 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  while (g * 2 <= gmax && (long long)N * g * 2 <= sms && (H + 2 * g - 1) / (2 * g) >= 2) g *= 2;
+  return g;
 }
 
 cudaError_t launch_tvflow(const TvFlowArgs& a, cudaStream_t st) {
   const char* env = getenv("TVS_TVFLOW_KERNEL");  // "global" forces the row-sweep kernel
-  const int g = (env && env[0] == 'g') ? 0 : tvflow_cluster_size(a.H, a.W);
+  const int g = (env && env[0] == 'g') ? 0 : tvflow_cluster_size(a.N, a.H, a.W);
   if (g == 0) {
     tvflow_kernel<<<a.N, kTvThreads, 0, st>>>(a);
     return cudaGetLastError();
@@ -605,7 +703,7 @@ cudaError_t launch_tvflow(const TvFlowArgs& a, cudaStream_t st) {
   at[0].val.clusterDim.z = 1;
   cfg.gridDim = dim3(a.N * g);
   cfg.blockDim = dim3(kTcThreads);
-  cfg.dynamicSmemBytes = (size_t)rows_per * a.W * 5 * sizeof(double);
+  cfg.dynamicSmemBytes = (size_t)kTcMaxPx * 5 * sizeof(double);
   cfg.stream = st;
   cfg.attrs = at;
   cfg.numAttrs = 1;

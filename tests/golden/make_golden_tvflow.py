@@ -9,7 +9,9 @@ ModelDrivenDecomposer.analyze (pipeline.py:105-145) on small seeded images;
 the per-step prox iteration counts come from its rof_prox (solver.py:323-372)
 called in analyze's order with its warm duals.  Writes golden_tvflow.npz.
 
-Cases: name -> (image, dt, n_steps, schedule or None, solver kwargs)
+Cases: name -> (image, dt, n_steps, schedule or None, solver kwargs), plus
+gt_planes / gt_manifest: a dataset written by the reference's
+generate_ground_truth (dataset.py:131-200) from gt_images.make_images.
 """
 
 from __future__ import annotations
@@ -20,6 +22,7 @@ from pathlib import Path
 import numpy as np
 
 HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE))
 sys.path.insert(0, "/root/reference/pkg/src")
 
 from spectv.pipeline import DecompositionConfig, ModelDrivenDecomposer  # noqa: E402  (reference)
@@ -67,6 +70,22 @@ def main():
         out[f"{name}_warnings"] = np.array(r.warnings, dtype=np.int64)
         out[f"{name}_iterations"] = np.array(its, dtype=np.int64)
         print(name, f.shape, "warnings", r.warnings, "iters", its[:6], "...")
+    # a ground-truth dataset made by the reference generator (dataset.py:131-200)
+    import json
+    import tempfile
+
+    from gt_images import GT_CFG, GT_KW, make_images
+    from spectv.dataset import generate_ground_truth
+    from spectv.tensorfile import read_tensor
+
+    with tempfile.TemporaryDirectory() as td:
+        paths = make_images(Path(td) / "img")
+        cfg = DecompositionConfig(**GT_CFG)
+        man = generate_ground_truth(paths, Path(td) / "ds", config=cfg, **GT_KW)
+        out["gt_planes"] = np.stack([read_tensor(Path(td) / "ds" / e["tensor_file"]) for e in man["entries"]])
+        for e in man["entries"]:
+            e["source"] = Path(e["source"]).name
+        out["gt_manifest"] = np.array(json.dumps(man, sort_keys=True))
     np.savez_compressed(HERE / "golden_tvflow.npz", **out)
     print("wrote", HERE / "golden_tvflow.npz")
 

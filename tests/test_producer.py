@@ -87,3 +87,34 @@ def test_abi_validation():
     for bad in (dict(n=9), dict(dt=0.0), dict(W=2049), dict(mi=0), dict(tol=0.0), dict(tau=1.0), dict(nb=17),
                 dict(H=0), dict(n=1)):
         assert call(**bad) == _native.TVS_E_INVALID, bad
+
+
+def test_dataset_crops_match_reference(golden_tv, tmp_path):
+    """Host half of generate_ground_truth (dataset.py:113-170): seeded crops,
+    2x box-mean augmentation, dataset-global standardisation -> plane 0 of
+    every entry and the manifest bookkeeping, bitwise vs the reference."""
+    import json
+    import sys
+
+    sys.path.insert(0, str(GOLD.parent))
+    from gt_images import GT_KW, make_images
+
+    from paper_2006_10004_b200 import groundtruth as gt
+
+    ref = json.loads(str(golden_tv["gt_manifest"]))
+    paths = make_images(tmp_path / "img")
+    crops, metas = gt._draw_entries([str(p) for p in paths], GT_KW["count"], GT_KW["crop_size"], GT_KW["seed"],
+                                    GT_KW["augment_fraction"])
+    stacked = np.stack(crops)
+    mean, std = float(stacked.mean()), float(stacked.std())
+    assert mean == ref["preprocessing"]["mean"] and std == ref["preprocessing"]["std"]
+    grids = ((stacked - mean) / std).astype("<f4")
+    assert np.array_equal(grids, golden_tv["gt_planes"][:, 0])
+    for m, e in zip(metas, ref["entries"]):
+        assert list(m.crop_offset) == e["crop_offset"] and m.downsample_factor == e["downsample_factor"]
+        assert list(m.crop_size) == e["crop_size"] and m.seed_spawn == e["seed_spawn"]
+    # preprocess() reproduces an entry's input plane (dataset.py:96-110)
+    e0 = ref["entries"][1]
+    one = gt.preprocess(paths[1], GT_KW["crop_size"], GT_KW["seed"], mean, std, index=1,
+                        augment=e0["downsample_factor"] == 2)
+    assert np.array_equal(one.astype("<f4"), golden_tv["gt_planes"][1, 0])

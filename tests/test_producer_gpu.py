@@ -75,7 +75,9 @@ def test_producer_matches_reference(golden_tv, name, kernel):
 
 
 def test_batch_equals_single(golden_tv, kernel):
-    """One launch over a stack == per-image launches, bitwise (images are independent CTAs)."""
+    """One launch over a stack == per-image launches (images are independent
+    clusters; bitwise here because both launches pick the same cluster split —
+    in general a different split only reorders the certificate sums)."""
     from paper_2006_10004_b200.producer import DecompositionConfig, ModelDrivenDecomposer
 
     rng = np.random.default_rng(3)
@@ -144,3 +146,34 @@ def test_cluster_partitions_vs_oracle(shape):
     r = ModelDrivenDecomposer(DecompositionConfig(**kw, solver=SolverConfig(max_iters=150))).analyze(f)
     assert _rel(r.bands.bands, ref["bands"]) <= TOL
     assert _rel(r.spectrum.values, ref["spectrum"]) <= TOL
+
+
+def test_generate_ground_truth_matches_reference(golden_tv, tmp_path):
+    """generate_ground_truth end to end (crops -> batched GPU decomposition ->
+    BTF + manifest) vs a dataset written by the reference generator."""
+    import json
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).parent / "golden"))
+    from gt_images import GT_CFG, GT_KW, make_images
+
+    from paper_2006_10004_b200.export import read_tensor
+    from paper_2006_10004_b200.groundtruth import generate_ground_truth, verify_manifest
+    from paper_2006_10004_b200.producer import DecompositionConfig
+
+    paths = make_images(tmp_path / "img")
+    man = generate_ground_truth(paths, tmp_path / "ds", config=DecompositionConfig(**GT_CFG), batch_images=3, **GT_KW)
+    verify_manifest(tmp_path / "ds")
+    ref = json.loads(str(golden_tv["gt_manifest"]))
+    planes = np.stack([read_tensor(tmp_path / "ds" / e["tensor_file"]) for e in man["entries"]])
+    want = golden_tv["gt_planes"]
+    assert planes.shape == want.shape
+    assert np.array_equal(planes[:, 0], want[:, 0])
+    scale = np.abs(want).max()
+    assert np.abs(planes.astype(np.float64) - want).max() <= 1e-5 * scale
+    for k in ("format_version", "master_seed", "preprocessing", "decomposition", "plane_layout"):
+        assert man[k] == ref[k], k
+    for e, r in zip(man["entries"], ref["entries"]):
+        assert Path(e["source"]).name == r["source"] and e["tensor_file"] == r["tensor_file"]
+        assert e["crop_offset"] == r["crop_offset"] and e["downsample_factor"] == r["downsample_factor"]
