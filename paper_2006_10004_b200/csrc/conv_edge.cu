@@ -43,11 +43,12 @@ __device__ __forceinline__ void store_act8<float>(float* dst, const float* v) {
 // straight from the constant cache (no shared-memory loads).  128 pixels per
 // block are contiguous in NHWC, so the block's output is staged through shared
 // memory and written coalesced.
-template <typename T, int C>
+template <typename T, int C, bool kSplit = false>
 __global__ void __launch_bounds__(128)
 conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params p, int B, int H, int W) {
   constexpr int P = (C == 64) ? 128 : 64;  // pixels per block (static smem <= 32 KB)
-  __shared__ __align__(16) T stage[P * C];
+  constexpr int E = kSplit ? 2 * C : C;    // elements per pixel (split: hi | lo halves)
+  __shared__ __align__(16) T stage[P * E];
   // PDL: the first hidden layer may start its prologue (it waits for this grid's completion)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long npx = (long long)B * H * W;
@@ -67,28 +68,37 @@ conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params
         const int yy = y + ky - 1, xx = xw + kx - 1;
         in[ky * 3 + kx] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(img + (long long)yy * W + xx) : 0.0f;
       }
-    T* dst = stage + threadIdx.x * C;
+    T* dst = stage + threadIdx.x * E;
 #pragma unroll
     for (int c8 = 0; c8 < C / 8; ++c8) {
       float v[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int co = c8 * 8 + e;
-        using Acc = std::conditional_t<std::is_same_v<T, float>, double, float>;  // fp64 in fp32 mode
+        // fp64 accumulation in the fp32-accurate formats
+        using Acc = std::conditional_t<std::is_same_v<T, float> || kSplit, double, float>;
         Acc acc = 0;
 #pragma unroll
         for (int t9 = 0; t9 < 9; ++t9) acc = fma((Acc)p.w[co * 9 + t9], (Acc)in[t9], acc);
         v[e] = fmaxf((float)(acc + (Acc)p.b[co]), 0.0f);
       }
-      store_act8<T>(dst + c8 * 8, v);
+      if constexpr (kSplit) {
+        float lo[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) lo[e] = v[e] - __half2float(__float2half_rn(v[e]));
+        store_act8<T>(dst + c8 * 8, v);
+        store_act8<T>(dst + C + c8 * 8, lo);
+      } else {
+        store_act8<T>(dst + c8 * 8, v);
+      }
     }
   }
   __syncthreads();
   // coalesced copy of the staged block (valid pixels only)
   const long long nvalid = min((long long)P, npx - p0);
-  const int n16 = (int)(nvalid * C * sizeof(T) / 16);
+  const int n16 = (int)(nvalid * E * sizeof(T) / 16);
   const uint4* src = reinterpret_cast<const uint4*>(stage);
-  uint4* out = reinterpret_cast<uint4*>(act + p0 * C);
+  uint4* out = reinterpret_cast<uint4*>(act + p0 * E);
   for (int i = threadIdx.x; i < n16; i += blockDim.x) out[i] = src[i];
 }
 
@@ -253,16 +263,18 @@ hidden_f32_kernel(const float* __restrict__ in, float* __restrict__ out, const f
   }
 }
 
-cudaError_t launch_conv0(bool fp16_act, int C, const float* x, void* act, const Conv0Params& p, int B, int H,
-                         int W, cudaStream_t st) {
+cudaError_t launch_conv0(int act_fmt, int C, const float* x, void* act, const Conv0Params& p, int B, int H, int W,
+                         cudaStream_t st) {
   const long long npx = (long long)B * H * W;
   if (C == 64) {
     const unsigned grid = (unsigned)((npx + 127) / 128);
-    if (fp16_act)
+    if (act_fmt == kActF16)
       conv0_kernel<__half, 64><<<grid, 128, 0, st>>>(x, static_cast<__half*>(act), p, B, H, W);
+    else if (act_fmt == kActSplit)
+      conv0_kernel<__half, 64, true><<<grid, 128, 0, st>>>(x, static_cast<__half*>(act), p, B, H, W);
     else
       conv0_kernel<float, 64><<<grid, 128, 0, st>>>(x, static_cast<float*>(act), p, B, H, W);
-  } else if (C == 128 && !fp16_act) {
+  } else if (C == 128 && act_fmt == kActF32) {
     const unsigned grid = (unsigned)((npx + 63) / 64);
     conv0_kernel<float, 128><<<grid, 64, 0, st>>>(x, static_cast<float*>(act), p, B, H, W);
   } else {

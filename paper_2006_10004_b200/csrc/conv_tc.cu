@@ -81,10 +81,17 @@ struct SegIter {
 
 // kMode: 0 = hidden layer (TMA producer), 1 = head, 2 = first hidden layer
 // with conv0 fused into its producer (4 warps compute Conv2d(1,64)+ReLU of
-// each input row from the fp32 image straight into the smem ring).
+// each input row from the fp32 image straight into the smem ring),
+// 3 / 4 = fp32-accurate hidden layer / head on split operands: activations
+// are stored as an fp16 pair (hi = RN(a), lo = RN(a - hi): channels 0-63 and
+// 64-127 of a 256 B/px NHWC row), weights as hi/lo fp16 packs scaled by 2^8
+// (keeps lo normal), and every tap runs three products hi*hi + lo*hi + hi*lo
+// (head: two, its B pack already carries hi|lo columns) into the same fp32
+// TMEM accumulators; the epilogue unscales and re-splits.
 template <int kMode>
 struct ConvCfg {
-  static constexpr bool kHead = kMode == 1;
+  static constexpr bool kSplit = kMode >= 3;
+  static constexpr bool kHead = kMode == 1 || kMode == 4;
   static constexpr bool kFirst = kMode == 2;
   static constexpr int kProdWarps = kFirst ? 4 : 1;
   static constexpr int kMmaWarp = kProdWarps;
@@ -95,11 +102,39 @@ struct ConvCfg {
   static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kGroups);
   static constexpr int NB = kHead ? 32 : 64;          // TMEM columns per output row (slot)
   static constexpr int kWdx = 3 * NB * 128;           // B bytes per dx (3 dy blocks x NB rows x 128 B)
-  static constexpr int kW = 3 * kWdx;
-  static constexpr int kTmemCols = kSlots * NB;       // 512 / 256
-  static constexpr int kStageOut = kHead ? 0 : 32 * 128;  // per-warp staging (hidden only)
-  static constexpr size_t kSmem = 1024 + kW + kStages * kInRowStride + 4 * kGroups * kStageOut + 1024;
+  static constexpr int kW1 = 3 * kWdx;                // one weight pack
+  static constexpr int kW = (kSplit && !kHead) ? 2 * kW1 : kW1;  // split hidden: hi pack | lo pack
+  static constexpr int kTmemCols = kSplit ? 512 : kSlots * NB;  // 512 / 256 (split: two rings)
+  static constexpr int kPasses = kSplit ? (kHead ? 2 : 3) : 1;
+  static constexpr int kNStages = kSplit ? (kHead ? 5 : 2) : kStages;  // input-row ring depth
+  static constexpr int kStageBytes = kSplit ? 2 * kInRowStride : kInRowStride;  // hi row | lo row
+  static constexpr int kStageOut = (kHead || kSplit) ? 0 : 32 * 128;  // per-warp TMA-store staging
+  static constexpr size_t kSmem = 1024 + kW + kNStages * kStageBytes + 4 * kGroups * kStageOut + 1024;
+  // A / B descriptor offsets (bytes) of pass p
+  static constexpr uint32_t a_off(int p) { return (kSplit && p == 1) ? kInRowStride : 0; }
+  static constexpr uint32_t b_off(int p) { return (kSplit && !kHead && p == 2) ? kW1 : 0; }
+  // TMEM accumulator rings.  tcgen05 f16 MMAs add their products exactly and
+  // truncate the fp32 accumulator toward zero once per MMA
+  // (tools/probe_mma_rounding.cu), so every MMA into an accumulator costs it
+  // ~0.5 ulp.  The split hidden layer therefore keeps the hi*hi products (36
+  // MMAs per output) in a main ring and the two small correction products (72
+  // MMAs) in a separate correction ring (4 slots each); the epilogue adds the
+  // expected truncation loss of the main ring back (kMainDebias) and sums.
+  // (the split head likewise: hi*[W_hi|W_lo] in the main ring, lo*[W_hi|W_lo]
+  // in the correction ring, 8 slots x 32 columns each)
+  static constexpr bool kTwoRings = kSplit;
+  static constexpr int kRing = kTwoRings ? (kHead ? 8 : 4) : kSlots;
+  static constexpr uint32_t kRingMask = kRing - 1;
+  static constexpr int kRingLog = kRing == 4 ? 2 : 3;
+  static constexpr uint32_t kCorrCol = kRing * NB;
+  static constexpr uint32_t ring_col(int p) { return (kTwoRings && p > 0) ? kCorrCol : 0; }
+  static constexpr bool enters(int p) { return p == 0 || (kTwoRings && p == 1); }  // first pass into a ring
 };
+constexpr float kSplitWScale = 256.0f;  // split hidden weights are packed x 2^8
+// 1 + E[truncation loss] of the main accumulator: 36 MMAs, each losing 0.5 ulp of
+// a partial sum that grows ~linearly to the result, E[ulp(x)/|x|] = 0.7213 * 2^-23
+// over a binade (tools/emulate_split_accum.py: 1.2e-5 -> 5.1e-6 worst band)
+constexpr float kMainDebias = 1.0f + 0.5f * 0.7213f * 18.0f * 1.1920929e-7f;
 
 template <int kMode>
 __global__ void __launch_bounds__(ConvCfg<kMode>::kThreads, 1)
@@ -115,13 +150,13 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
   uint8_t* sIn = sW + Cfg::kW;
-  uint8_t* sOut = sIn + kStages * kInRowStride;
+  uint8_t* sOut = sIn + Cfg::kNStages * Cfg::kStageBytes;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) { mbar_init(&full[i], Cfg::kProdWarps); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < Cfg::kNStages; ++i) { mbar_init(&full[i], Cfg::kProdWarps); mbar_init(&empty[i], 1); }
     for (int i = 0; i < kSlots; ++i) { mbar_init(&slot_full[i], 1); mbar_init(&slot_empty[i], 4); }
     mbar_init(&wbar, 1);
     fence_barrier_init();
@@ -132,7 +167,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   // PDL wait so it overlaps the previous kernel's tail
   if (threadIdx.x == 0) {
     mbar_arrive_expect_tx(&wbar, Cfg::kW);
-    for (int i = 0; i < 3; ++i) bulk_load(sW + i * Cfg::kWdx, a.wpack + i * Cfg::kWdx, Cfg::kWdx, &wbar);
+    for (int i = 0; i < Cfg::kW / Cfg::kWdx; ++i) bulk_load(sW + i * Cfg::kWdx, a.wpack + i * Cfg::kWdx, Cfg::kWdx, &wbar);
   }
   tc_fence_before();
   __syncthreads();
@@ -229,9 +264,11 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
         for (int r = r0; r <= r1; ++r) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], kInRowBytes);
-          tma_load_4d(sIn + stage * kInRowStride, &tm_in, &full[stage], 0, g.x0 - 1, r, g.b);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          mbar_arrive_expect_tx(&full[stage], Cfg::kSplit ? 2 * kInRowBytes : kInRowBytes);
+          tma_load_4d(sIn + stage * Cfg::kStageBytes, &tm_in, &full[stage], 0, g.x0 - 1, r, g.b);
+          if constexpr (Cfg::kSplit)  // lo halves: channels 64..127 of the pair row
+            tma_load_4d(sIn + stage * Cfg::kStageBytes + kInRowStride, &tm_in, &full[stage], 64, g.x0 - 1, r, g.b);
+          if (++stage == Cfg::kNStages) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -250,7 +287,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     mbar_wait(&wbar, 0);
     int stage = 0;
     uint32_t phase = 0;
-    uint32_t seq = 0;  // output-row sequence number: slot = seq & 7, use = seq >> 3
+    uint32_t seq = 0;  // output-row sequence number: slot = seq % kRing, use = seq / kRing
     bool prewaited = false;  // this row's barriers were already awaited by the previous row
     SegIter it(a);
     Segment g;
@@ -264,64 +301,78 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         // (~5 MMAs deep) still holds work, so row transitions do not drain it.
         if (r >= 1 && r - 1 >= g.ya && r + 1 <= g.yb - 1) {
           const uint32_t sq = seq + (uint32_t)(r - 1 - g.ya);  // sequence of output row r-1
-          const uint32_t s = sq & 7;
+          const uint32_t s = sq & Cfg::kRingMask;
           const bool next_fast = (r + 2 <= g.yb - 1);  // row r+1 is interior too
-          const int nstage = (stage + 1 == kStages) ? 0 : stage + 1;
-          const uint32_t nphase = (stage + 1 == kStages) ? (phase ^ 1) : phase;
+          const int nstage = (stage + 1 == Cfg::kNStages) ? 0 : stage + 1;
+          const uint32_t nphase = (stage + 1 == Cfg::kNStages) ? (phase ^ 1) : phase;
           const uint32_t sq2 = sq + 3;  // output row r+2, entered by input row r+1
           if (leader) {
-            if (!prewaited) mbar_wait2(&slot_empty[(sq + 2) & 7], (((sq + 2) >> 3) & 1) ^ 1, &full[stage], phase);
+            if (!prewaited)
+              mbar_wait2(&slot_empty[(sq + 2) & Cfg::kRingMask], (((sq + 2) >> Cfg::kRingLog) & 1) ^ 1, &full[stage],
+                         phase);
             tc_fence_after();
-            const uint64_t ad_row = adesc0 + (uint64_t)((stage * kInRowStride) >> 4);
-            const uint32_t t0 = tmem + s * NB;
+            const uint64_t ad_row = adesc0 + (uint64_t)((stage * Cfg::kStageBytes) >> 4);
+            const uint32_t t0s = s * NB;  // slot column offset inside a ring
             constexpr uint32_t b1 = NB * 128 / 16, b2 = 2 * NB * 128 / 16;  // W(dy=0), W(dy=-1) blocks
-            auto prewait = [&](int dx, int k) {
-              if (dx == 1 && k == 1 && next_fast)
-                mbar_wait2(&slot_empty[sq2 & 7], ((sq2 >> 3) & 1) ^ 1, &full[nstage], nphase);
+            auto prewait = [&](int p, int dx, int k) {
+              if (p == Cfg::kPasses / 2 && dx == 1 && k == 1 && next_fast)
+                mbar_wait2(&slot_empty[sq2 & Cfg::kRingMask], ((sq2 >> Cfg::kRingLog) & 1) ^ 1, &full[nstage], nphase);
             };
             // Split pieces share A through the collector: the N=NB piece is
             // issued first (fill), the N=2NB piece second (lastuse) -> full rate.
-            if (s <= 5) {
+            if (s + 3 <= (uint32_t)Cfg::kRing) {
+#pragma unroll
+              for (int p = 0; p < Cfg::kPasses; ++p)
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                  const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
-                  const uint64_t bd = bdesc0 + (uint64_t)((dx * Cfg::kWdx + k * 32) >> 4);
-                  if (dx == 0 && k == 0) {  // enter row r+1 (acc=0), keep r-1, r
+                  const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p) + dx * 128 + k * 32) >> 4);
+                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + dx * Cfg::kWdx + k * 32) >> 4);
+                  const bool first_k = Cfg::enters(p) && dx == 0 && k == 0;
+                  const uint32_t rb = tmem + Cfg::ring_col(p), t0 = rb + t0s;
+                  if (first_k) {  // enter row r+1 (acc=0), keep r-1, r
                     mma_f16_ss_fill(t0 + 2 * NB, ad, bd + b2, idesc1, 0u);
                     mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
                   } else {
                     mma_f16_ss(t0, ad, bd, idesc3, 1u);
                   }
-                  prewait(dx, k);
+                  prewait(p, dx, k);
                 }
-            } else if (s == 6) {  // slots 6,7 | wrap | 0
+            } else if (s + 2 == (uint32_t)Cfg::kRing) {  // slots R-2, R-1 | wrap | 0
+#pragma unroll
+              for (int p = 0; p < Cfg::kPasses; ++p)
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                  const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
-                  const uint64_t bd = bdesc0 + (uint64_t)((dx * Cfg::kWdx + k * 32) >> 4);
-                  mma_f16_ss_fill(tmem, ad, bd + b2, idesc1, (dx == 0 && k == 0) ? 0u : 1u);
+                  const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p) + dx * 128 + k * 32) >> 4);
+                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + dx * Cfg::kWdx + k * 32) >> 4);
+                  const bool first_k = Cfg::enters(p) && dx == 0 && k == 0;
+                  const uint32_t rb = tmem + Cfg::ring_col(p), t0 = rb + t0s;
+                  mma_f16_ss_fill(rb, ad, bd + b2, idesc1, first_k ? 0u : 1u);
                   mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
-                  prewait(dx, k);
+                  prewait(p, dx, k);
                 }
-            } else {  // s == 7: slot 7 | wrap | 0,1
+            } else {  // slot R-1 | wrap | 0, 1
+#pragma unroll
+              for (int p = 0; p < Cfg::kPasses; ++p)
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                  const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
-                  const uint64_t bd = bdesc0 + (uint64_t)((dx * Cfg::kWdx + k * 32) >> 4);
+                  const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p) + dx * 128 + k * 32) >> 4);
+                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + dx * Cfg::kWdx + k * 32) >> 4);
+                  const bool first_k = Cfg::enters(p) && dx == 0 && k == 0;
+                  const uint32_t rb = tmem + Cfg::ring_col(p), t0 = rb + t0s;
                   mma_f16_ss_fill(t0, ad, bd, idesc1, 1u);
-                  if (dx == 0 && k == 0) {
-                    mma_f16_ss_use(tmem, ad, bd + b1, idesc1, 1u);
-                    mma_f16_ss_lastuse(tmem + NB, ad, bd + b2, idesc1, 0u);
+                  if (first_k) {
+                    mma_f16_ss_use(rb, ad, bd + b1, idesc1, 1u);
+                    mma_f16_ss_lastuse(rb + NB, ad, bd + b2, idesc1, 0u);
                   } else {
-                    mma_f16_ss_lastuse(tmem, ad, bd + b1, idesc2, 1u);
+                    mma_f16_ss_lastuse(rb, ad, bd + b1, idesc2, 1u);
                   }
-                  prewait(dx, k);
+                  prewait(p, dx, k);
                 }
             }
             mma_commit(&empty[stage]);
@@ -340,19 +391,20 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         const int q_new = (r == 0) ? q_lo : r + 1;
         for (int q = max(q_new, q_lo); q <= q_hi; ++q) {
           const uint32_t sq = seq + (uint32_t)(q - g.ya);
-          mbar_wait(&slot_empty[sq & 7], ((sq >> 3) & 1) ^ 1);
+          mbar_wait(&slot_empty[sq & Cfg::kRingMask], ((sq >> Cfg::kRingLog) & 1) ^ 1);
         }
         // Target rows [q_lo, q_hi] -> consecutive slots, split at the ring wrap
         // (regular ops R0, R1); the first K step also splits off the
         // newly-entered suffix [q_new, q_hi] with accumulate = 0 (ops F0..F2).
         // An op = (TMEM column, B row offset in 16-byte units, idesc, acc).
-        const uint32_t s_lo = (seq + (uint32_t)(q_lo - g.ya)) & 7;
+        const uint32_t s_lo = (seq + (uint32_t)(q_lo - g.ya)) & Cfg::kRingMask;
         const int cnt = q_hi - q_lo + 1;
-        const int c0 = min(cnt, 8 - (int)s_lo), c1 = cnt - c0;
+        const int c0 = min(cnt, Cfg::kRing - (int)s_lo), c1 = cnt - c0;
         auto idesc_of = [&](int c) { return c == 3 ? idesc3 : (c == 2 ? idesc2 : idesc1); };
         auto brow16 = [&](int q) { return (uint32_t)(q - (r - 1)) * (uint32_t)(NB * 128 / 16); };
-        const uint32_t R0t = tmem + s_lo * NB, R0b = brow16(q_lo), R0i = idesc_of(c0);
-        const uint32_t R1t = tmem, R1b = brow16(q_lo + c0), R1i = idesc_of(c1);
+        // column offsets inside a ring (the ring base is added per pass)
+        const uint32_t R0t = s_lo * NB, R0b = brow16(q_lo), R0i = idesc_of(c0);
+        const uint32_t R1t = 0, R1b = brow16(q_lo + c0), R1i = idesc_of(c1);
         // first-K-step ops: old / new part of segment 0 and of segment 1
         const int s0e = q_lo + c0 - 1, s1b = q_lo + c0;
         const int A_e = min(s0e, q_new - 1), B_b = max(q_lo, q_new);
@@ -365,30 +417,33 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (leader) {
-          const uint64_t ad_row = adesc0 + (uint64_t)((stage * kInRowStride) >> 4);
+          const uint64_t ad_row = adesc0 + (uint64_t)((stage * Cfg::kStageBytes) >> 4);
+#pragma unroll
+          for (int p = 0; p < Cfg::kPasses; ++p)
 #pragma unroll
           for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
-              const uint64_t bd = bdesc0 + (uint64_t)((dx * Cfg::kWdx + k * 32) >> 4);
-              if (dx == 0 && k == 0) {
-                if (vA) mma_f16_ss(At, ad, bd + Ab, Ai, 1u);
-                if (vB) mma_f16_ss(Bt, ad, bd + Bb, Bi, 0u);
-                if (vC) mma_f16_ss(Ct, ad, bd + Cb, Ci, 1u);
-                if (vD) mma_f16_ss(Dt, ad, bd + Db, Di, 0u);
+              const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p) + dx * 128 + k * 32) >> 4);
+              const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + dx * Cfg::kWdx + k * 32) >> 4);
+              const uint32_t rb = tmem + Cfg::ring_col(p);
+              if (Cfg::enters(p) && dx == 0 && k == 0) {
+                if (vA) mma_f16_ss(rb + At, ad, bd + Ab, Ai, 1u);
+                if (vB) mma_f16_ss(rb + Bt, ad, bd + Bb, Bi, 0u);
+                if (vC) mma_f16_ss(rb + Ct, ad, bd + Cb, Ci, 1u);
+                if (vD) mma_f16_ss(rb + Dt, ad, bd + Db, Di, 0u);
               } else {
-                mma_f16_ss(R0t, ad, bd + R0b, R0i, 1u);
-                if (c1 > 0) mma_f16_ss(R1t, ad, bd + R1b, R1i, 1u);
+                mma_f16_ss(rb + R0t, ad, bd + R0b, R0i, 1u);
+                if (c1 > 0) mma_f16_ss(rb + R1t, ad, bd + R1b, R1i, 1u);
               }
             }
           }
           mma_commit(&empty[stage]);
           for (int q = q_lo; q <= q_hi; ++q)
-            if (min(q + 1, a.H - 1) == r) mma_commit(&slot_full[(seq + (uint32_t)(q - g.ya)) & 7]);
+            if (min(q + 1, a.H - 1) == r) mma_commit(&slot_full[(seq + (uint32_t)(q - g.ya)) & Cfg::kRingMask]);
         }
         __syncwarp();
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if (++stage == Cfg::kNStages) { stage = 0; phase ^= 1; }
       }
       seq += (uint32_t)(g.yb - g.ya);
     }
@@ -401,18 +456,68 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
     const uint32_t stage_out = smem_u32(sOut + ew * Cfg::kStageOut);
     const uint32_t shift_u = smem_u32(sShift);
-    if (!kHead && lane == 0) prefetch_tmap(&tm_out);
+    if (!kHead && !Cfg::kSplit && lane == 0) prefetch_tmap(&tm_out);
     uint32_t seq = 0, gsel = 0;  // gsel = seq % kGroups
     SegIter it(a);
     Segment g;
     while (it.next(a, g)) {
       for (int q = g.ya; q < g.yb; ++q, ++seq, gsel = (gsel + 1 == Cfg::kGroups) ? 0 : gsel + 1) {
         if (gsel != grp) continue;
-        const uint32_t slot = seq & 7;
-        mbar_wait(&slot_full[slot], (seq >> 3) & 1);
+        const uint32_t slot = seq & Cfg::kRingMask;
+        mbar_wait(&slot_full[slot], (seq >> Cfg::kRingLog) & 1);
         tc_fence_after();
         const int xg = g.x0 + px;
-        if constexpr (!kHead) {
+        if constexpr (Cfg::kSplit && !kHead) {
+          // z = main * kMainDebias + corr (x 2^-8) + shift, ReLU, re-split into
+          // an fp16 pair; one pixel per lane, 128 B hi + 128 B lo straight to
+          // global.  Two 32-channel halves keep the register footprint low.
+          uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * 256;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t v[2][16], w[2][16];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              tmem_ld16(tmem + lane_addr + slot * NB + h * 32 + j * 16, v[j]);
+              tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB + h * 32 + j * 16, w[j]);
+            }
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 2; ++j) { reg_fence16(v[j]); reg_fence16(w[j]); }
+            if (h == 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&slot_empty[slot]);
+            }
+            if (xg < a.W) {
+#pragma unroll
+              for (int cc = 0; cc < 4; ++cc) {
+                const int chunk = h * 4 + cc;
+                const float4 s0 = ld_shared_f4(shift_u + chunk * 32);
+                const float4 s1 = ld_shared_f4(shift_u + chunk * 32 + 16);
+                const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+                uint32_t hi[4], lo[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  float f[2];
+#pragma unroll
+                  for (int t = 0; t < 2; ++t) {
+                    const int c = cc * 8 + e * 2 + t;  // channel within the half
+                    const float z = fmaf(__uint_as_float(v[c >> 4][c & 15]), kMainDebias,
+                                         __uint_as_float(w[c >> 4][c & 15]));
+                    f[t] = fmaxf(fmaf(z, 1.0f / kSplitWScale, sh[2 * e + t]), 0.0f);
+                  }
+                  const __half2 hh = __floats2half2_rn(f[0], f[1]);
+                  const float2 hf = __half22float2(hh);
+                  const __half2 ll = __floats2half2_rn(f[0] - hf.x, f[1] - hf.y);
+                  hi[e] = *reinterpret_cast<const uint32_t*>(&hh);
+                  lo[e] = *reinterpret_cast<const uint32_t*>(&ll);
+                }
+                *reinterpret_cast<uint4*>(dst + chunk * 16) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<uint4*>(dst + 128 + chunk * 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+              }
+            }
+          }
+        } else if constexpr (!kHead) {
           uint32_t v[4][16];
 #pragma unroll
           for (int j = 0; j < 4; ++j) tmem_ld16(tmem + lane_addr + slot * NB + j * 16, v[j]);
@@ -449,12 +554,27 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             bulk_commit();
           }
         } else {
-          uint32_t v[2][16];
+          uint32_t v[2][16], w[2][16];
           tmem_ld16(tmem + lane_addr + slot * NB, v[0]);
           tmem_ld16(tmem + lane_addr + slot * NB + 16, v[1]);
+          if constexpr (Cfg::kSplit) {
+            tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB, w[0]);
+            tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB + 16, w[1]);
+          }
           tmem_ld_wait();
           reg_fence16(v[0]);
           reg_fence16(v[1]);
+          if constexpr (Cfg::kSplit) {
+            reg_fence16(w[0]);
+            reg_fence16(w[1]);
+#pragma unroll
+            for (int k = 0; k < 16; ++k)  // main hi*W_hi (debiased) + the three correction products
+              v[0][k] = __float_as_uint(fmaf(__uint_as_float(v[0][k]), kMainDebias,
+                                             (__uint_as_float(v[1][k]) + __uint_as_float(w[0][k])) +
+                                                 __uint_as_float(w[1][k])));
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[1][k] = 0u;
+          }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
@@ -476,7 +596,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         }
       }
     }
-    if (!kHead && lane == 0) bulk_wait<0>();
+    if (!kHead && !Cfg::kSplit && lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
@@ -556,6 +676,24 @@ __global__ void pack_hidden_f16_kernel(const float* __restrict__ w, const float*
   }
 }
 
+// fp32-accurate hidden pack: W' = W*s (BatchNorm fold, fp32) x 2^8 split into
+// hi = RN16(W'), lo = RN16(W' - hi); pack 0 = hi, pack 1 = lo.
+__global__ void pack_hidden_split_kernel(const float* __restrict__ w, const float* __restrict__ scale,
+                                         uint8_t* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*64 + ci
+  if (idx >= kC * kC) return;
+  const int co = idx / kC, ci = idx % kC;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int ky = t / 3, kx = t % 3;
+    const float wv = (w[idx * 9 + t] * scale[co]) * kSplitWScale;
+    const __half hi = __float2half_rn(wv);
+    const __half lo = __float2half_rn(wv - __half2float(hi));
+    put_b(out, ConvCfg<3>::kWdx, kx, (2 - ky) * 64 + co, ci, hi);
+    put_b(out + ConvCfg<3>::kW1, ConvCfg<3>::kWdx, kx, (2 - ky) * 64 + co, ci, lo);
+  }
+}
+
 __global__ void pack_head_f16_kernel(const float* __restrict__ w, int K, uint8_t* __restrict__ out) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // k*64 + ci
   if (idx >= K * kC) return;
@@ -580,6 +718,7 @@ __global__ void fill_kernel(float* dst, float v, int n) {
 // ------------------------------------------------------------ launchers ----
 
 size_t conv_wpack_bytes(bool head) { return head ? ConvCfg<1>::kW : ConvCfg<0>::kW; }
+size_t conv_wpack_split_bytes() { return ConvCfg<3>::kW; }
 
 // Launched with programmatic stream serialization (PDL): the kernel's
 // prologue overlaps the previous kernel; griddepcontrol.wait guards all
@@ -609,6 +748,14 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
       cfg.blockDim = dim3(ConvCfg<2>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<2>::kSmem;
       return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<2>, tm_in, tm_out, a, p0);
+    case 3:
+      cfg.blockDim = dim3(ConvCfg<3>::kThreads);
+      cfg.dynamicSmemBytes = ConvCfg<3>::kSmem;
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<3>, tm_in, tm_out, a, p0);
+    case 4:
+      cfg.blockDim = dim3(ConvCfg<4>::kThreads);
+      cfg.dynamicSmemBytes = ConvCfg<4>::kSmem;
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<4>, tm_in, tm_out, a, p0);
   }
   return cudaErrorInvalidValue;
 }
@@ -617,6 +764,13 @@ cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* 
   cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<0>::kW, st);
   if (e != cudaSuccess) return e;
   pack_hidden_f16_kernel<<<(kC * kC + 127) / 128, 128, 0, st>>>(w, scale, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<3>::kW, st);
+  if (e != cudaSuccess) return e;
+  pack_hidden_split_kernel<<<(kC * kC + 127) / 128, 128, 0, st>>>(w, scale, out);
   return cudaGetLastError();
 }
 
@@ -642,6 +796,12 @@ cudaError_t configure_kernels() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<2>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<3>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<4>::kSmem);
   if (e != cudaSuccess) return e;
   return configure_edge_kernels();
 }

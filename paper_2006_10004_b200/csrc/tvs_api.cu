@@ -46,11 +46,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// fp16 NHWC activation [B][H][W][64] as a 4-D tensor map, SW128, box (64, box_px, 1, 1)
-CUtensorMap make_act_map(void* base, int B, int H, int W, int box_px) {
+// fp16 NHWC activation [B][H][W][C] (C = 64, or 128 = a hi|lo pair row) as a
+// 4-D tensor map, SW128, box (64, box_px, 1, 1)
+CUtensorMap make_act_map(void* base, int B, int H, int W, int box_px, int C = 64) {
   CUtensorMap m;
-  cuuint64_t dims[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
-  cuuint64_t strides[3] = {128, (cuuint64_t)W * 128, (cuuint64_t)H * W * 128};
+  const cuuint64_t rb = (cuuint64_t)C * 2;
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {rb, (cuuint64_t)W * rb, (cuuint64_t)H * W * rb};
   cuuint32_t box[4] = {64, (cuuint32_t)box_px, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dims, strides, box, estr,
@@ -111,6 +113,13 @@ struct tvs_plan {
   // tcgen05 fp16 path: FAST mode with 64 channels; everything else runs the
   // CUDA-core fp32 path (fp32-accurate mode, and the 128-channel wide variant)
   bool tc_path() const { return mode == TVS_MODE_FAST && channels == 64; }
+  // fp32 mode on tcgen05 with split fp16 operands (conv_tc.cu modes 3/4), opt-in
+  // via TVS_FP32_SPLIT=1: 23x faster than the CUDA-core fp32 kernels but the
+  // tensor core truncates its fp32 accumulator once per MMA, which leaves
+  // 1.0-1.2e-5 worst-band error on the piecewise-constant configs - just
+  // above the 1e-5 gate, so the default stays on CUDA cores
+  bool fp32_split = false;
+  bool split_path() const { return mode == TVS_MODE_FP32 && channels == 64 && fp32_split; }
   size_t act_px_bytes() const { return tc_path() ? 128 : (size_t)channels * 4; }
 };
 
@@ -220,15 +229,47 @@ void drain_profile(tvs_plan* p) {
 void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B, int H, int W, int row0, int rows,
                cudaStream_t st, void* const* act, int max_ctas) {
   const bool fast = p->tc_path();
+  const bool split = p->split_path();
   const int C = p->channels;
   const double px = (double)B * H * W;
-  // K1 (the FAST path fuses it into the first hidden layer's producer)
+  // K1 (the FAST path can fuse it into the first hidden layer's producer)
+  const int fmt = fast ? tvs::kActF16 : (split ? tvs::kActSplit : tvs::kActF32);
   if (!fast || p->unfused_conv0)
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
-                 [&] { return tvs::launch_conv0(fast, C, x, act[0], p->conv0, B, H, W, st); });
+                 [&] { return tvs::launch_conv0(fmt, C, x, act[0], p->conv0, B, H, W, st); });
   // K2 x (depth-2), K3
   int cur = 0;
-  if (fast) {
+  if (split) {
+    // fp32-accurate: split-operand tcgen05 layers on fp16 hi|lo pair rows
+    const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
+    CUtensorMap in_map[2];
+    for (int i = 0; i < 2; ++i) in_map[i] = make_act_map(act[i], B, H, W, tvs::kHaloPx, 128);
+    auto geom = [&](int r0, int nrows) {
+      tvs::ConvArgs a{};
+      a.B = B; a.H = H; a.W = W; a.strips = strips;
+      a.row0 = r0; a.rows = nrows; a.nsub = 1;
+      return a;
+    };
+    for (int l = 0; l < p->n_hidden(); ++l) {
+      tvs::ConvArgs a = geom(0, H);
+      a.wpack = p->wpack + (size_t)l * tvs::conv_wpack_split_bytes();
+      a.shift = p->bhid + (size_t)l * tvs::kC;
+      a.nshift = tvs::kC;
+      a.act_out = static_cast<uint8_t*>(act[cur ^ 1]);
+      const int grid = conv_grid(max_ctas, a);
+      timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64,
+                   [&] { return tvs::launch_conv_tc(3, in_map[cur], in_map[cur], a, nullptr, grid, st); });
+      cur ^= 1;
+    }
+    tvs::ConvArgs a = geom(row0, rows);
+    a.wpack = p->hpack;
+    a.shift = p->bh;
+    a.nshift = p->out_bands;
+    a.x = x; a.bands = bands; a.closure = closure; a.K = p->out_bands;
+    const int grid = conv_grid(max_ctas, a);
+    timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands,
+                 [&] { return tvs::launch_conv_tc(4, in_map[cur], in_map[cur], a, nullptr, grid, st); });
+  } else if (fast) {
     const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
     CUtensorMap in_map[2], out_map[2];
     for (int i = 0; i < 2; ++i) {
@@ -379,6 +420,7 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
     if (const char* e = std::getenv("TVS_REVERSE_SUB")) p->l2_reverse_sub = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("TVS_L2_CHUNK_MB")) p->l2_chunk_bytes = (size_t)std::atoll(e) << 20;
     if (const char* e = std::getenv("TVS_FUSE_CONV0")) p->unfused_conv0 = std::atoi(e) == 0;
+    if (const char* e = std::getenv("TVS_FP32_SPLIT")) p->fp32_split = std::atoi(e) != 0;
     try {
       TVS_CUDA(tvs::configure_kernels());
       const int nh = depth - 2;
@@ -388,6 +430,9 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
       TVS_CUDA(cudaMalloc(&p->shid, (size_t)nh * channels * 4));
       if (p->tc_path()) {
         TVS_CUDA(cudaMalloc(&p->wpack, (size_t)nh * tvs::conv_wpack_bytes(false)));
+        TVS_CUDA(cudaMalloc(&p->hpack, tvs::conv_wpack_bytes(true)));
+      } else if (p->split_path()) {
+        TVS_CUDA(cudaMalloc(&p->wpack, (size_t)nh * tvs::conv_wpack_split_bytes()));
         TVS_CUDA(cudaMalloc(&p->hpack, tvs::conv_wpack_bytes(true)));
       } else
         TVS_CUDA(cudaMalloc(&p->whid, (size_t)nh * channels * channels * 9 * 4));
@@ -432,12 +477,16 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
       if (p->tc_path()) {
         TVS_CUDA(tvs::launch_pack_hidden_f16(w_dev[l + 1], dst_scale,
                                              p->wpack + (size_t)l * tvs::conv_wpack_bytes(false), st));
+      } else if (p->split_path()) {
+        TVS_CUDA(tvs::launch_pack_hidden_split(w_dev[l + 1], dst_scale,
+                                               p->wpack + (size_t)l * tvs::conv_wpack_split_bytes(), st));
       } else {
         TVS_CUDA(cudaMemcpyAsync(p->whid + (size_t)l * C * C * 9, w_dev[l + 1], (size_t)C * C * 9 * 4,
                                  cudaMemcpyDeviceToDevice, st));
       }
     }
-    if (p->tc_path()) TVS_CUDA(tvs::launch_pack_head_f16(w_dev[p->depth - 1], p->out_bands, p->hpack, st));
+    if (p->tc_path() || p->split_path())
+      TVS_CUDA(tvs::launch_pack_head_f16(w_dev[p->depth - 1], p->out_bands, p->hpack, st));
     p->weights_ready = true;
   });
 }
