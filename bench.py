@@ -243,27 +243,27 @@ def run_ours(args, spec):
     total_px = (spec.batch * spec.height * spec.width) if _scaling(spec) == "strong" else world * px_out
     flush = torch.empty(256 << 20 >> 2, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
-    precs = ["fast"] + (["fp32", "fp32split"] if args.fp32_steps > 0 else [])
-    if spec.channels != 64:
-        precs = [p for p in precs if p != "fp32split"]
+    precs = ["fast"] + (["fp32"] if args.fp32_fast_steps > 0 else [])
+    if args.fp32_steps > 0 and spec.channels == 64:
+        precs.append("fp32cuda")
     results = {}
     for prec in precs:
-        model = TVSpecNet(spec.depth, spec.channels, 5, precision="fp32" if prec == "fp32split" else prec).eval()
+        model = TVSpecNet(spec.depth, spec.channels, 5, precision="fp32" if prec == "fp32cuda" else prec).eval()
         model.load_state_dict(state)
         bands = torch.empty((B, 5, nrows, W), device=dev)
         clos = torch.empty((B, 1, nrows, W), device=dev)
-        if prec == "fp32split":  # opt-in tcgen05 split-operand fp32 mode (read at plan creation)
-            os.environ["TVS_FP32_SPLIT"] = "1"
+        if prec == "fp32cuda":  # the CUDA-core fp32 kernels (read at plan creation)
+            os.environ["TVS_FP32_CUDA"] = "1"
         plan = model._plan_for(dev)
-        os.environ.pop("TVS_FP32_SPLIT", None)
+        os.environ.pop("TVS_FP32_CUDA", None)
 
         def step():
             plan.forward(x.data_ptr(), bands.data_ptr(), clos.data_ptr(), B, H, W, row0, nrows,
                          torch.cuda.current_stream().cuda_stream)
 
         steps = args.steps if prec == "fast" else max(1, min(args.steps, args.fp32_steps))
-        if prec == "fp32split":
-            steps = max(1, min(args.steps, 10))
+        if prec == "fp32":
+            steps = max(1, min(args.steps, args.fp32_fast_steps))
         warm = args.warmup if prec == "fast" else max(1, min(args.warmup, 3))
         if world > 1:
             dist.barrier()
@@ -363,12 +363,11 @@ def run_ours(args, spec):
         r32 = results["fp32"]
         line["fp32_mode"] = {"value": round(r32["value"], 3), "unit": UNIT, "ms_per_step": round(r32["ms"], 3),
                              "steps": r32["steps"], "e2e": round(r32["e2e"], 3)}
-    if "fp32split" in results:
-        r = results["fp32split"]
-        line["fp32_split_mode"] = {"value": round(r["value"], 3), "unit": UNIT, "ms_per_step": round(r["ms"], 3),
-                                   "steps": r["steps"], "opt_in": "TVS_FP32_SPLIT=1",
-                                   "note": "tcgen05 split fp16 operands; 1.0-1.2e-5 worst-band on "
-                                           "piecewise-constant inputs (gate 1e-5), see DESIGN.md"}
+    if "fp32cuda" in results:
+        r = results["fp32cuda"]
+        line["fp32_mode_cuda_cores"] = {"value": round(r["value"], 3), "unit": UNIT,
+                                        "ms_per_step": round(r["ms"], 3), "steps": r["steps"],
+                                        "note": "TVS_FP32_CUDA=1: fp32 FFMA + fp64 combine kernels"}
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         mp_s, secs = cpu_reference(spec, 1, 0, spec.batch, threads, budget_s=args.cpu_seconds)
@@ -391,7 +390,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample budget (s)")
     ap.add_argument("--ref-step-seconds", type=float, default=4.0, help="--impl reference: seconds per step")
-    ap.add_argument("--fp32-steps", type=int, default=None, help="fp32-accurate mode steps (0 = skip)")
+    ap.add_argument("--fp32-steps", type=int, default=None,
+                    help="steps of the CUDA-core fp32 kernels (TVS_FP32_CUDA=1) (0 = skip)")
+    ap.add_argument("--fp32-fast-steps", type=int, default=10,
+                    help="steps of the fp32-accurate mode (tcgen05 split operands) (0 = skip)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-max-images", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")

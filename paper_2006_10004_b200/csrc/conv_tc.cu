@@ -42,6 +42,7 @@ namespace tvs {
 // segments: maximal runs of consecutive rows inside one (image, strip) column.
 struct Segment {
   int b, x0, ya, yb;
+  int h;  // output-channel half (split hidden layer visits every segment twice)
 };
 struct SegIter {
   // [cur, end) of the current sub-range; sub-ranges are visited last-first
@@ -49,7 +50,10 @@ struct SegIter {
   // wrote last (those are still L2-resident).
   long long lo, hi, cur, end;
   int sub, nsub;
-  TVS_DEV SegIter(const ConvArgs& a) {
+  int nh = 1;          // visits per segment (2: once per output-channel half)
+  bool pend = false;   // second visit of `last` outstanding
+  Segment last;
+  TVS_DEV SegIter(const ConvArgs& a, int halves = 1) : nh(halves) {
     const long long T = (long long)a.B * a.strips * a.rows;
     lo = T * blockIdx.x / gridDim.x;
     hi = T * (blockIdx.x + 1) / gridDim.x;
@@ -63,6 +67,12 @@ struct SegIter {
     end = lo + (hi - lo) * (k + 1) / nsub;
   }
   TVS_DEV bool next(const ConvArgs& a, Segment& g) {
+    if (pend) {
+      g = last;
+      g.h = 1;
+      pend = false;
+      return true;
+    }
     while (cur >= end) {
       if (++sub >= nsub) return false;
       set_sub();
@@ -74,7 +84,12 @@ struct SegIter {
     g.x0 = (int)(col % a.strips) * kStripPx;
     g.ya = a.row0 + y0;
     g.yb = g.ya + n;
+    g.h = 0;
     cur += n;
+    if (nh == 2) {
+      last = g;
+      pend = true;
+    }
     return true;
   }
 };
@@ -100,9 +115,12 @@ struct ConvCfg {
   // SM sub-partition (register file: 16K regs per SMSP, so 128 regs/thread)
   static constexpr int kGroups = kFirst ? 2 : kEpiGroups;
   static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kGroups);
-  static constexpr int NB = kHead ? 32 : 64;          // TMEM columns per output row (slot)
+  // split hidden layer: two passes of 32 output channels (TMEM room for three rings)
+  static constexpr bool kHalves = kSplit && !kHead;
+  static constexpr int NB = (kHead || kHalves) ? 32 : 64;  // TMEM columns per output row (slot)
   static constexpr int kWdx = 3 * NB * 128;           // B bytes per dx (3 dy blocks x NB rows x 128 B)
-  static constexpr int kW1 = 3 * kWdx;                // one weight pack
+  static constexpr int kWhalf = 3 * kWdx;             // one channel half (all dx)
+  static constexpr int kW1 = kWhalf * (kHalves ? 2 : 1);  // one weight pack
   static constexpr int kW = (kSplit && !kHead) ? 2 * kW1 : kW1;  // split hidden: hi pack | lo pack
   static constexpr int kTmemCols = kSplit ? 512 : kSlots * NB;  // 512 / 256 (split: two rings)
   static constexpr int kPasses = kSplit ? (kHead ? 2 : 3) : 1;
@@ -122,19 +140,30 @@ struct ConvCfg {
   // expected truncation loss of the main ring back (kMainDebias) and sums.
   // (the split head likewise: hi*[W_hi|W_lo] in the main ring, lo*[W_hi|W_lo]
   // in the correction ring, 8 slots x 32 columns each)
+  // The split hidden layer goes one step further: its 32-channel passes leave
+  // room for the hi*hi products of input channels 0-31 and 32-63 in two
+  // separate rings (18 MMAs each: half the accumulated magnitude, half the
+  // truncations), plus the correction ring.
   static constexpr bool kTwoRings = kSplit;
   static constexpr int kRing = kTwoRings ? (kHead ? 8 : 4) : kSlots;
   static constexpr uint32_t kRingMask = kRing - 1;
   static constexpr int kRingLog = kRing == 4 ? 2 : 3;
-  static constexpr uint32_t kCorrCol = kRing * NB;
-  static constexpr uint32_t ring_col(int p) { return (kTwoRings && p > 0) ? kCorrCol : 0; }
-  static constexpr bool enters(int p) { return p == 0 || (kTwoRings && p == 1); }  // first pass into a ring
+  static constexpr uint32_t kOddCol = kRing * NB;                      // split hidden: 2nd main ring
+  static constexpr uint32_t kCorrCol = kHalves ? 2 * kRing * NB : kRing * NB;
+  // TMEM ring of pass p, K step k; whether (p, k) (at dx 0) is the first MMA into that ring
+  static constexpr uint32_t ring_col(int p, int k) {
+    return !kTwoRings ? 0 : (kHalves ? (p == 0 ? (k < 2 ? 0 : kOddCol) : kCorrCol) : (p > 0 ? kCorrCol : 0));
+  }
+  static constexpr bool enters(int p, int k) {
+    return kHalves ? ((p == 0 && (k == 0 || k == 2)) || (p == 1 && k == 0)) : (k == 0 && (p == 0 || (kTwoRings && p == 1)));
+  }
 };
 constexpr float kSplitWScale = 256.0f;  // split hidden weights are packed x 2^8
 // 1 + E[truncation loss] of the main accumulator: 36 MMAs, each losing 0.5 ulp of
 // a partial sum that grows ~linearly to the result, E[ulp(x)/|x|] = 0.7213 * 2^-23
 // over a binade (tools/emulate_split_accum.py: 1.2e-5 -> 5.1e-6 worst band)
 constexpr float kMainDebias = 1.0f + 0.5f * 0.7213f * 18.0f * 1.1920929e-7f;
+constexpr float kMainDebias18 = 1.0f + 0.5f * 0.7213f * 9.0f * 1.1920929e-7f;  // a ring of 18 MMAs
 
 template <int kMode>
 __global__ void __launch_bounds__(ConvCfg<kMode>::kThreads, 1)
@@ -191,7 +220,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const int hco = pt & 63;                         // its channel
     int stage = 0;
     uint32_t phase = 0;
-    SegIter it(a);
+    SegIter it(a, Cfg::kHalves ? 2 : 1);
     Segment g;
     while (it.next(a, g)) {
       const float* img = a.x + (long long)g.b * a.H * a.W;
@@ -258,7 +287,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
       prefetch_tmap(&tm_in);
       int stage = 0;
       uint32_t phase = 0;
-      SegIter it(a);
+      SegIter it(a, Cfg::kHalves ? 2 : 1);
       Segment g;
       while (it.next(a, g)) {
         const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
@@ -289,7 +318,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     uint32_t phase = 0;
     uint32_t seq = 0;  // output-row sequence number: slot = seq % kRing, use = seq / kRing
     bool prewaited = false;  // this row's barriers were already awaited by the previous row
-    SegIter it(a);
+    SegIter it(a, Cfg::kHalves ? 2 : 1);
     Segment g;
     while (it.next(a, g)) {
       const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
@@ -313,6 +342,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             tc_fence_after();
             const uint64_t ad_row = adesc0 + (uint64_t)((stage * Cfg::kStageBytes) >> 4);
             const uint32_t t0s = s * NB;  // slot column offset inside a ring
+            const uint32_t hoff = (uint32_t)g.h * Cfg::kWhalf;  // B offset of the channel half
             constexpr uint32_t b1 = NB * 128 / 16, b2 = 2 * NB * 128 / 16;  // W(dy=0), W(dy=-1) blocks
             auto prewait = [&](int p, int dx, int k) {
               if (p == Cfg::kPasses / 2 && dx == 1 && k == 1 && next_fast)
@@ -328,9 +358,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                   const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p) + dx * 128 + k * 32) >> 4);
-                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + dx * Cfg::kWdx + k * 32) >> 4);
-                  const bool first_k = Cfg::enters(p) && dx == 0 && k == 0;
-                  const uint32_t rb = tmem + Cfg::ring_col(p), t0 = rb + t0s;
+                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + k * 32) >> 4);
+                  const bool first_k = Cfg::enters(p, k) && dx == 0;
+                  const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + t0s;
                   if (first_k) {  // enter row r+1 (acc=0), keep r-1, r
                     mma_f16_ss_fill(t0 + 2 * NB, ad, bd + b2, idesc1, 0u);
                     mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
@@ -347,9 +377,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                   const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p) + dx * 128 + k * 32) >> 4);
-                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + dx * Cfg::kWdx + k * 32) >> 4);
-                  const bool first_k = Cfg::enters(p) && dx == 0 && k == 0;
-                  const uint32_t rb = tmem + Cfg::ring_col(p), t0 = rb + t0s;
+                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + k * 32) >> 4);
+                  const bool first_k = Cfg::enters(p, k) && dx == 0;
+                  const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + t0s;
                   mma_f16_ss_fill(rb, ad, bd + b2, idesc1, first_k ? 0u : 1u);
                   mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
                   prewait(p, dx, k);
@@ -362,9 +392,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                   const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p) + dx * 128 + k * 32) >> 4);
-                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + dx * Cfg::kWdx + k * 32) >> 4);
-                  const bool first_k = Cfg::enters(p) && dx == 0 && k == 0;
-                  const uint32_t rb = tmem + Cfg::ring_col(p), t0 = rb + t0s;
+                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + k * 32) >> 4);
+                  const bool first_k = Cfg::enters(p, k) && dx == 0;
+                  const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + t0s;
                   mma_f16_ss_fill(t0, ad, bd, idesc1, 1u);
                   if (first_k) {
                     mma_f16_ss_use(rb, ad, bd + b1, idesc1, 1u);
@@ -425,9 +455,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p) + dx * 128 + k * 32) >> 4);
-              const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + dx * Cfg::kWdx + k * 32) >> 4);
-              const uint32_t rb = tmem + Cfg::ring_col(p);
-              if (Cfg::enters(p) && dx == 0 && k == 0) {
+              const uint64_t bd =
+                  bdesc0 + (uint64_t)((Cfg::b_off(p) + (uint32_t)g.h * Cfg::kWhalf + dx * Cfg::kWdx + k * 32) >> 4);
+              const uint32_t rb = tmem + Cfg::ring_col(p, k);
+              if (Cfg::enters(p, k) && dx == 0) {
                 if (vA) mma_f16_ss(rb + At, ad, bd + Ab, Ai, 1u);
                 if (vB) mma_f16_ss(rb + Bt, ad, bd + Bb, Bi, 0u);
                 if (vC) mma_f16_ss(rb + Ct, ad, bd + Cb, Ci, 1u);
@@ -458,7 +489,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const uint32_t shift_u = smem_u32(sShift);
     if (!kHead && !Cfg::kSplit && lane == 0) prefetch_tmap(&tm_out);
     uint32_t seq = 0, gsel = 0;  // gsel = seq % kGroups
-    SegIter it(a);
+    SegIter it(a, Cfg::kHalves ? 2 : 1);
     Segment g;
     while (it.next(a, g)) {
       for (int q = g.ya; q < g.yb; ++q, ++seq, gsel = (gsel + 1 == Cfg::kGroups) ? 0 : gsel + 1) {
@@ -468,53 +499,50 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         tc_fence_after();
         const int xg = g.x0 + px;
         if constexpr (Cfg::kSplit && !kHead) {
-          // z = main * kMainDebias + corr (x 2^-8) + shift, ReLU, re-split into
-          // an fp16 pair; one pixel per lane, 128 B hi + 128 B lo straight to
-          // global.  Two 32-channel halves keep the register footprint low.
-          uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * 256;
+          // channels 32h..32h+31: z = (E + O) debiased + corrections (x 2^-8) +
+          // shift, ReLU, re-split into an fp16 pair; one pixel per lane, 64 B hi
+          // + 64 B lo straight to global
+          uint32_t e[2][16], o[2][16], c[2][16];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t v[2][16], w[2][16];
+          for (int j = 0; j < 2; ++j) {
+            tmem_ld16(tmem + lane_addr + slot * NB + j * 16, e[j]);
+            tmem_ld16(tmem + lane_addr + Cfg::kOddCol + slot * NB + j * 16, o[j]);
+            tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB + j * 16, c[j]);
+          }
+          tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              tmem_ld16(tmem + lane_addr + slot * NB + h * 32 + j * 16, v[j]);
-              tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB + h * 32 + j * 16, w[j]);
-            }
-            tmem_ld_wait();
+          for (int j = 0; j < 2; ++j) { reg_fence16(e[j]); reg_fence16(o[j]); reg_fence16(c[j]); }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&slot_empty[slot]);
+          if (xg < a.W) {
+            uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * 256 + g.h * 64;
 #pragma unroll
-            for (int j = 0; j < 2; ++j) { reg_fence16(v[j]); reg_fence16(w[j]); }
-            if (h == 1) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&slot_empty[slot]);
-            }
-            if (xg < a.W) {
+            for (int chunk = 0; chunk < 4; ++chunk) {
+              const uint32_t sh_u = shift_u + (uint32_t)(g.h * 32 + chunk * 8) * 4;
+              const float4 s0 = ld_shared_f4(sh_u);
+              const float4 s1 = ld_shared_f4(sh_u + 16);
+              const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+              uint32_t hi[4], lo[4];
 #pragma unroll
-              for (int cc = 0; cc < 4; ++cc) {
-                const int chunk = h * 4 + cc;
-                const float4 s0 = ld_shared_f4(shift_u + chunk * 32);
-                const float4 s1 = ld_shared_f4(shift_u + chunk * 32 + 16);
-                const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-                uint32_t hi[4], lo[4];
+              for (int t2 = 0; t2 < 4; ++t2) {
+                float f[2];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  float f[2];
-#pragma unroll
-                  for (int t = 0; t < 2; ++t) {
-                    const int c = cc * 8 + e * 2 + t;  // channel within the half
-                    const float z = fmaf(__uint_as_float(v[c >> 4][c & 15]), kMainDebias,
-                                         __uint_as_float(w[c >> 4][c & 15]));
-                    f[t] = fmaxf(fmaf(z, 1.0f / kSplitWScale, sh[2 * e + t]), 0.0f);
-                  }
-                  const __half2 hh = __floats2half2_rn(f[0], f[1]);
-                  const float2 hf = __half22float2(hh);
-                  const __half2 ll = __floats2half2_rn(f[0] - hf.x, f[1] - hf.y);
-                  hi[e] = *reinterpret_cast<const uint32_t*>(&hh);
-                  lo[e] = *reinterpret_cast<const uint32_t*>(&ll);
+                for (int t = 0; t < 2; ++t) {
+                  const int ch = chunk * 8 + t2 * 2 + t;  // channel within the half
+                  const float z = fmaf(__uint_as_float(e[ch >> 4][ch & 15]), kMainDebias18,
+                                       fmaf(__uint_as_float(o[ch >> 4][ch & 15]), kMainDebias18,
+                                            __uint_as_float(c[ch >> 4][ch & 15])));
+                  f[t] = fmaxf(fmaf(z, 1.0f / kSplitWScale, sh[t2 * 2 + t]), 0.0f);
                 }
-                *reinterpret_cast<uint4*>(dst + chunk * 16) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                *reinterpret_cast<uint4*>(dst + 128 + chunk * 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                const __half2 hh = __floats2half2_rn(f[0], f[1]);
+                const float2 hf = __half22float2(hh);
+                const __half2 ll = __floats2half2_rn(f[0] - hf.x, f[1] - hf.y);
+                hi[t2] = *reinterpret_cast<const uint32_t*>(&hh);
+                lo[t2] = *reinterpret_cast<const uint32_t*>(&ll);
               }
+              *reinterpret_cast<uint4*>(dst + chunk * 16) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+              *reinterpret_cast<uint4*>(dst + 128 + chunk * 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
             }
           }
         } else if constexpr (!kHead) {
@@ -689,8 +717,10 @@ __global__ void pack_hidden_split_kernel(const float* __restrict__ w, const floa
     const float wv = (w[idx * 9 + t] * scale[co]) * kSplitWScale;
     const __half hi = __float2half_rn(wv);
     const __half lo = __float2half_rn(wv - __half2float(hi));
-    put_b(out, ConvCfg<3>::kWdx, kx, (2 - ky) * 64 + co, ci, hi);
-    put_b(out + ConvCfg<3>::kW1, ConvCfg<3>::kWdx, kx, (2 - ky) * 64 + co, ci, lo);
+    // channel half h = co / 32: rows (2-ky)*32 + co%32 of that half's dx block
+    uint8_t* base = out + (co >> 5) * ConvCfg<3>::kWhalf;
+    put_b(base, ConvCfg<3>::kWdx, kx, (2 - ky) * 32 + (co & 31), ci, hi);
+    put_b(base + ConvCfg<3>::kW1, ConvCfg<3>::kWdx, kx, (2 - ky) * 32 + (co & 31), ci, lo);
   }
 }
 

@@ -113,12 +113,10 @@ struct tvs_plan {
   // tcgen05 fp16 path: FAST mode with 64 channels; everything else runs the
   // CUDA-core fp32 path (fp32-accurate mode, and the 128-channel wide variant)
   bool tc_path() const { return mode == TVS_MODE_FAST && channels == 64; }
-  // fp32 mode on tcgen05 with split fp16 operands (conv_tc.cu modes 3/4), opt-in
-  // via TVS_FP32_SPLIT=1: 23x faster than the CUDA-core fp32 kernels but the
-  // tensor core truncates its fp32 accumulator once per MMA, which leaves
-  // 1.0-1.2e-5 worst-band error on the piecewise-constant configs - just
-  // above the 1e-5 gate, so the default stays on CUDA cores
-  bool fp32_split = false;
+  // fp32-accurate mode on tcgen05 with split fp16 operands (conv_tc.cu modes
+  // 3/4).  TVS_FP32_CUDA=1 selects the CUDA-core fp32 kernels
+  // (also used for the 128-channel wide variant).
+  bool fp32_split = true;
   bool split_path() const { return mode == TVS_MODE_FP32 && channels == 64 && fp32_split; }
   size_t act_px_bytes() const { return tc_path() ? 128 : (size_t)channels * 4; }
 };
@@ -420,7 +418,7 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
     if (const char* e = std::getenv("TVS_REVERSE_SUB")) p->l2_reverse_sub = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("TVS_L2_CHUNK_MB")) p->l2_chunk_bytes = (size_t)std::atoll(e) << 20;
     if (const char* e = std::getenv("TVS_FUSE_CONV0")) p->unfused_conv0 = std::atoi(e) == 0;
-    if (const char* e = std::getenv("TVS_FP32_SPLIT")) p->fp32_split = std::atoi(e) != 0;
+    if (const char* e = std::getenv("TVS_FP32_CUDA")) p->fp32_split = std::atoi(e) == 0;
     try {
       TVS_CUDA(tvs::configure_kernels());
       const int nh = depth - 2;

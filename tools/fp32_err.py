@@ -23,3 +23,17 @@ for case in ("small", "nonsq", "crop", "cfg1"):
         out = m(torch.from_numpy(g[f"{case}_x"]).cuda()).cpu().numpy()
     e = band_rel_l2(out, g[f"{case}_y"])
     print(f"{case:6s} worst {e.max():.3e} mean {e.mean():.3e}", flush=True)
+if "--configs" in sys.argv:
+    from paper_2006_10004_b200.workloads import CONFIGS, make_batch
+
+    ora = oracle_from_state(state)
+    for cfg, n, crop in ((3, 1, None), (5, 2, None), (4, 1, (0, 0, 512, 1024))):
+        x = make_batch(CONFIGS[cfg], 0, n)
+        if crop:
+            y0, x0, h, w = crop
+            x = np.ascontiguousarray(x[:, :, y0:y0 + h, x0:x0 + w])
+        with torch.no_grad():
+            ref = ora(torch.from_numpy(x)).numpy()
+            out = m(torch.from_numpy(x).cuda()).cpu().numpy()
+        e = band_rel_l2(out, ref)
+        print(f"cfg{cfg}{'crop' if crop else ''} worst {e.max():.3e} mean {e.mean():.3e}", flush=True)
