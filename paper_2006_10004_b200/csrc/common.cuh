@@ -48,18 +48,21 @@ constexpr int kMaxBands = 8;
 // host-side launchers (defined next to their kernels)
 size_t conv_wpack_bytes(bool head);
 size_t conv_wpack_split_bytes();  // fp32-accurate hidden layer: hi pack | lo pack
+size_t conv_wpack_wide_bytes(bool head);  // wide variant (128 ch) on tcgen05: 4 quarter packs / head pack
 struct Conv0Params;
 cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a,
                            const Conv0Params* c0, int grid, cudaStream_t st);
 cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
 cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
+cudaError_t launch_pack_hidden_wide(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
+cudaError_t launch_pack_head_wide(const float* w, int K, uint8_t* out, cudaStream_t st);
 cudaError_t launch_pack_head_f16(const float* w, int K, uint8_t* out, cudaStream_t st);
 cudaError_t launch_fill(float* dst, float v, int n, cudaStream_t st);
 struct Conv0Params {  // passed by value: lives in the kernel's constant bank
   float w[kMaxC * 9];  // [co][ky*3+kx]
   float b[kMaxC];
 };
-// act_fmt: 0 = fp16 NHWC, 1 = fp32 NHWC, 2 = fp16 hi/lo pair NHWC (256 B/px, C = 64)
+// act_fmt: 0 = fp16 NHWC, 1 = fp32 NHWC, 2 = fp16 hi/lo pair NHWC (4*C bytes/px: hi C | lo C)
 constexpr int kActF16 = 0, kActF32 = 1, kActSplit = 2;
 cudaError_t launch_conv0(int act_fmt, int C, const float* x, void* act, const Conv0Params& p, int B, int H,
                          int W, cudaStream_t st);

@@ -30,6 +30,8 @@
 // then kEpiGroups groups of 4 epilogue warps (output rows round-robin over the
 // groups); every epilogue warp owns one TMEM lane quarter (32 pixels) and
 // stores independently.
+#include <algorithm>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -53,10 +55,13 @@ struct SegIter {
   int nh = 1;          // visits per segment (2: once per output-channel half)
   bool pend = false;   // second visit of `last` outstanding
   Segment last;
-  TVS_DEV SegIter(const ConvArgs& a, int halves = 1) : nh(halves) {
+  // `parts` = 4: the grid is split into groups of 4 CTAs (one per output-channel
+  // quarter) that walk the same strip-row range
+  TVS_DEV SegIter(const ConvArgs& a, int halves = 1, int parts = 1) : nh(halves) {
     const long long T = (long long)a.B * a.strips * a.rows;
-    lo = T * blockIdx.x / gridDim.x;
-    hi = T * (blockIdx.x + 1) / gridDim.x;
+    const long long part = blockIdx.x / parts, nparts = gridDim.x / parts;
+    lo = T * part / nparts;
+    hi = T * (part + 1) / nparts;
     nsub = a.reverse ? a.nsub : 1;
     sub = 0;
     set_sub();
@@ -103,11 +108,21 @@ struct SegIter {
 // (keeps lo normal), and every tap runs three products hi*hi + lo*hi + hi*lo
 // (head: two, its B pack already carries hi|lo columns) into the same fp32
 // TMEM accumulators; the epilogue unscales and re-splits.
+// 5 / 6 = the wide variant (128 channels, fast mode) hidden layer / head on
+// split activations (hi/lo fp16 pairs) and single fp16 weights: fp16 rounding
+// of the activations alone would cost 1.06e-2 over 26 layers (gate 1e-2).
+// Mode 5 CTAs come in groups of 4, one 32-output-channel quarter each (its
+// 72 KB weight slice stays resident; the 4 CTAs share input rows via L2).
 template <int kMode>
 struct ConvCfg {
   static constexpr bool kSplit = kMode >= 3;
-  static constexpr bool kHead = kMode == 1 || kMode == 4;
+  static constexpr bool kHead = kMode == 1 || kMode == 4 || kMode == 6;
   static constexpr bool kFirst = kMode == 2;
+  static constexpr bool kWide = kMode >= 5;
+  static constexpr bool kQuarters = kMode == 5;
+  static constexpr int kCin = kWide ? 128 : 64;
+  static constexpr int kKBlk = kCin / 64;        // 64-channel K blocks (one SW128 row buffer each)
+  static constexpr int kKSteps = 4 * kKBlk;      // K16 steps per tap
   static constexpr int kProdWarps = kFirst ? 4 : 1;
   static constexpr int kMmaWarp = kProdWarps;
   static constexpr int kEpiWarp0 = kProdWarps + 1;
@@ -116,21 +131,25 @@ struct ConvCfg {
   static constexpr int kGroups = kFirst ? 2 : kEpiGroups;
   static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kGroups);
   // split hidden layer: two passes of 32 output channels (TMEM room for three rings)
-  static constexpr bool kHalves = kSplit && !kHead;
-  static constexpr int NB = (kHead || kHalves) ? 32 : 64;  // TMEM columns per output row (slot)
-  static constexpr int kWdx = 3 * NB * 128;           // B bytes per dx (3 dy blocks x NB rows x 128 B)
+  static constexpr bool kHalves = kMode == 3;
+  static constexpr int NB = (kHead || kHalves || kQuarters) ? 32 : 64;  // TMEM columns per output row (slot)
+  static constexpr int kWdxBlk = 3 * NB * 128;        // B bytes per dx and K block (3 dy x NB rows x 128 B)
+  static constexpr int kWdx = kKBlk * kWdxBlk;        // B bytes per dx
   static constexpr int kWhalf = 3 * kWdx;             // one channel half (all dx)
   static constexpr int kW1 = kWhalf * (kHalves ? 2 : 1);  // one weight pack
-  static constexpr int kW = (kSplit && !kHead) ? 2 * kW1 : kW1;  // split hidden: hi pack | lo pack
-  static constexpr int kTmemCols = kSplit ? 512 : kSlots * NB;  // 512 / 256 (split: two rings)
-  static constexpr int kPasses = kSplit ? (kHead ? 2 : 3) : 1;
-  static constexpr int kNStages = kSplit ? (kHead ? 5 : 2) : kStages;  // input-row ring depth
-  static constexpr int kStageBytes = kSplit ? 2 * kInRowStride : kInRowStride;  // hi row | lo row
+  static constexpr int kW = kHalves ? 2 * kW1 : kW1;  // fp32 hidden: hi pack | lo pack
+  static constexpr int kPasses = kMode == 3 ? 3 : (kSplit ? 2 : 1);
+  static constexpr int kNStages = kSplit ? ((kMode == 4) ? 5 : 2) : kStages;  // input-row ring depth
+  // one stage: [hi K blocks][lo K blocks], one 17 KB SW128 row buffer each
+  static constexpr int kStageBytes = (kSplit ? 2 : 1) * kKBlk * kInRowStride;
   static constexpr int kStageOut = (kHead || kSplit) ? 0 : 32 * 128;  // per-warp TMA-store staging
   static constexpr size_t kSmem = 1024 + kW + kNStages * kStageBytes + 4 * kGroups * kStageOut + 1024;
-  // A / B descriptor offsets (bytes) of pass p
-  static constexpr uint32_t a_off(int p) { return (kSplit && p == 1) ? kInRowStride : 0; }
-  static constexpr uint32_t b_off(int p) { return (kSplit && !kHead && p == 2) ? kW1 : 0; }
+  // A / B descriptor offsets (bytes) of pass p, K step k (within-block k%4 added by the caller)
+  static constexpr uint32_t a_off(int p, int k) {
+    return ((kSplit && p == 1) ? kKBlk * kInRowStride : 0) + (k / 4) * kInRowStride;
+  }
+  static constexpr uint32_t b_off(int p) { return (kHalves && p == 2) ? kW1 : 0; }
+  static constexpr uint32_t b_koff(int k) { return (k / 4) * kWdxBlk + (k % 4) * 32; }
   // TMEM accumulator rings.  tcgen05 f16 MMAs add their products exactly and
   // truncate the fp32 accumulator toward zero once per MMA
   // (tools/probe_mma_rounding.cu), so every MMA into an accumulator costs it
@@ -144,8 +163,9 @@ struct ConvCfg {
   // room for the hi*hi products of input channels 0-31 and 32-63 in two
   // separate rings (18 MMAs each: half the accumulated magnitude, half the
   // truncations), plus the correction ring.
-  static constexpr bool kTwoRings = kSplit;
+  static constexpr bool kTwoRings = kMode == 3 || kMode == 4;  // the fp32-accurate modes
   static constexpr int kRing = kTwoRings ? (kHead ? 8 : 4) : kSlots;
+  static constexpr int kTmemCols = kTwoRings ? 512 : kSlots * NB;  // 512 / 256
   static constexpr uint32_t kRingMask = kRing - 1;
   static constexpr int kRingLog = kRing == 4 ? 2 : 3;
   static constexpr uint32_t kOddCol = kRing * NB;                      // split hidden: 2nd main ring
@@ -155,8 +175,12 @@ struct ConvCfg {
     return !kTwoRings ? 0 : (kHalves ? (p == 0 ? (k < 2 ? 0 : kOddCol) : kCorrCol) : (p > 0 ? kCorrCol : 0));
   }
   static constexpr bool enters(int p, int k) {
-    return kHalves ? ((p == 0 && (k == 0 || k == 2)) || (p == 1 && k == 0)) : (k == 0 && (p == 0 || (kTwoRings && p == 1)));
+    return kHalves ? ((p == 0 && (k == 0 || k == 2)) || (p == 1 && k == 0))
+                   : (k == 0 && (p == 0 || (kTwoRings && p == 1)));
   }
+  static constexpr int kParts = kQuarters ? 4 : 1;   // SegIter grid partition
+  static constexpr int kVisits = kHalves ? 2 : 1;    // SegIter visits per segment
+  static constexpr int kPxBytes = kSplit ? 4 * kCin : 2 * kCin;  // activation bytes per pixel
 };
 constexpr float kSplitWScale = 256.0f;  // split hidden weights are packed x 2^8
 // 1 + E[truncation loss] of the main accumulator: 36 MMAs, each losing 0.5 ulp of
@@ -175,7 +199,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t full[kStages], empty[kStages], slot_full[kSlots], slot_empty[kSlots], wbar;
   __shared__ uint32_t tmem_base_smem;
-  __shared__ __align__(16) float sShift[kC];
+  __shared__ __align__(16) float sShift[kMaxC];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
   uint8_t* sIn = sW + Cfg::kW;
@@ -190,13 +214,14 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     mbar_init(&wbar, 1);
     fence_barrier_init();
   }
-  if (threadIdx.x < kC) sShift[threadIdx.x] = (threadIdx.x < a.nshift) ? a.shift[threadIdx.x] : 0.0f;
+  if (threadIdx.x < kMaxC) sShift[threadIdx.x] = (threadIdx.x < a.nshift) ? a.shift[threadIdx.x] : 0.0f;
   if (warp == Cfg::kMmaWarp) tmem_alloc<Cfg::kTmemCols>(&tmem_base_smem);
   // weights do not depend on the previous layer: start their load before the
   // PDL wait so it overlaps the previous kernel's tail
   if (threadIdx.x == 0) {
     mbar_arrive_expect_tx(&wbar, Cfg::kW);
-    for (int i = 0; i < Cfg::kW / Cfg::kWdx; ++i) bulk_load(sW + i * Cfg::kWdx, a.wpack + i * Cfg::kWdx, Cfg::kWdx, &wbar);
+    const uint8_t* wsrc = a.wpack + (Cfg::kQuarters ? (blockIdx.x & 3) * Cfg::kW : 0);
+    for (int i = 0; i < Cfg::kW / Cfg::kWdx; ++i) bulk_load(sW + i * Cfg::kWdx, wsrc + i * Cfg::kWdx, Cfg::kWdx, &wbar);
   }
   tc_fence_before();
   __syncthreads();
@@ -220,7 +245,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const int hco = pt & 63;                         // its channel
     int stage = 0;
     uint32_t phase = 0;
-    SegIter it(a, Cfg::kHalves ? 2 : 1);
+    SegIter it(a, Cfg::kVisits, Cfg::kParts);
     Segment g;
     while (it.next(a, g)) {
       const float* img = a.x + (long long)g.b * a.H * a.W;
@@ -287,16 +312,18 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
       prefetch_tmap(&tm_in);
       int stage = 0;
       uint32_t phase = 0;
-      SegIter it(a, Cfg::kHalves ? 2 : 1);
+      SegIter it(a, Cfg::kVisits, Cfg::kParts);
       Segment g;
       while (it.next(a, g)) {
         const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
         for (int r = r0; r <= r1; ++r) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], Cfg::kSplit ? 2 * kInRowBytes : kInRowBytes);
-          tma_load_4d(sIn + stage * Cfg::kStageBytes, &tm_in, &full[stage], 0, g.x0 - 1, r, g.b);
-          if constexpr (Cfg::kSplit)  // lo halves: channels 64..127 of the pair row
-            tma_load_4d(sIn + stage * Cfg::kStageBytes + kInRowStride, &tm_in, &full[stage], 64, g.x0 - 1, r, g.b);
+          constexpr int nbuf = (Cfg::kSplit ? 2 : 1) * Cfg::kKBlk;  // [hi blocks][lo blocks]
+          mbar_arrive_expect_tx(&full[stage], nbuf * kInRowBytes);
+#pragma unroll
+          for (int i = 0; i < nbuf; ++i)  // buffer i = channels 64i..64i+63 of the pixel row
+            tma_load_4d(sIn + stage * Cfg::kStageBytes + i * kInRowStride, &tm_in, &full[stage], 64 * i, g.x0 - 1,
+                        r, g.b);
           if (++stage == Cfg::kNStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -318,7 +345,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     uint32_t phase = 0;
     uint32_t seq = 0;  // output-row sequence number: slot = seq % kRing, use = seq / kRing
     bool prewaited = false;  // this row's barriers were already awaited by the previous row
-    SegIter it(a, Cfg::kHalves ? 2 : 1);
+    SegIter it(a, Cfg::kVisits, Cfg::kParts);
     Segment g;
     while (it.next(a, g)) {
       const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
@@ -356,9 +383,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p) + dx * 128 + k * 32) >> 4);
-                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + k * 32) >> 4);
+                for (int k = 0; k < Cfg::kKSteps; ++k) {
+                  const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p, k) + dx * 128 + (k % 4) * 32) >> 4);
+                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + Cfg::b_koff(k)) >> 4);
                   const bool first_k = Cfg::enters(p, k) && dx == 0;
                   const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + t0s;
                   if (first_k) {  // enter row r+1 (acc=0), keep r-1, r
@@ -375,9 +402,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p) + dx * 128 + k * 32) >> 4);
-                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + k * 32) >> 4);
+                for (int k = 0; k < Cfg::kKSteps; ++k) {
+                  const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p, k) + dx * 128 + (k % 4) * 32) >> 4);
+                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + Cfg::b_koff(k)) >> 4);
                   const bool first_k = Cfg::enters(p, k) && dx == 0;
                   const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + t0s;
                   mma_f16_ss_fill(rb, ad, bd + b2, idesc1, first_k ? 0u : 1u);
@@ -390,9 +417,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p) + dx * 128 + k * 32) >> 4);
-                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + k * 32) >> 4);
+                for (int k = 0; k < Cfg::kKSteps; ++k) {
+                  const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p, k) + dx * 128 + (k % 4) * 32) >> 4);
+                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + Cfg::b_koff(k)) >> 4);
                   const bool first_k = Cfg::enters(p, k) && dx == 0;
                   const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + t0s;
                   mma_f16_ss_fill(t0, ad, bd, idesc1, 1u);
@@ -453,10 +480,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
           for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p) + dx * 128 + k * 32) >> 4);
-              const uint64_t bd =
-                  bdesc0 + (uint64_t)((Cfg::b_off(p) + (uint32_t)g.h * Cfg::kWhalf + dx * Cfg::kWdx + k * 32) >> 4);
+            for (int k = 0; k < Cfg::kKSteps; ++k) {
+              const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p, k) + dx * 128 + (k % 4) * 32) >> 4);
+              const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + (uint32_t)g.h * Cfg::kWhalf +
+                                                       dx * Cfg::kWdx + Cfg::b_koff(k)) >> 4);
               const uint32_t rb = tmem + Cfg::ring_col(p, k);
               if (Cfg::enters(p, k) && dx == 0) {
                 if (vA) mma_f16_ss(rb + At, ad, bd + Ab, Ai, 1u);
@@ -489,7 +516,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const uint32_t shift_u = smem_u32(sShift);
     if (!kHead && !Cfg::kSplit && lane == 0) prefetch_tmap(&tm_out);
     uint32_t seq = 0, gsel = 0;  // gsel = seq % kGroups
-    SegIter it(a, Cfg::kHalves ? 2 : 1);
+    SegIter it(a, Cfg::kVisits, Cfg::kParts);
     Segment g;
     while (it.next(a, g)) {
       for (int q = g.ya; q < g.yb; ++q, ++seq, gsel = (gsel + 1 == Cfg::kGroups) ? 0 : gsel + 1) {
@@ -498,7 +525,44 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         mbar_wait(&slot_full[slot], (seq >> Cfg::kRingLog) & 1);
         tc_fence_after();
         const int xg = g.x0 + px;
-        if constexpr (Cfg::kSplit && !kHead) {
+        if constexpr (Cfg::kQuarters) {
+          // wide hidden: channels 32*qtr..+31 of this CTA's quarter, + shift, ReLU,
+          // re-split into an fp16 pair: 64 B hi + 64 B lo per pixel straight to global
+          const int qtr = blockIdx.x & 3;
+          uint32_t v[2][16];
+          tmem_ld16(tmem + lane_addr + slot * NB, v[0]);
+          tmem_ld16(tmem + lane_addr + slot * NB + 16, v[1]);
+          tmem_ld_wait();
+          reg_fence16(v[0]);
+          reg_fence16(v[1]);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&slot_empty[slot]);
+          if (xg < a.W) {
+            uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * Cfg::kPxBytes + qtr * 64;
+#pragma unroll
+            for (int chunk = 0; chunk < 4; ++chunk) {
+              const uint32_t sh_u = shift_u + (uint32_t)(qtr * 32 + chunk * 8) * 4;
+              const float4 s0 = ld_shared_f4(sh_u);
+              const float4 s1 = ld_shared_f4(sh_u + 16);
+              const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+              uint32_t hi[4], lo[4];
+#pragma unroll
+              for (int t2 = 0; t2 < 4; ++t2) {
+                const int ch = chunk * 8 + t2 * 2;
+                const float f0 = fmaxf(__uint_as_float(v[ch >> 4][ch & 15]) + sh[t2 * 2], 0.0f);
+                const float f1 = fmaxf(__uint_as_float(v[ch >> 4][(ch & 15) + 1]) + sh[t2 * 2 + 1], 0.0f);
+                const __half2 hh = __floats2half2_rn(f0, f1);
+                const float2 hf = __half22float2(hh);
+                const __half2 ll = __floats2half2_rn(f0 - hf.x, f1 - hf.y);
+                hi[t2] = *reinterpret_cast<const uint32_t*>(&hh);
+                lo[t2] = *reinterpret_cast<const uint32_t*>(&ll);
+              }
+              *reinterpret_cast<uint4*>(dst + chunk * 16) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+              *reinterpret_cast<uint4*>(dst + 2 * Cfg::kCin + chunk * 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            }
+          }
+        } else if constexpr (Cfg::kHalves) {
           // channels 32h..32h+31: z = (E + O) debiased + corrections (x 2^-8) +
           // shift, ReLU, re-split into an fp16 pair; one pixel per lane, 64 B hi
           // + 64 B lo straight to global
@@ -585,14 +649,14 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           uint32_t v[2][16], w[2][16];
           tmem_ld16(tmem + lane_addr + slot * NB, v[0]);
           tmem_ld16(tmem + lane_addr + slot * NB + 16, v[1]);
-          if constexpr (Cfg::kSplit) {
+          if constexpr (Cfg::kTwoRings) {
             tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB, w[0]);
             tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB + 16, w[1]);
           }
           tmem_ld_wait();
           reg_fence16(v[0]);
           reg_fence16(v[1]);
-          if constexpr (Cfg::kSplit) {
+          if constexpr (Cfg::kTwoRings) {
             reg_fence16(w[0]);
             reg_fence16(w[1]);
 #pragma unroll
@@ -670,16 +734,12 @@ __device__ __forceinline__ void put_b(uint8_t* out, int wdx, int kx, int n, int 
   *reinterpret_cast<__half*>(out + off) = v;
 }
 
-__global__ void pack_hidden_f16_kernel(const float* __restrict__ w, const float* __restrict__ scale,
-                                       uint8_t* __restrict__ out) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*64 + ci
-  if (idx >= kC * kC) return;
-  const int co = idx / kC, ci = idx % kC;
-  float wv[9], rn[9], alt[9], cost[9];
+// Tap-sum compensated fp16 rounding of one (co, ci) filter's 9 taps (see above).
+__device__ __forceinline__ void dc_round9(const float* wv, float* rn) {
+  float alt[9], cost[9];
   float s = 0.0f;
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
-    wv[t] = w[idx * 9 + t] * scale[co];  // BatchNorm fold W' = W*s (fp32)
     const __half h = __float2half_rn(wv[t]);
     rn[t] = __half2float(h);
     alt[t] = half_other_side(wv[t], h);
@@ -697,10 +757,60 @@ __global__ void pack_hidden_f16_kernel(const float* __restrict__ w, const float*
     const float d = (alt[best] - wv[best]) - (rn[best] - wv[best]);
     if (fabsf(s + d) < fabsf(s)) { s += d; rn[best] = alt[best]; }
   }
+}
+
+__global__ void pack_hidden_f16_kernel(const float* __restrict__ w, const float* __restrict__ scale,
+                                       uint8_t* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*64 + ci
+  if (idx >= kC * kC) return;
+  const int co = idx / kC, ci = idx % kC;
+  float wv[9], rn[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) wv[t] = w[idx * 9 + t] * scale[co];  // BatchNorm fold W' = W*s (fp32)
+  dc_round9(wv, rn);
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
     const int ky = t / 3, kx = t % 3;
     put_b(out, ConvCfg<0>::kWdx, kx, (2 - ky) * 64 + co, ci, __float2half_rn(rn[t]));
+  }
+}
+
+// Wide hidden (mode 5): 128x128 filters, DC-compensated fp16, packed per output
+// quarter qtr = co/32: [qtr][dx][K block ci/64][3 dy x 32 rows x 128 B]
+__global__ void pack_hidden_wide_kernel(const float* __restrict__ w, const float* __restrict__ scale,
+                                        uint8_t* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*128 + ci
+  if (idx >= 128 * 128) return;
+  const int co = idx / 128, ci = idx % 128;
+  float wv[9], rn[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) wv[t] = w[idx * 9 + t] * scale[co];
+  dc_round9(wv, rn);
+  using C5 = ConvCfg<5>;
+  uint8_t* base = out + (co >> 5) * C5::kW + (ci >> 6) * C5::kWdxBlk;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int ky = t / 3, kx = t % 3;
+    put_b(base, C5::kWdx, kx, (2 - ky) * 32 + (co & 31), ci & 63, __float2half_rn(rn[t]));
+  }
+}
+
+// Wide head (mode 6): W = W_hi + W_lo over 128 input channels, [dx][K block][96 rows]
+__global__ void pack_head_wide_kernel(const float* __restrict__ w, int K, uint8_t* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // k*128 + ci
+  if (idx >= K * 128) return;
+  const int k = idx / 128, ci = idx % 128;
+  using C6 = ConvCfg<6>;
+  uint8_t* base = out + (ci >> 6) * C6::kWdxBlk;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int ky = t / 3, kx = t % 3;
+    const float wf = w[idx * 9 + t];
+    const __half hi = __float2half_rn(wf);
+    const __half lo = __float2half_rn(wf - __half2float(hi));
+    const int nb = (2 - ky) * 32;
+    put_b(base, C6::kWdx, kx, nb + k, ci & 63, hi);
+    put_b(base, C6::kWdx, kx, nb + 16 + k, ci & 63, lo);
   }
 }
 
@@ -749,6 +859,7 @@ __global__ void fill_kernel(float* dst, float v, int n) {
 
 size_t conv_wpack_bytes(bool head) { return head ? ConvCfg<1>::kW : ConvCfg<0>::kW; }
 size_t conv_wpack_split_bytes() { return ConvCfg<3>::kW; }
+size_t conv_wpack_wide_bytes(bool head) { return head ? ConvCfg<6>::kW : 4 * ConvCfg<5>::kW; }
 
 // Launched with programmatic stream serialization (PDL): the kernel's
 // prologue overlaps the previous kernel; griddepcontrol.wait guards all
@@ -786,6 +897,15 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
       cfg.blockDim = dim3(ConvCfg<4>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<4>::kSmem;
       return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<4>, tm_in, tm_out, a, p0);
+    case 5:
+      cfg.gridDim = dim3(std::max(4, grid & ~3));  // groups of 4 CTAs (output-channel quarters)
+      cfg.blockDim = dim3(ConvCfg<5>::kThreads);
+      cfg.dynamicSmemBytes = ConvCfg<5>::kSmem;
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<5>, tm_in, tm_out, a, p0);
+    case 6:
+      cfg.blockDim = dim3(ConvCfg<6>::kThreads);
+      cfg.dynamicSmemBytes = ConvCfg<6>::kSmem;
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<6>, tm_in, tm_out, a, p0);
   }
   return cudaErrorInvalidValue;
 }
@@ -801,6 +921,20 @@ cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t
   cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<3>::kW, st);
   if (e != cudaSuccess) return e;
   pack_hidden_split_kernel<<<(kC * kC + 127) / 128, 128, 0, st>>>(w, scale, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_hidden_wide(const float* w, const float* scale, uint8_t* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, 4 * ConvCfg<5>::kW, st);
+  if (e != cudaSuccess) return e;
+  pack_hidden_wide_kernel<<<(128 * 128 + 127) / 128, 128, 0, st>>>(w, scale, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_head_wide(const float* w, int K, uint8_t* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<6>::kW, st);
+  if (e != cudaSuccess) return e;
+  pack_head_wide_kernel<<<(K * 128 + 127) / 128, 128, 0, st>>>(w, K, out);
   return cudaGetLastError();
 }
 
@@ -832,6 +966,12 @@ cudaError_t configure_kernels() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<4>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<5>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<6>::kSmem);
   if (e != cudaSuccess) return e;
   return configure_edge_kernels();
 }

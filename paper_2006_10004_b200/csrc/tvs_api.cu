@@ -118,6 +118,10 @@ struct tvs_plan {
   // (also used for the 128-channel wide variant).
   bool fp32_split = true;
   bool split_path() const { return mode == TVS_MODE_FP32 && channels == 64 && fp32_split; }
+  // wide variant (128 channels) fast mode on tcgen05: split activations, fp16 weights
+  // (conv_tc.cu modes 5/6); TVS_WIDE_CUDA=1 keeps it on the CUDA-core kernels
+  bool wide_cuda = false;
+  bool wide_path() const { return mode == TVS_MODE_FAST && channels == 128 && !wide_cuda; }
   size_t act_px_bytes() const { return tc_path() ? 128 : (size_t)channels * 4; }
 };
 
@@ -228,16 +232,49 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
                cudaStream_t st, void* const* act, int max_ctas) {
   const bool fast = p->tc_path();
   const bool split = p->split_path();
+  const bool wide = p->wide_path();
   const int C = p->channels;
   const double px = (double)B * H * W;
   // K1 (the FAST path can fuse it into the first hidden layer's producer)
-  const int fmt = fast ? tvs::kActF16 : (split ? tvs::kActSplit : tvs::kActF32);
+  const int fmt = fast ? tvs::kActF16 : ((split || wide) ? tvs::kActSplit : tvs::kActF32);
   if (!fast || p->unfused_conv0)
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
                  [&] { return tvs::launch_conv0(fmt, C, x, act[0], p->conv0, B, H, W, st); });
   // K2 x (depth-2), K3
   int cur = 0;
-  if (split) {
+  if (wide) {
+    // wide variant: split activations (hi 128 | lo 128 halves per pixel), groups
+    // of 4 CTAs per strip-row range (one 32-channel quarter each)
+    const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
+    CUtensorMap in_map[2];
+    for (int i = 0; i < 2; ++i) in_map[i] = make_act_map(act[i], B, H, W, tvs::kHaloPx, 256);
+    auto geom = [&](int r0, int nrows) {
+      tvs::ConvArgs a{};
+      a.B = B; a.H = H; a.W = W; a.strips = strips;
+      a.row0 = r0; a.rows = nrows; a.nsub = 1;
+      return a;
+    };
+    for (int l = 0; l < p->n_hidden(); ++l) {
+      tvs::ConvArgs a = geom(0, H);
+      a.wpack = p->wpack + (size_t)l * tvs::conv_wpack_wide_bytes(false);
+      a.shift = p->bhid + (size_t)l * C;
+      a.nshift = C;
+      a.act_out = static_cast<uint8_t*>(act[cur ^ 1]);
+      // 4 CTAs per strip-row range: size the grid by groups
+      const int grid = 4 * std::max(1, std::min(max_ctas / 4, conv_grid(max_ctas, a)));
+      timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * C * C,
+                   [&] { return tvs::launch_conv_tc(5, in_map[cur], in_map[cur], a, nullptr, grid, st); });
+      cur ^= 1;
+    }
+    tvs::ConvArgs a = geom(row0, rows);
+    a.wpack = p->hpack;
+    a.shift = p->bh;
+    a.nshift = p->out_bands;
+    a.x = x; a.bands = bands; a.closure = closure; a.K = p->out_bands;
+    const int grid = conv_grid(max_ctas, a);
+    timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * C * p->out_bands,
+                 [&] { return tvs::launch_conv_tc(6, in_map[cur], in_map[cur], a, nullptr, grid, st); });
+  } else if (split) {
     // fp32-accurate: split-operand tcgen05 layers on fp16 hi|lo pair rows
     const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
     CUtensorMap in_map[2];
@@ -399,7 +436,7 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
     *out_plan = nullptr;
     if (depth < 3) throw TvsError(TVS_E_INVALID, "depth must be at least 3 (first, hidden, last)");
     if (channels != 64 && channels != 128)
-      throw TvsError(TVS_E_UNSUPPORTED, "this build supports channels 64 (tcgen05 + CUDA-core paths) and 128 (CUDA-core path)");
+      throw TvsError(TVS_E_UNSUPPORTED, "this build supports channels 64 and 128");
     if (out_bands < 1 || out_bands > 8) throw TvsError(TVS_E_UNSUPPORTED, "out_bands must be in [1, 8]");
     if (mode != TVS_MODE_FP32 && mode != TVS_MODE_FAST) throw TvsError(TVS_E_INVALID, "unknown mode");
     int ndev = 0;
@@ -419,6 +456,7 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
     if (const char* e = std::getenv("TVS_L2_CHUNK_MB")) p->l2_chunk_bytes = (size_t)std::atoll(e) << 20;
     if (const char* e = std::getenv("TVS_FUSE_CONV0")) p->unfused_conv0 = std::atoi(e) == 0;
     if (const char* e = std::getenv("TVS_FP32_CUDA")) p->fp32_split = std::atoi(e) == 0;
+    if (const char* e = std::getenv("TVS_WIDE_CUDA")) p->wide_cuda = std::atoi(e) != 0;
     try {
       TVS_CUDA(tvs::configure_kernels());
       const int nh = depth - 2;
@@ -432,6 +470,9 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
       } else if (p->split_path()) {
         TVS_CUDA(cudaMalloc(&p->wpack, (size_t)nh * tvs::conv_wpack_split_bytes()));
         TVS_CUDA(cudaMalloc(&p->hpack, tvs::conv_wpack_bytes(true)));
+      } else if (p->wide_path()) {
+        TVS_CUDA(cudaMalloc(&p->wpack, (size_t)nh * tvs::conv_wpack_wide_bytes(false)));
+        TVS_CUDA(cudaMalloc(&p->hpack, tvs::conv_wpack_wide_bytes(true)));
       } else
         TVS_CUDA(cudaMalloc(&p->whid, (size_t)nh * channels * channels * 9 * 4));
     } catch (...) {
@@ -478,6 +519,9 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
       } else if (p->split_path()) {
         TVS_CUDA(tvs::launch_pack_hidden_split(w_dev[l + 1], dst_scale,
                                                p->wpack + (size_t)l * tvs::conv_wpack_split_bytes(), st));
+      } else if (p->wide_path()) {
+        TVS_CUDA(tvs::launch_pack_hidden_wide(w_dev[l + 1], dst_scale,
+                                              p->wpack + (size_t)l * tvs::conv_wpack_wide_bytes(false), st));
       } else {
         TVS_CUDA(cudaMemcpyAsync(p->whid + (size_t)l * C * C * 9, w_dev[l + 1], (size_t)C * C * 9 * 4,
                                  cudaMemcpyDeviceToDevice, st));
@@ -485,6 +529,7 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
     }
     if (p->tc_path() || p->split_path())
       TVS_CUDA(tvs::launch_pack_head_f16(w_dev[p->depth - 1], p->out_bands, p->hpack, st));
+    if (p->wide_path()) TVS_CUDA(tvs::launch_pack_head_wide(w_dev[p->depth - 1], p->out_bands, p->hpack, st));
     p->weights_ready = true;
   });
 }
