@@ -246,10 +246,20 @@ def run_ours(args, spec):
     precs = ["fast"] + (["fp32"] if args.fp32_fast_steps > 0 else [])
     if args.fp32_steps > 0 and spec.channels == 64:
         precs.append("fp32cuda")
+    if args.unshuffle_steps > 0 and spec.channels == 64 and H % 2 == 0 and W % 2 == 0 \
+            and row0 % 2 == 0 and nrows % 2 == 0:
+        precs.append("fast_u2")  # opt-in unshuffle = 2 variant (not the reference architecture)
     results = {}
     for prec in precs:
-        model = TVSpecNet(spec.depth, spec.channels, 5, precision="fp32" if prec == "fp32cuda" else prec).eval()
-        model.load_state_dict(state)
+        if prec == "fast_u2":
+            from oracle.tvspecnet_oracle import build_seeded_state  # checker-side weight recipe only
+
+            model = TVSpecNet(spec.depth, spec.channels, 5, unshuffle=2).eval()
+            model.load_state_dict(build_seeded_state(spec.depth, spec.channels, 5, unshuffle=2))
+        else:
+            model = TVSpecNet(spec.depth, spec.channels, 5,
+                              precision="fp32" if prec == "fp32cuda" else prec).eval()
+            model.load_state_dict(state)
         bands = torch.empty((B, 5, nrows, W), device=dev)
         clos = torch.empty((B, 1, nrows, W), device=dev)
         if prec == "fp32cuda":  # the CUDA-core fp32 kernels (read at plan creation)
@@ -264,6 +274,8 @@ def run_ours(args, spec):
         steps = args.steps if prec == "fast" else max(1, min(args.steps, args.fp32_steps))
         if prec == "fp32":
             steps = max(1, min(args.steps, args.fp32_fast_steps))
+        if prec == "fast_u2":
+            steps = max(1, min(args.steps, args.unshuffle_steps))
         warm = args.warmup if prec == "fast" else max(1, min(args.warmup, 3))
         if world > 1:
             dist.barrier()
@@ -363,6 +375,14 @@ def run_ours(args, spec):
         r32 = results["fp32"]
         line["fp32_mode"] = {"value": round(r32["value"], 3), "unit": UNIT, "ms_per_step": round(r32["ms"], 3),
                              "steps": r32["steps"], "e2e": round(r32["e2e"], 3)}
+    if "fast_u2" in results:
+        r = results["fast_u2"]
+        line["unshuffle2_variant"] = {
+            "value": round(r["value"], 3), "unit": UNIT, "ms_per_step": round(r["ms"], 3), "steps": r["steps"],
+            "e2e": round(r["e2e"], 3),
+            "note": "opt-in TVSpecNet(unshuffle=2): pixel_unshuffle folded into conv0 loads, pixel_shuffle into "
+                    "the head stores, hidden stack on the (H/2, W/2) grid; NOT the reference architecture "
+                    "(SURVEY F2), parity vs a torch composition oracle"}
     if "fp32cuda" in results:
         r = results["fp32cuda"]
         line["fp32_mode_cuda_cores"] = {"value": round(r["value"], 3), "unit": UNIT,
@@ -392,6 +412,8 @@ def main():
     ap.add_argument("--ref-step-seconds", type=float, default=4.0, help="--impl reference: seconds per step")
     ap.add_argument("--fp32-steps", type=int, default=None,
                     help="steps of the CUDA-core fp32 kernels (TVS_FP32_CUDA=1) (0 = skip)")
+    ap.add_argument("--unshuffle-steps", type=int, default=10,
+                    help="steps of the opt-in unshuffle=2 variant (0 = skip)")
     ap.add_argument("--fp32-fast-steps", type=int, default=10,
                     help="steps of the fp32-accurate mode (tcgen05 split operands) (0 = skip)")
     ap.add_argument("--e2e-steps", type=int, default=5)

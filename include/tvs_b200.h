@@ -37,17 +37,27 @@ extern "C" {
 #define TVS_E_STATE (-4)       /* forward before set_weights, etc. */
 
 /* numerics modes */
-#define TVS_MODE_FP32 0 /* fp32-accurate: fp32 activations + fp32 FFMA hidden layers   */
-#define TVS_MODE_FAST 1 /* fp16 tcgen05 hidden layers, exact fp32 conv0 + head          */
+#define TVS_MODE_FP32 0 /* fp32-accurate (<= 1e-5): split fp16 hi/lo operands on tcgen05 */
+#define TVS_MODE_FAST 1 /* fp16 tcgen05 hidden layers, exact fp32 conv0 + head (<= 1e-2) */
 
 typedef struct tvs_plan tvs_plan;
 
 int tvs_abi_version(void);
 const char* tvs_last_error(void);
 
-/* depth >= 3 (model.py:34-35); channels 64 (FAST: tcgen05) or 128 (both modes run the fp32
- * CUDA-core path in this build); 1 <= out_bands <= 8 */
+/* depth >= 3 (model.py:34-35); channels 64 or 128 (the wide variant: FAST on tcgen05,
+ * FP32 on CUDA cores); 1 <= out_bands <= 8 */
 int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode, tvs_plan** out_plan);
+
+/* As tvs_plan_create, plus unshuffle in {1, 2}.  unshuffle = 2 is the opt-in
+ * F-TVSpecNET-style variant (not the reference architecture):
+ * pixel_unshuffle(x, 2) -> Conv2d(4, C) ... Conv2d(C, 4K) -> pixel_shuffle(., 2),
+ * with the unshuffle folded into conv0's loads and the shuffle into the head's
+ * stores; the hidden stack runs on the (H/2, W/2) grid.  Weights:
+ * conv0 (C, 4, 3, 3), head (4K, C, 3, 3), 4K <= 32.  H, W and the row window
+ * must be even.  FAST mode, channels 64 only. */
+int tvs_plan_create_ex(int device, int depth, int channels, int out_bands, int mode, int unshuffle,
+                       tvs_plan** out_plan);
 
 /* n_layers == depth.  Layer i computes  y[co] = scale[co] * conv(W_i, a)[co] + shift[co]
  * (then ReLU for all but the head).  w_dev[i]: DEVICE pointer to the conv

@@ -82,14 +82,38 @@ class TVSpecNetOracle(nn.Module):
         return self.body(x)
 
 
+class UnshuffledOracle(nn.Module):
+    """The opt-in unshuffle = 2 variant as a plain torch composition (SURVEY F2:
+    not in the reference, so this oracle is unpinned by it):
+    F.pixel_unshuffle(x, 2) -> Conv2d(4, C)+ReLU -> (depth-2) x [Conv2d(C,C)+BN+ReLU]
+    -> Conv2d(C, 4K) -> F.pixel_shuffle(., 2).  Module order matches
+    TVSpecNet(..., unshuffle=2), so state_dicts are interchangeable."""
+
+    def __init__(self, depth: int = 17, channels: int = 64, out_bands: int = 5):
+        super().__init__()
+        layers: list[nn.Module] = [nn.Conv2d(4, channels, 3, padding=1, bias=True), nn.ReLU(inplace=True)]
+        for _ in range(depth - 2):
+            layers += [nn.Conv2d(channels, channels, 3, padding=1, bias=False), nn.BatchNorm2d(channels),
+                       nn.ReLU(inplace=True)]
+        layers.append(nn.Conv2d(channels, 4 * out_bands, 3, padding=1, bias=True))
+        self.body = nn.Sequential(*layers)
+        self.depth, self.out_bands = depth, out_bands
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        import torch.nn.functional as F
+
+        return F.pixel_shuffle(self.body(F.pixel_unshuffle(x, 2)), 2)
+
+
 def receptive_field(depth: int = 17, kernel: int = 3) -> int:
     return depth * (kernel - 1) + 1
 
 
-def build_seeded_state(depth: int = 17, channels: int = 64, out_bands: int = 5, seed: int = 0) -> dict:
+def build_seeded_state(depth: int = 17, channels: int = 64, out_bands: int = 5, seed: int = 0,
+                       unshuffle: int = 1) -> dict:
     """The seeded weights every parity case and benchmark uses."""
     torch.manual_seed(seed)
-    m = TVSpecNetOracle(depth, channels, out_bands)
+    m = TVSpecNetOracle(depth, channels, out_bands) if unshuffle == 1 else UnshuffledOracle(depth, channels, out_bands)
     for mod in m.modules():
         if isinstance(mod, nn.Conv2d):
             nn.init.kaiming_normal_(mod.weight, mode="fan_in", nonlinearity="relu")

@@ -25,6 +25,7 @@ EXPORTS = (
     "tvs_abi_version",
     "tvs_last_error",
     "tvs_plan_create",
+    "tvs_plan_create_ex",
     "tvs_plan_set_weights",
     "tvs_forward",
     "tvs_forward_host",
@@ -67,6 +68,8 @@ def load() -> ctypes.CDLL:
         lib.tvs_last_error.argtypes = []
         lib.tvs_plan_create.restype = i
         lib.tvs_plan_create.argtypes = [i, i, i, i, i, ctypes.POINTER(P)]
+        lib.tvs_plan_create_ex.restype = i
+        lib.tvs_plan_create_ex.argtypes = [i, i, i, i, i, i, ctypes.POINTER(P)]
         lib.tvs_plan_set_weights.restype = i
         lib.tvs_plan_set_weights.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), i, P]
         lib.tvs_forward.restype = i
@@ -104,11 +107,13 @@ def check(code: int) -> None:
 class Plan:
     """RAII owner of one ``tvs_plan`` (one device, one architecture, one mode)."""
 
-    def __init__(self, device: int, depth: int, channels: int, out_bands: int, mode: int):
+    def __init__(self, device: int, depth: int, channels: int, out_bands: int, mode: int, unshuffle: int = 1):
         self.lib = load()
         self.handle = ctypes.c_void_p()
-        check(self.lib.tvs_plan_create(device, depth, channels, out_bands, mode, ctypes.byref(self.handle)))
+        check(self.lib.tvs_plan_create_ex(device, depth, channels, out_bands, mode, unshuffle,
+                                          ctypes.byref(self.handle)))
         self.device, self.depth, self.channels, self.out_bands, self.mode = device, depth, channels, out_bands, mode
+        self.unshuffle = unshuffle
 
     def set_weights(self, w_ptrs, scale_ptrs, shift_ptrs, stream: int) -> None:
         """Device pointers per layer; scale_ptrs entries may be 0 (= no BatchNorm)."""

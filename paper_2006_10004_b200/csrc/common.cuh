@@ -49,6 +49,11 @@ constexpr int kMaxBands = 8;
 size_t conv_wpack_bytes(bool head);
 size_t conv_wpack_split_bytes();  // fp32-accurate hidden layer: hi pack | lo pack
 size_t conv_wpack_wide_bytes(bool head);  // wide variant (128 ch) on tcgen05: 4 quarter packs / head pack
+size_t conv_wpack_unshuf_head_bytes();    // unshuffle = 2 variant: Conv2d(64, 4K) head pack
+cudaError_t launch_pack_head_unshuf(const float* w, int K4, uint8_t* out, cudaStream_t st);
+// unshuffle = 2: Conv2d(4, 64) + ReLU over pixel_unshuffle(x, 2); H, W = half-res grid
+cudaError_t launch_conv0_unshuffle(const float* x, void* act, const float* w, const float* b, int B, int H, int W,
+                                   cudaStream_t st);
 struct Conv0Params;
 cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a,
                            const Conv0Params* c0, int grid, cudaStream_t st);

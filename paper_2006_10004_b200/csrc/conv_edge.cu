@@ -286,6 +286,75 @@ cudaError_t launch_conv0(int act_fmt, int C, const float* x, void* act, const Co
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------- K1, unshuffle = 2 ----
+// Conv2d(4, 64, 3, p=1) + ReLU over pixel_unshuffle(x, 2), computed straight
+// from the full-resolution plane: input channel c = 2i + j of half-res pixel
+// (Y, X) is x[2Y + i][2X + j] (torch pixel_unshuffle order), zero outside the
+// half-res grid.  One thread per half-res pixel, weights (64 x 36) staged in
+// shared memory, output staged and written coalesced as fp16 NHWC.
+__global__ void __launch_bounds__(128)
+conv0_unshuffle_kernel(const float* __restrict__ x, __half* __restrict__ act, const float* __restrict__ w,
+                       const float* __restrict__ bias, int B, int H, int W) {
+  constexpr int P = 128, C = 64;
+  __shared__ float sw[C * 36];
+  __shared__ float sb[C];
+  __shared__ __align__(16) __half stage[P * C];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  for (int i = threadIdx.x; i < C * 36; i += blockDim.x) sw[i] = w[i];
+  if (threadIdx.x < C) sb[threadIdx.x] = bias[threadIdx.x];
+  __syncthreads();
+  const long long npx = (long long)B * H * W;
+  const long long p0 = (long long)blockIdx.x * P;
+  const long long pix = p0 + threadIdx.x;
+  if (pix < npx) {
+    const int X = (int)(pix % W);
+    const long long t = pix / W;
+    const int Y = (int)(t % H);
+    const long long b = t / H;
+    const int Wf = 2 * W;
+    const float* img = x + b * (long long)(2 * H) * Wf;
+    float in[36];  // [c = 2i + j][ky][kx]
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        const int yy = Y + ky - 1, xx = X + kx - 1;
+        const bool ok = yy >= 0 && yy < H && xx >= 0 && xx < W;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          in[c * 9 + ky * 3 + kx] = ok ? __ldg(img + (long long)(2 * yy + (c >> 1)) * Wf + 2 * xx + (c & 1)) : 0.0f;
+      }
+    __half* dst = stage + threadIdx.x * C;
+#pragma unroll
+    for (int c8 = 0; c8 < C / 8; ++c8) {
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int co = c8 * 8 + e;
+        float acc = 0.0f;
+#pragma unroll
+        for (int t36 = 0; t36 < 36; ++t36) acc = fmaf(sw[co * 36 + t36], in[t36], acc);
+        v[e] = fmaxf(acc + sb[co], 0.0f);
+      }
+      store_act8<__half>(dst + c8 * 8, v);
+    }
+  }
+  __syncthreads();
+  const long long nvalid = min((long long)P, npx - p0);
+  const int n16 = (int)(nvalid * C * 2 / 16);
+  const uint4* src = reinterpret_cast<const uint4*>(stage);
+  uint4* out = reinterpret_cast<uint4*>(act + p0 * C);
+  for (int i = threadIdx.x; i < n16; i += blockDim.x) out[i] = src[i];
+}
+
+cudaError_t launch_conv0_unshuffle(const float* x, void* act, const float* w, const float* b, int B, int H, int W,
+                                   cudaStream_t st) {
+  const long long npx = (long long)B * H * W;
+  conv0_unshuffle_kernel<<<(unsigned)((npx + 127) / 128), 128, 0, st>>>(x, static_cast<__half*>(act), w, b, B, H, W);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_head_f32(int C, const float* act, const float* x, const float* wh, const float* bh, float* bands,
                             float* closure, int B, int H, int W, int K, int row0, int rows, cudaStream_t st) {
   const long long nout = (long long)B * rows * W;

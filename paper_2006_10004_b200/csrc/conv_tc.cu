@@ -113,12 +113,16 @@ struct SegIter {
 // of the activations alone would cost 1.06e-2 over 26 layers (gate 1e-2).
 // Mode 5 CTAs come in groups of 4, one 32-output-channel quarter each (its
 // 72 KB weight slice stays resident; the 4 CTAs share input rows via L2).
+// 7 = head of the opt-in unshuffle = 2 variant (fast mode): Conv2d(C, 4K)
+// with N block 64 = [32 hi | 32 lo] columns and pixel_shuffle folded into the
+// band stores (head channel k*4 + i*2 + j -> band k at (2y+i, 2x+j)).
 template <int kMode>
 struct ConvCfg {
-  static constexpr bool kSplit = kMode >= 3;
-  static constexpr bool kHead = kMode == 1 || kMode == 4 || kMode == 6;
+  static constexpr bool kSplit = kMode >= 3 && kMode <= 6;
+  static constexpr bool kUnshuf = kMode == 7;
+  static constexpr bool kHead = kMode == 1 || kMode == 4 || kMode == 6 || kMode == 7;
   static constexpr bool kFirst = kMode == 2;
-  static constexpr bool kWide = kMode >= 5;
+  static constexpr bool kWide = kMode == 5 || kMode == 6;
   static constexpr bool kQuarters = kMode == 5;
   static constexpr int kCin = kWide ? 128 : 64;
   static constexpr int kKBlk = kCin / 64;        // 64-channel K blocks (one SW128 row buffer each)
@@ -132,7 +136,7 @@ struct ConvCfg {
   static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kGroups);
   // split hidden layer: two passes of 32 output channels (TMEM room for three rings)
   static constexpr bool kHalves = kMode == 3;
-  static constexpr int NB = (kHead || kHalves || kQuarters) ? 32 : 64;  // TMEM columns per output row (slot)
+  static constexpr int NB = kUnshuf ? 64 : ((kHead || kHalves || kQuarters) ? 32 : 64);  // TMEM cols per row
   static constexpr int kWdxBlk = 3 * NB * 128;        // B bytes per dx and K block (3 dy x NB rows x 128 B)
   static constexpr int kWdx = kKBlk * kWdxBlk;        // B bytes per dx
   static constexpr int kWhalf = 3 * kWdx;             // one channel half (all dx)
@@ -645,6 +649,50 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             tma_store_4d(&tm_out, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b);
             bulk_commit();
           }
+        } else if constexpr (Cfg::kUnshuf) {
+          uint32_t v[4][16];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tmem_ld16(tmem + lane_addr + slot * NB + j * 16, v[j]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 4; ++j) reg_fence16(v[j]);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&slot_empty[slot]);
+          if (xg < a.W) {
+            // half-res pixel (q, xg) -> full-res 2x2 block at rows 2q+i, cols 2xg+j
+            const int Wf = 2 * a.W;
+            const long long planef = (long long)(2 * a.rows) * Wf;
+            const long long r0f = 2LL * (q - a.row0);
+            float sum[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int k = 0; k < kMaxBands; ++k) {
+              if (k < a.K) {
+                float* ob = a.bands + ((long long)g.b * a.K + k) * planef;
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                  float f[2];
+#pragma unroll
+                  for (int jj = 0; jj < 2; ++jj) {
+                    const int o = k * 4 + i * 2 + jj;  // head channel (pixel_shuffle order)
+                    f[jj] = (__uint_as_float(v[o >> 4][o & 15]) + __uint_as_float(v[(32 + o) >> 4][(32 + o) & 15])) +
+                            sShift[o];
+                    sum[i * 2 + jj] += f[jj];
+                  }
+                  *reinterpret_cast<float2*>(ob + (r0f + i) * Wf + 2 * xg) = make_float2(f[0], f[1]);
+                }
+              }
+            }
+            if (a.closure) {
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                const float2 xi =
+                    *reinterpret_cast<const float2*>(a.x + ((long long)g.b * 2 * a.H + 2 * q + i) * Wf + 2 * xg);
+                *reinterpret_cast<float2*>(a.closure + (long long)g.b * planef + (r0f + i) * Wf + 2 * xg) =
+                    make_float2(xi.x - sum[i * 2], xi.y - sum[i * 2 + 1]);
+              }
+            }
+          }
         } else {
           uint32_t v[2][16], w[2][16];
           tmem_ld16(tmem + lane_addr + slot * NB, v[0]);
@@ -850,6 +898,23 @@ __global__ void pack_head_f16_kernel(const float* __restrict__ w, int K, uint8_t
   }
 }
 
+// Unshuffled head (mode 7): Conv2d(64, K4) weights, hi rows (2-ky)*64 + o,
+// lo rows (2-ky)*64 + 32 + o
+__global__ void pack_head_unshuf_kernel(const float* __restrict__ w, int K4, uint8_t* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // o*64 + ci
+  if (idx >= K4 * kC) return;
+  const int o = idx / kC, ci = idx % kC;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int ky = t / 3, kx = t % 3;
+    const float wf = w[idx * 9 + t];
+    const __half hi = __float2half_rn(wf);
+    const __half lo = __float2half_rn(wf - __half2float(hi));
+    put_b(out, ConvCfg<7>::kWdx, kx, (2 - ky) * 64 + o, ci, hi);
+    put_b(out, ConvCfg<7>::kWdx, kx, (2 - ky) * 64 + 32 + o, ci, lo);
+  }
+}
+
 __global__ void fill_kernel(float* dst, float v, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[i] = v;
@@ -860,6 +925,7 @@ __global__ void fill_kernel(float* dst, float v, int n) {
 size_t conv_wpack_bytes(bool head) { return head ? ConvCfg<1>::kW : ConvCfg<0>::kW; }
 size_t conv_wpack_split_bytes() { return ConvCfg<3>::kW; }
 size_t conv_wpack_wide_bytes(bool head) { return head ? ConvCfg<6>::kW : 4 * ConvCfg<5>::kW; }
+size_t conv_wpack_unshuf_head_bytes() { return ConvCfg<7>::kW; }
 
 // Launched with programmatic stream serialization (PDL): the kernel's
 // prologue overlaps the previous kernel; griddepcontrol.wait guards all
@@ -906,6 +972,10 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
       cfg.blockDim = dim3(ConvCfg<6>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<6>::kSmem;
       return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<6>, tm_in, tm_out, a, p0);
+    case 7:
+      cfg.blockDim = dim3(ConvCfg<7>::kThreads);
+      cfg.dynamicSmemBytes = ConvCfg<7>::kSmem;
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<7>, tm_in, tm_out, a, p0);
   }
   return cudaErrorInvalidValue;
 }
@@ -935,6 +1005,13 @@ cudaError_t launch_pack_head_wide(const float* w, int K, uint8_t* out, cudaStrea
   cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<6>::kW, st);
   if (e != cudaSuccess) return e;
   pack_head_wide_kernel<<<(K * 128 + 127) / 128, 128, 0, st>>>(w, K, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_head_unshuf(const float* w, int K4, uint8_t* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<7>::kW, st);
+  if (e != cudaSuccess) return e;
+  pack_head_unshuf_kernel<<<(K4 * kC + 127) / 128, 128, 0, st>>>(w, K4, out);
   return cudaGetLastError();
 }
 
@@ -972,6 +1049,9 @@ cudaError_t configure_kernels() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<6>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<7>::kSmem);
   if (e != cudaSuccess) return e;
   return configure_edge_kernels();
 }

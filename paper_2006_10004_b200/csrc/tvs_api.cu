@@ -75,6 +75,10 @@ struct tvs_plan {
   // hidden: fast -> packed fp16 (n_hidden * conv_wpack_bytes(false)) ; fp32 -> [co][ci][9] fp32
   uint8_t* wpack = nullptr;
   uint8_t* hpack = nullptr;  // fast-mode head: fp16 hi/lo pack
+  // opt-in unshuffle = 2 variant: conv0 Conv2d(4, 64) weights on the device
+  int unshuffle = 1;
+  float* w0u = nullptr;
+  float* b0u = nullptr;
   float* whid = nullptr;
   float* bhid = nullptr;  // per hidden layer: shift (beta - mu*s)
   float* shid = nullptr;  // per hidden layer: BatchNorm scale s (fp32 mode epilogue; folded in FAST)
@@ -143,7 +147,8 @@ void free_all(tvs_plan* p) {
   for (auto e : p->event_pool) cudaEventDestroy(e);
   p->recs.clear();
   p->event_pool.clear();
-  void* ptrs[] = {p->wh, p->bh, p->wpack, p->hpack, p->whid, p->bhid, p->shid, p->act[0], p->act[1], p->dx};
+  void* ptrs[] = {p->wh, p->bh, p->wpack, p->hpack, p->whid, p->bhid, p->shid, p->act[0], p->act[1], p->dx,
+                  p->w0u, p->b0u};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -237,7 +242,11 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
   const double px = (double)B * H * W;
   // K1 (the FAST path can fuse it into the first hidden layer's producer)
   const int fmt = fast ? tvs::kActF16 : ((split || wide) ? tvs::kActSplit : tvs::kActF32);
-  if (!fast || p->unfused_conv0)
+  const int us = p->unshuffle;  // 2: the layer stack runs on the (H/2, W/2) grid
+  if (us == 2)
+    timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
+                 [&] { return tvs::launch_conv0_unshuffle(x, act[0], p->w0u, p->b0u, B, H / 2, W / 2, st); });
+  else if (!fast || p->unfused_conv0)
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
                  [&] { return tvs::launch_conv0(fmt, C, x, act[0], p->conv0, B, H, W, st); });
   // K2 x (depth-2), K3
@@ -305,22 +314,24 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands,
                  [&] { return tvs::launch_conv_tc(4, in_map[cur], in_map[cur], a, nullptr, grid, st); });
   } else if (fast) {
-    const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
+    const int Hg = H / us, Wg = W / us;  // layer grid (half-res when unshuffled)
+    const double pxg = px / (us * us);
+    const int strips = (Wg + tvs::kStripPx - 1) / tvs::kStripPx;
     CUtensorMap in_map[2], out_map[2];
     for (int i = 0; i < 2; ++i) {
-      in_map[i] = make_act_map(act[i], B, H, W, tvs::kHaloPx);
-      out_map[i] = make_act_map(act[i], B, H, W, 32);
+      in_map[i] = make_act_map(act[i], B, Hg, Wg, tvs::kHaloPx);
+      out_map[i] = make_act_map(act[i], B, Hg, Wg, 32);
     }
     auto geom = [&](int r0, int nrows) {
       tvs::ConvArgs a{};
-      a.B = B; a.H = H; a.W = W; a.strips = strips;
+      a.B = B; a.H = Hg; a.W = Wg; a.strips = strips;
       a.row0 = r0; a.rows = nrows;
       return a;
     };
     const bool fuse0 = !p->unfused_conv0;
     if (fuse0) cur = 1;  // the first hidden layer reads x and writes act[0]
     for (int l = 0; l < p->n_hidden(); ++l) {
-      tvs::ConvArgs a = geom(0, H);
+      tvs::ConvArgs a = geom(0, Hg);
       a.wpack = p->wpack + (size_t)l * tvs::conv_wpack_bytes(false);
       a.shift = p->bhid + (size_t)l * tvs::kC;
       a.nshift = tvs::kC;
@@ -329,22 +340,22 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       const bool first = fuse0 && l == 0;
       a.reverse = (p->l2_reverse_sub > 1) && (l & 1);
       a.nsub = p->l2_reverse_sub;
-      timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64 + (first ? px * 2.0 * 9 * 64 : 0.0), [&] {
+      timed_launch(p, st, TVS_KIND_HIDDEN, pxg * 2.0 * 9 * 64 * 64 + (first ? pxg * 2.0 * 9 * 64 : 0.0), [&] {
         return tvs::launch_conv_tc(first ? 2 : 0, in_map[cur], out_map[cur ^ 1], a, first ? &p->conv0 : nullptr,
                                    grid, st);
       });
       cur ^= 1;
     }
-    tvs::ConvArgs a = geom(row0, rows);
+    tvs::ConvArgs a = geom(row0 / us, rows / us);
     a.wpack = p->hpack;
     a.shift = p->bh;
-    a.nshift = p->out_bands;
+    a.nshift = p->out_bands * us * us;
     a.x = x; a.bands = bands; a.closure = closure; a.K = p->out_bands;
     a.reverse = (p->l2_reverse_sub > 1) && (p->n_hidden() & 1);
     a.nsub = p->l2_reverse_sub;
     const int grid = conv_grid(max_ctas, a);
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands,
-                 [&] { return tvs::launch_conv_tc(1, in_map[cur], in_map[cur], a, nullptr, grid, st); });
+                 [&] { return tvs::launch_conv_tc(us == 2 ? 7 : 1, in_map[cur], in_map[cur], a, nullptr, grid, st); });
   } else {
     for (int l = 0; l < p->n_hidden(); ++l) {
       timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * C * C, [&] {
@@ -368,10 +379,12 @@ void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int
   if (B < 0 || H < 1 || W < 1) throw TvsError(TVS_E_INVALID, "bad shape B/H/W");
   if (rows < 0) { row0 = 0; rows = H; }
   if (row0 < 0 || rows < 1 || row0 + rows > H) throw TvsError(TVS_E_INVALID, "bad valid row window");
+  if (p->unshuffle == 2 && (H % 2 || W % 2 || row0 % 2 || rows % 2))
+    throw TvsError(TVS_E_INVALID, "unshuffle = 2 needs even H, W and an even row window");
   p->last_launches = 0;
   if (B == 0) return;
   ensure_device(p);
-  const size_t per_img = (size_t)H * W * p->act_px_bytes();
+  const size_t per_img = (size_t)H * W * p->act_px_bytes() / ((size_t)p->unshuffle * p->unshuffle);
   const size_t in_img = (size_t)H * W, out_img = (size_t)rows * W;
   // concurrent L2-resident chunks: only when an image fits the chunk budget
   const int S = p->tc_path() ? std::min(p->n_streams, B) : 1;
@@ -431,9 +444,17 @@ int tvs_abi_version(void) { return TVS_ABI_VERSION; }
 const char* tvs_last_error(void) { return g_last_error.c_str(); }
 
 int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode, tvs_plan** out_plan) {
+  return tvs_plan_create_ex(device, depth, channels, out_bands, mode, 1, out_plan);
+}
+
+int tvs_plan_create_ex(int device, int depth, int channels, int out_bands, int mode, int unshuffle,
+                       tvs_plan** out_plan) {
   return guarded([&] {
     if (!out_plan) throw TvsError(TVS_E_INVALID, "out_plan is null");
     *out_plan = nullptr;
+    if (unshuffle != 1 && unshuffle != 2) throw TvsError(TVS_E_INVALID, "unshuffle must be 1 or 2");
+    if (unshuffle == 2 && (mode != TVS_MODE_FAST || channels != 64))
+      throw TvsError(TVS_E_UNSUPPORTED, "unshuffle = 2 is built for FAST mode with 64 channels");
     if (depth < 3) throw TvsError(TVS_E_INVALID, "depth must be at least 3 (first, hidden, last)");
     if (channels != 64 && channels != 128)
       throw TvsError(TVS_E_UNSUPPORTED, "this build supports channels 64 and 128");
@@ -449,6 +470,8 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
       throw TvsError(TVS_E_UNSUPPORTED, "libtvsb200 is built for sm_100a (B200) only");
     auto* p = new tvs_plan();
     p->device = device; p->depth = depth; p->channels = channels; p->out_bands = out_bands; p->mode = mode;
+    p->unshuffle = unshuffle;
+    if (unshuffle == 2) p->unfused_conv0 = true;
     p->num_sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("TVS_CHUNK_MB")) p->chunk_budget = (size_t)std::atoll(e) << 20;
     if (const char* e = std::getenv("TVS_STREAMS")) p->n_streams = std::max(1, std::atoi(e));
@@ -461,12 +484,16 @@ int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode
       TVS_CUDA(tvs::configure_kernels());
       const int nh = depth - 2;
       TVS_CUDA(cudaMalloc(&p->wh, (size_t)out_bands * channels * 9 * 4));
-      TVS_CUDA(cudaMalloc(&p->bh, (size_t)out_bands * 4));
+      TVS_CUDA(cudaMalloc(&p->bh, (size_t)out_bands * unshuffle * unshuffle * 4));  // head bias (4K if unshuffled)
       TVS_CUDA(cudaMalloc(&p->bhid, (size_t)nh * channels * 4));
       TVS_CUDA(cudaMalloc(&p->shid, (size_t)nh * channels * 4));
       if (p->tc_path()) {
         TVS_CUDA(cudaMalloc(&p->wpack, (size_t)nh * tvs::conv_wpack_bytes(false)));
-        TVS_CUDA(cudaMalloc(&p->hpack, tvs::conv_wpack_bytes(true)));
+        TVS_CUDA(cudaMalloc(&p->hpack, unshuffle == 2 ? tvs::conv_wpack_unshuf_head_bytes() : tvs::conv_wpack_bytes(true)));
+        if (unshuffle == 2) {
+          TVS_CUDA(cudaMalloc(&p->w0u, (size_t)channels * 36 * 4));
+          TVS_CUDA(cudaMalloc(&p->b0u, (size_t)channels * 4));
+        }
       } else if (p->split_path()) {
         TVS_CUDA(cudaMalloc(&p->wpack, (size_t)nh * tvs::conv_wpack_split_bytes()));
         TVS_CUDA(cudaMalloc(&p->hpack, tvs::conv_wpack_bytes(true)));
@@ -498,13 +525,18 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
     if (scale_of(0) || scale_of(p->depth - 1))
       throw TvsError(TVS_E_UNSUPPORTED, "conv0/head take no BatchNorm scale (model.py:37,44)");
     const int C = p->channels;
-    TVS_CUDA(cudaMemcpyAsync(p->conv0.w, w_dev[0], (size_t)C * 9 * 4, cudaMemcpyDeviceToHost, st));
-    TVS_CUDA(cudaMemcpyAsync(p->conv0.b, shift_dev[0], (size_t)C * 4, cudaMemcpyDeviceToHost, st));
-    TVS_CUDA(cudaStreamSynchronize(st));  // conv0 weights are kernel parameters (host side)
-    TVS_CUDA(cudaMemcpyAsync(p->wh, w_dev[p->depth - 1], (size_t)p->out_bands * C * 9 * 4,
+    if (p->unshuffle == 2) {  // conv0 Conv2d(4, C) on the device; head Conv2d(C, 4K) packed below
+      TVS_CUDA(cudaMemcpyAsync(p->w0u, w_dev[0], (size_t)C * 36 * 4, cudaMemcpyDeviceToDevice, st));
+      TVS_CUDA(cudaMemcpyAsync(p->b0u, shift_dev[0], (size_t)C * 4, cudaMemcpyDeviceToDevice, st));
+    } else {
+      TVS_CUDA(cudaMemcpyAsync(p->conv0.w, w_dev[0], (size_t)C * 9 * 4, cudaMemcpyDeviceToHost, st));
+      TVS_CUDA(cudaMemcpyAsync(p->conv0.b, shift_dev[0], (size_t)C * 4, cudaMemcpyDeviceToHost, st));
+      TVS_CUDA(cudaStreamSynchronize(st));  // conv0 weights are kernel parameters (host side)
+      TVS_CUDA(cudaMemcpyAsync(p->wh, w_dev[p->depth - 1], (size_t)p->out_bands * C * 9 * 4,
+                               cudaMemcpyDeviceToDevice, st));
+    }
+    TVS_CUDA(cudaMemcpyAsync(p->bh, shift_dev[p->depth - 1], (size_t)p->out_bands * p->unshuffle * p->unshuffle * 4,
                              cudaMemcpyDeviceToDevice, st));
-    TVS_CUDA(cudaMemcpyAsync(p->bh, shift_dev[p->depth - 1], (size_t)p->out_bands * 4, cudaMemcpyDeviceToDevice,
-                             st));
     for (int l = 0; l < nh; ++l) {
       const float* sc = scale_of(l + 1);
       float* dst_scale = p->shid + l * C;
@@ -527,8 +559,11 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
                                  cudaMemcpyDeviceToDevice, st));
       }
     }
-    if (p->tc_path() || p->split_path())
+    if (p->unshuffle == 2) {
+      TVS_CUDA(tvs::launch_pack_head_unshuf(w_dev[p->depth - 1], 4 * p->out_bands, p->hpack, st));
+    } else if (p->tc_path() || p->split_path()) {
       TVS_CUDA(tvs::launch_pack_head_f16(w_dev[p->depth - 1], p->out_bands, p->hpack, st));
+    }
     if (p->wide_path()) TVS_CUDA(tvs::launch_pack_head_wide(w_dev[p->depth - 1], p->out_bands, p->hpack, st));
     p->weights_ready = true;
   });

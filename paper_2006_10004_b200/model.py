@@ -22,7 +22,15 @@ CPU fallback and no train-mode path: ``forward`` raises in ``train()`` mode
 
 ``precision`` selects the numerics: ``"fast"`` (default; fp16 tcgen05 hidden
 layers, exact fp32 conv0/head; <= 1e-2 relative L2 per band vs the fp32
-reference) or ``"fp32"`` (fp32 activations and arithmetic; <= 1e-5).
+reference) or ``"fp32"`` (split fp16 hi/lo operands on tcgen05; <= 1e-5).
+
+``unshuffle=2`` (keyword-only, default 1 = the reference architecture) builds
+the opt-in F-TVSpecNET-style variant BASELINE.json's north_star describes but
+the reference does not have: pixel_unshuffle(x, 2) -> Conv2d(4, C)
+-> hidden stack on the (H/2, W/2) grid -> Conv2d(C, 4K) -> pixel_shuffle(., 2).
+The unshuffle is folded into conv0's loads and the shuffle into the head's
+stores (no separate passes).  Its parity reference is the torch composition in
+oracle/tvspecnet_oracle.py (unpinned by the reference).  Fast mode only.
 """
 
 from __future__ import annotations
@@ -49,20 +57,27 @@ _PRECISIONS = {"fp32": _native.MODE_FP32, "fast": _native.MODE_FAST}
 class TVSpecNet(nn.Module):
     """DnCNN-shaped regressor from an image to its first ``out_bands`` bands."""
 
-    def __init__(self, depth: int = 17, channels: int = 64, out_bands: int = 5, *, precision: str = "fast"):
+    def __init__(self, depth: int = 17, channels: int = 64, out_bands: int = 5, *, precision: str = "fast",
+                 unshuffle: int = 1):
         super().__init__()
         if depth < 3:
             raise ValueError("depth must be at least 3 (first, hidden, last)")
-        layers: list[nn.Module] = [nn.Conv2d(1, channels, 3, padding=1, bias=True), nn.ReLU(inplace=True)]
+        if unshuffle not in (1, 2):
+            raise ValueError("unshuffle must be 1 or 2")
+        if unshuffle == 2 and precision != "fast":
+            raise ValueError("unshuffle=2 is built for precision='fast'")
+        u2 = unshuffle * unshuffle
+        layers: list[nn.Module] = [nn.Conv2d(u2, channels, 3, padding=1, bias=True), nn.ReLU(inplace=True)]
         for _ in range(depth - 2):
             layers.append(nn.Conv2d(channels, channels, 3, padding=1, bias=False))
             layers.append(nn.BatchNorm2d(channels))
             layers.append(nn.ReLU(inplace=True))
-        layers.append(nn.Conv2d(channels, out_bands, 3, padding=1, bias=True))
+        layers.append(nn.Conv2d(channels, out_bands * u2, 3, padding=1, bias=True))
         self.body = nn.Sequential(*layers)
         self.depth = depth
         self.out_bands = out_bands
         self.channels = channels
+        self.unshuffle = unshuffle
         if precision not in _PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(_PRECISIONS)}")
         self._precision = precision
@@ -77,6 +92,8 @@ class TVSpecNet(nn.Module):
     def precision(self, value: str) -> None:
         if value not in _PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(_PRECISIONS)}")
+        if getattr(self, "unshuffle", 1) == 2 and value != "fast":
+            raise ValueError("unshuffle=2 is built for precision='fast'")
         if value != self._precision:
             self._precision = value
             self._drop_plans()
@@ -126,7 +143,7 @@ class TVSpecNet(nn.Module):
         if entry is not None and entry[1] == key:
             return entry[0]
         plan = entry[0] if entry is not None else _native.Plan(
-            idx, self.depth, self.channels, self.out_bands, _PRECISIONS[self._precision]
+            idx, self.depth, self.channels, self.out_bands, _PRECISIONS[self._precision], self.unshuffle
         )
         with torch.cuda.device(idx):
             stream = torch.cuda.current_stream(idx)
@@ -162,6 +179,8 @@ class TVSpecNet(nn.Module):
             raise RuntimeError(f"Input type ({x.dtype}) and weight type (torch.float32) should be the same")
         if self.training:
             raise RuntimeError("TVSpecNet (B200) implements the eval-mode forward only; call .eval() first")
+        if self.unshuffle == 2 and (x.shape[2] % 2 or x.shape[3] % 2):
+            raise ValueError(f"unshuffle=2 needs even height and width, got {tuple(x.shape[2:])}")
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         return self.forward_planes(x)[0]
@@ -178,6 +197,8 @@ class TVSpecNet(nn.Module):
         row0, nrows = (0, H) if rows is None else rows
         if not (0 <= row0 and nrows >= 1 and row0 + nrows <= H):
             raise ValueError(f"bad row window {rows} for height {H}")
+        if self.unshuffle == 2 and (row0 % 2 or nrows % 2):
+            raise ValueError(f"unshuffle=2 needs an even row window, got {rows}")
         if not x.is_cuda:
             return self._forward_host(plan, x, dev, closure, row0, nrows)
         with torch.cuda.device(dev):

@@ -87,3 +87,28 @@ def test_precision_validation():
     m = TVSpecNet()
     m.precision = "fp32"
     assert m.precision == "fp32"
+
+
+def test_unshuffle_variant_structure():
+    """unshuffle=2 (the opt-in F-TVSpecNET-style variant): Conv2d(4, C)
+    first layer, Conv2d(C, 4K) head, state_dict interchangeable with the torch
+    composition oracle; fast mode only; the default stays the reference layout."""
+    import torch
+
+    from oracle.tvspecnet_oracle import UnshuffledOracle, build_seeded_state
+    from paper_2006_10004_b200 import TVSpecNet
+
+    m = TVSpecNet(unshuffle=2)
+    sd = m.state_dict()
+    assert sd["body.0.weight"].shape == (64, 4, 3, 3)
+    assert sd["body.47.weight"].shape == (20, 64, 3, 3) and sd["body.47.bias"].shape == (20,)
+    m.load_state_dict(build_seeded_state(unshuffle=2))
+    assert UnshuffledOracle().state_dict().keys() == sd.keys()
+    assert TVSpecNet().state_dict()["body.0.weight"].shape == (64, 1, 3, 3)
+    with pytest.raises(ValueError):
+        TVSpecNet(unshuffle=2, precision="fp32")
+    with pytest.raises(ValueError):
+        TVSpecNet(unshuffle=3)
+    # the oracle composes exactly as torch's pixel_(un)shuffle: identity body check
+    x = torch.randn(1, 1, 6, 8)
+    assert torch.equal(torch.nn.functional.pixel_shuffle(torch.nn.functional.pixel_unshuffle(x, 2), 2), x)
