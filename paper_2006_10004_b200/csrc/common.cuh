@@ -36,7 +36,22 @@ struct ConvArgs {
   int K;
   // fp32-accurate split hidden layer: output fp16 pair rows [B][H][W][hi 64 | lo 64]
   uint8_t* act_out;
+  // L2 eviction hints of the fast hidden layer (TVS_L2_HINTS): bit 0 = input
+  // rows evict_first (read once), bit 1 = output rows evict_last
+  int l2_hints;
 };
+
+// two fused hidden layers (conv_pair.cu): cluster of S = ceil(W/128) CTAs
+struct PairArgs {
+  int B, H, W, S;
+  const uint8_t* wpack0;  // layer L pack (conv_tc.cu mode 0 format)
+  const uint8_t* wpack1;  // layer L+1 pack
+  const float* shift0;
+  const float* shift1;
+  uint8_t* act_out;       // fp16 NHWC [B][H][W][64] output of layer L+1
+  int dbg;                // bring-up switches (TVS_PAIR_DBG): 1 no DSMEM halo, 2 no layer-L+1 MMAs, 4 no mid stores
+};
+cudaError_t launch_conv_pair(const CUtensorMap& tm_in, const PairArgs& a, int max_ctas, cudaStream_t st);
 
 // fp32 hidden layer (conv_edge.cu)
 constexpr int kF32TileRows = 4, kF32TilePx = 32, kF32CiChunk = 16;

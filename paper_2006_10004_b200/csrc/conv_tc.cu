@@ -314,6 +314,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     // ------------------------------------------------ TMA producer ----
     if (elect_one()) {
       prefetch_tmap(&tm_in);
+      const uint64_t pol_in = l2_policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
       SegIter it(a, Cfg::kVisits, Cfg::kParts);
@@ -325,9 +326,14 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           constexpr int nbuf = (Cfg::kSplit ? 2 : 1) * Cfg::kKBlk;  // [hi blocks][lo blocks]
           mbar_arrive_expect_tx(&full[stage], nbuf * kInRowBytes);
 #pragma unroll
-          for (int i = 0; i < nbuf; ++i)  // buffer i = channels 64i..64i+63 of the pixel row
-            tma_load_4d(sIn + stage * Cfg::kStageBytes + i * kInRowStride, &tm_in, &full[stage], 64 * i, g.x0 - 1,
-                        r, g.b);
+          for (int i = 0; i < nbuf; ++i) {  // buffer i = channels 64i..64i+63 of the pixel row
+            if (a.l2_hints & 1)
+              tma_load_4d_hint(sIn + stage * Cfg::kStageBytes + i * kInRowStride, &tm_in, &full[stage], 64 * i,
+                               g.x0 - 1, r, g.b, pol_in);
+            else
+              tma_load_4d(sIn + stage * Cfg::kStageBytes + i * kInRowStride, &tm_in, &full[stage], 64 * i, g.x0 - 1,
+                          r, g.b);
+          }
           if (++stage == Cfg::kNStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -646,7 +652,11 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_4d(&tm_out, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b);
+            if (a.l2_hints & 2)
+              tma_store_4d_hint(&tm_out, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b,
+                                l2_policy_evict_last());
+            else
+              tma_store_4d(&tm_out, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b);
             bulk_commit();
           }
         } else if constexpr (Cfg::kUnshuf) {

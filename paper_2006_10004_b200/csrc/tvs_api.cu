@@ -112,6 +112,8 @@ struct tvs_plan {
   // (saves the K1 kernel and 2x128 B/px of HBM traffic, but on B200 the
   // producer's ~600 FFMA/px-row currently cost more than they save)
   bool unfused_conv0 = true;  // activation bytes per chunk (TVS_CHUNK_MB)
+  int l2_hints = 0;           // TVS_L2_HINTS (ConvArgs::l2_hints)
+  bool pair_fuse = false;     // TVS_PAIR: fuse consecutive hidden layers (conv_pair.cu)
 
   int n_hidden() const { return depth - 2; }
   // tcgen05 fp16 path: FAST mode with 64 channels; everything else runs the
@@ -330,7 +332,27 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     };
     const bool fuse0 = !p->unfused_conv0;
     if (fuse0) cur = 1;  // the first hidden layer reads x and writes act[0]
-    for (int l = 0; l < p->n_hidden(); ++l) {
+    // fused layer pairs: strips form a cluster (<= 8 CTAs), enough rows per cluster
+    const int S = strips;
+    const bool pairs = p->pair_fuse && !fuse0 && S <= 8 &&
+                       (long long)B * Hg >= 16LL * std::max(1, max_ctas / S);
+    int l0 = 0;
+    if (pairs) {
+      for (; l0 + 1 < p->n_hidden(); l0 += 2) {
+        tvs::PairArgs pa{};
+        pa.B = B; pa.H = Hg; pa.W = Wg; pa.S = S;
+        pa.wpack0 = p->wpack + (size_t)l0 * tvs::conv_wpack_bytes(false);
+        pa.wpack1 = p->wpack + (size_t)(l0 + 1) * tvs::conv_wpack_bytes(false);
+        pa.shift0 = p->bhid + (size_t)l0 * tvs::kC;
+        pa.shift1 = p->bhid + (size_t)(l0 + 1) * tvs::kC;
+        pa.act_out = static_cast<uint8_t*>(act[cur ^ 1]);
+        if (const char* e = std::getenv("TVS_PAIR_DBG")) pa.dbg = std::atoi(e);
+        timed_launch(p, st, TVS_KIND_HIDDEN, 2 * pxg * 2.0 * 9 * 64 * 64,
+                     [&] { return tvs::launch_conv_pair(in_map[cur], pa, max_ctas, st); });
+        cur ^= 1;
+      }
+    }
+    for (int l = l0; l < p->n_hidden(); ++l) {
       tvs::ConvArgs a = geom(0, Hg);
       a.wpack = p->wpack + (size_t)l * tvs::conv_wpack_bytes(false);
       a.shift = p->bhid + (size_t)l * tvs::kC;
@@ -340,6 +362,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       const bool first = fuse0 && l == 0;
       a.reverse = (p->l2_reverse_sub > 1) && (l & 1);
       a.nsub = p->l2_reverse_sub;
+      a.l2_hints = p->l2_hints;
       timed_launch(p, st, TVS_KIND_HIDDEN, pxg * 2.0 * 9 * 64 * 64 + (first ? pxg * 2.0 * 9 * 64 : 0.0), [&] {
         return tvs::launch_conv_tc(first ? 2 : 0, in_map[cur], out_map[cur ^ 1], a, first ? &p->conv0 : nullptr,
                                    grid, st);
@@ -479,6 +502,8 @@ int tvs_plan_create_ex(int device, int depth, int channels, int out_bands, int m
     if (const char* e = std::getenv("TVS_L2_CHUNK_MB")) p->l2_chunk_bytes = (size_t)std::atoll(e) << 20;
     if (const char* e = std::getenv("TVS_FUSE_CONV0")) p->unfused_conv0 = std::atoi(e) == 0;
     if (const char* e = std::getenv("TVS_FP32_CUDA")) p->fp32_split = std::atoi(e) == 0;
+    if (const char* e = std::getenv("TVS_L2_HINTS")) p->l2_hints = std::atoi(e);
+    if (const char* e = std::getenv("TVS_PAIR")) p->pair_fuse = std::atoi(e) != 0;
     if (const char* e = std::getenv("TVS_WIDE_CUDA")) p->wide_cuda = std::atoi(e) != 0;
     try {
       TVS_CUDA(tvs::configure_kernels());
