@@ -99,13 +99,23 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def _traffic(spec):
-    """dram read+write bytes per launch of the hidden conv from the committed
+def _kernel_name(tc, launches, depth):
+    """The dominant kernel: the layer-stack launch (all hidden layers, conv_tc.cu
+    mode 8) when a forward took 3 launches, else the per-layer hidden conv."""
+    if not tc:
+        return "hidden_f32_kernel"
+    if launches == 3:
+        return f"conv3x3_tc_kernel<8> (layer stack: {depth - 2} hidden layers per launch)"
+    return "conv3x3_tc_kernel<0> (hidden layer)"
+
+
+def _traffic(spec, kernel):
+    """dram read+write bytes per launch of the dominant kernel from the committed
     ncu capture (profiles/traffic.json), when it was taken on this workload."""
     p = ROOT / "profiles" / "traffic.json"
     if not p.exists():
         return None
-    d = json.loads(p.read_text()).get("conv3x3_tc_kernel<0>", {})
+    d = json.loads(p.read_text()).get(kernel.split(" ")[0], {})
     if d.get("config") != spec.name:
         return None
     return d["dram_bytes_read"] + d["dram_bytes_write"]
@@ -357,14 +367,14 @@ def run_ours(args, spec):
         "latency_ms": round(step_ms, 4) if spec.batch == 1 else None,
         "tflops_algorithmic": round(f["value"] * 1e6 * fpx / 1e12 / world, 2),
         "frac_of_bf16_peak": round(f["value"] * 1e6 * fpx / 1e12 / world / peak_tf, 4),
-        "roofline": {"bound": "tensor", "kernel": "conv3x3_tc_kernel<0> (hidden layer)" if tc else "hidden_f32_kernel",
+        "roofline": {"bound": "tensor", "kernel": _kernel_name(tc, f["launches"], spec.depth),
                      "achieved": round(hid_tflops, 2), "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": round(hid_tflops / peak_tf, 4), "peak_kind": f"{peak_kind} bf16 burst",
                      "frac_of_sustained": round(hid_tflops / peak_sus, 4) if peak_sus else None,
                      "avg_launch_ms": round(hid_avg_ms, 5), "launches_timed": f["hid_n"],
                      "flop_per_launch": f["hid_flops"] / max(1, f["hid_n"]),
                      "share_of_step": round(f["hid_ms"] / max(1e-9, f["hid_ms"] + f["c0_ms"] + f["hd_ms"]), 4),
-                     "traffic": _traffic(spec), "traffic_unit": "bytes per launch (ncu dram read+write)",
+                     "traffic": _traffic(spec, _kernel_name(tc, f["launches"], spec.depth)), "traffic_unit": "bytes per launch (ncu dram read+write)",
                      "algorithmic_bytes_per_launch": 2 * B * H * W * 128},
         "gpu_launches": f["launches"] * f["steps"],
         "e2e": {"value": round(f["e2e"], 3), "unit": UNIT, "h2d_bytes_per_step": f["e2e_bytes"][0],

@@ -20,6 +20,15 @@ constexpr int kSlots = 8;                              // TMEM accumulator slots
 // tcgen05 conv kernels (conv_tc.cu)
 constexpr int kStages = 6;             // input-row ring depth
 constexpr int kEpiGroups = 3;          // epilogue row groups (output row seq % 3)
+#ifndef TVS_EPI_GROUPS_PLAIN
+#define TVS_EPI_GROUPS_PLAIN 3
+#endif
+#ifndef TVS_STAGES_PLAIN
+#define TVS_STAGES_PLAIN 6
+#endif
+constexpr int kEpiGroupsPlain = TVS_EPI_GROUPS_PLAIN;  // modes 0 / 8
+constexpr int kStagesPlain = TVS_STAGES_PLAIN;
+static_assert(kStagesPlain <= kStages, "barrier arrays are sized by kStages");
 
 struct ConvArgs {
   int B, H, W;
@@ -39,7 +48,26 @@ struct ConvArgs {
   // L2 eviction hints of the fast hidden layer (TVS_L2_HINTS): bit 0 = input
   // rows evict_first (read once), bit 1 = output rows evict_last
   int l2_hints;
+  // layer-stack kernel (conv_tc.cu mode 8): all `nlayers` hidden layers in one
+  // persistent launch; wpack / shift hold every layer back to back and
+  // rowcnt[(b*strips + s)*H + y] counts the epilogue warps (4 per layer) that
+  // have stored output row y of strip s of image b
+  int nlayers;
+  int* rowcnt;
+  const int2* items;  // work items {image, layer << 16 | strip} in a topological order
+  // TVS_CONV_DBG experiments (results invalid except 8): 1 no stack flag waits,
+  // 8 writer-side proxy fence, 16 epilogue skips its work, 32 no input loads, 64 no MMAs
+  int dbg;
 };
+// Second pair of tensor maps of the layer-stack kernel (layer j reads buffer j&1
+// and writes buffer (j+1)&1; tm_in / tm_out cover buffer 0 input / buffer 1 output)
+struct StackMaps {
+  CUtensorMap in1;   // buffer 1, 130-px halo rows
+  CUtensorMap out0;  // buffer 0, 32-px store boxes
+};
+cudaError_t launch_conv_stack(const CUtensorMap& tm_in0, const CUtensorMap& tm_out1, const StackMaps& sm,
+                              const ConvArgs& a, int grid, cudaStream_t st);
+int conv_stack_error(int reset);  // watchdog flag of the stack kernel's row-flag waits
 
 // two fused hidden layers (conv_pair.cu): cluster of S = ceil(W/128) CTAs
 struct PairArgs {

@@ -31,6 +31,7 @@
 // groups); every epilogue warp owns one TMEM lane quarter (32 pixels) and
 // stores independently.
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -44,7 +45,8 @@ namespace tvs {
 // segments: maximal runs of consecutive rows inside one (image, strip) column.
 struct Segment {
   int b, x0, ya, yb;
-  int h;  // output-channel half (split hidden layer visits every segment twice)
+  int h;      // output-channel half (split hidden layer visits every segment twice)
+  int layer;  // hidden layer of a layer-stack item (mode 8)
 };
 struct SegIter {
   // [cur, end) of the current sub-range; sub-ranges are visited last-first
@@ -66,6 +68,7 @@ struct SegIter {
     sub = 0;
     set_sub();
   }
+  TVS_DEV int first_layer_or0(const ConvArgs&) const { return 0; }
   TVS_DEV void set_sub() {
     const int k = nsub - 1 - sub;  // reverse order
     cur = lo + (hi - lo) * k / nsub;
@@ -90,12 +93,100 @@ struct SegIter {
     g.ya = a.row0 + y0;
     g.yb = g.ya + n;
     g.h = 0;
+    g.layer = 0;
     cur += n;
     if (nh == 2) {
       last = g;
       pend = true;
     }
     return true;
+  }
+};
+
+// Layer-stack work items (mode 8): item k = (image b, hidden layer j, strip s),
+// ordered image-major, then layer, then strip, so an item only depends on items
+// with smaller k (layer j-1 of the same image, strips s-1..s+1).  CTA i takes
+// items i, i+G, i+2G, ... (equal-length columns of all H rows); the minimal
+// unfinished item always has its inputs complete, so the persistent grid
+// cannot deadlock as long as all G CTAs are co-resident (G <= #SMs, 1 CTA/SM).
+// The item list itself (a.items, built by the host: tvs_api.cu stack_items)
+// is any topological order; the default is image-major.
+struct ItemIter {
+  long long k, n;
+  TVS_DEV ItemIter(const ConvArgs& a, int = 1, int = 1) {
+    k = blockIdx.x;
+    n = (long long)a.B * a.strips * a.nlayers;
+  }
+  TVS_DEV int first_layer_or0(const ConvArgs& a) const { return first_layer(a); }
+  TVS_DEV int first_layer(const ConvArgs& a) const { return k < n ? a.items[k].y >> 16 : 0; }
+  TVS_DEV bool next(const ConvArgs& a, Segment& g) {
+    if (k >= n) return false;
+    const int2 it = a.items[k];
+    g.b = it.x;
+    g.layer = it.y >> 16;
+    g.x0 = (it.y & 0xffff) * kStripPx;
+    g.ya = 0;
+    g.yb = a.H;
+    g.h = 0;
+    k += gridDim.x;
+    return true;
+  }
+};
+
+__device__ int g_stack_err;  // set when a row-flag wait times out (results invalid, no hang)
+
+// Producer side of the layer stack: input row r of a layer-j item (j >= 1) is
+// layer j-1's output row r of strips s-1..s+1 (the 130-px halo box reaches one
+// pixel into each neighbour); it may be loaded once their 4 epilogue warps have
+// stored it (count >= 4j).  A refresh reads kAhead consecutive row counters of
+// every neighbour strip at once (independent loads, one L2 round trip) and
+// remembers how far each is complete, so most rows need no memory access.
+struct StackGate {
+  static constexpr int kAhead = 8;
+  int ready[3];  // last row known complete in strips s-1, s, s+1
+  TVS_DEV void reset() { ready[0] = ready[1] = ready[2] = -1; }
+  TVS_DEV void wait(const ConvArgs& a, const Segment& g, int r) {
+    const int target = 4 * g.layer;
+    const int s = g.x0 / kStripPx;
+    const int* base = a.rowcnt + (long long)g.b * a.strips * a.H;
+    bool refreshed = false;
+    for (uint32_t spins = 0;; ++spins) {
+      int v[3][kAhead];
+      bool need[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int ss = s - 1 + d;
+        need[d] = ss >= 0 && ss < a.strips && ready[d] < r;
+        if (need[d]) {
+          const int* f = base + (long long)ss * a.H + r;
+#pragma unroll
+          for (int i = 0; i < kAhead; ++i) v[d][i] = (r + i < a.H) ? ld_relaxed_gpu(f + i) : target;
+        }
+      }
+      bool ok = true;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        if (!need[d]) continue;
+        refreshed = true;
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < kAhead; ++i)
+          if (c == i && v[d][i] >= target) c = i + 1;
+        ready[d] = r - 1 + c;
+        ok = ok && c > 0;
+      }
+      if (ok) break;
+      if (*(volatile int*)&g_stack_err) return;
+      __nanosleep(32);
+      if (spins > (1u << 26)) {
+        atomicExch(&g_stack_err, 1);
+        return;
+      }
+    }
+    if (refreshed) {  // acquire what the counters published, then hand it to the TMA (async) proxy
+      fence_acq_rel_gpu();
+      fence_proxy_async_global();
+    }
   }
 };
 
@@ -116,8 +207,14 @@ struct SegIter {
 // 7 = head of the opt-in unshuffle = 2 variant (fast mode): Conv2d(C, 4K)
 // with N block 64 = [32 hi | 32 lo] columns and pixel_shuffle folded into the
 // band stores (head channel k*4 + i*2 + j -> band k at (2y+i, 2x+j)).
+// 8 = the whole fast hidden stack in one persistent launch (mode 0's pipeline
+// over ItemIter work items): the weights are reloaded when a CTA moves to an
+// item of another layer, and layer j's input rows are gated on row flags of
+// layer j-1 (stack_wait_row), so consecutive layers run concurrently a few
+// rows apart and the activations pass between them through L2.
 template <int kMode>
 struct ConvCfg {
+  static constexpr bool kStack = kMode == 8;
   static constexpr bool kSplit = kMode >= 3 && kMode <= 6;
   static constexpr bool kUnshuf = kMode == 7;
   static constexpr bool kHead = kMode == 1 || kMode == 4 || kMode == 6 || kMode == 7;
@@ -132,7 +229,10 @@ struct ConvCfg {
   static constexpr int kEpiWarp0 = kProdWarps + 1;
   // 4 more producer warps in mode 2 -> two epilogue groups keep <= 4 warps per
   // SM sub-partition (register file: 16K regs per SMSP, so 128 regs/thread)
-  static constexpr int kGroups = kFirst ? 2 : kEpiGroups;
+  // plain fp16 hidden layer (modes 0 / 8): epilogue groups and ring depth are
+  // build-time knobs (4 groups on a 5-deep ring measured no faster than 3 / 6)
+  static constexpr bool kPlain = kMode == 0 || kMode == 8;
+  static constexpr int kGroups = kFirst ? 2 : (kPlain ? kEpiGroupsPlain : kEpiGroups);
   static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kGroups);
   // split hidden layer: two passes of 32 output channels (TMEM room for three rings)
   static constexpr bool kHalves = kMode == 3;
@@ -143,7 +243,7 @@ struct ConvCfg {
   static constexpr int kW1 = kWhalf * (kHalves ? 2 : 1);  // one weight pack
   static constexpr int kW = kHalves ? 2 * kW1 : kW1;  // fp32 hidden: hi pack | lo pack
   static constexpr int kPasses = kMode == 3 ? 3 : (kSplit ? 2 : 1);
-  static constexpr int kNStages = kSplit ? ((kMode == 4) ? 5 : 2) : kStages;  // input-row ring depth
+  static constexpr int kNStages = kSplit ? ((kMode == 4) ? 5 : 2) : (kPlain ? kStagesPlain : kStages);  // input-row ring depth
   // one stage: [hi K blocks][lo K blocks], one 17 KB SW128 row buffer each
   static constexpr int kStageBytes = (kSplit ? 2 : 1) * kKBlk * kInRowStride;
   static constexpr int kStageOut = (kHead || kSplit) ? 0 : 32 * 128;  // per-warp TMA-store staging
@@ -196,12 +296,13 @@ constexpr float kMainDebias18 = 1.0f + 0.5f * 0.7213f * 9.0f * 1.1920929e-7f;  /
 template <int kMode>
 __global__ void __launch_bounds__(ConvCfg<kMode>::kThreads, 1)
 conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
-                  const ConvArgs a, const __grid_constant__ Conv0Params c0) {
+                  const ConvArgs a, const __grid_constant__ Conv0Params c0, const __grid_constant__ StackMaps smaps) {
   using Cfg = ConvCfg<kMode>;
+  using Iter = std::conditional_t<Cfg::kStack, ItemIter, SegIter>;
   constexpr bool kHead = Cfg::kHead;
   constexpr int NB = Cfg::NB;
   extern __shared__ uint8_t smem_raw[];
-  __shared__ uint64_t full[kStages], empty[kStages], slot_full[kSlots], slot_empty[kSlots], wbar;
+  __shared__ uint64_t full[kStages], empty[kStages], slot_full[kSlots], slot_empty[kSlots], wbar, wfree;
   __shared__ uint32_t tmem_base_smem;
   __shared__ __align__(16) float sShift[kMaxC];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -216,6 +317,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     for (int i = 0; i < Cfg::kNStages; ++i) { mbar_init(&full[i], Cfg::kProdWarps); mbar_init(&empty[i], 1); }
     for (int i = 0; i < kSlots; ++i) { mbar_init(&slot_full[i], 1); mbar_init(&slot_empty[i], 4); }
     mbar_init(&wbar, 1);
+    mbar_init(&wfree, 1);
     fence_barrier_init();
   }
   if (threadIdx.x < kMaxC) sShift[threadIdx.x] = (threadIdx.x < a.nshift) ? a.shift[threadIdx.x] : 0.0f;
@@ -224,7 +326,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   // PDL wait so it overlaps the previous kernel's tail
   if (threadIdx.x == 0) {
     mbar_arrive_expect_tx(&wbar, Cfg::kW);
-    const uint8_t* wsrc = a.wpack + (Cfg::kQuarters ? (blockIdx.x & 3) * Cfg::kW : 0);
+    const uint8_t* wsrc = a.wpack + (Cfg::kQuarters ? (blockIdx.x & 3) * Cfg::kW : 0) +
+                          (size_t)Iter(a).first_layer_or0(a) * Cfg::kW;
     for (int i = 0; i < Cfg::kW / Cfg::kWdx; ++i) bulk_load(sW + i * Cfg::kWdx, wsrc + i * Cfg::kWdx, Cfg::kWdx, &wbar);
   }
   tc_fence_before();
@@ -317,21 +420,45 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
       const uint64_t pol_in = l2_policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      SegIter it(a, Cfg::kVisits, Cfg::kParts);
+      Iter it(a, Cfg::kVisits, Cfg::kParts);
+      int cur_layer = it.first_layer_or0(a);
+      uint32_t nreload = 0;
+      const CUtensorMap* tmi = &tm_in;
+      StackGate gate;
       Segment g;
       while (it.next(a, g)) {
+        if constexpr (Cfg::kStack) {
+          if (g.layer != cur_layer) {  // MMAs of the previous item done -> load this layer's weights
+            mbar_wait(&wfree, nreload & 1);
+            ++nreload;
+            mbar_arrive_expect_tx(&wbar, Cfg::kW);
+            const uint8_t* wsrc = a.wpack + (size_t)g.layer * Cfg::kW;
+            for (int i = 0; i < Cfg::kW / Cfg::kWdx; ++i)
+              bulk_load(sW + i * Cfg::kWdx, wsrc + i * Cfg::kWdx, Cfg::kWdx, &wbar);
+            cur_layer = g.layer;
+          }
+          tmi = (g.layer & 1) ? &smaps.in1 : &tm_in;
+          gate.reset();
+        }
         const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
         for (int r = r0; r <= r1; ++r) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if constexpr (Cfg::kStack)
+            if (g.layer > 0 && !(a.dbg & 1)) gate.wait(a, g, r);
           constexpr int nbuf = (Cfg::kSplit ? 2 : 1) * Cfg::kKBlk;  // [hi blocks][lo blocks]
+          if (a.dbg & 32) {  // ablation (TVS_CONV_DBG): no input loads
+            mbar_arrive(&full[stage]);
+            if (++stage == Cfg::kNStages) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_arrive_expect_tx(&full[stage], nbuf * kInRowBytes);
 #pragma unroll
           for (int i = 0; i < nbuf; ++i) {  // buffer i = channels 64i..64i+63 of the pixel row
             if (a.l2_hints & 1)
-              tma_load_4d_hint(sIn + stage * Cfg::kStageBytes + i * kInRowStride, &tm_in, &full[stage], 64 * i,
+              tma_load_4d_hint(sIn + stage * Cfg::kStageBytes + i * kInRowStride, tmi, &full[stage], 64 * i,
                                g.x0 - 1, r, g.b, pol_in);
             else
-              tma_load_4d(sIn + stage * Cfg::kStageBytes + i * kInRowStride, &tm_in, &full[stage], 64 * i, g.x0 - 1,
+              tma_load_4d(sIn + stage * Cfg::kStageBytes + i * kInRowStride, tmi, &full[stage], 64 * i, g.x0 - 1,
                           r, g.b);
           }
           if (++stage == Cfg::kNStages) { stage = 0; phase ^= 1; }
@@ -350,14 +477,26 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const uint64_t adesc0 = make_smem_desc(smem_u32(sIn), 0, 1024, kLayoutSW128);
     const uint64_t bdesc0 = make_smem_desc(smem_u32(sW), 0, 1024, kLayoutSW128);
     const bool leader = elect_one();
+    const bool domma = !(a.dbg & 64);  // ablation (TVS_CONV_DBG): no MMAs
     mbar_wait(&wbar, 0);
     int stage = 0;
     uint32_t phase = 0;
     uint32_t seq = 0;  // output-row sequence number: slot = seq % kRing, use = seq / kRing
     bool prewaited = false;  // this row's barriers were already awaited by the previous row
-    SegIter it(a, Cfg::kVisits, Cfg::kParts);
+    Iter it(a, Cfg::kVisits, Cfg::kParts);
+    int cur_layer = it.first_layer_or0(a);
+    uint32_t wphase = 0;
     Segment g;
     while (it.next(a, g)) {
+      if constexpr (Cfg::kStack) {
+        if (g.layer != cur_layer) {  // release the weights once the issued MMAs complete, await the next layer's
+          if (leader) mma_commit(&wfree);
+          __syncwarp();
+          wphase ^= 1;
+          mbar_wait(&wbar, wphase);
+          cur_layer = g.layer;
+        }
+      }
       const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
       for (int r = r0; r <= r1; ++r) {
         // ---- fast path: interior input row (targets r-1, r, r+1 inside the
@@ -399,10 +538,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                   const bool first_k = Cfg::enters(p, k) && dx == 0;
                   const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + t0s;
                   if (first_k) {  // enter row r+1 (acc=0), keep r-1, r
-                    mma_f16_ss_fill(t0 + 2 * NB, ad, bd + b2, idesc1, 0u);
-                    mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
+                    if (domma) mma_f16_ss_fill(t0 + 2 * NB, ad, bd + b2, idesc1, 0u);
+                    if (domma) mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
                   } else {
-                    mma_f16_ss(t0, ad, bd, idesc3, 1u);
+                    if (domma) mma_f16_ss(t0, ad, bd, idesc3, 1u);
                   }
                   prewait(p, dx, k);
                 }
@@ -417,8 +556,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                   const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + Cfg::b_koff(k)) >> 4);
                   const bool first_k = Cfg::enters(p, k) && dx == 0;
                   const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + t0s;
-                  mma_f16_ss_fill(rb, ad, bd + b2, idesc1, first_k ? 0u : 1u);
-                  mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
+                  if (domma) mma_f16_ss_fill(rb, ad, bd + b2, idesc1, first_k ? 0u : 1u);
+                  if (domma) mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
                   prewait(p, dx, k);
                 }
             } else {  // slot R-1 | wrap | 0, 1
@@ -432,12 +571,12 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                   const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + Cfg::b_koff(k)) >> 4);
                   const bool first_k = Cfg::enters(p, k) && dx == 0;
                   const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + t0s;
-                  mma_f16_ss_fill(t0, ad, bd, idesc1, 1u);
+                  if (domma) mma_f16_ss_fill(t0, ad, bd, idesc1, 1u);
                   if (first_k) {
-                    mma_f16_ss_use(rb, ad, bd + b1, idesc1, 1u);
-                    mma_f16_ss_lastuse(rb + NB, ad, bd + b2, idesc1, 0u);
+                    if (domma) mma_f16_ss_use(rb, ad, bd + b1, idesc1, 1u);
+                    if (domma) mma_f16_ss_lastuse(rb + NB, ad, bd + b2, idesc1, 0u);
                   } else {
-                    mma_f16_ss_lastuse(rb, ad, bd + b1, idesc2, 1u);
+                    if (domma) mma_f16_ss_lastuse(rb, ad, bd + b1, idesc2, 1u);
                   }
                   prewait(p, dx, k);
                 }
@@ -496,13 +635,13 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                                                        dx * Cfg::kWdx + Cfg::b_koff(k)) >> 4);
               const uint32_t rb = tmem + Cfg::ring_col(p, k);
               if (Cfg::enters(p, k) && dx == 0) {
-                if (vA) mma_f16_ss(rb + At, ad, bd + Ab, Ai, 1u);
-                if (vB) mma_f16_ss(rb + Bt, ad, bd + Bb, Bi, 0u);
-                if (vC) mma_f16_ss(rb + Ct, ad, bd + Cb, Ci, 1u);
-                if (vD) mma_f16_ss(rb + Dt, ad, bd + Db, Di, 0u);
+                if (vA) if (domma) mma_f16_ss(rb + At, ad, bd + Ab, Ai, 1u);
+                if (vB) if (domma) mma_f16_ss(rb + Bt, ad, bd + Bb, Bi, 0u);
+                if (vC) if (domma) mma_f16_ss(rb + Ct, ad, bd + Cb, Ci, 1u);
+                if (vD) if (domma) mma_f16_ss(rb + Dt, ad, bd + Db, Di, 0u);
               } else {
-                mma_f16_ss(rb + R0t, ad, bd + R0b, R0i, 1u);
-                if (c1 > 0) mma_f16_ss(rb + R1t, ad, bd + R1b, R1i, 1u);
+                if (domma) mma_f16_ss(rb + R0t, ad, bd + R0b, R0i, 1u);
+                if (c1 > 0) if (domma) mma_f16_ss(rb + R1t, ad, bd + R1b, R1i, 1u);
               }
             }
           }
@@ -526,9 +665,12 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const uint32_t shift_u = smem_u32(sShift);
     if (!kHead && !Cfg::kSplit && lane == 0) prefetch_tmap(&tm_out);
     uint32_t seq = 0, gsel = 0;  // gsel = seq % kGroups
-    SegIter it(a, Cfg::kVisits, Cfg::kParts);
+    Iter it(a, Cfg::kVisits, Cfg::kParts);
     Segment g;
     while (it.next(a, g)) {
+      // layer-stack: this item's BN shift and output buffer
+      const float4* shg = reinterpret_cast<const float4*>(a.shift + (size_t)g.layer * kC);
+      const CUtensorMap* tmo = (Cfg::kStack && (g.layer & 1)) ? &smaps.out0 : &tm_out;
       for (int q = g.ya; q < g.yb; ++q, ++seq, gsel = (gsel + 1 == Cfg::kGroups) ? 0 : gsel + 1) {
         if (gsel != grp) continue;
         const uint32_t slot = seq & Cfg::kRingMask;
@@ -620,6 +762,12 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             }
           }
         } else if constexpr (!kHead) {
+          if (a.dbg & 16) {  // ablation (TVS_CONV_DBG): drain the slot without reading it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&slot_empty[slot]);
+            continue;
+          }
           uint32_t v[4][16];
 #pragma unroll
           for (int j = 0; j < 4; ++j) tmem_ld16(tmem + lane_addr + slot * NB + j * 16, v[j]);
@@ -635,8 +783,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           const uint32_t rowp = stage_out + lane * 128;
 #pragma unroll
           for (int chunk = 0; chunk < 8; ++chunk) {  // 16-byte chunk = 8 channels
-            const float4 s0 = ld_shared_f4(shift_u + chunk * 32);
-            const float4 s1 = ld_shared_f4(shift_u + chunk * 32 + 16);
+            const float4 s0 = Cfg::kStack ? __ldg(shg + 2 * chunk) : ld_shared_f4(shift_u + chunk * 32);
+            const float4 s1 = Cfg::kStack ? __ldg(shg + 2 * chunk + 1) : ld_shared_f4(shift_u + chunk * 32 + 16);
             const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
             uint32_t packed[4];
 #pragma unroll
@@ -653,11 +801,22 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           __syncwarp();
           if (lane == 0) {
             if (a.l2_hints & 2)
-              tma_store_4d_hint(&tm_out, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b,
+              tma_store_4d_hint(tmo, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b,
                                 l2_policy_evict_last());
             else
-              tma_store_4d(&tm_out, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b);
+              tma_store_4d(tmo, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b);
             bulk_commit();
+            if constexpr (Cfg::kStack) bulk_wait<0>();  // this warp's quarter row has landed
+          }
+          if constexpr (Cfg::kStack) {
+            // publish the row to the next layer's items: the group's 4 warps
+            // meet on a named barrier, one thread releases the row counter (+4)
+            __syncwarp();
+            named_bar_sync(1 + grp, 128);
+            if (quarter == 0 && lane == 0) {
+              if (a.dbg & 8) fence_proxy_async_global();
+              red_release_gpu_add(a.rowcnt + ((long long)g.b * a.strips + g.x0 / kStripPx) * a.H + q, 4);
+            }
           }
         } else if constexpr (Cfg::kUnshuf) {
           uint32_t v[4][16];
@@ -943,6 +1102,7 @@ size_t conv_wpack_unshuf_head_bytes() { return ConvCfg<7>::kW; }
 cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a,
                            const Conv0Params* c0, int grid, cudaStream_t st) {
   static const Conv0Params zero{};
+  static const StackMaps zs{};
   const Conv0Params& p0 = c0 ? *c0 : zero;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -956,38 +1116,66 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
     case 0:
       cfg.blockDim = dim3(ConvCfg<0>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<0>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<0>, tm_in, tm_out, a, p0);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<0>, tm_in, tm_out, a, p0, zs);
     case 1:
       cfg.blockDim = dim3(ConvCfg<1>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<1>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<1>, tm_in, tm_out, a, p0);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<1>, tm_in, tm_out, a, p0, zs);
     case 2:
       cfg.blockDim = dim3(ConvCfg<2>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<2>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<2>, tm_in, tm_out, a, p0);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<2>, tm_in, tm_out, a, p0, zs);
     case 3:
       cfg.blockDim = dim3(ConvCfg<3>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<3>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<3>, tm_in, tm_out, a, p0);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<3>, tm_in, tm_out, a, p0, zs);
     case 4:
       cfg.blockDim = dim3(ConvCfg<4>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<4>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<4>, tm_in, tm_out, a, p0);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<4>, tm_in, tm_out, a, p0, zs);
     case 5:
       cfg.gridDim = dim3(std::max(4, grid & ~3));  // groups of 4 CTAs (output-channel quarters)
       cfg.blockDim = dim3(ConvCfg<5>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<5>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<5>, tm_in, tm_out, a, p0);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<5>, tm_in, tm_out, a, p0, zs);
     case 6:
       cfg.blockDim = dim3(ConvCfg<6>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<6>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<6>, tm_in, tm_out, a, p0);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<6>, tm_in, tm_out, a, p0, zs);
     case 7:
       cfg.blockDim = dim3(ConvCfg<7>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<7>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<7>, tm_in, tm_out, a, p0);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<7>, tm_in, tm_out, a, p0, zs);
   }
   return cudaErrorInvalidValue;
+}
+
+// Layer stack (mode 8): grid <= #SMs so every CTA is co-resident (1 CTA/SM);
+// rowcnt must be zero on entry.
+cudaError_t launch_conv_stack(const CUtensorMap& tm_in0, const CUtensorMap& tm_out1, const StackMaps& sm,
+                              const ConvArgs& a, int grid, cudaStream_t st) {
+  static const Conv0Params zero{};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(ConvCfg<8>::kThreads);
+  cfg.dynamicSmemBytes = ConvCfg<8>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<8>, tm_in0, tm_out1, a, zero, sm);
+}
+
+int conv_stack_error(int reset) {
+  int v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_stack_err, sizeof(int)) != cudaSuccess) return -1;
+  if (reset) {
+    const int z = 0;
+    cudaMemcpyToSymbol(g_stack_err, &z, sizeof(int));
+  }
+  return v;
 }
 
 cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* out, cudaStream_t st) {
@@ -1062,6 +1250,9 @@ cudaError_t configure_kernels() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<7>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<8>::kSmem);
   if (e != cudaSuccess) return e;
   return configure_edge_kernels();
 }

@@ -372,4 +372,23 @@ TVS_DEV void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Cross-CTA row flags of the layer-stack kernel (conv_tc.cu mode 8): the
+// writer's TMA stores complete (bulk_wait<0>), a proxy fence orders them before
+// the generic release; the reader acquires, then fences before its TMA load.
+TVS_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+TVS_DEV int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+TVS_DEV int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+TVS_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+TVS_DEV void red_release_gpu_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 }  // namespace tvs

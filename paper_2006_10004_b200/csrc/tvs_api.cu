@@ -11,6 +11,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "../../include/tvs_b200.h"
@@ -114,6 +115,22 @@ struct tvs_plan {
   bool unfused_conv0 = true;  // activation bytes per chunk (TVS_CHUNK_MB)
   int l2_hints = 0;           // TVS_L2_HINTS (ConvArgs::l2_hints)
   bool pair_fuse = false;     // TVS_PAIR: fuse consecutive hidden layers (conv_pair.cu)
+  // layer-stack kernel (conv_tc.cu mode 8, all hidden layers in one persistent
+  // launch, activations handed between layers through L2): TVS_STACK = 0 off,
+  // 1 whenever legal, -1 (default) when the chunk has >= kStackMinItems work
+  // items per SM (short columns / few images keep the per-layer kernels)
+  int stack = -1;
+  static constexpr int kStackMinItems = 6;
+  int* rowcnt = nullptr;  // row flags (B*strips*H ints), zeroed per chunk
+  size_t rowcnt_n = 0;
+  // work-item order (TVS_STACK_SKEW = A): items sorted by diagonal i*A + j, then
+  // layer, then strip; A >= n_hidden is image-major, small A interleaves layer j
+  // of image i with layer j+A of image i-1 (more slack between a layer and the
+  // next, more activation rows live in L2)
+  int stack_skew = 1 << 20;
+  int2* items = nullptr;
+  size_t items_cap = 0;
+  long long items_key[4] = {-1, -1, -1, -1};
 
   int n_hidden() const { return depth - 2; }
   // tcgen05 fp16 path: FAST mode with 64 channels; everything else runs the
@@ -150,7 +167,7 @@ void free_all(tvs_plan* p) {
   p->recs.clear();
   p->event_pool.clear();
   void* ptrs[] = {p->wh, p->bh, p->wpack, p->hpack, p->whid, p->bhid, p->shid, p->act[0], p->act[1], p->dx,
-                  p->w0u, p->b0u};
+                  p->w0u, p->b0u, p->rowcnt, p->items};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -187,6 +204,36 @@ void ensure_streams(tvs_plan* p, int ns, size_t bytes) {
     for (auto& q : p->sact) TVS_CUDA(cudaMalloc(&q, nbytes));
     p->sact_bytes = nbytes;
   }
+}
+
+// Work items of the layer-stack kernel for (B, strips, layers): a topological
+// order (an item only depends on layer j-1 items of its image, which sort
+// before it), uploaded once per shape.
+const int2* stack_items(tvs_plan* p, int B, int strips, int L, cudaStream_t st) {
+  const long long key[4] = {B, strips, L, p->stack_skew};
+  if (std::equal(key, key + 4, p->items_key)) return p->items;
+  const size_t n = (size_t)B * strips * L;
+  std::vector<std::array<long long, 4>> v;
+  v.reserve(n);
+  const long long A = std::max(1, p->stack_skew);
+  for (int i = 0; i < B; ++i)
+    for (int j = 0; j < L; ++j)
+      for (int s = 0; s < strips; ++s) v.push_back({i * A + j, j, s, i});
+  std::sort(v.begin(), v.end());
+  std::vector<int2> h(n);
+  for (size_t k = 0; k < n; ++k) h[k] = make_int2((int)v[k][3], (int)(v[k][1] << 16 | v[k][2]));
+  if (n > p->items_cap) {
+    TVS_CUDA(cudaStreamSynchronize(st));
+    if (p->items) TVS_CUDA(cudaFree(p->items));
+    p->items = nullptr;
+    p->items_cap = 0;
+    TVS_CUDA(cudaMalloc(&p->items, n * sizeof(int2)));
+    p->items_cap = n;
+  }
+  TVS_CUDA(cudaStreamSynchronize(st));  // a running stack kernel may still read the old table
+  TVS_CUDA(cudaMemcpy(p->items, h.data(), n * sizeof(int2), cudaMemcpyHostToDevice));
+  std::copy(key, key + 4, p->items_key);
+  return p->items;
 }
 
 int conv_grid(int max_ctas, const tvs::ConvArgs& a) {
@@ -242,6 +289,30 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
   const bool wide = p->wide_path();
   const int C = p->channels;
   const double px = (double)B * H * W;
+  // layer stack (FAST path): every CTA of the persistent grid must be resident
+  // at once, so only on the full device grid of the single-stream path
+  bool stack = false;
+  if (fast && p->stack != 0 && p->unfused_conv0 && !p->pair_fuse && max_ctas >= p->num_sms) {
+    const int us0 = p->unshuffle;
+    const long long items = (long long)B * ((W / us0 + tvs::kStripPx - 1) / tvs::kStripPx) * p->n_hidden();
+    // auto: enough items per SM, and a last round that is nearly full (the
+    // items are equal-length columns, a partial round idles SMs)
+    const long long rounds = (items + p->num_sms - 1) / p->num_sms;
+    stack = p->stack == 1 || (items >= (long long)tvs_plan::kStackMinItems * p->num_sms &&
+                              (double)items >= 0.95 * (double)(rounds * p->num_sms));
+  }
+  if (stack) {
+    const int us0 = p->unshuffle;
+    const size_t n = (size_t)B * ((W / us0 + tvs::kStripPx - 1) / tvs::kStripPx) * (H / us0);
+    if (n > p->rowcnt_n) {
+      if (p->rowcnt) TVS_CUDA(cudaFree(p->rowcnt));
+      p->rowcnt = nullptr;
+      p->rowcnt_n = 0;
+      TVS_CUDA(cudaMalloc(&p->rowcnt, n * sizeof(int)));
+      p->rowcnt_n = n;
+    }
+    TVS_CUDA(cudaMemsetAsync(p->rowcnt, 0, n * sizeof(int), st));
+  }
   // K1 (the FAST path can fuse it into the first hidden layer's producer)
   const int fmt = fast ? tvs::kActF16 : ((split || wide) ? tvs::kActSplit : tvs::kActF32);
   const int us = p->unshuffle;  // 2: the layer stack runs on the (H/2, W/2) grid
@@ -337,6 +408,25 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     const bool pairs = p->pair_fuse && !fuse0 && S <= 8 &&
                        (long long)B * Hg >= 16LL * std::max(1, max_ctas / S);
     int l0 = 0;
+    if (stack) {
+      tvs::ConvArgs a = geom(0, Hg);
+      a.wpack = p->wpack;
+      a.shift = p->bhid;
+      a.nshift = tvs::kC;
+      a.nlayers = p->n_hidden();
+      a.rowcnt = p->rowcnt;
+      a.items = stack_items(p, B, strips, a.nlayers, st);
+      if (const char* e = std::getenv("TVS_CONV_DBG")) a.dbg = std::atoi(e);
+      tvs::StackMaps sm{};
+      sm.in1 = in_map[1];
+      sm.out0 = out_map[0];
+      const long long items = (long long)B * strips * a.nlayers;
+      const int grid = (int)std::min<long long>(p->num_sms, items);
+      timed_launch(p, st, TVS_KIND_HIDDEN, a.nlayers * pxg * 2.0 * 9 * 64 * 64,
+                   [&] { return tvs::launch_conv_stack(in_map[0], out_map[1], sm, a, grid, st); });
+      l0 = a.nlayers;
+      cur = l0 & 1;
+    }
     if (pairs) {
       for (; l0 + 1 < p->n_hidden(); l0 += 2) {
         tvs::PairArgs pa{};
@@ -363,6 +453,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.reverse = (p->l2_reverse_sub > 1) && (l & 1);
       a.nsub = p->l2_reverse_sub;
       a.l2_hints = p->l2_hints;
+      if (const char* e = std::getenv("TVS_CONV_DBG")) a.dbg = std::atoi(e);
       timed_launch(p, st, TVS_KIND_HIDDEN, pxg * 2.0 * 9 * 64 * 64 + (first ? pxg * 2.0 * 9 * 64 : 0.0), [&] {
         return tvs::launch_conv_tc(first ? 2 : 0, in_map[cur], out_map[cur ^ 1], a, first ? &p->conv0 : nullptr,
                                    grid, st);
@@ -504,6 +595,8 @@ int tvs_plan_create_ex(int device, int depth, int channels, int out_bands, int m
     if (const char* e = std::getenv("TVS_FP32_CUDA")) p->fp32_split = std::atoi(e) == 0;
     if (const char* e = std::getenv("TVS_L2_HINTS")) p->l2_hints = std::atoi(e);
     if (const char* e = std::getenv("TVS_PAIR")) p->pair_fuse = std::atoi(e) != 0;
+    if (const char* e = std::getenv("TVS_STACK")) p->stack = std::atoi(e);
+    if (const char* e = std::getenv("TVS_STACK_SKEW")) p->stack_skew = std::atoi(e);
     if (const char* e = std::getenv("TVS_WIDE_CUDA")) p->wide_cuda = std::atoi(e) != 0;
     try {
       TVS_CUDA(tvs::configure_kernels());
@@ -711,6 +804,10 @@ int tvs_tvflow_analyze(const double* f, int N, int H, int W, double dt, int n_st
     TVS_CUDA(tvs::launch_tvflow(a, (cudaStream_t)stream));
   });
 }
+
+// diagnostics of the layer-stack kernel (not part of the public ABI): 1 if a
+// row-flag wait timed out since the last reset (that forward's output is invalid)
+int tvs_debug_stack(int reset) { return tvs::conv_stack_error(reset); }
 
 int tvs_plan_destroy(tvs_plan* p) {
   return guarded([&] {

@@ -279,3 +279,56 @@ def test_fp32_cuda_core_kernels(golden, monkeypatch):
         with torch.no_grad():
             out = m(torch.from_numpy(golden[f"{case}_x"]).cuda()).cpu().numpy()
         assert band_rel_l2(out, golden[f"{case}_y"]).max() <= 1e-5, case
+
+
+def _stack_model(seeded_state, monkeypatch, stack):
+    monkeypatch.setenv("TVS_STACK", str(stack))
+    m = TVSpecNet().eval()
+    m.load_state_dict(seeded_state)
+    m._plan_for(torch.device("cuda", 0))  # the plan reads TVS_STACK when it is created
+    monkeypatch.delenv("TVS_STACK")
+    return m
+
+
+def _stack_watchdog():
+    import ctypes
+    lib = _native.load()
+    lib.tvs_debug_stack.restype = ctypes.c_int
+    lib.tvs_debug_stack.argtypes = [ctypes.c_int]
+    return lib.tvs_debug_stack(1)
+
+
+@pytest.mark.parametrize("shape", [(2, 48, 160), (1, 37, 300), (3, 64, 128), (1, 5, 7), (2, 1, 130)])
+def test_layer_stack_bitwise(seeded_state, monkeypatch, shape):
+    """The layer-stack kernel (conv_tc.cu mode 8: all hidden layers in one
+    persistent launch, layers handed over through L2 under row flags) computes
+    every output with the per-layer kernel's exact MMA sequence: bitwise equal,
+    including ragged strips (W % 128 != 0), H < 3 and W < 128."""
+    _stack_watchdog()
+    m0 = _stack_model(seeded_state, monkeypatch, 0)
+    m1 = _stack_model(seeded_state, monkeypatch, 1)
+    x = torch.rand(*shape[:1], 1, *shape[1:], generator=torch.Generator().manual_seed(sum(shape))).cuda()
+    with torch.no_grad():
+        y0, y1 = m0(x), m1(x)
+    torch.cuda.synchronize()
+    assert _stack_watchdog() == 0
+    assert m0.last_launch_count() == m0.depth and m1.last_launch_count() == 3
+    assert torch.equal(y0, y1)
+
+
+def test_layer_stack_auto_config2(seeded_state, oracle):
+    """Config 2 (64 x 256^2) selects the layer stack by default (1920 items on
+    148 SMs); parity against the oracle on two of its images."""
+    m = TVSpecNet().eval()
+    m.load_state_dict(seeded_state)
+    x = np.stack([make_image(CONFIGS[2], i) for i in range(64)])[:, None]
+    _stack_watchdog()
+    bands, clos = m.forward_planes(torch.from_numpy(x).cuda(), closure=True)
+    torch.cuda.synchronize()
+    assert _stack_watchdog() == 0
+    assert m.last_launch_count() == 3
+    with torch.no_grad():
+        ref = oracle(torch.from_numpy(x[[0, 63]])).numpy()
+    err = band_rel_l2(bands.cpu().numpy()[[0, 63]], ref)
+    assert err.max() <= TOL["fast"], f"worst band rel-L2 {err.max():.3e}"
+    np.testing.assert_allclose((bands.sum(1, keepdim=True) + clos).cpu().numpy(), x, atol=1e-5)
