@@ -511,6 +511,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           const int nstage = (stage + 1 == Cfg::kNStages) ? 0 : stage + 1;
           const uint32_t nphase = (stage + 1 == Cfg::kNStages) ? (phase ^ 1) : phase;
           const uint32_t sq2 = sq + 3;  // output row r+2, entered by input row r+1
+          bool pre_ok = false;  // (issuing lane) the next row's barriers have completed
           if (leader) {
             if (!prewaited)
               mbar_wait2(&slot_empty[(sq + 2) & Cfg::kRingMask], (((sq + 2) >> Cfg::kRingLog) & 1) ^ 1, &full[stage],
@@ -520,13 +521,23 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             const uint32_t t0s = s * NB;  // slot column offset inside a ring
             const uint32_t hoff = (uint32_t)g.h * Cfg::kWhalf;  // B offset of the channel half
             constexpr uint32_t b1 = NB * 128 / 16, b2 = 2 * NB * 128 / 16;  // W(dy=0), W(dy=-1) blocks
+            // Non-blocking probes (mid-row and near the row's end): a blocking
+            // wait here would hold back the rest of this row's MMAs whenever
+            // the next input row is late, draining the tensor-core queue.
             auto prewait = [&](int p, int dx, int k) {
-              if (p == Cfg::kPasses / 2 && dx == 1 && k == 1 && next_fast)
-                mbar_wait2(&slot_empty[sq2 & Cfg::kRingMask], ((sq2 >> Cfg::kRingLog) & 1) ^ 1, &full[nstage], nphase);
+              if (((p == Cfg::kPasses / 2 && dx == 1 && k == 1) ||
+                   (p == Cfg::kPasses - 1 && dx == 2 && k == Cfg::kKSteps - 2)) &&
+                  next_fast && !pre_ok && !(a.dbg & 2048))
+                pre_ok = mbar_test(&slot_empty[sq2 & Cfg::kRingMask], ((sq2 >> Cfg::kRingLog) & 1) ^ 1) &&
+                         mbar_test(&full[nstage], nphase);
             };
             // Split pieces share A through the collector: the N=NB piece is
             // issued first (fill), the N=2NB piece second (lastuse) -> full rate.
-            if (s + 3 <= (uint32_t)Cfg::kRing) {
+            // ablation (TVS_CONV_DBG): 512 = wrap rows issue the unsplit pattern at
+            // slot 0, 1024 = no first-step split (results invalid)
+            const bool nowrap = (a.dbg & 512) && s + 3 > (uint32_t)Cfg::kRing;
+            const bool nosplit = (a.dbg & 1024);
+            if (s + 3 <= (uint32_t)Cfg::kRing || nowrap) {
 #pragma unroll
               for (int p = 0; p < Cfg::kPasses; ++p)
 #pragma unroll
@@ -535,8 +546,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                 for (int k = 0; k < Cfg::kKSteps; ++k) {
                   const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p, k) + dx * 128 + (k % 4) * 32) >> 4);
                   const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + Cfg::b_koff(k)) >> 4);
-                  const bool first_k = Cfg::enters(p, k) && dx == 0;
-                  const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + t0s;
+                  const bool first_k = Cfg::enters(p, k) && dx == 0 && !nosplit;
+                  const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + (nowrap ? 0u : t0s);
                   if (first_k) {  // enter row r+1 (acc=0), keep r-1, r
                     if (domma) mma_f16_ss_fill(t0 + 2 * NB, ad, bd + b2, idesc1, 0u);
                     if (domma) mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
@@ -585,7 +596,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             mma_commit(&slot_full[s]);
           }
           __syncwarp();
-          prewaited = next_fast;
+          prewaited = next_fast && pre_ok;
           stage = nstage;
           phase = nphase;
           continue;
@@ -777,6 +788,15 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
+          if (a.dbg & 128) {  // ablation: TMEM read only (keep the values alive)
+            uint32_t acc = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int i = 0; i < 16; ++i) acc ^= v[j][i];
+            if (acc == 0x7fc00123u) a.rowcnt[0] = 1;
+            continue;
+          }
           // this warp's staging buffer: its previous TMA store must have read it
           if (lane == 0) bulk_wait_read<0>();
           __syncwarp();
@@ -799,6 +819,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           }
           fence_async_smem();
           __syncwarp();
+          if (a.dbg & 256) continue;  // ablation: no TMA store
           if (lane == 0) {
             if (a.l2_hints & 2)
               tma_store_4d_hint(tmo, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b,

@@ -54,6 +54,16 @@ TVS_DEV bool mbar_try_wait(uint32_t bar_addr, uint32_t parity) {
       : "=r"(ok) : "r"(bar_addr), "r"(parity) : "memory");
   return ok != 0;
 }
+// Non-blocking probe of phase `parity` (test_wait never suspends the thread).
+TVS_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
 // Blocking wait on phase `parity`.  try_wait sleeps in hardware between
 // polls; the loop only re-issues after the hardware time limit.
 TVS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
