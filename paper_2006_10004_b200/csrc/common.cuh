@@ -52,6 +52,7 @@ struct ConvArgs {
   // persistent launch; wpack / shift hold every layer back to back and
   // rowcnt[(b*strips + s)*H + y] counts the epilogue warps (4 per layer) that
   // have stored output row y of strip s of image b
+  int out_single;  // wide hidden (modes 5 / 9): write single fp16 output instead of the hi/lo pair
   int nlayers;
   int* rowcnt;
   const int2* items;  // work items {image, layer << 16 | strip} in a topological order

@@ -277,6 +277,9 @@ cudaError_t launch_conv0(int act_fmt, int C, const float* x, void* act, const Co
   } else if (C == 128 && act_fmt == kActF32) {
     const unsigned grid = (unsigned)((npx + 63) / 64);
     conv0_kernel<float, 128><<<grid, 64, 0, st>>>(x, static_cast<float*>(act), p, B, H, W);
+  } else if (C == 128 && act_fmt == kActF16) {
+    const unsigned grid = (unsigned)((npx + 63) / 64);
+    conv0_kernel<__half, 128><<<grid, 64, 0, st>>>(x, static_cast<__half*>(act), p, B, H, W);
   } else if (C == 128 && act_fmt == kActSplit) {
     const unsigned grid = (unsigned)((npx + 63) / 64);
     conv0_kernel<__half, 128, true><<<grid, 64, 0, st>>>(x, static_cast<__half*>(act), p, B, H, W);

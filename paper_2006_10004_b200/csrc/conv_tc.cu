@@ -207,6 +207,10 @@ struct StackGate {
 // 7 = head of the opt-in unshuffle = 2 variant (fast mode): Conv2d(C, 4K)
 // with N block 64 = [32 hi | 32 lo] columns and pixel_shuffle folded into the
 // band stores (head channel k*4 + i*2 + j -> band k at (2y+i, 2x+j)).
+// 9 / 10 = the wide variant's hidden layer / head on SINGLE fp16 input
+// activations (one pass; mode 9's output is a pair or single per a.out_single):
+// the fast wide stack stores the first layers' activations as pairs and the
+// rest as single fp16 (tools/emulate_wide.py), trading MMA work for accuracy.
 // 8 = the whole fast hidden stack in one persistent launch (mode 0's pipeline
 // over ItemIter work items): the weights are reloaded when a CTA moves to an
 // item of another layer, and layer j's input rows are gated on row flags of
@@ -217,10 +221,10 @@ struct ConvCfg {
   static constexpr bool kStack = kMode == 8;
   static constexpr bool kSplit = kMode >= 3 && kMode <= 6;
   static constexpr bool kUnshuf = kMode == 7;
-  static constexpr bool kHead = kMode == 1 || kMode == 4 || kMode == 6 || kMode == 7;
+  static constexpr bool kHead = kMode == 1 || kMode == 4 || kMode == 6 || kMode == 7 || kMode == 10;
   static constexpr bool kFirst = kMode == 2;
-  static constexpr bool kWide = kMode == 5 || kMode == 6;
-  static constexpr bool kQuarters = kMode == 5;
+  static constexpr bool kWide = kMode == 5 || kMode == 6 || kMode == 9 || kMode == 10;
+  static constexpr bool kQuarters = kMode == 5 || kMode == 9;
   static constexpr int kCin = kWide ? 128 : 64;
   static constexpr int kKBlk = kCin / 64;        // 64-channel K blocks (one SW128 row buffer each)
   static constexpr int kKSteps = 4 * kKBlk;      // K16 steps per tap
@@ -243,10 +247,11 @@ struct ConvCfg {
   static constexpr int kW1 = kWhalf * (kHalves ? 2 : 1);  // one weight pack
   static constexpr int kW = kHalves ? 2 * kW1 : kW1;  // fp32 hidden: hi pack | lo pack
   static constexpr int kPasses = kMode == 3 ? 3 : (kSplit ? 2 : 1);
-  static constexpr int kNStages = kSplit ? ((kMode == 4) ? 5 : 2) : (kPlain ? kStagesPlain : kStages);  // input-row ring depth
+  static constexpr int kNStages =
+      kSplit ? ((kMode == 4) ? 5 : 2) : (kPlain ? kStagesPlain : (kWide ? 4 : kStages));  // input-row ring depth
   // one stage: [hi K blocks][lo K blocks], one 17 KB SW128 row buffer each
   static constexpr int kStageBytes = (kSplit ? 2 : 1) * kKBlk * kInRowStride;
-  static constexpr int kStageOut = (kHead || kSplit) ? 0 : 32 * 128;  // per-warp TMA-store staging
+  static constexpr int kStageOut = (kHead || kSplit || kWide) ? 0 : 32 * 128;  // per-warp TMA-store staging
   static constexpr size_t kSmem = 1024 + kW + kNStages * kStageBytes + 4 * kGroups * kStageOut + 1024;
   // A / B descriptor offsets (bytes) of pass p, K step k (within-block k%4 added by the caller)
   static constexpr uint32_t a_off(int p, int k) {
@@ -286,6 +291,7 @@ struct ConvCfg {
   static constexpr int kVisits = kHalves ? 2 : 1;    // SegIter visits per segment
   static constexpr int kPxBytes = kSplit ? 4 * kCin : 2 * kCin;  // activation bytes per pixel
 };
+static_assert(ConvCfg<9>::kSmem <= 232448 && ConvCfg<10>::kSmem <= 232448, "wide single-input smem");
 constexpr float kSplitWScale = 256.0f;  // split hidden weights are packed x 2^8
 // 1 + E[truncation loss] of the main accumulator: 36 MMAs, each losing 0.5 ulp of
 // a partial sum that grows ~linearly to the result, E[ulp(x)/|x|] = 0.7213 * 2^-23
@@ -674,7 +680,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
     const uint32_t stage_out = smem_u32(sOut + ew * Cfg::kStageOut);
     const uint32_t shift_u = smem_u32(sShift);
-    if (!kHead && !Cfg::kSplit && lane == 0) prefetch_tmap(&tm_out);
+    if (!kHead && !Cfg::kSplit && !Cfg::kWide && lane == 0) prefetch_tmap(&tm_out);
     uint32_t seq = 0, gsel = 0;  // gsel = seq % kGroups
     Iter it(a, Cfg::kVisits, Cfg::kParts);
     Segment g;
@@ -702,7 +708,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           __syncwarp();
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
           if (xg < a.W) {
-            uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * Cfg::kPxBytes + qtr * 64;
+            // output pixel stride: pair 4*C bytes (hi C | lo C), single 2*C
+            const int opx = a.out_single ? 2 * Cfg::kCin : 4 * Cfg::kCin;
+            uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * opx + qtr * 64;
 #pragma unroll
             for (int chunk = 0; chunk < 4; ++chunk) {
               const uint32_t sh_u = shift_u + (uint32_t)(qtr * 32 + chunk * 8) * 4;
@@ -722,7 +730,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                 lo[t2] = *reinterpret_cast<const uint32_t*>(&ll);
               }
               *reinterpret_cast<uint4*>(dst + chunk * 16) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-              *reinterpret_cast<uint4*>(dst + 2 * Cfg::kCin + chunk * 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+              if (!a.out_single)
+                *reinterpret_cast<uint4*>(dst + 2 * Cfg::kCin + chunk * 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
             }
           }
         } else if constexpr (Cfg::kHalves) {
@@ -926,7 +935,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         }
       }
     }
-    if (!kHead && !Cfg::kSplit && lane == 0) bulk_wait<0>();
+    if (!kHead && !Cfg::kSplit && !Cfg::kWide && lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
@@ -1167,6 +1176,15 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
       cfg.blockDim = dim3(ConvCfg<7>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<7>::kSmem;
       return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<7>, tm_in, tm_out, a, p0, zs);
+    case 9:
+      cfg.gridDim = dim3(std::max(4, grid & ~3));  // groups of 4 CTAs (output-channel quarters)
+      cfg.blockDim = dim3(ConvCfg<9>::kThreads);
+      cfg.dynamicSmemBytes = ConvCfg<9>::kSmem;
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<9>, tm_in, tm_out, a, p0, zs);
+    case 10:
+      cfg.blockDim = dim3(ConvCfg<10>::kThreads);
+      cfg.dynamicSmemBytes = ConvCfg<10>::kSmem;
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<10>, tm_in, tm_out, a, p0, zs);
   }
   return cudaErrorInvalidValue;
 }
@@ -1274,6 +1292,12 @@ cudaError_t configure_kernels() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<8>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<9>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<10>::kSmem);
   if (e != cudaSuccess) return e;
   return configure_edge_kernels();
 }

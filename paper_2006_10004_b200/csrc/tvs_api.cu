@@ -120,6 +120,11 @@ struct tvs_plan {
   // 1 whenever legal, -1 (default) when the chunk has >= kStackMinItems work
   // items per SM (short columns / few images keep the per-layer kernels)
   int stack = -1;
+  // wide variant, fast mode: hidden layers reading fp16 hi/lo pairs (the rest
+  // read single fp16; TVS_WIDE_PAIR).  12 of 24 keeps the worst band at
+  // 6.6-8.0e-3 on config 5 (tools/emulate_wide.py), 0 is the plain-fp16
+  // roofline probe (1.1-1.3e-2, over the 1e-2 gate)
+  int wide_pair_layers = 12;
   static constexpr int kStackMinItems = 6;
   int* rowcnt = nullptr;  // row flags (B*strips*H ints), zeroed per chunk
   size_t rowcnt_n = 0;
@@ -314,7 +319,13 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     TVS_CUDA(cudaMemsetAsync(p->rowcnt, 0, n * sizeof(int), st));
   }
   // K1 (the FAST path can fuse it into the first hidden layer's producer)
-  const int fmt = fast ? tvs::kActF16 : ((split || wide) ? tvs::kActSplit : tvs::kActF32);
+  // wide fast stack: hidden layer j reads an fp16 hi/lo pair for j < P, single
+  // fp16 after (j == n_hidden is the head); P = n_hidden keeps every layer paired
+  const int nh = p->n_hidden();
+  const int P = std::max(0, std::min(p->wide_pair_layers, nh));
+  auto pair_in = [&](int j) { return j < P || P >= nh; };
+  const int fmt = fast ? tvs::kActF16
+                       : (split ? tvs::kActSplit : (wide ? (pair_in(0) ? tvs::kActSplit : tvs::kActF16) : tvs::kActF32));
   const int us = p->unshuffle;  // 2: the layer stack runs on the (H/2, W/2) grid
   if (us == 2)
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
@@ -328,8 +339,11 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     // wide variant: split activations (hi 128 | lo 128 halves per pixel), groups
     // of 4 CTAs per strip-row range (one 32-channel quarter each)
     const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
-    CUtensorMap in_map[2];
-    for (int i = 0; i < 2; ++i) in_map[i] = make_act_map(act[i], B, H, W, tvs::kHaloPx, 256);
+    CUtensorMap pair_map[2], single_map[2];
+    for (int i = 0; i < 2; ++i) {
+      pair_map[i] = make_act_map(act[i], B, H, W, tvs::kHaloPx, 256);
+      single_map[i] = make_act_map(act[i], B, H, W, tvs::kHaloPx, 128);
+    }
     auto geom = [&](int r0, int nrows) {
       tvs::ConvArgs a{};
       a.B = B; a.H = H; a.W = W; a.strips = strips;
@@ -342,10 +356,12 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.shift = p->bhid + (size_t)l * C;
       a.nshift = C;
       a.act_out = static_cast<uint8_t*>(act[cur ^ 1]);
+      a.out_single = pair_in(l + 1) ? 0 : 1;
+      const CUtensorMap& m = pair_in(l) ? pair_map[cur] : single_map[cur];
       // 4 CTAs per strip-row range: size the grid by groups
       const int grid = 4 * std::max(1, std::min(max_ctas / 4, conv_grid(max_ctas, a)));
       timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * C * C,
-                   [&] { return tvs::launch_conv_tc(5, in_map[cur], in_map[cur], a, nullptr, grid, st); });
+                   [&] { return tvs::launch_conv_tc(pair_in(l) ? 5 : 9, m, m, a, nullptr, grid, st); });
       cur ^= 1;
     }
     tvs::ConvArgs a = geom(row0, rows);
@@ -354,8 +370,9 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     a.nshift = p->out_bands;
     a.x = x; a.bands = bands; a.closure = closure; a.K = p->out_bands;
     const int grid = conv_grid(max_ctas, a);
+    const CUtensorMap& mh = pair_in(nh) ? pair_map[cur] : single_map[cur];
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * C * p->out_bands,
-                 [&] { return tvs::launch_conv_tc(6, in_map[cur], in_map[cur], a, nullptr, grid, st); });
+                 [&] { return tvs::launch_conv_tc(pair_in(nh) ? 6 : 10, mh, mh, a, nullptr, grid, st); });
   } else if (split) {
     // fp32-accurate: split-operand tcgen05 layers on fp16 hi|lo pair rows
     const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
@@ -596,6 +613,7 @@ int tvs_plan_create_ex(int device, int depth, int channels, int out_bands, int m
     if (const char* e = std::getenv("TVS_L2_HINTS")) p->l2_hints = std::atoi(e);
     if (const char* e = std::getenv("TVS_PAIR")) p->pair_fuse = std::atoi(e) != 0;
     if (const char* e = std::getenv("TVS_STACK")) p->stack = std::atoi(e);
+    if (const char* e = std::getenv("TVS_WIDE_PAIR")) p->wide_pair_layers = std::atoi(e);
     if (const char* e = std::getenv("TVS_STACK_SKEW")) p->stack_skew = std::atoi(e);
     if (const char* e = std::getenv("TVS_WIDE_CUDA")) p->wide_cuda = std::atoi(e) != 0;
     try {

@@ -332,3 +332,22 @@ def test_layer_stack_auto_config2(seeded_state, oracle):
     err = band_rel_l2(bands.cpu().numpy()[[0, 63]], ref)
     assert err.max() <= TOL["fast"], f"worst band rel-L2 {err.max():.3e}"
     np.testing.assert_allclose((bands.sum(1, keepdim=True) + clos).cpu().numpy(), x, atol=1e-5)
+
+
+@pytest.mark.parametrize("pairs,tol", [(24, 1e-2), (12, 1e-2), (6, 1.5e-2), (0, 2e-2)])
+def test_wide_pair_schedules(wide_case, monkeypatch, pairs, tol):
+    """Wide variant, fast mode: the first `pairs` hidden layers read fp16 hi/lo
+    pair activations (conv_tc.cu mode 5), the rest single fp16 (mode 9, head
+    mode 10).  24 (all) and 12 (the default) meet the 1e-2 gate; fewer pairs
+    trade accuracy for MMA work (tools/emulate_wide.py: 6 -> ~1.06e-2, 0 ->
+    1.1-1.3e-2, the plain-fp16 roofline probe)."""
+    state, x, y32, _ = wide_case
+    monkeypatch.setenv("TVS_WIDE_PAIR", str(pairs))
+    m = TVSpecNet(26, 128, 5).eval()
+    m.load_state_dict(state)
+    m._plan_for(torch.device("cuda", 0))
+    monkeypatch.delenv("TVS_WIDE_PAIR")
+    out, clos = _run(m, x)
+    err = band_rel_l2(out, y32).max()
+    assert err <= tol, f"pairs={pairs}: worst band rel-L2 {err:.3e}"
+    np.testing.assert_allclose(out.sum(1, keepdims=True) + clos, x[:, 0:1], atol=1e-5)
