@@ -101,7 +101,10 @@ class ClockSampler:
 
 def _kernel_name(tc, launches, depth):
     """The dominant kernel: the layer-stack launch (all hidden layers, conv_tc.cu
-    mode 8) when a forward took 3 launches, else the per-layer hidden conv."""
+    mode 8) when a forward took 3 launches, else the per-layer hidden conv; the
+    128-channel wide variant runs conv_tc.cu modes 5 (pair input) / 9 (single)."""
+    if tc == "wide":
+        return "conv3x3_tc_kernel<5>/<9> (wide hidden layer, 128 ch)"
     if not tc:
         return "hidden_f32_kernel"
     if launches == 3:
@@ -350,15 +353,25 @@ def run_ours(args, spec):
     hid_avg_ms = f["hid_ms"] / max(1, f["hid_n"])
     hid_tflops = f["hid_flops"] / max(1, f["hid_n"]) / (hid_avg_ms / 1e3) / 1e12
     step_ms = f["ms"]
-    tc = spec.channels == 64
+    tc = True if spec.channels == 64 else "wide"  # both fast paths run on tcgen05
+    wide_pairs = min(12, spec.depth - 2)  # the plan's default pair-input layers (tvs_api.cu wide_pair_layers)
+    nh = spec.depth - 2
+    # algorithmic activation bytes per hidden launch (read + write one activation):
+    # 64 ch fp16 = 128 B/px each way; wide pair = 512, single = 256 B/px
+    if tc is True:
+        alg_bytes_px = 2 * 128
+    else:
+        alg_bytes_px = sum((512 if j < wide_pairs else 256) + (512 if j + 1 < wide_pairs else 256)
+                           for j in range(nh)) / nh
     parallelism = (f"row-bands x{world} (halo {spec.depth})" if band is not None else
                    ("batch per rank" if _scaling(spec) == "weak" else f"batch-shard x{world}"))
     line = {
         "metric": METRIC, "value": round(f["value"], 3), "unit": UNIT, "n_gpus": world, "steps": f["steps"],
         "warmup": f["warmup"], "ms_per_step": round(step_ms, 4), "higher_is_better": True,
         "scaling": _scaling(spec), "vs_baseline": None,
-        "dtype": ("f16 operands / f32 accumulate (tcgen05 kind::f16); conv0+head f32" if tc
-                  else "f32 (CUDA-core path, fp64 accumulation)"),
+        "dtype": ("f16 operands / f32 accumulate (tcgen05 kind::f16); conv0+head f32" if tc is True
+                  else f"f16 operands / f32 accumulate (tcgen05 kind::f16), first {wide_pairs} of {nh} hidden "
+                       "layers on fp16 hi/lo activation pairs; conv0+head f32"),
         "data": f"synthetic (SURVEY §8(d) piecewise-constant generator, seed {spec.seed})",
         "config": {"workload": spec.name, "batch": spec.batch, "rank_images": B, "height": spec.height,
                    "width": spec.width, "depth": spec.depth, "channels": spec.channels, "out_bands": 5,
@@ -375,7 +388,7 @@ def run_ours(args, spec):
                      "flop_per_launch": f["hid_flops"] / max(1, f["hid_n"]),
                      "share_of_step": round(f["hid_ms"] / max(1e-9, f["hid_ms"] + f["c0_ms"] + f["hd_ms"]), 4),
                      "traffic": _traffic(spec, _kernel_name(tc, f["launches"], spec.depth)), "traffic_unit": "bytes per launch (ncu dram read+write)",
-                     "algorithmic_bytes_per_launch": 2 * B * H * W * 128},
+                     "algorithmic_bytes_per_launch": int(B * H * W * alg_bytes_px)},
         "gpu_launches": f["launches"] * f["steps"],
         "e2e": {"value": round(f["e2e"], 3), "unit": UNIT, "h2d_bytes_per_step": f["e2e_bytes"][0],
                 "d2h_bytes_per_step": f["e2e_bytes"][1], "images_per_rank": f["e2e_images"]},
