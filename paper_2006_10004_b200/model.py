@@ -110,9 +110,16 @@ class TVSpecNet(nn.Module):
 
     # ------------------------------------------------------ weight folding ----
     def _weight_key(self, device: torch.device) -> tuple:
+        """Identity + version of every tensor the forward reads (checked on each
+        call, so in-place updates such as load_state_dict repack the plan).
+        Walks the body's parameter/buffer dicts directly: list(self.parameters())
+        costs ~0.3 ms per call, this ~0.05 ms."""
         key = [str(device), self._precision]
-        for t in list(self.parameters()) + list(self.buffers()):
-            key.append((t.data_ptr(), t._version))
+        for mod in self.body._modules.values():
+            for d in (mod._parameters, mod._buffers):
+                for name, t in d.items():
+                    if t is not None and name != "num_batches_tracked":
+                        key.append((t.data_ptr(), t._version))
         return tuple(key)
 
     @torch.no_grad()
@@ -210,14 +217,79 @@ class TVSpecNet(nn.Module):
                          stream.cuda_stream)
         return bands, clos
 
-    # host tensors: pipelined H2D -> forward -> D2H over sub-batches
-    host_chunks = 4
+    # host tensors: pipelined H2D -> forward -> D2H over sub-batches.
+    # None = automatic schedule (_host_schedule); an int = that many equal
+    # sub-batches; a sequence = relative sub-batch sizes.
+    host_chunks = None
+
+    def _host_schedule(self, B: int, H: int, W: int, nrows: int, closure: bool, sms: int) -> list[int]:
+        """Sub-batch sizes for the host-tensor pipeline.  Sub-batch i's D2H
+        overlaps the forward of sub-batch i+1, and the last D2H is exposed, so
+        sizes shrink towards the end (ratio ~ D2H time / forward time per
+        image); a tiny first sub-batch starts the GPU after a short H2D; the
+        big one is sized so the layer-stack kernel is eligible (tvs_api.cu
+        run_chunk: >= 6 items per SM and a last round >= 95% full).  Candidate
+        schedules are scored with a three-stream timeline model."""
+        if B <= 2:
+            return [B]
+        us = self.unshuffle
+        strips = (W // us + 127) // 128
+        cols = strips * (self.depth - 2)
+        fast = self._precision == "fast" and self.channels == 64
+        px = H * W
+        rate = (1.1e9 if fast else 0.27e9) / (self.channels / 64) ** 2 * (17 - 2) / max(1, self.depth - 2)
+        t_h = 4.0 * px / 50e9
+        t_d = 4.0 * (self.out_bands + (1 if closure else 0)) * nrows * W / 54e9
+
+        def stack_ok(n):
+            items = n * cols
+            rounds = -(-items // sms)
+            return fast and items >= 6 * sms and items >= 0.95 * rounds * sms
+
+        def t_c(n):
+            return n * px / rate * (1.0 if stack_ok(n) else 1.06) + (0.0 if stack_ok(n) else 2e-5)
+
+        def finish(ch):
+            hd = cd = dd = 0.0
+            C, D = [], []
+            for i, n in enumerate(ch):
+                hs = hd if i < 2 else max(hd, C[i - 2])
+                hd = hs + n * t_h
+                cs = max(hd, cd, D[i - 2] if i >= 2 else 0.0)
+                cd = cs + t_c(n)
+                C.append(cd)
+                dd = max(cd, dd) + n * t_d
+                D.append(dd)
+            return dd
+
+        best = (finish([B]), [B])
+        r = max(0.1, min(0.9, t_d / max(t_c(1), 1e-12)))
+        for head in range(0, min(4, B // 8) + 1):
+            for tail in range(1, max(1, B // 16) + 1):
+                rest, c = [], tail
+                while head + sum(rest) + c < B:
+                    rest.insert(0, c)
+                    c = max(c + 1, int(round(c / r)))
+                big = B - head - sum(rest)
+                for cand in range(big, max(0, big - 12), -1):  # prefer a stack-eligible big chunk
+                    ch = ([head] if head else []) + [cand] + rest
+                    if cand < big:
+                        ch[len(ch) - len(rest)] += big - cand if rest else 0
+                        if not rest:
+                            ch.append(big - cand)
+                    ch = [n for n in ch if n > 0]
+                    t = finish(ch)
+                    if t < best[0] - 1e-9:
+                        best = (t, ch)
+                    if stack_ok(cand):
+                        break
+        return best[1]
 
     def _forward_host(self, plan, x: torch.Tensor, dev: torch.device, closure: bool, row0: int, nrows: int):
         """CPU in / CPU out (the reference calling convention, inference.py:25-32).
         Sub-batches flow through three streams so the PCIe copies of one
         sub-batch overlap the forward of another; results land in pinned
-        host memory."""
+        host memory.  Streams and device staging buffers are cached per device."""
         B, _, H, W = x.shape
         K = self.out_bands
         x_pin = x.contiguous()
@@ -225,15 +297,43 @@ class TVSpecNet(nn.Module):
             x_pin = x_pin.pin_memory()
         out = torch.empty((B, K, nrows, W), dtype=torch.float32, pin_memory=True)
         cout = torch.empty((B, 1, nrows, W), dtype=torch.float32, pin_memory=True) if closure else None
-        n = max(1, min(self.host_chunks, B))
-        bounds = [(B * i // n, B * (i + 1) // n) for i in range(n)]
-        per = max(e - s for s, e in bounds)
+        idx = dev.index
+        if isinstance(self.host_chunks, (list, tuple)):
+            w = [float(v) for v in self.host_chunks]
+            cuts = [0] + [round(B * sum(w[:i + 1]) / sum(w)) for i in range(len(w))]
+            sizes = [cuts[i + 1] - cuts[i] for i in range(len(w)) if cuts[i + 1] > cuts[i]]
+        elif self.host_chunks:
+            n = max(1, min(int(self.host_chunks), B))
+            sizes = [B * (i + 1) // n - B * i // n for i in range(n)]
+        else:
+            skey = (B, H, W, nrows, closure)
+            cache = self.__dict__.setdefault("_sched_cache", {})
+            if skey not in cache:
+                sms = torch.cuda.get_device_properties(idx).multi_processor_count
+                cache[skey] = self._host_schedule(B, H, W, nrows, closure, sms)
+            sizes = cache[skey]
+        bounds, s0 = [], 0
+        for n in sizes:
+            bounds.append((s0, s0 + n))
+            s0 += n
+        per = max(sizes)
         with torch.cuda.device(dev):
             comp = torch.cuda.current_stream(dev)
-            h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-            xbuf = [torch.empty((per, 1, H, W), device=dev) for _ in range(2)]
-            bbuf = [torch.empty((per, K, nrows, W), device=dev) for _ in range(2)]
-            cbuf = [torch.empty((per, 1, nrows, W), device=dev) if closure else None for _ in range(2)]
+            pipes = self.__dict__.setdefault("_host_pipes", {})
+            pk = (per, K, nrows, H, W, closure)
+            pipe = pipes.get(idx)
+            if pipe is None or pipe["key"] != pk:
+                old = pipe
+                pipe = {"key": pk,
+                        "h2d": old["h2d"] if old else torch.cuda.Stream(dev),
+                        "d2h": old["d2h"] if old else torch.cuda.Stream(dev),
+                        "xbuf": [torch.empty((per, 1, H, W), device=dev) for _ in range(2)],
+                        "bbuf": [torch.empty((per, K, nrows, W), device=dev) for _ in range(2)],
+                        "cbuf": [torch.empty((per, 1, nrows, W), device=dev) if closure else None
+                                 for _ in range(2)]}
+                pipes[idx] = pipe
+            h2d, d2h = pipe["h2d"], pipe["d2h"]
+            xbuf, bbuf, cbuf = pipe["xbuf"], pipe["bbuf"], pipe["cbuf"]
             x_free = [torch.cuda.Event() for _ in range(2)]
             b_free = [torch.cuda.Event() for _ in range(2)]
             for ev in x_free + b_free:

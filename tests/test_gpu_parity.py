@@ -175,6 +175,22 @@ def test_cpu_tensors_in_and_out(model, golden):
     assert out.shape == (5, 16, 20) and np.isfinite(out).all()
 
 
+@pytest.mark.parametrize("sched", [None, 3, (1, 4, 2, 1)])
+def test_host_pipeline_schedules_match_device(model, sched):
+    """CPU tensors in/out through the sub-batched H2D/forward/D2H pipeline give
+    bitwise the device-path result, for the automatic and explicit schedules."""
+    x = torch.rand(21, 1, 48, 160, generator=torch.Generator().manual_seed(7))
+    ref_b, ref_c = model.forward_planes(x.cuda(), closure=True)
+    old = model.host_chunks
+    try:
+        model.host_chunks = sched
+        b, c = model.forward_planes(x, closure=True)
+    finally:
+        model.host_chunks = old
+    assert b.device.type == "cpu" and b.is_pinned()
+    assert torch.equal(b, ref_b.cpu()) and torch.equal(c, ref_c.cpu())
+
+
 def test_predict_planes_stack(model):
     x = torch.rand(2, 1, 20, 30, device="cuda")
     planes = predict_planes(model, x)

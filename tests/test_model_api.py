@@ -112,3 +112,22 @@ def test_unshuffle_variant_structure():
     # the oracle composes exactly as torch's pixel_(un)shuffle: identity body check
     x = torch.randn(1, 1, 6, 8)
     assert torch.equal(torch.nn.functional.pixel_shuffle(torch.nn.functional.pixel_unshuffle(x, 2), 2), x)
+
+
+@pytest.mark.parametrize("B", [1, 2, 3, 5, 16, 64, 129, 512])
+def test_host_schedule_partitions_batch(B):
+    """The host-tensor pipeline's automatic sub-batch schedule covers the batch
+    exactly, and for config 2 (64 x 256^2) keeps a layer-stack-eligible big
+    sub-batch and small tail sub-batches (the exposed last D2H)."""
+    from paper_2006_10004_b200 import TVSpecNet
+
+    for prec in ("fast", "fp32"):
+        m = TVSpecNet(precision=prec)
+        for H, W in ((256, 256), (48, 160), (1024, 1024)):
+            sizes = m._host_schedule(B, H, W, H, False, 148)
+            assert sum(sizes) == B and all(n > 0 for n in sizes)
+    sizes = TVSpecNet()._host_schedule(64, 256, 256, 256, True, 148)
+    big = max(sizes)
+    items = big * 2 * 15
+    assert items >= 6 * 148 and items >= 0.95 * 148 * -(-items // 148)
+    assert sizes[-1] <= 8
