@@ -17,11 +17,14 @@ from paper_2006_10004_b200 import TVSpecNet, _native  # noqa: E402
 from paper_2006_10004_b200.workloads import CONFIGS, make_batch  # noqa: E402
 
 
+PREC = "fast"
+
+
 def model(env, wide=False):
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     arch = dict(depth=26, channels=128) if wide else {}
-    m = TVSpecNet(**arch).eval()
+    m = TVSpecNet(**arch, precision=PREC).eval()
     m.load_state_dict(build_seeded_state(**arch) if wide else build_seeded_state())
     m = m.cuda()
     m._plan_for(torch.device("cuda", 0))
@@ -39,6 +42,7 @@ opt = {sys.argv[i]: sys.argv[i + 1] for i in range(1, len(sys.argv) - 1) if sys.
 nimg = int(opt.get("--imgs", 64))
 reps = int(opt.get("--reps", 20))
 cfg = int(opt.get("--config", 2))
+PREC = opt.get("--precision", "fast")
 lib = _native.load()
 lib.tvs_debug_stack.restype = ctypes.c_int
 lib.tvs_debug_stack.argtypes = [ctypes.c_int]
