@@ -18,11 +18,12 @@ ap.add_argument("--config", default="2")
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--precision", default="fast")
 ap.add_argument("--batch", type=int, default=None)
+ap.add_argument("--unshuffle", type=int, default=1)
 a = ap.parse_args()
 spec = CONFIGS[a.config if a.config == "5w" else int(a.config)]
 B = a.batch or spec.batch
-m = TVSpecNet(spec.depth, spec.channels, 5, precision=a.precision).eval()
-m.load_state_dict(build_seeded_state(spec.depth, spec.channels, 5))
+m = TVSpecNet(spec.depth, spec.channels, 5, precision=a.precision, unshuffle=a.unshuffle).eval()
+m.load_state_dict(build_seeded_state(spec.depth, spec.channels, 5, unshuffle=a.unshuffle))
 x = torch.rand(B, 1, spec.height, spec.width, device="cuda")
 for _ in range(a.iters):
     y = m(x)
