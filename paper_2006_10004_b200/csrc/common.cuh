@@ -120,6 +120,12 @@ cudaError_t launch_head_f32(int C, const float* act, const float* x, const float
 cudaError_t launch_hidden_f32(int C, const float* in, float* out, const float* w, const float* scale,
                               const float* shift, int B, int H, int W, cudaStream_t st);
 cudaError_t configure_kernels();  // one-time smem opt-ins
+// conv0_tc.cu: K1 on tcgen05 (fast path, fp16 NHWC output), TF32 hi/lo split;
+// in_ch = 1 (reference conv0) or 4 (unshuffle = 2 variant, H/W = half-res grid)
+size_t conv0_tc_pack_bytes(int in_ch);
+cudaError_t launch_pack_conv0_tc(const float* w, int in_ch, uint8_t* out, cudaStream_t st);
+cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t* bpack, const float* bias, int B,
+                            int H, int W, int num_sms, cudaStream_t st);
 // metrics.cu: per-plane scoring statistics (8 doubles per plane)
 cudaError_t launch_band_stats(const float* gt, const float* pred, int planes, int H, int W,
                               const double* range_override, double* stats, cudaStream_t st);

@@ -1,0 +1,308 @@
+// conv0_tc.cu — K1 (the first conv, Conv2d(1|4, 64, 3, p=1, bias) + ReLU,
+// /root/reference/pkg/trainer/src/tvsurrogate/model.py:37-38) on tcgen05 for
+// the fast path, which stores fp16 NHWC activations.
+//
+// The CUDA-core K1 spends ~750 issue slots per pixel on 576 FFMAs and the
+// ReLU/convert/store around them (issue-bound at 89%, 170 us on config 2).
+// Here each 128-pixel strip row is one M=128, N=64 GEMM with the 3x3 taps as
+// K, kept fp32-accurate by splitting both operands into TF32 hi + lo parts:
+//
+//   A[px] = [x_hi(t) | x_lo(t) | x_hi(t) | 0]    B[co] = [W_hi | W_hi | W_lo | 0]
+//
+// so one K chain sums x_hi*W_hi + x_lo*W_hi + x_hi*W_lo (x_lo*W_lo ~ 2^-22 is
+// dropped).  hi = RNA_tf32(v), lo = RNA_tf32(v - hi): 22 significant bits of
+// each operand, fp32 range (an fp16 split would overflow past 65504).  The
+// tf32 products are exact in the fp32 accumulator, so the pre-activation
+// matches the fp32 FFMA sum to a few fp32 ulps before the fp16 rounding.
+//
+// kKB = 1: full-resolution conv0, 9 taps -> K = 27 of one 32-element SW128
+//          block (128 B per pixel row).
+// kKB = 4: the unshuffle = 2 variant's Conv2d(4, 64): input channel c = 2i + j
+//          of half-res pixel (Y, X) is x[2Y+i][2X+j] (torch pixel_unshuffle
+//          order), 36 taps -> K = 108 of four blocks.
+//
+// A CTA (4 warps, one pixel per thread) takes kTiles strip rows per round:
+// builds their A rows, one thread issues the MMA chains into kTiles TMEM
+// accumulators, and the next round's taps are loaded while they run.  The
+// epilogue adds the bias, applies ReLU with the fp16 rounding
+// (cvt.rn.relu.f16x2.f32), stages the rows in the freed A tile and copies each
+// strip row's 16 KB out coalesced.  Several CTAs share an SM (4 for K = 9,
+// register bound; 2 for K = 36, smem bound), so one CTA's tile build overlaps
+// another's MMAs and stores.  Config 2: 149 us (CUDA-core K1: 170 us; the
+// 537 MB write alone is 84 us at the copy bandwidth).
+#include <algorithm>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace tvs {
+
+template <int kKB>
+struct Conv0TcCfg {
+  static constexpr int kTaps = kKB == 1 ? 9 : 36;
+  static constexpr int kTiles = kKB == 1 ? 2 : 1;     // strip rows per CTA iteration (one accumulator each)
+  static constexpr int kPerSm = kKB == 1 ? 4 : 2;     // resident CTAs per SM (TMEM / smem bound)
+  static constexpr int kTileA = kKB * 128 * 128;      // 128 pixel rows x 128 B per K block
+  static constexpr int kABytes = kTiles * kTileA;
+  static constexpr int kBBytes = kKB * 64 * 128;      // 64 output-channel rows x 128 B per K block
+  static constexpr size_t kSmem = 1024 + kABytes + kBBytes;
+  static constexpr int kTmemCols = kTiles * 64 <= 64 ? 64 : (kTiles * 64 <= 128 ? 128 : 256);
+};
+
+__device__ __forceinline__ float tf32_rna(float v) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return __uint_as_float(r);
+}
+
+// element kk (0 .. 32*kKB-1) of SW128 K-major row `row` inside a tile of
+// 8-row / 1024-byte swizzle atoms, one 128-row (or 64-row) tile per K block
+__device__ __forceinline__ uint32_t sw128_off(int row, int kk, int rows_per_block) {
+  const int kb = kk >> 5, c = (kk & 31) >> 2;
+  return (uint32_t)(kb * rows_per_block * 128 + row * 128 + ((c ^ (row & 7)) << 4) + (kk & 3) * 4);
+}
+
+// taps of pixel px (strip row `tile`); zero outside the image
+template <int kKB>
+__device__ __forceinline__ void conv0_taps(const float* __restrict__ x, long long tile, long long tiles, int strips,
+                                           int H, int W, int t, float (&tap)[Conv0TcCfg<kKB>::kTaps]) {
+  if (tile >= tiles) tile = tiles - 1;  // past the end: any valid row (result unused)
+  const int px = (int)(tile % strips) * 128 + t;
+  const long long by = tile / strips;
+  const int y = (int)(by % H);
+  const long long b = by / H;
+  if constexpr (kKB == 1) {
+    const float* img = x + b * (long long)H * W;
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        const int yy = y + ky - 1, xx = px + kx - 1;
+        tap[ky * 3 + kx] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(img + (long long)yy * W + xx) : 0.0f;
+      }
+  } else {  // half-res grid (H, W); full-res plane (2H, 2W)
+    const float* img = x + b * (long long)(2 * H) * (2 * W);
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        const int yy = y + ky - 1, xx = px + kx - 1;
+        const bool ok = yy >= 0 && yy < H && xx >= 0 && xx < W;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const float2 v = ok ? __ldg(reinterpret_cast<const float2*>(img + (long long)(2 * yy + i) * (2 * W) + 2 * xx))
+                              : make_float2(0.0f, 0.0f);
+          tap[(2 * i) * 9 + ky * 3 + kx] = v.x;      // channel c = 2i + 0
+          tap[(2 * i + 1) * 9 + ky * 3 + kx] = v.y;  // channel c = 2i + 1
+        }
+      }
+  }
+}
+
+template <int kKB>
+__global__ void __launch_bounds__(128) conv0_tc_kernel(const float* __restrict__ x, __half* __restrict__ act,
+                                                       const uint8_t* __restrict__ bpack,
+                                                       const float* __restrict__ bias, int B, int H, int W) {
+  using Cfg = Conv0TcCfg<kKB>;
+  constexpr int n = Cfg::kTaps;
+  constexpr int NT = Cfg::kTiles;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ uint64_t mma_done;
+  __shared__ uint32_t tmem_base;
+  __shared__ float sBias[64];
+  uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sA + Cfg::kABytes;
+  const int t = threadIdx.x, warp = t >> 5;
+
+  // PDL: the first hidden layer may start its prologue (it waits for this grid)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (warp == 0) tmem_alloc<Cfg::kTmemCols>(&tmem_base);
+  {  // weights: packed SW128 tf32 rows, a plain copy into shared memory
+    const uint4* src = reinterpret_cast<const uint4*>(bpack);
+    uint4* dst = reinterpret_cast<uint4*>(sB);
+    for (int i = t; i < Cfg::kBBytes / 16; i += 128) dst[i] = __ldg(src + i);
+  }
+  if (t < 64) sBias[t] = bias[t];
+  if (t == 0) {
+    mbar_init(&mma_done, 1);
+    fence_barrier_init();
+  }
+  fence_async_smem();  // generic smem writes (B) -> the tensor core's async proxy
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t idesc = make_idesc(128, 64, kFmtTF32, kFmtTF32);
+  const uint64_t adesc0 = make_smem_desc(smem_u32(sA), 0, 1024, kLayoutSW128);
+  const uint64_t bdesc0 = make_smem_desc(smem_u32(sB), 0, 1024, kLayoutSW128);
+  const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
+  const int strips = (W + 127) / 128;
+  const long long tiles = (long long)B * H * strips;
+  const long long step = (long long)gridDim.x * NT;
+  uint32_t phase = 0;
+  // tiles blockIdx.x*NT + i of each round; the next round's taps are loaded
+  // while this round's MMAs and epilogue run
+  float tap[NT][n];
+  long long base = (long long)blockIdx.x * NT;
+#pragma unroll
+  for (int i = 0; i < NT; ++i) conv0_taps<kKB>(x, base + i, tiles, strips, H, W, t, tap[i]);
+  for (; base < tiles; base += step) {
+    // ---- A rows of this thread's pixel in each tile: taps split hi / lo
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+      const uint32_t arow = smem_u32(sA + i * Cfg::kTileA);
+#pragma unroll
+      for (int c4 = 0; c4 < 8 * kKB; ++c4) {  // 16-byte chunks of the row
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int kk = c4 * 4 + e;
+          float r = 0.0f;
+          if (kk < n) {
+            r = tf32_rna(tap[i][kk]);
+          } else if (kk < 2 * n) {
+            const float h = tf32_rna(tap[i][kk - n]);
+            r = tf32_rna(tap[i][kk - n] - h);
+          } else if (kk < 3 * n) {
+            r = tf32_rna(tap[i][kk - 2 * n]);
+          }
+          v[e] = r;
+        }
+        st_shared_v4(arow + sw128_off(t, c4 * 4, 128), __float_as_uint(v[0]), __float_as_uint(v[1]),
+                     __float_as_uint(v[2]), __float_as_uint(v[3]));
+      }
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();  // A complete; every warp's TMEM reads of the previous round are done
+    tc_fence_after();
+    if (t == 0) {
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int k = 0; k < 4 * kKB; ++k) {  // K8 steps: 32 B along the row, blocks of 16 / 8 KB
+          const uint32_t ka = (uint32_t)(i * Cfg::kTileA + (k >> 2) * 128 * 128 + (k & 3) * 32) >> 4;
+          const uint32_t kb = (uint32_t)((k >> 2) * 64 * 128 + (k & 3) * 32) >> 4;
+          mma_tf32_ss(tmem + i * 64, adesc0 + ka, bdesc0 + kb, idesc, k > 0 ? 1u : 0u);
+        }
+      mma_commit(&mma_done);
+    }
+    // next round's taps (global loads in flight during the MMAs and the epilogue)
+#pragma unroll
+    for (int i = 0; i < NT; ++i) conv0_taps<kKB>(x, base + step + i, tiles, strips, H, W, t, tap[i]);
+    mbar_wait(&mma_done, phase);
+    phase ^= 1;
+    tc_fence_after();
+    // ---- epilogue: lane quarter `warp` = pixels 32*warp .. +31 of each tile,
+    // staged through the (now free) A tile in an XOR-swizzled layout, then
+    // copied out coalesced: the strip row's 128 pixels are 16 KB contiguous
+    // in NHWC (per-lane 128 B stores would cost 32 LSU wavefronts each)
+#pragma unroll 1
+    for (int i = 0; i < NT; ++i) {
+      uint32_t acc[4][16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tmem_ld16(tmem + lane_addr + i * 64 + j * 16, acc[j]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) reg_fence16(acc[j]);
+      const uint32_t srow = smem_u32(sA + i * Cfg::kTileA) + t * 128;
+#pragma unroll
+      for (int c8 = 0; c8 < 8; ++c8) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = c8 * 8 + e * 2;
+          const float f0 = __uint_as_float(acc[c >> 4][c & 15]) + sBias[c];
+          const float f1 = __uint_as_float(acc[c >> 4][(c & 15) + 1]) + sBias[c + 1];
+          asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[e]) : "f"(f1), "f"(f0));
+        }
+        st_shared_v4(srow + ((c8 ^ (t & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+#pragma unroll 1
+    for (int i = 0; i < NT; ++i) {
+      const long long tile = base + i;
+      if (tile >= tiles) break;
+      const int x0 = (int)(tile % strips) * 128;
+      const long long by = tile / strips;
+      const int nvalid = min(128, W - x0);
+      uint4* dst = reinterpret_cast<uint4*>(act + (by * W + x0) * 64);
+      // thread t moves chunk c = t % 8 of rows r0 + 16k (r0 = t / 8): the
+      // swizzle term r & 7 == r0 & 7 is fixed per thread
+      const int c = t & 7, r0 = t >> 3;
+      const uint32_t stg = smem_u32(sA + i * Cfg::kTileA) + (uint32_t)(r0 * 128 + ((c ^ (r0 & 7)) << 4));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int r = r0 + 16 * k;
+        if (r < nvalid) {
+          uint4 v;
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(stg + k * 16 * 128));
+          dst[r * 8 + c] = v;
+        }
+      }
+    }
+    __syncthreads();  // staging read before the next round's A rows overwrite it
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::kTmemCols>(tmem);
+  }
+}
+
+// B pack: 64 rows (output channels) x 32*kKB tf32 [W_hi | W_hi | W_lo | 0],
+// SW128 K-major, from fp32 weights w[co][tap] (n taps per channel).
+__global__ void pack_conv0_tc_kernel(const float* __restrict__ w, int n, int kb_count, uint8_t* __restrict__ out) {
+  const int co = blockIdx.x, kk = threadIdx.x;
+  if (kk >= 32 * kb_count) return;
+  float r = 0.0f;
+  if (kk < n) {
+    r = tf32_rna(w[co * n + kk]);
+  } else if (kk < 2 * n) {
+    r = tf32_rna(w[co * n + kk - n]);
+  } else if (kk < 3 * n) {
+    const float v = w[co * n + kk - 2 * n];
+    r = tf32_rna(v - tf32_rna(v));
+  }
+  *reinterpret_cast<float*>(out + sw128_off(co, kk, 64)) = r;
+}
+
+size_t conv0_tc_pack_bytes(int in_ch) { return in_ch == 1 ? Conv0TcCfg<1>::kBBytes : Conv0TcCfg<4>::kBBytes; }
+
+cudaError_t launch_pack_conv0_tc(const float* w, int in_ch, uint8_t* out, cudaStream_t st) {
+  const int kb = in_ch == 1 ? 1 : 4;
+  pack_conv0_tc_kernel<<<64, 32 * kb, 0, st>>>(w, 9 * in_ch, kb, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t* bpack, const float* bias, int B,
+                            int H, int W, int num_sms, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(conv0_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Conv0TcCfg<1>::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv0_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)Conv0TcCfg<4>::kSmem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const long long tiles = (long long)B * H * ((W + 127) / 128);
+  const int nt = in_ch == 1 ? Conv0TcCfg<1>::kTiles : Conv0TcCfg<4>::kTiles;
+  const int per_sm = in_ch == 1 ? Conv0TcCfg<1>::kPerSm : Conv0TcCfg<4>::kPerSm;
+  const int grid = (int)std::max(1LL, std::min<long long>((tiles + nt - 1) / nt, (long long)num_sms * per_sm));
+  // plain launch (no PDL attribute): K1 is a forward's first kernel and has
+  // no griddepcontrol.wait, so it must not overlap the previous forward's head
+  if (in_ch == 1) {
+    conv0_tc_kernel<1><<<grid, 128, Conv0TcCfg<1>::kSmem, st>>>(x, static_cast<__half*>(act), bpack, bias, B, H, W);
+  } else {
+    conv0_tc_kernel<4><<<grid, 128, Conv0TcCfg<4>::kSmem, st>>>(x, static_cast<__half*>(act), bpack, bias, B, H, W);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace tvs

@@ -114,6 +114,12 @@ struct tvs_plan {
   // producer's ~600 FFMA/px-row currently cost more than they save)
   bool unfused_conv0 = true;  // activation bytes per chunk (TVS_CHUNK_MB)
   int l2_hints = 0;           // TVS_L2_HINTS (ConvArgs::l2_hints)
+  // K1 on tcgen05 (conv0_tc.cu, TF32 hi/lo split) for the fast path: config 2
+  // 149 vs 170 us (reference conv0, K = 9) and 96 vs 212 us (the unshuffle = 2
+  // variant's Conv2d(4, 64), K = 36).  TVS_CONV0_TC=0 selects the CUDA-core K1.
+  int conv0_tc = 1;
+  uint8_t* c0pack = nullptr;  // packed TF32 hi/lo B operand
+  float* c0bias = nullptr;
   bool pair_fuse = false;     // TVS_PAIR: fuse consecutive hidden layers (conv_pair.cu)
   // layer-stack kernel (conv_tc.cu mode 8, all hidden layers in one persistent
   // launch, activations handed between layers through L2): TVS_STACK = 0 off,
@@ -172,7 +178,7 @@ void free_all(tvs_plan* p) {
   p->recs.clear();
   p->event_pool.clear();
   void* ptrs[] = {p->wh, p->bh, p->wpack, p->hpack, p->whid, p->bhid, p->shid, p->act[0], p->act[1], p->dx,
-                  p->w0u, p->b0u, p->rowcnt, p->items};
+                  p->w0u, p->b0u, p->rowcnt, p->items, p->c0pack, p->c0bias};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -327,9 +333,17 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
   const int fmt = fast ? tvs::kActF16
                        : (split ? tvs::kActSplit : (wide ? (pair_in(0) ? tvs::kActSplit : tvs::kActF16) : tvs::kActF32));
   const int us = p->unshuffle;  // 2: the layer stack runs on the (H/2, W/2) grid
-  if (us == 2)
+  if (us == 2 && p->conv0_tc)
+    timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C, [&] {
+      return tvs::launch_conv0_tc(4, x, act[0], p->c0pack, p->c0bias, B, H / 2, W / 2, p->num_sms, st);
+    });
+  else if (us == 2)
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
                  [&] { return tvs::launch_conv0_unshuffle(x, act[0], p->w0u, p->b0u, B, H / 2, W / 2, st); });
+  else if (fast && p->unfused_conv0 && p->conv0_tc)
+    timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C, [&] {
+      return tvs::launch_conv0_tc(1, x, act[0], p->c0pack, p->c0bias, B, H, W, p->num_sms, st);
+    });
   else if (!fast || p->unfused_conv0)
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
                  [&] { return tvs::launch_conv0(fmt, C, x, act[0], p->conv0, B, H, W, st); });
@@ -611,6 +625,7 @@ int tvs_plan_create_ex(int device, int depth, int channels, int out_bands, int m
     if (const char* e = std::getenv("TVS_FUSE_CONV0")) p->unfused_conv0 = std::atoi(e) == 0;
     if (const char* e = std::getenv("TVS_FP32_CUDA")) p->fp32_split = std::atoi(e) == 0;
     if (const char* e = std::getenv("TVS_L2_HINTS")) p->l2_hints = std::atoi(e);
+    if (const char* e = std::getenv("TVS_CONV0_TC")) p->conv0_tc = std::atoi(e);
     if (const char* e = std::getenv("TVS_PAIR")) p->pair_fuse = std::atoi(e) != 0;
     if (const char* e = std::getenv("TVS_STACK")) p->stack = std::atoi(e);
     if (const char* e = std::getenv("TVS_WIDE_PAIR")) p->wide_pair_layers = std::atoi(e);
@@ -670,6 +685,13 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
       TVS_CUDA(cudaStreamSynchronize(st));  // conv0 weights are kernel parameters (host side)
       TVS_CUDA(cudaMemcpyAsync(p->wh, w_dev[p->depth - 1], (size_t)p->out_bands * C * 9 * 4,
                                cudaMemcpyDeviceToDevice, st));
+    }
+    if (p->tc_path()) {  // K1 on tcgen05: TF32 hi/lo B pack + bias
+      const int in_ch = p->unshuffle == 2 ? 4 : 1;
+      if (!p->c0pack) TVS_CUDA(cudaMalloc(&p->c0pack, tvs::conv0_tc_pack_bytes(in_ch)));
+      if (!p->c0bias) TVS_CUDA(cudaMalloc(&p->c0bias, 64 * sizeof(float)));
+      TVS_CUDA(tvs::launch_pack_conv0_tc(w_dev[0], in_ch, p->c0pack, st));
+      TVS_CUDA(cudaMemcpyAsync(p->c0bias, shift_dev[0], 64 * sizeof(float), cudaMemcpyDeviceToDevice, st));
     }
     TVS_CUDA(cudaMemcpyAsync(p->bh, shift_dev[p->depth - 1], (size_t)p->out_bands * p->unshuffle * p->unshuffle * 4,
                              cudaMemcpyDeviceToDevice, st));

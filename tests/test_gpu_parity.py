@@ -5,6 +5,8 @@ Tolerances (BASELINE.json north_star), relative L2 per image per band:
   * precision="fast": <= 1e-2, closure (band-sum reconstruction) <= 1e-2
 All calls go through the C ABI (libtvsb200.so) via the drop-in module.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -259,12 +261,43 @@ def test_fused_conv0_path(seeded_state, oracle, monkeypatch):
         ref = oracle(torch.from_numpy(x)).numpy()
     _check(m, x, ref)
     assert m.last_launch_count() == m.depth - 1
-    # bitwise equal to the unfused path (same fp32 conv0 arithmetic, fp16 rounding)
+    # bitwise equal to the unfused CUDA-core K1 (same fp32 FFMA arithmetic, fp16
+    # rounding); the tcgen05 K1 (TF32 hi/lo split) agrees to fp16 rounding
     monkeypatch.setenv("TVS_FUSE_CONV0", "0")
+    monkeypatch.setenv("TVS_CONV0_TC", "0")
     m2 = TVSpecNet().eval()
     m2.load_state_dict(seeded_state)
     xd = torch.from_numpy(x).cuda()
     assert torch.equal(m(xd), m2(xd))
+    monkeypatch.setenv("TVS_CONV0_TC", "1")
+    m3 = TVSpecNet().eval()
+    m3.load_state_dict(seeded_state)
+    _check(m3, x, ref)
+    a, b = m3(xd), m2(xd)  # fp16 rounding flips, amplified over 16 fp16 layers
+    assert (torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(b)).item() < 5e-3
+
+
+def test_conv0_tcgen05_matches_fp32_conv0(seeded_state):
+    """The tcgen05 K1 (TF32 hi/lo split, conv0_tc.cu) against the CUDA-core fp32
+    FFMA K1: both round the same fp32 pre-activation to fp16, so the first-layer
+    activations may differ by one fp16 ulp where the sums differ in the last
+    fp32 bits.  Signed inputs of larger magnitude exercise the hi/lo split."""
+    outs = []
+    for env in ("1", "0"):
+        os.environ["TVS_CONV0_TC"] = env
+        try:
+            m = TVSpecNet(depth=3).eval()  # conv0 -> 1 hidden -> head: conv0 dominates
+            m.load_state_dict(build_seeded_state(3, 64, 5))
+            m._plan_for(torch.device("cuda", 0))
+        finally:
+            os.environ.pop("TVS_CONV0_TC")
+        outs.append(m)
+    g = torch.Generator().manual_seed(3)
+    for x in (torch.rand(2, 1, 40, 300, generator=g), torch.randn(2, 1, 40, 300, generator=g) * 30):
+        x = x.cuda()
+        a, b = outs[0](x), outs[1](x)
+        rel = (torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(b)).item()
+        assert torch.isfinite(a).all() and rel < 1e-3, rel
 
 
 def test_abi_errors_on_gpu(model):
