@@ -99,15 +99,16 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def _kernel_name(tc, launches, depth):
+def _kernel_name(tc, launches, depth, hidden_per_fwd=None):
     """The dominant kernel: the layer-stack launch (all hidden layers, conv_tc.cu
-    mode 8) when a forward took 3 launches, else the per-layer hidden conv; the
-    128-channel wide variant runs conv_tc.cu modes 5 (pair input) / 9 (single)."""
+    mode 8) when each batch chunk took 3 launches (conv0, stack, head), else the
+    per-layer hidden conv; the 128-channel wide variant runs conv_tc.cu modes 5
+    (pair input) / 9 (single)."""
     if tc == "wide":
         return "conv3x3_tc_kernel<5>/<9> (wide hidden layer, 128 ch)"
     if not tc:
         return "hidden_f32_kernel"
-    if launches == 3:
+    if launches == 3 or (hidden_per_fwd is not None and abs(hidden_per_fwd * 3 - launches) < 1e-6):
         return f"conv3x3_tc_kernel<8> (layer stack: {depth - 2} hidden layers per launch)"
     return "conv3x3_tc_kernel<0> (hidden layer)"
 
@@ -305,7 +306,8 @@ def run_ours(args, spec):
 
         # live per-kernel timing of the dominant kernel (hidden conv), separate pass
         plan.profile_enable(True)
-        for _ in range(max(1, min(steps, 3))):
+        prof_steps = max(1, min(steps, 3))
+        for _ in range(prof_steps):
             _flush_l2(flush)
             step()
         torch.cuda.synchronize()
@@ -337,7 +339,7 @@ def run_ours(args, spec):
         e2e_px = ne * nrows * W * (world if _scaling(spec) == "weak" or band is not None else world)
         results[prec] = dict(value=value, ms=tot_ms / steps, ms_list=ms, launches=launches, steps=steps,
                              warmup=warm, clocks=clk.summary(), hid_ms=hid_ms, hid_n=hid_n, hid_flops=hid_flops,
-                             c0_ms=c0_ms, hd_ms=hd_ms, e2e=e2e_px / 1e6 / e2e_s,
+                             c0_ms=c0_ms, hd_ms=hd_ms, e2e=e2e_px / 1e6 / e2e_s, hid_per_fwd=hid_n / prof_steps,
                              e2e_bytes=(xe.numel() * 4, out_host.numel() * 4), e2e_images=ne)
         del model, plan, bands, clos
 
@@ -380,14 +382,14 @@ def run_ours(args, spec):
         "latency_ms": round(step_ms, 4) if spec.batch == 1 else None,
         "tflops_algorithmic": round(f["value"] * 1e6 * fpx / 1e12 / world, 2),
         "frac_of_bf16_peak": round(f["value"] * 1e6 * fpx / 1e12 / world / peak_tf, 4),
-        "roofline": {"bound": "tensor", "kernel": _kernel_name(tc, f["launches"], spec.depth),
+        "roofline": {"bound": "tensor", "kernel": _kernel_name(tc, f["launches"], spec.depth, f["hid_per_fwd"]),
                      "achieved": round(hid_tflops, 2), "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": round(hid_tflops / peak_tf, 4), "peak_kind": f"{peak_kind} bf16 burst",
                      "frac_of_sustained": round(hid_tflops / peak_sus, 4) if peak_sus else None,
                      "avg_launch_ms": round(hid_avg_ms, 5), "launches_timed": f["hid_n"],
                      "flop_per_launch": f["hid_flops"] / max(1, f["hid_n"]),
                      "share_of_step": round(f["hid_ms"] / max(1e-9, f["hid_ms"] + f["c0_ms"] + f["hd_ms"]), 4),
-                     "traffic": _traffic(spec, _kernel_name(tc, f["launches"], spec.depth)), "traffic_unit": "bytes per launch (ncu dram read+write)",
+                     "traffic": _traffic(spec, _kernel_name(tc, f["launches"], spec.depth, f["hid_per_fwd"])), "traffic_unit": "bytes per launch (ncu dram read+write)",
                      "algorithmic_bytes_per_launch": int(B * H * W * alg_bytes_px)},
         "gpu_launches": f["launches"] * f["steps"],
         "e2e": {"value": round(f["e2e"], 3), "unit": UNIT, "h2d_bytes_per_step": f["e2e_bytes"][0],
