@@ -6,7 +6,7 @@
 //     N block = 64 output channels, epilogue +shift, ReLU, fp16 -> TMA store.
 //  K3 head          (Conv2d(64,K,3,p=1,bias), model.py:44, + closure plane
 //     image - sum(bands), inference.py:34-42)
-//     N block = 32 = [16 cols W_hi | 16 cols W_lo] with W = W_hi + W_lo both
+//     N block = 16 per dy = [8 cols W_hi | 8 cols W_lo] with W = W_hi + W_lo both
 //     fp16 (exact split of the fp32 weight to ~2^-22), so the head stays
 //     fp32-accurate on fp16 activations; epilogue sums hi+lo+bias and writes
 //     fp32 NCHW bands (+ closure) for a row window.
@@ -240,7 +240,9 @@ struct ConvCfg {
   static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kGroups);
   // split hidden layer: two passes of 32 output channels (TMEM room for three rings)
   static constexpr bool kHalves = kMode == 3;
-  static constexpr int NB = kUnshuf ? 64 : ((kHead || kHalves || kQuarters) ? 32 : 64);  // TMEM cols per row
+  // TMEM cols per row; the 64-channel heads (modes 1 / 4) use 8 hi + 8 lo
+  // weight columns per dy (K <= kMaxBands = 8): N = 48 per MMA instead of 96
+  static constexpr int NB = kUnshuf ? 64 : ((kMode == 1 || kMode == 4) ? 16 : ((kHead || kHalves || kQuarters) ? 32 : 64));
   static constexpr int kWdxBlk = 3 * NB * 128;        // B bytes per dx and K block (3 dy x NB rows x 128 B)
   static constexpr int kWdx = kKBlk * kWdxBlk;        // B bytes per dx
   static constexpr int kWhalf = 3 * kWdx;             // one channel half (all dx)
@@ -893,26 +895,41 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             }
           }
         } else {
+          // v[0][k] = [x * W_hi]_k, v[1][k] = [x * W_lo]_k (w: the correction ring)
           uint32_t v[2][16], w[2][16];
-          tmem_ld16(tmem + lane_addr + slot * NB, v[0]);
-          tmem_ld16(tmem + lane_addr + slot * NB + 16, v[1]);
-          if constexpr (Cfg::kTwoRings) {
-            tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB, w[0]);
-            tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB + 16, w[1]);
-          }
-          tmem_ld_wait();
-          reg_fence16(v[0]);
-          reg_fence16(v[1]);
-          if constexpr (Cfg::kTwoRings) {
-            reg_fence16(w[0]);
-            reg_fence16(w[1]);
+          if constexpr (NB == 16) {  // one load: cols 0-7 hi, 8-15 lo
+            uint32_t t[16], c[16];
+            tmem_ld16(tmem + lane_addr + slot * NB, t);
+            if constexpr (Cfg::kTwoRings) tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB, c);
+            tmem_ld_wait();
+            reg_fence16(t);
+            if constexpr (Cfg::kTwoRings) reg_fence16(c);
 #pragma unroll
-            for (int k = 0; k < 16; ++k)  // main hi*W_hi (debiased) + the three correction products
+            for (int k = 0; k < 8; ++k) {
+              v[0][k] = t[k];
+              v[1][k] = t[8 + k];
+              if constexpr (Cfg::kTwoRings) { w[0][k] = c[k]; w[1][k] = c[8 + k]; }
+            }
+          } else {
+            tmem_ld16(tmem + lane_addr + slot * NB, v[0]);
+            tmem_ld16(tmem + lane_addr + slot * NB + 16, v[1]);
+            if constexpr (Cfg::kTwoRings) {
+              tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB, w[0]);
+              tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB + 16, w[1]);
+            }
+            tmem_ld_wait();
+            reg_fence16(v[0]);
+            reg_fence16(v[1]);
+            if constexpr (Cfg::kTwoRings) { reg_fence16(w[0]); reg_fence16(w[1]); }
+          }
+          if constexpr (Cfg::kTwoRings) {
+#pragma unroll
+            for (int k = 0; k < kMaxBands; ++k)  // main hi*W_hi (debiased) + the three correction products
               v[0][k] = __float_as_uint(fmaf(__uint_as_float(v[0][k]), kMainDebias,
                                              (__uint_as_float(v[1][k]) + __uint_as_float(w[0][k])) +
                                                  __uint_as_float(w[1][k])));
 #pragma unroll
-            for (int k = 0; k < 16; ++k) v[1][k] = 0u;
+            for (int k = 0; k < kMaxBands; ++k) v[1][k] = 0u;
           }
           tc_fence_before();
           __syncwarp();
@@ -1091,9 +1108,9 @@ __global__ void pack_head_f16_kernel(const float* __restrict__ w, int K, uint8_t
     const float wf = w[idx * 9 + t];
     const __half hi = __float2half_rn(wf);
     const __half lo = __float2half_rn(wf - __half2float(hi));
-    const int nb = (2 - ky) * 32;
+    const int nb = (2 - ky) * ConvCfg<1>::NB;  // per dy: 8 hi rows, then 8 lo rows
     put_b(out, ConvCfg<1>::kWdx, kx, nb + k, ci, hi);
-    put_b(out, ConvCfg<1>::kWdx, kx, nb + 16 + k, ci, lo);
+    put_b(out, ConvCfg<1>::kWdx, kx, nb + ConvCfg<1>::NB / 2 + k, ci, lo);
   }
 }
 
