@@ -223,8 +223,13 @@ struct ConvCfg {
   static constexpr bool kUnshuf = kMode == 7;
   static constexpr bool kHead = kMode == 1 || kMode == 4 || kMode == 6 || kMode == 7 || kMode == 10;
   static constexpr bool kFirst = kMode == 2;
-  static constexpr bool kWide = kMode == 5 || kMode == 6 || kMode == 9 || kMode == 10;
+  static constexpr bool kWide = kMode == 5 || kMode == 6 || kMode == 9 || kMode == 10 || kMode == 11;
   static constexpr bool kQuarters = kMode == 5 || kMode == 9;
+  // mode 11: wide single-input layer split into output-channel HALVES (pairs of
+  // CTAs, 64 channels each, N = 192 dy-stacked MMAs at full rate) instead of
+  // quarters (N = 96, shared-memory-operand bound)
+  static constexpr bool kWideHalves = kMode == 11;
+  static constexpr bool kPartsW = kQuarters || kWideHalves;  // wide output-channel partition
   static constexpr int kCin = kWide ? 128 : 64;
   static constexpr int kKBlk = kCin / 64;        // 64-channel K blocks (one SW128 row buffer each)
   static constexpr int kKSteps = 4 * kKBlk;      // K16 steps per tap
@@ -250,7 +255,8 @@ struct ConvCfg {
   static constexpr int kW = kHalves ? 2 * kW1 : kW1;  // fp32 hidden: hi pack | lo pack
   static constexpr int kPasses = kMode == 3 ? 3 : (kSplit ? 2 : 1);
   static constexpr int kNStages =
-      kSplit ? ((kMode == 4) ? 5 : 2) : (kPlain ? kStagesPlain : (kWide ? 4 : kStages));  // input-row ring depth
+      kSplit ? ((kMode == 4) ? 5 : 2)
+             : (kPlain ? kStagesPlain : (kWideHalves ? 2 : (kWide ? 4 : kStages)));  // input-row ring depth
   // one stage: [hi K blocks][lo K blocks], one 17 KB SW128 row buffer each
   static constexpr int kStageBytes = (kSplit ? 2 : 1) * kKBlk * kInRowStride;
   static constexpr int kStageOut = (kHead || kSplit || kWide) ? 0 : 32 * 128;  // per-warp TMA-store staging
@@ -289,11 +295,12 @@ struct ConvCfg {
     return kHalves ? ((p == 0 && (k == 0 || k == 2)) || (p == 1 && k == 0))
                    : (k == 0 && (p == 0 || (kTwoRings && p == 1)));
   }
-  static constexpr int kParts = kQuarters ? 4 : 1;   // SegIter grid partition
+  static constexpr int kParts = kQuarters ? 4 : (kWideHalves ? 2 : 1);  // SegIter grid partition
   static constexpr int kVisits = kHalves ? 2 : 1;    // SegIter visits per segment
   static constexpr int kPxBytes = kSplit ? 4 * kCin : 2 * kCin;  // activation bytes per pixel
 };
-static_assert(ConvCfg<9>::kSmem <= 232448 && ConvCfg<10>::kSmem <= 232448, "wide single-input smem");
+static_assert(ConvCfg<9>::kSmem <= 232448 && ConvCfg<10>::kSmem <= 232448 && ConvCfg<11>::kSmem <= 232448,
+              "wide single-input smem");
 constexpr float kSplitWScale = 256.0f;  // split hidden weights are packed x 2^8
 // 1 + E[truncation loss] of the main accumulator: 36 MMAs, each losing 0.5 ulp of
 // a partial sum that grows ~linearly to the result, E[ulp(x)/|x|] = 0.7213 * 2^-23
@@ -334,7 +341,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   // PDL wait so it overlaps the previous kernel's tail
   if (threadIdx.x == 0) {
     mbar_arrive_expect_tx(&wbar, Cfg::kW);
-    const uint8_t* wsrc = a.wpack + (Cfg::kQuarters ? (blockIdx.x & 3) * Cfg::kW : 0) +
+    const uint8_t* wsrc = a.wpack + (Cfg::kPartsW ? (blockIdx.x % Cfg::kParts) * Cfg::kW : 0) +
                           (size_t)Iter(a).first_layer_or0(a) * Cfg::kW;
     for (int i = 0; i < Cfg::kW / Cfg::kWdx; ++i) bulk_load(sW + i * Cfg::kWdx, wsrc + i * Cfg::kWdx, Cfg::kWdx, &wbar);
   }
@@ -696,26 +703,27 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         mbar_wait(&slot_full[slot], (seq >> Cfg::kRingLog) & 1);
         tc_fence_after();
         const int xg = g.x0 + px;
-        if constexpr (Cfg::kQuarters) {
-          // wide hidden: channels 32*qtr..+31 of this CTA's quarter, + shift, ReLU,
-          // re-split into an fp16 pair: 64 B hi + 64 B lo per pixel straight to global
-          const int qtr = blockIdx.x & 3;
-          uint32_t v[2][16];
-          tmem_ld16(tmem + lane_addr + slot * NB, v[0]);
-          tmem_ld16(tmem + lane_addr + slot * NB + 16, v[1]);
+        if constexpr (Cfg::kPartsW) {
+          // wide hidden: channels NB*part..+NB-1 of this CTA's part (quarter: 32,
+          // half: 64), + shift, ReLU, re-split into an fp16 pair: 2*NB B hi +
+          // 2*NB B lo per pixel straight to global (single output: hi only)
+          const int qtr = blockIdx.x % Cfg::kParts;
+          uint32_t v[NB / 16][16];
+#pragma unroll
+          for (int j = 0; j < NB / 16; ++j) tmem_ld16(tmem + lane_addr + slot * NB + j * 16, v[j]);
           tmem_ld_wait();
-          reg_fence16(v[0]);
-          reg_fence16(v[1]);
+#pragma unroll
+          for (int j = 0; j < NB / 16; ++j) reg_fence16(v[j]);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
           if (xg < a.W) {
             // output pixel stride: pair 4*C bytes (hi C | lo C), single 2*C
             const int opx = a.out_single ? 2 * Cfg::kCin : 4 * Cfg::kCin;
-            uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * opx + qtr * 64;
+            uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * opx + qtr * NB * 2;
 #pragma unroll
-            for (int chunk = 0; chunk < 4; ++chunk) {
-              const uint32_t sh_u = shift_u + (uint32_t)(qtr * 32 + chunk * 8) * 4;
+            for (int chunk = 0; chunk < NB / 8; ++chunk) {
+              const uint32_t sh_u = shift_u + (uint32_t)(qtr * NB + chunk * 8) * 4;
               const float4 s0 = ld_shared_f4(sh_u);
               const float4 s1 = ld_shared_f4(sh_u + 16);
               const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
@@ -1042,7 +1050,7 @@ __global__ void pack_hidden_f16_kernel(const float* __restrict__ w, const float*
 // Wide hidden (mode 5): 128x128 filters, DC-compensated fp16, packed per output
 // quarter qtr = co/32: [qtr][dx][K block ci/64][3 dy x 32 rows x 128 B]
 __global__ void pack_hidden_wide_kernel(const float* __restrict__ w, const float* __restrict__ scale,
-                                        uint8_t* __restrict__ out) {
+                                        uint8_t* __restrict__ out, int parts) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*128 + ci
   if (idx >= 128 * 128) return;
   const int co = idx / 128, ci = idx % 128;
@@ -1050,12 +1058,15 @@ __global__ void pack_hidden_wide_kernel(const float* __restrict__ w, const float
 #pragma unroll
   for (int t = 0; t < 9; ++t) wv[t] = w[idx * 9 + t] * scale[co];
   dc_round9(wv, rn);
-  using C5 = ConvCfg<5>;
-  uint8_t* base = out + (co >> 5) * C5::kW + (ci >> 6) * C5::kWdxBlk;
+  // quarters (modes 5 / 9): 4 packs of 32 output channels; halves (mode 11): 2 of 64
+  const int nbp = 128 / parts;
+  const size_t wpart = parts == 4 ? ConvCfg<5>::kW : ConvCfg<11>::kW;
+  const int wdxblk = 3 * nbp * 128, wdx = 2 * wdxblk;
+  uint8_t* base = out + (co / nbp) * wpart + (ci >> 6) * wdxblk;
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
     const int ky = t / 3, kx = t % 3;
-    put_b(base, C5::kWdx, kx, (2 - ky) * 32 + (co & 31), ci & 63, __float2half_rn(rn[t]));
+    put_b(base, wdx, kx, (2 - ky) * nbp + (co % nbp), ci & 63, __float2half_rn(rn[t]));
   }
 }
 
@@ -1198,6 +1209,11 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
       cfg.blockDim = dim3(ConvCfg<9>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<9>::kSmem;
       return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<9>, tm_in, tm_out, a, p0, zs);
+    case 11:
+      cfg.gridDim = dim3(std::max(2, grid & ~1));  // pairs of CTAs (output-channel halves)
+      cfg.blockDim = dim3(ConvCfg<11>::kThreads);
+      cfg.dynamicSmemBytes = ConvCfg<11>::kSmem;
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<11>, tm_in, tm_out, a, p0, zs);
     case 10:
       cfg.blockDim = dim3(ConvCfg<10>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<10>::kSmem;
@@ -1248,10 +1264,11 @@ cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_hidden_wide(const float* w, const float* scale, uint8_t* out, cudaStream_t st) {
+cudaError_t launch_pack_hidden_wide(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int parts) {
+  static_assert(4 * ConvCfg<5>::kW == 2 * ConvCfg<11>::kW, "quarter and half packs share the layer stride");
   cudaError_t e = cudaMemsetAsync(out, 0, 4 * ConvCfg<5>::kW, st);
   if (e != cudaSuccess) return e;
-  pack_hidden_wide_kernel<<<(128 * 128 + 127) / 128, 128, 0, st>>>(w, scale, out);
+  pack_hidden_wide_kernel<<<(128 * 128 + 127) / 128, 128, 0, st>>>(w, scale, out, parts);
   return cudaGetLastError();
 }
 
@@ -1312,6 +1329,9 @@ cudaError_t configure_kernels() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<9>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<11>::kSmem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<10>::kSmem);

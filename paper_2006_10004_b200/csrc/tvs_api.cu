@@ -131,6 +131,9 @@ struct tvs_plan {
   // 6.6-8.0e-3 on config 5 (tools/emulate_wide.py), 0 is the plain-fp16
   // roofline probe (1.1-1.3e-2, over the 1e-2 gate)
   int wide_pair_layers = 12;
+  // wide single-input layers on output-channel halves (mode 11, N = 192) instead
+  // of quarters (mode 9, N = 96); TVS_WIDE_HALVES = 0 / 1
+  bool wide_halves = true;
   static constexpr int kStackMinItems = 6;
   int* rowcnt = nullptr;  // row flags (B*strips*H ints), zeroed per chunk
   size_t rowcnt_n = 0;
@@ -372,10 +375,12 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.act_out = static_cast<uint8_t*>(act[cur ^ 1]);
       a.out_single = pair_in(l + 1) ? 0 : 1;
       const CUtensorMap& m = pair_in(l) ? pair_map[cur] : single_map[cur];
-      // 4 CTAs per strip-row range: size the grid by groups
-      const int grid = 4 * std::max(1, std::min(max_ctas / 4, conv_grid(max_ctas, a)));
+      // 4 (quarters) or 2 (halves) CTAs per strip-row range: size the grid by groups
+      const int mode = pair_in(l) ? 5 : (p->wide_halves ? 11 : 9);
+      const int parts = mode == 11 ? 2 : 4;
+      const int grid = parts * std::max(1, std::min(max_ctas / parts, conv_grid(max_ctas, a)));
       timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * C * C,
-                   [&] { return tvs::launch_conv_tc(pair_in(l) ? 5 : 9, m, m, a, nullptr, grid, st); });
+                   [&] { return tvs::launch_conv_tc(mode, m, m, a, nullptr, grid, st); });
       cur ^= 1;
     }
     tvs::ConvArgs a = geom(row0, rows);
@@ -629,6 +634,7 @@ int tvs_plan_create_ex(int device, int depth, int channels, int out_bands, int m
     if (const char* e = std::getenv("TVS_PAIR")) p->pair_fuse = std::atoi(e) != 0;
     if (const char* e = std::getenv("TVS_STACK")) p->stack = std::atoi(e);
     if (const char* e = std::getenv("TVS_WIDE_PAIR")) p->wide_pair_layers = std::atoi(e);
+    if (const char* e = std::getenv("TVS_WIDE_HALVES")) p->wide_halves = std::atoi(e) != 0;
     if (const char* e = std::getenv("TVS_STACK_SKEW")) p->stack_skew = std::atoi(e);
     if (const char* e = std::getenv("TVS_WIDE_CUDA")) p->wide_cuda = std::atoi(e) != 0;
     try {
@@ -709,9 +715,12 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
       } else if (p->split_path()) {
         TVS_CUDA(tvs::launch_pack_hidden_split(w_dev[l + 1], dst_scale,
                                                p->wpack + (size_t)l * tvs::conv_wpack_split_bytes(), st));
-      } else if (p->wide_path()) {
+      } else if (p->wide_path()) {  // pair-input layers: quarters (mode 5); single-input: halves (mode 11)
+        const int P = std::max(0, std::min(p->wide_pair_layers, nh));
+        const bool pair_in = l < P || P >= nh;
         TVS_CUDA(tvs::launch_pack_hidden_wide(w_dev[l + 1], dst_scale,
-                                              p->wpack + (size_t)l * tvs::conv_wpack_wide_bytes(false), st));
+                                              p->wpack + (size_t)l * tvs::conv_wpack_wide_bytes(false), st,
+                                              pair_in || !p->wide_halves ? 4 : 2));
       } else {
         TVS_CUDA(cudaMemcpyAsync(p->whid + (size_t)l * C * C * 9, w_dev[l + 1], (size_t)C * C * 9 * 4,
                                  cudaMemcpyDeviceToDevice, st));

@@ -46,7 +46,8 @@ PREC = opt.get("--precision", "fast")
 lib = _native.load()
 lib.tvs_debug_stack.restype = ctypes.c_int
 lib.tvs_debug_stack.argtypes = [ctypes.c_int]
-m0, m1 = model({}), model(env)
+WIDE = opt.get("--wide", "0") == "1"
+m0, m1 = model({}, WIDE), model(env, WIDE)
 RUNTIME = ("TVS_CONV_DBG", "TVS_PAIR_DBG")  # read at every launch, not at plan creation
 
 
