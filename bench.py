@@ -105,7 +105,7 @@ def _kernel_name(tc, launches, depth, hidden_per_fwd=None):
     per-layer hidden conv; the 128-channel wide variant runs conv_tc.cu modes 5
     (pair input) / 9 (single)."""
     if tc == "wide":
-        return "conv3x3_tc_kernel<5>/<9> (wide hidden layer, 128 ch)"
+        return "conv3x3_tc_kernel<5>/<11> (wide hidden layers, 128 ch: pair input on quarters, single on halves)"
     if not tc:
         return "hidden_f32_kernel"
     if launches == 3 or (hidden_per_fwd is not None and abs(hidden_per_fwd * 3 - launches) < 1e-6):
