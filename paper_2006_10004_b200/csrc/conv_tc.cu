@@ -320,6 +320,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   __shared__ uint64_t full[kStages], empty[kStages], slot_full[kSlots], slot_empty[kSlots], wbar, wfree;
   __shared__ uint32_t tmem_base_smem;
   __shared__ __align__(16) float sShift[kMaxC];
+  // layer stack: each epilogue group's copy of its current layer's BN shift
+  // (a per-row __ldg of the shift missed L1 every row: the store-completion
+  // wait cp.async.bulk.wait_group invalidates L1)
+  __shared__ __align__(16) float sShiftG[Cfg::kStack ? Cfg::kGroups : 1][kC];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
   uint8_t* sIn = sW + Cfg::kW;
@@ -691,12 +695,24 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const uint32_t shift_u = smem_u32(sShift);
     if (!kHead && !Cfg::kSplit && !Cfg::kWide && lane == 0) prefetch_tmap(&tm_out);
     uint32_t seq = 0, gsel = 0;  // gsel = seq % kGroups
+    int grp_layer = -1;          // layer stack: layer whose shift sShiftG[grp] holds
+    const uint32_t shift_g = smem_u32(&sShiftG[Cfg::kStack ? grp : 0][0]);
     Iter it(a, Cfg::kVisits, Cfg::kParts);
     Segment g;
     while (it.next(a, g)) {
       // layer-stack: this item's BN shift and output buffer
       const float4* shg = reinterpret_cast<const float4*>(a.shift + (size_t)g.layer * kC);
       const CUtensorMap* tmo = (Cfg::kStack && (g.layer & 1)) ? &smaps.out0 : &tm_out;
+      if constexpr (Cfg::kStack) {
+        if (g.layer != grp_layer && !(a.dbg & 16384)) {
+          // every warp of the group is past the previous item's last per-row
+          // barrier, so nobody still reads the old shift
+          const int t = quarter * 32 + lane;
+          if (t < kC) sShiftG[grp][t] = a.shift[(size_t)g.layer * kC + t];
+          named_bar_sync(1 + grp, 128);
+          grp_layer = g.layer;
+        }
+      }
       for (int q = g.ya; q < g.yb; ++q, ++seq, gsel = (gsel + 1 == Cfg::kGroups) ? 0 : gsel + 1) {
         if (gsel != grp) continue;
         const uint32_t slot = seq & Cfg::kRingMask;
@@ -822,8 +838,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           const uint32_t rowp = stage_out + lane * 128;
 #pragma unroll
           for (int chunk = 0; chunk < 8; ++chunk) {  // 16-byte chunk = 8 channels
-            const float4 s0 = Cfg::kStack ? __ldg(shg + 2 * chunk) : ld_shared_f4(shift_u + chunk * 32);
-            const float4 s1 = Cfg::kStack ? __ldg(shg + 2 * chunk + 1) : ld_shared_f4(shift_u + chunk * 32 + 16);
+            const bool gl = Cfg::kStack && (a.dbg & 16384);  // A/B: the per-row global loads
+            const float4 s0 = gl ? __ldg(shg + 2 * chunk) : ld_shared_f4((Cfg::kStack ? shift_g : shift_u) + chunk * 32);
+            const float4 s1 = gl ? __ldg(shg + 2 * chunk + 1)
+                                 : ld_shared_f4((Cfg::kStack ? shift_g : shift_u) + chunk * 32 + 16);
             const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
             uint32_t packed[4];
 #pragma unroll
