@@ -69,6 +69,7 @@ struct StackMaps {
 cudaError_t launch_conv_stack(const CUtensorMap& tm_in0, const CUtensorMap& tm_out1, const StackMaps& sm,
                               const ConvArgs& a, int grid, cudaStream_t st);
 int conv_stack_error(int reset);  // watchdog flag of the stack kernel's row-flag waits
+int debug_cycles(unsigned long long* out, int reset);  // TVS_CONV_DBG bit 15 counters
 
 // two fused hidden layers (conv_pair.cu): cluster of S = ceil(W/128) CTAs
 struct PairArgs {

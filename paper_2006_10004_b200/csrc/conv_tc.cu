@@ -134,6 +134,10 @@ struct ItemIter {
 };
 
 __device__ int g_stack_err;  // set when a row-flag wait times out (results invalid, no hang)
+// TVS_CONV_DBG bit 15 (layer stack): MMA-issuer cycle accounting (sum over CTAs): [0] total,
+// [1] waiting for a free accumulator slot, [2] waiting for the input row,
+// [3] waiting for a layer's weights, [4] general-path rows, [5] fast-path rows
+__device__ unsigned long long g_dbg_cycles[8];
 
 // Producer side of the layer stack: input row r of a layer-j item (j >= 1) is
 // layer j-1's output row r of strips s-1..s+1 (the 130-px halo box reaches one
@@ -497,6 +501,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const uint64_t bdesc0 = make_smem_desc(smem_u32(sW), 0, 1024, kLayoutSW128);
     const bool leader = elect_one();
     const bool domma = !(a.dbg & 64);  // ablation (TVS_CONV_DBG): no MMAs
+    unsigned long long cyc[6] = {0, 0, 0, 0, 0, 0};
+    const long long tstart = clock64();
     mbar_wait(&wbar, 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -512,7 +518,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           if (leader) mma_commit(&wfree);
           __syncwarp();
           wphase ^= 1;
+          long long tw = (a.dbg & 32768) ? clock64() : 0;
           mbar_wait(&wbar, wphase);
+          if (a.dbg & 32768) cyc[3] += clock64() - tw;
           cur_layer = g.layer;
         }
       }
@@ -532,7 +540,17 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           const uint32_t sq2 = sq + 3;  // output row r+2, entered by input row r+1
           bool pre_ok = false;  // (issuing lane) the next row's barriers have completed
           if (leader) {
-            if (!prewaited)
+            if (Cfg::kStack && (a.dbg & 32768)) {
+              ++cyc[5];
+              if (!prewaited) {
+                long long t0 = clock64();
+                mbar_wait(&slot_empty[(sq + 2) & Cfg::kRingMask], (((sq + 2) >> Cfg::kRingLog) & 1) ^ 1);
+                long long t1 = clock64();
+                mbar_wait(&full[stage], phase);
+                cyc[1] += t1 - t0;
+                cyc[2] += clock64() - t1;
+              }
+            } else if (!prewaited)
               mbar_wait2(&slot_empty[(sq + 2) & Cfg::kRingMask], (((sq + 2) >> Cfg::kRingLog) & 1) ^ 1, &full[stage],
                          phase);
             tc_fence_after();
@@ -625,10 +643,12 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         const int q_lo = max(r - 1, g.ya), q_hi = min(r + 1, g.yb - 1);
         // output rows whose first contributing input row is r: first(q) = max(q-1, 0)
         const int q_new = (r == 0) ? q_lo : r + 1;
+        long long tg0 = (Cfg::kStack && (a.dbg & 32768)) ? clock64() : 0;
         for (int q = max(q_new, q_lo); q <= q_hi; ++q) {
           const uint32_t sq = seq + (uint32_t)(q - g.ya);
           mbar_wait(&slot_empty[sq & Cfg::kRingMask], ((sq >> Cfg::kRingLog) & 1) ^ 1);
         }
+        long long tg1 = (Cfg::kStack && (a.dbg & 32768)) ? clock64() : 0;
         // Target rows [q_lo, q_hi] -> consecutive slots, split at the ring wrap
         // (regular ops R0, R1); the first K step also splits off the
         // newly-entered suffix [q_new, q_hi] with accumulate = 0 (ops F0..F2).
@@ -651,6 +671,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         const uint32_t Ct = R1t, Cb = R1b, Ci = idesc_of(C_e - s1b + 1);
         const uint32_t Dt = R1t + (uint32_t)(D_b - s1b) * NB, Db = brow16(D_b), Di = idesc_of(q_hi - D_b + 1);
         mbar_wait(&full[stage], phase);
+        if (Cfg::kStack && (a.dbg & 32768)) { cyc[1] += tg1 - tg0; cyc[2] += clock64() - tg1; ++cyc[4]; }
         tc_fence_after();
         if (leader) {
           const uint64_t ad_row = adesc0 + (uint64_t)((stage * Cfg::kStageBytes) >> 4);
@@ -683,6 +704,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         if (++stage == Cfg::kNStages) { stage = 0; phase ^= 1; }
       }
       seq += (uint32_t)(g.yb - g.ya);
+    }
+    if (Cfg::kStack && (a.dbg & 32768) && leader) {
+      cyc[0] = clock64() - tstart;
+      for (int i = 0; i < 6; ++i) atomicAdd(&g_dbg_cycles[i], cyc[i]);
     }
   } else {
     // ------------------------------------------------ epilogue ----
@@ -1256,6 +1281,15 @@ cudaError_t launch_conv_stack(const CUtensorMap& tm_in0, const CUtensorMap& tm_o
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<8>, tm_in0, tm_out1, a, zero, sm);
+}
+
+int debug_cycles(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_dbg_cycles, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
+  if (reset) {
+    const unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_dbg_cycles, z, sizeof(z));
+  }
+  return 0;
 }
 
 int conv_stack_error(int reset) {

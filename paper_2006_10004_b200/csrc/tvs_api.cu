@@ -857,6 +857,7 @@ int tvs_tvflow_analyze(const double* f, int N, int H, int W, double dt, int n_st
 // diagnostics of the layer-stack kernel (not part of the public ABI): 1 if a
 // row-flag wait timed out since the last reset (that forward's output is invalid)
 int tvs_debug_stack(int reset) { return tvs::conv_stack_error(reset); }
+int tvs_debug_cycles(unsigned long long* out, int reset) { return tvs::debug_cycles(out, reset); }
 
 int tvs_plan_destroy(tvs_plan* p) {
   return guarded([&] {
