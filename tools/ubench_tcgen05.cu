@@ -94,9 +94,16 @@ k_layout(const __half* __restrict__ Ag, const __half* __restrict__ Bg, float* __
 // variant: 0..3 f16 N=64/128/192/256 ; 4 tf32 N=64 ; 5 e4m3 N=64 ;
 //          6 f16 N=64 with 3 taps sharing A via collector::a ;  7 f16 N=64
 //          with A address shifted by +16 B per MMA (tap walk, no-swizzle).
+// 16 / 17 / 18: the N=192 conv pattern (as 8) while warp 1 streams TMA bulk
+// traffic through shared memory: 16 = global->smem loads, 17 = smem->global
+// stores, 18 = both, plus warps 2-3 flooding st.shared (the epilogue staging)
+__device__ __forceinline__ void bulk_store_g(void* gdst, uint32_t ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc), "r"(bytes)
+               : "memory");
+}
 template <int V>
 __global__ void __launch_bounds__(128, 1)
-k_rate(int iters, long long* cycles, int* err) {
+k_rate(int iters, long long* cycles, int* err, uint8_t* gbuf) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
@@ -136,7 +143,7 @@ k_rate(int iters, long long* cycles, int* err) {
                        ::"r"(tmem + 64), "l"(ad), "l"(bd1), "r"(idesc) : "memory");
           asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::lastuse [%0], %1, %2, %3, 1;"
                        ::"r"(tmem + 128), "l"(ad), "l"(bd2), "r"(idesc) : "memory");
-        } else if constexpr (V == 8 || V == 9 || V == 11 || V == 12) {
+        } else if constexpr (V == 8 || V == 9 || V == 11 || V == 12 || V >= 16) {
           // conv row pattern: A shifted by dx*128 B (V=8) or aligned (V=9), B = N192 block of dx
           const int dx = it % 3;
           const uint32_t ash = (V == 9) ? 0u : (uint32_t)dx * 128u;
@@ -186,7 +193,53 @@ k_rate(int iters, long long* cycles, int* err) {
     long long t1 = clock64();
     if (!ok) atomicAdd(err, 1);
     cycles[blockIdx.x] = t1 - t0;
-    if constexpr (V == 11 || V == 12) *reinterpret_cast<volatile uint32_t*>(smem + 110 * 1024) = 1;
+    if constexpr (V == 11 || V == 12 || V >= 16) *reinterpret_cast<volatile uint32_t*>(smem + 110 * 1024) = 1;
+  }
+  if constexpr (V >= 16) {
+    // warp 1, lanes 0-3: bulk traffic, each lane through its own 8 KB buffer
+    // at 112 + 8*lane KB (4 copies in flight)
+    volatile uint32_t* flag = reinterpret_cast<volatile uint32_t*>(smem + 110 * 1024);
+    __shared__ uint64_t tb[4];
+    __shared__ unsigned long long moved[4];
+    const int ln = tid & 31;
+    if (warp == 1 && ln < 4) { mbar_init(&tb[ln], 1); moved[ln] = 0; }
+    if (tid == 32) fence_barrier_init();
+    __syncwarp();
+    if (warp == 1 && ln < 4) {
+      uint32_t ph = 0;
+      unsigned long long n = 0;
+      uint8_t* buf = smem + (112 + 8 * ln) * 1024;
+      for (uint32_t i = 0; *flag == 0; ++i) {
+        uint8_t* g = gbuf + (size_t)(((blockIdx.x * 4 + ln) * 64 + (i % 64)) % 16384) * 8192;
+        if constexpr (V == 16 || V == 18) {
+          mbar_arrive_expect_tx(&tb[ln], 8192);
+          bulk_load(buf, g, 8192, &tb[ln]);
+          mbar_wait(&tb[ln], ph);
+          ph ^= 1;
+          n += 8192;
+        }
+        if constexpr (V == 17 || V == 18) {
+          bulk_store_g(g + (size_t)8192 * 16384, smem_u32(buf), 8192);
+          bulk_commit();
+          bulk_wait_read<0>();
+          n += 8192;
+        }
+      }
+      bulk_wait<0>();
+      moved[ln] = n;
+    }
+    if constexpr (V == 18) {
+      if (warp >= 2) {
+        uint4* region = reinterpret_cast<uint4*>(smem + 104 * 1024) + (warp - 2) * 32 * 4;
+        const uint4 v = make_uint4(tid, 1, 2, 3);
+        while (*flag == 0) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) region[j * 32 + (tid & 31)] = v;
+        }
+      }
+    }
+    __syncwarp();
+    if (tid == 32) cycles[gridDim.x + blockIdx.x] = (long long)(moved[0] + moved[1] + moved[2] + moved[3]);
   }
   if constexpr (V == 11 || V == 12) {
     if (warp != 0) {
@@ -301,15 +354,18 @@ static void run_layout_tests() {
 template <int V>
 static void run_rate(const char* name, int ctas, double macs_per_iter) {
   long long* dC; int* dErr;
-  CK(cudaMalloc(&dC, ctas * sizeof(long long))); CK(cudaMalloc(&dErr, 4)); CK(cudaMemset(dErr, 0, 4));
-  const int smem = 112 * 1024 + 1024;
+  CK(cudaMalloc(&dC, 2 * ctas * sizeof(long long))); CK(cudaMalloc(&dErr, 4)); CK(cudaMemset(dErr, 0, 4));
+  CK(cudaMemset(dC, 0, 2 * ctas * sizeof(long long)));
+  static uint8_t* gbuf = nullptr;
+  if (!gbuf) CK(cudaMalloc(&gbuf, (size_t)2 * 16384 * 8192));
+  const int smem = (V >= 16 ? 144 : 112) * 1024 + 1024;
   CK(cudaFuncSetAttribute(k_rate<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int iters = 4096;
-  k_rate<V><<<ctas, 128, smem>>>(64, dC, dErr);  // warm
+  k_rate<V><<<ctas, 128, smem>>>(64, dC, dErr, gbuf);  // warm
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  k_rate<V><<<ctas, 128, smem>>>(iters, dC, dErr);
+  k_rate<V><<<ctas, 128, smem>>>(iters, dC, dErr, gbuf);
   cudaEventRecord(e1);
   CK(cudaDeviceSynchronize());
   float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -319,8 +375,11 @@ static void run_rate(const char* name, int ctas, double macs_per_iter) {
   double avg = 0; for (auto v : c) avg += v; avg /= ctas;
   double n_mma = (double)iters * (V == 6 || V == 15 ? 12 : (V == 10 || V == 13 || V == 14 ? 8 : 4));
   double tflops = 2.0 * macs_per_iter * iters * ctas / (ms * 1e-3) / 1e12;
-  printf("RATE %-26s ctas=%3d cyc/mma=%7.2f  cyc/iter=%8.2f  MAC/clk/SM=%7.1f  %.1f TFLOP/s  timeout=%d\n",
-         name, ctas, avg / n_mma, avg / iters, macs_per_iter * iters / avg, tflops, herr);
+  std::vector<long long> mv(ctas);
+  CK(cudaMemcpy(mv.data(), dC + ctas, ctas * sizeof(long long), cudaMemcpyDeviceToHost));
+  double bytes = 0; for (auto v : mv) bytes += v; bytes /= ctas;
+  printf("RATE %-26s ctas=%3d cyc/mma=%7.2f  cyc/iter=%8.2f  MAC/clk/SM=%7.1f  %.1f TFLOP/s  bulk B/clk/SM=%5.1f  timeout=%d\n",
+         name, ctas, avg / n_mma, avg / iters, macs_per_iter * iters / avg, tflops, bytes / avg, herr);
   cudaFree(dC); cudaFree(dErr);
 }
 
@@ -349,6 +408,9 @@ int main(int argc, char** argv) {
     run_rate<15>("3x N64 fill/use/lastuse", ctas, 128.0 * 192 * 64);
     run_rate<11>("N192 conv + STS flood", ctas, 128.0 * 192 * 64);
     run_rate<12>("N192 conv + STS throttled", ctas, 128.0 * 192 * 64);
+    run_rate<16>("N192 conv + bulk loads", ctas, 128.0 * 192 * 64);
+    run_rate<17>("N192 conv + bulk stores", ctas, 128.0 * 192 * 64);
+    run_rate<18>("N192 conv + loads+stores+STS", ctas, 128.0 * 192 * 64);
   }
   printf("DONE\n");
   return 0;
