@@ -872,10 +872,16 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int c = chunk * 8 + e * 2;
-              const float f0 = fmaxf(__uint_as_float(v[c >> 4][c & 15]) + sh[2 * e], 0.0f);
-              const float f1 = fmaxf(__uint_as_float(v[c >> 4][(c & 15) + 1]) + sh[2 * e + 1], 0.0f);
-              __half2 hv = __floats2half2_rn(f0, f1);
-              packed[e] = *reinterpret_cast<uint32_t*>(&hv);
+              const float f0 = __uint_as_float(v[c >> 4][c & 15]) + sh[2 * e];
+              const float f1 = __uint_as_float(v[c >> 4][(c & 15) + 1]) + sh[2 * e + 1];
+              if (a.dbg & 65536) {  // A/B: separate ReLU and conversion
+                __half2 hv = __floats2half2_rn(fmaxf(f0, 0.0f), fmaxf(f1, 0.0f));
+                packed[e] = *reinterpret_cast<uint32_t*>(&hv);
+              } else {
+                // ReLU fused into the fp16 rounding (fewer epilogue instructions
+                // competing with the MMA warp for issue slots)
+                asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(packed[e]) : "f"(f1), "f"(f0));
+              }
             }
             st_shared_v4(rowp + ((chunk ^ (lane & 7)) << 4), packed[0], packed[1], packed[2], packed[3]);
           }
