@@ -872,8 +872,12 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int c = chunk * 8 + e * 2;
-              const float f0 = __uint_as_float(v[c >> 4][c & 15]) + sh[2 * e];
-              const float f1 = __uint_as_float(v[c >> 4][(c & 15) + 1]) + sh[2 * e + 1];
+              // packed fp32x2 add (FADD2): channel pair (c, c+1) in one instruction
+              // (measured neutral against scalar adds; fewer issue slots)
+              const float2 fs = __fadd2_rn(make_float2(__uint_as_float(v[c >> 4][c & 15]),
+                                                       __uint_as_float(v[c >> 4][(c & 15) + 1])),
+                                           make_float2(sh[2 * e], sh[2 * e + 1]));
+              const float f0 = fs.x, f1 = fs.y;
               if (a.dbg & 65536) {  // A/B: separate ReLU and conversion
                 __half2 hv = __floats2half2_rn(fmaxf(f0, 0.0f), fmaxf(f1, 0.0f));
                 packed[e] = *reinterpret_cast<uint32_t*>(&hv);
