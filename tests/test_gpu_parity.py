@@ -400,3 +400,30 @@ def test_wide_pair_schedules(wide_case, monkeypatch, pairs, tol):
     err = band_rel_l2(out, y32).max()
     assert err <= tol, f"pairs={pairs}: worst band rel-L2 {err:.3e}"
     np.testing.assert_allclose(out.sum(1, keepdims=True) + clos, x[:, 0:1], atol=1e-5)
+
+
+@pytest.mark.parametrize("prec", ["fast", "fp32"])
+@pytest.mark.parametrize("bands", [1, 3, 8])
+def test_band_counts(prec, bands):
+    """Heads with 1..8 bands (the 8 hi + 8 lo weight columns per dy of the
+    tcgen05 head, kMaxBands) against the oracle, on ragged shapes."""
+    state = build_seeded_state(3, 64, bands)
+    ref_m = oracle_from_state(state, 3, 64, bands)
+    m = TVSpecNet(depth=3, out_bands=bands, precision=prec).eval()
+    m.load_state_dict(state)
+    x = np.random.default_rng(bands).random((2, 1, 37, 150)).astype(np.float32)
+    with torch.no_grad():
+        ref = ref_m(torch.from_numpy(x)).numpy()
+    _check(m, x, ref)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1, 1), (3, 1, 1, 300), (1, 1, 130, 1), (2, 1, 7, 129), (1, 1, 64, 257)])
+def test_conv0_tcgen05_ragged(seeded_state, oracle, shape):
+    """The tcgen05 K1 on ragged strips (partial 128-px strips, single rows and
+    columns) stays within the fast-mode tolerance of the oracle."""
+    m = TVSpecNet().eval()
+    m.load_state_dict(seeded_state)
+    x = np.random.default_rng(sum(shape)).random(shape).astype(np.float32)
+    with torch.no_grad():
+        ref = oracle(torch.from_numpy(x)).numpy()
+    _check(m, x, ref)
