@@ -69,6 +69,11 @@ struct StackMaps {
 cudaError_t launch_conv_stack(const CUtensorMap& tm_in0, const CUtensorMap& tm_out1, const StackMaps& sm,
                               const ConvArgs& a, int grid, cudaStream_t st);
 int conv_stack_error(int reset);  // watchdog flag of the stack kernel's row-flag waits
+// CTA-pair (cta_group::2) hidden layer, per-layer form (conv_tc.cu, TVS_PAIR2)
+size_t conv_pair2_wpack_bytes();
+cudaError_t launch_pack_hidden_pair2(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
+cudaError_t launch_conv_pair2(const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a, int grid,
+                              cudaStream_t st);
 int debug_cycles(unsigned long long* out, int reset);  // TVS_CONV_DBG bit 15 counters
 
 // two fused hidden layers (conv_pair.cu): cluster of S = ceil(W/128) CTAs

@@ -1401,4 +1401,429 @@ cudaError_t configure_kernels() {
   return configure_edge_kernels();
 }
 
+// --------------------------------------------------------------------------
+// CTA-pair hidden layer (cta_group::2), per-layer form (prototype, TVS_PAIR2).
+//
+// Two CTAs of a cluster take two adjacent 128-px strips of the same rows; the
+// leader issues tcgen05.mma.cta_group::2 with M = 256: each CTA's TMEM gets
+// its own 128 pixels x N columns, and each CTA supplies HALF of the B operand
+// (D columns [0, N/2) from the leader's shared memory, [N/2, N) from the
+// peer's, at the same offset: tools/probe_pair_mma.cu).  Per SM this halves
+// the B bytes read and the MMA instructions per output row.  Because an MMA's
+// N range is split in half across the pair, every dy-range the slot ring can
+// ask for is packed as its own layout: [W(+1)|W(0)|W(-1)], [W(+1)|W(0)],
+// [W(0)|W(-1)], W(+1), W(0), W(-1) (this CTA's half of each: 320 rows x 128 B
+// per dx, 120 KB).  The accumulation per output pixel is the same MMA sequence
+// as the single-CTA kernel, so results are bitwise equal to it.
+//
+// Barriers: the leader's full[stage] counts both CTAs' TMA input rows and its
+// slot_empty[s] both CTAs' epilogue warps (8 arrivals); commits multicast to
+// both CTAs (empty, slot_full).  The weights land on the leader's wbar.
+#ifndef TVS_P2_STAGES
+#define TVS_P2_STAGES 3
+#endif
+#ifndef TVS_P2_GROUPS
+#define TVS_P2_GROUPS 3
+#endif
+constexpr int kP2Stages = TVS_P2_STAGES;
+constexpr int kP2Groups = TVS_P2_GROUPS;
+constexpr int kP2Threads = 32 * (2 + 4 * kP2Groups);
+constexpr int kP2RowsDx = 320;
+constexpr int kP2W = 3 * kP2RowsDx * 128;  // 120 KB per CTA
+constexpr size_t kP2Smem = 1024 + kP2W + kP2Stages * kInRowStride + 4 * kP2Groups * 4096 + 1024;
+static_assert(kP2Smem <= 232448, "pair kernel smem");
+// layout of the dy-range (d0, c): rows [64 d0, 64 (d0 + c)) of [W(+1)|W(0)|W(-1)]
+__host__ __device__ constexpr int p2_layout(int d0, int c) { return c == 3 ? 0 : (c == 2 ? 1 + d0 : 3 + d0); }
+__host__ __device__ constexpr int p2_row0(int L) { return L == 0 ? 0 : (L == 1 ? 96 : (L == 2 ? 160 : 224 + 32 * (L - 3))); }
+
+template <int kColl>  // 0 plain, 1 collector::a::fill, 2 ::use, 3 ::lastuse
+TVS_DEV void mma2(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  if constexpr (kColl == 0)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                 ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+  else if constexpr (kColl == 1)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::2.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n\t}"
+                 ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+  else if constexpr (kColl == 2)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::2.kind::f16.collector::a::use [%0], %1, %2, %3, p;\n\t}"
+                 ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+  else
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}"
+                 ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
+}
+TVS_DEV void commit2(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
+}
+// .cta_group::2: the completing mbarrier may live in the peer CTA of the pair
+TVS_DEV void tma_load_4d_to(void* dst, const void* tmap, uint32_t bar_cluster, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster),
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+TVS_DEV void bulk_load_to(void* dst, const void* src, uint32_t bytes, uint32_t bar_cluster) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar_cluster) : "memory");
+}
+
+// segments of a pair: strip-pair rows ordered (image, strip pair, row); this
+// CTA's strip is 2 * pair_strip + rank
+struct SegIterP2 {
+  long long lo, hi, cur;
+  int half_strips, rank;
+  TVS_DEV SegIterP2(const ConvArgs& a, int rk) : rank(rk) {
+    half_strips = a.strips / 2;
+    const long long T = (long long)a.B * half_strips * a.rows;
+    const long long part = blockIdx.x / 2, nparts = gridDim.x / 2;
+    lo = T * part / nparts;
+    hi = T * (part + 1) / nparts;
+    cur = lo;
+  }
+  TVS_DEV bool next(const ConvArgs& a, Segment& g) {
+    if (cur >= hi) return false;
+    const long long col = cur / a.rows;
+    const int y0 = (int)(cur - col * a.rows);
+    const int n = (int)min((long long)(a.rows - y0), hi - cur);
+    g.b = (int)(col / half_strips);
+    g.x0 = ((int)(col % half_strips) * 2 + rank) * kStripPx;
+    g.ya = a.row0 + y0;
+    g.yb = g.ya + n;
+    g.h = 0;
+    g.layer = 0;
+    cur += n;
+    return true;
+  }
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
+conv3x3_pair2_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
+                     const ConvArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ uint64_t full[kP2Stages], empty[kP2Stages], slot_full[kSlots], slot_empty[kSlots], wbar, wpeer;
+  __shared__ uint32_t tmem_base_smem;
+  __shared__ __align__(16) float sShift[kC];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = smem;
+  uint8_t* sIn = sW + kP2W;
+  uint8_t* sOut = sIn + kP2Stages * kInRowStride;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  constexpr int NB = 64;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kP2Stages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < kSlots; ++i) { mbar_init(&slot_full[i], 1); mbar_init(&slot_empty[i], 8); }
+    mbar_init(&wbar, 1);
+    mbar_init(&wpeer, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < kC) sShift[threadIdx.x] = a.shift[threadIdx.x];
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_smem))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // peer barriers initialised before any remote arrival
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_smem;
+  if (threadIdx.x == 0) {  // weights (independent of the previous layer): this CTA's half
+    mbar_arrive_expect_tx(&wbar, kP2W);
+    const uint8_t* wsrc = a.wpack + (size_t)rank * kP2W;
+    for (int i = 0; i < 3; ++i) bulk_load(sW + i * (kP2W / 3), wsrc + i * (kP2W / 3), kP2W / 3, &wbar);
+  }
+  if (rank == 1 && warp == 1 && lane == 0) {  // tell the leader once the peer's half has landed
+    mbar_wait(&wbar, 0);
+    mbar_arrive_remote(mapa_shared(smem_u32(&wpeer), 0));
+  }
+  pdl_launch_dependents();
+  pdl_wait();
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer ----
+    if (elect_one()) {
+      prefetch_tmap(&tm_in);
+      int stage = 0;
+      uint32_t phase = 0;
+      SegIterP2 it(a, (int)rank);
+      Segment g;
+      while (it.next(a, g)) {
+        const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
+        for (int r = r0; r <= r1; ++r) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kInRowBytes);
+          tma_load_4d_to(sIn + stage * kInRowStride, &tm_in, mapa_shared(smem_u32(&full[stage]), 0), 0, g.x0 - 1,
+                         r, g.b);
+          if (++stage == kP2Stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (leader) ----
+    if (rank == 0) {
+      const uint64_t adesc0 = make_smem_desc(smem_u32(sIn), 0, 1024, kLayoutSW128);
+      const uint64_t bdesc0 = make_smem_desc(smem_u32(sW), 0, 1024, kLayoutSW128);
+      const bool leader = elect_one();
+      mbar_wait(&wbar, 0);
+      mbar_wait(&wpeer, 0);
+      int stage = 0;
+      uint32_t phase = 0, seq = 0;
+      SegIterP2 it(a, 0);
+      Segment g;
+      // one MMA op of the dy-range (d0, c) into TMEM column tcol
+      auto op = [&](uint64_t ad, int dx, int k, int d0, int c, uint32_t tcol, uint32_t acc, int coll) {
+        const int L = p2_layout(d0, c);
+        const uint64_t bd = bdesc0 + (uint64_t)((dx * kP2RowsDx * 128 + p2_row0(L) * 128 + k * 32) >> 4);
+        const uint32_t idesc = make_idesc(256, 64 * c, kFmtF16, kFmtF16);
+        if (coll == 1) mma2<1>(tmem + tcol, ad, bd, idesc, acc);
+        else if (coll == 3) mma2<3>(tmem + tcol, ad, bd, idesc, acc);
+        else mma2<0>(tmem + tcol, ad, bd, idesc, acc);
+      };
+      const uint32_t i64 = make_idesc(256, 64, kFmtF16, kFmtF16), i128 = make_idesc(256, 128, kFmtF16, kFmtF16),
+                     i192 = make_idesc(256, 192, kFmtF16, kFmtF16);
+      auto bdl = [&](int dx, int k, int L) {  // B descriptor of layout L, dx block, K step k
+        return bdesc0 + (uint64_t)((dx * kP2RowsDx * 128 + p2_row0(L) * 128 + k * 32) >> 4);
+      };
+      bool prewaited = false;
+      while (it.next(a, g)) {
+        const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
+        for (int r = r0; r <= r1; ++r) {
+          // ---- fast path: interior input row (targets r-1, r, r+1 in the
+          // segment; r+1 enters its slot): fixed op patterns per slot phase,
+          // split pieces share A through the collector, next row's barriers
+          // probed mid-row (as in the single-CTA kernel)
+          if (r >= 1 && r - 1 >= g.ya && r + 1 <= g.yb - 1) {
+            const uint32_t sq = seq + (uint32_t)(r - 1 - g.ya);
+            const uint32_t sl = sq & (kSlots - 1);
+            const bool next_fast = (r + 2 <= g.yb - 1);
+            const int nstage = (stage + 1 == kP2Stages) ? 0 : stage + 1;
+            const uint32_t nphase = (stage + 1 == kP2Stages) ? (phase ^ 1) : phase;
+            const uint32_t sq2 = sq + 3;
+            bool pre_ok = false;
+            if (leader) {
+              if (!prewaited)
+                mbar_wait2(&slot_empty[(sq + 2) & (kSlots - 1)], (((sq + 2) >> 3) & 1) ^ 1, &full[stage], phase);
+              tc_fence_after();
+              const uint64_t ad_row = adesc0 + (uint64_t)((stage * kInRowStride) >> 4);
+              const uint32_t t0 = tmem + sl * NB;
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
+                  const bool first = dx == 0 && k == 0;
+                  if (sl + 3 <= (uint32_t)kSlots) {
+                    if (first) {  // enter row r+1 (acc 0), keep r-1, r
+                      mma2<1>(t0 + 2 * NB, ad, bdl(dx, k, 5), i64, 0u);
+                      mma2<3>(t0, ad, bdl(dx, k, 1), i128, 1u);
+                    } else {
+                      mma2<0>(t0, ad, bdl(dx, k, 0), i192, 1u);
+                    }
+                  } else if (sl + 2 == (uint32_t)kSlots) {  // slots 6, 7 | wrap | 0
+                    mma2<1>(tmem, ad, bdl(dx, k, 5), i64, first ? 0u : 1u);
+                    mma2<3>(t0, ad, bdl(dx, k, 1), i128, 1u);
+                  } else {  // slot 7 | wrap | 0, 1
+                    mma2<1>(t0, ad, bdl(dx, k, 3), i64, 1u);
+                    if (first) {
+                      mma2<2>(tmem, ad, bdl(dx, k, 4), i64, 1u);
+                      mma2<3>(tmem + NB, ad, bdl(dx, k, 5), i64, 0u);
+                    } else {
+                      mma2<3>(tmem, ad, bdl(dx, k, 2), i128, 1u);
+                    }
+                  }
+                  if (((dx == 1 && k == 1) || (dx == 2 && k == 2)) && next_fast && !pre_ok)
+                    pre_ok = mbar_test(&slot_empty[sq2 & (kSlots - 1)], ((sq2 >> 3) & 1) ^ 1) &&
+                             mbar_test(&full[nstage], nphase);
+                }
+              commit2(&empty[stage]);
+              commit2(&slot_full[sl]);
+            }
+            __syncwarp();
+            prewaited = next_fast && pre_ok;
+            stage = nstage;
+            phase = nphase;
+            continue;
+          }
+          prewaited = false;
+          const int q_lo = max(r - 1, g.ya), q_hi = min(r + 1, g.yb - 1);
+          const int q_new = (r == 0) ? q_lo : r + 1;
+          for (int q = max(q_new, q_lo); q <= q_hi; ++q) {
+            const uint32_t sq = seq + (uint32_t)(q - g.ya);
+            mbar_wait(&slot_empty[sq & (kSlots - 1)], ((sq >> 3) & 1) ^ 1);
+          }
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (leader && q_lo <= q_hi) {
+            // target rows [q_lo, q_hi] -> consecutive slots, split at the ring
+            // wrap; rows >= q_new enter their slot on the first K step (acc 0)
+            const uint32_t s_lo = (seq + (uint32_t)(q_lo - g.ya)) & (kSlots - 1);
+            const int cnt = q_hi - q_lo + 1;
+            const int c0 = min(cnt, kSlots - (int)s_lo), c1 = cnt - c0;
+            const uint64_t ad_row = adesc0 + (uint64_t)((stage * kInRowStride) >> 4);
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
+                const bool first = dx == 0 && k == 0;
+                // pieces: [q_lo, q_lo + c0) at slot s_lo, [q_lo + c0, q_hi] at slot 0; on the
+                // first step each piece splits at q_new (old rows acc 1, new rows acc 0)
+                for (int piece = 0; piece < 2; ++piece) {
+                  const int pa = piece == 0 ? q_lo : q_lo + c0;
+                  const int pb = piece == 0 ? q_lo + c0 - 1 : q_hi;
+                  if (pa > pb) continue;
+                  const uint32_t pslot = piece == 0 ? s_lo : 0u;
+                  if (!first) {
+                    op(ad, dx, k, pa - (r - 1), pb - pa + 1, pslot * NB, 1u, 0);
+                  } else {
+                    const int ae = min(pb, q_new - 1), bb = max(pa, q_new);
+                    if (pa <= ae) op(ad, dx, k, pa - (r - 1), ae - pa + 1, pslot * NB, 1u, 0);
+                    if (bb <= pb) op(ad, dx, k, bb - (r - 1), pb - bb + 1, (pslot + (uint32_t)(bb - pa)) * NB, 0u, 0);
+                  }
+                }
+              }
+            commit2(&empty[stage]);
+            for (int q = q_lo; q <= q_hi; ++q)
+              if (min(q + 1, a.H - 1) == r) commit2(&slot_full[(seq + (uint32_t)(q - g.ya)) & (kSlots - 1)]);
+          } else if (leader) {
+            commit2(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == kP2Stages) { stage = 0; phase ^= 1; }
+        }
+        seq += (uint32_t)(g.yb - g.ya);
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (both CTAs) ----
+    const int ew = warp - 2;                   // 0 .. 4*kP2Groups-1
+    const uint32_t grp = (uint32_t)(ew >> 2);
+    const int quarter = warp & 3;
+    const int px = quarter * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+    const int stg = (int)(grp * 4) + quarter;
+    const uint32_t stage_out = smem_u32(sOut + stg * 4096);
+    const uint32_t shift_u = smem_u32(sShift);
+    if (lane == 0) prefetch_tmap(&tm_out);
+    uint32_t seq = 0, gsel = 0;
+    SegIterP2 it(a, (int)rank);
+    Segment g;
+    while (it.next(a, g)) {
+      for (int q = g.ya; q < g.yb; ++q, ++seq, gsel = (gsel + 1 == kP2Groups) ? 0 : gsel + 1) {
+        if (gsel != grp) continue;
+        const uint32_t slot = seq & (kSlots - 1);
+        mbar_wait(&slot_full[slot], (seq >> 3) & 1);
+        tc_fence_after();
+        uint32_t v[4][16];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tmem_ld16(tmem + lane_addr + slot * NB + j * 16, v[j]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) reg_fence16(v[j]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (rank == 0) mbar_arrive(&slot_empty[slot]);
+          else mbar_arrive_remote(mapa_shared(smem_u32(&slot_empty[slot]), 0));
+        }
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        const uint32_t rowp = stage_out + lane * 128;
+#pragma unroll
+        for (int chunk = 0; chunk < 8; ++chunk) {
+          const float4 s0 = ld_shared_f4(shift_u + chunk * 32);
+          const float4 s1 = ld_shared_f4(shift_u + chunk * 32 + 16);
+          const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+          uint32_t packed[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = chunk * 8 + e * 2;
+            const float2 fs = __fadd2_rn(make_float2(__uint_as_float(v[c >> 4][c & 15]),
+                                                     __uint_as_float(v[c >> 4][(c & 15) + 1])),
+                                         make_float2(sh[2 * e], sh[2 * e + 1]));
+            asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(packed[e]) : "f"(fs.y), "f"(fs.x));
+          }
+          st_shared_v4(rowp + ((chunk ^ (lane & 7)) << 4), packed[0], packed[1], packed[2], packed[3]);
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(&tm_out, sOut + stg * 4096, 0, g.x0 + quarter * 32, q, g.b);
+          bulk_commit();
+        }
+        (void)px;
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // remote arrivals and the leader's MMAs into the peer's TMEM are done
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+__global__ void pack_hidden_pair2_kernel(const float* __restrict__ w, const float* __restrict__ scale,
+                                         uint8_t* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*64 + ci
+  if (idx >= kC * kC) return;
+  const int co = idx / kC, ci = idx % kC;
+  float wv[9], rn[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) wv[t] = w[idx * 9 + t] * scale[co];
+  dc_round9(wv, rn);
+  for (int t = 0; t < 9; ++t) {
+    const int ky = t / 3, kx = t % 3;
+    const int n = (2 - ky) * 64 + co;  // row of [W(+1)|W(0)|W(-1)]
+    const __half v = __float2half_rn(rn[t]);
+    for (int L = 0; L < 6; ++L) {
+      const int d0 = L == 0 ? 0 : (L <= 2 ? L - 1 : L - 3), c = L == 0 ? 3 : (L <= 2 ? 2 : 1);
+      if (n < 64 * d0 || n >= 64 * (d0 + c)) continue;
+      const int local = n - 64 * d0, half = local / (32 * c), r = p2_row0(L) + local % (32 * c);
+      uint8_t* base = out + (size_t)half * kP2W + (size_t)kx * kP2RowsDx * 128;
+      *reinterpret_cast<__half*>(base + r * 128 + (((ci >> 3) ^ (r & 7)) << 4) + (ci & 7) * 2) = v;
+    }
+  }
+}
+
+size_t conv_pair2_wpack_bytes() { return 2 * (size_t)kP2W; }
+
+cudaError_t launch_pack_hidden_pair2(const float* w, const float* scale, uint8_t* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, 2 * (size_t)kP2W, st);
+  if (e != cudaSuccess) return e;
+  pack_hidden_pair2_kernel<<<(kC * kC + 127) / 128, 128, 0, st>>>(w, scale, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_pair2(const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a, int grid,
+                              cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(conv3x3_pair2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kP2Smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::max(2, grid & ~1));
+  cfg.blockDim = dim3(kP2Threads);
+  cfg.dynamicSmemBytes = kP2Smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, conv3x3_pair2_kernel, tm_in, tm_out, a);
+}
+
 }  // namespace tvs

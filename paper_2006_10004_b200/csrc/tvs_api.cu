@@ -114,6 +114,10 @@ struct tvs_plan {
   // producer's ~600 FFMA/px-row currently cost more than they save)
   bool unfused_conv0 = true;  // activation bytes per chunk (TVS_CHUNK_MB)
   int l2_hints = 0;           // TVS_L2_HINTS (ConvArgs::l2_hints)
+  // TVS_PAIR2=1: per-layer fast hidden layers on CTA pairs (cta_group::2,
+  // conv_tc.cu conv3x3_pair2_kernel; prototype, disables the layer stack)
+  bool pair2 = false;
+  uint8_t* wpack2 = nullptr;
   // K1 on tcgen05 (conv0_tc.cu, TF32 hi/lo split) for the fast path: config 2
   // 149 vs 170 us (reference conv0, K = 9) and 96 vs 212 us (the unshuffle = 2
   // variant's Conv2d(4, 64), K = 36).  TVS_CONV0_TC=0 selects the CUDA-core K1.
@@ -181,7 +185,7 @@ void free_all(tvs_plan* p) {
   p->recs.clear();
   p->event_pool.clear();
   void* ptrs[] = {p->wh, p->bh, p->wpack, p->hpack, p->whid, p->bhid, p->shid, p->act[0], p->act[1], p->dx,
-                  p->w0u, p->b0u, p->rowcnt, p->items, p->c0pack, p->c0bias};
+                  p->w0u, p->b0u, p->rowcnt, p->items, p->c0pack, p->c0bias, p->wpack2};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -306,7 +310,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
   // layer stack (FAST path): every CTA of the persistent grid must be resident
   // at once, so only on the full device grid of the single-stream path
   bool stack = false;
-  if (fast && p->stack != 0 && p->unfused_conv0 && !p->pair_fuse && max_ctas >= p->num_sms) {
+  if (fast && p->stack != 0 && p->unfused_conv0 && !p->pair_fuse && !p->pair2 && max_ctas >= p->num_sms) {
     const int us0 = p->unshuffle;
     const long long items = (long long)B * ((W / us0 + tvs::kStripPx - 1) / tvs::kStripPx) * p->n_hidden();
     // auto: enough items per SM, and a last round that is nearly full (the
@@ -490,10 +494,19 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.nsub = p->l2_reverse_sub;
       a.l2_hints = p->l2_hints;
       if (const char* e = std::getenv("TVS_CONV_DBG")) a.dbg = std::atoi(e);
-      timed_launch(p, st, TVS_KIND_HIDDEN, pxg * 2.0 * 9 * 64 * 64 + (first ? pxg * 2.0 * 9 * 64 : 0.0), [&] {
-        return tvs::launch_conv_tc(first ? 2 : 0, in_map[cur], out_map[cur ^ 1], a, first ? &p->conv0 : nullptr,
-                                   grid, st);
-      });
+      const bool use_pair2 = p->pair2 && !first && strips % 2 == 0 && p->wpack2;
+      if (use_pair2) {
+        a.wpack = p->wpack2 + (size_t)l * tvs::conv_pair2_wpack_bytes();
+        const long long tp = (long long)B * (strips / 2) * Hg;
+        const int grid2 = 2 * (int)std::max(1LL, std::min<long long>(max_ctas / 2, (tp + 2) / 3));
+        timed_launch(p, st, TVS_KIND_HIDDEN, pxg * 2.0 * 9 * 64 * 64,
+                     [&] { return tvs::launch_conv_pair2(in_map[cur], out_map[cur ^ 1], a, grid2, st); });
+      } else {
+        timed_launch(p, st, TVS_KIND_HIDDEN, pxg * 2.0 * 9 * 64 * 64 + (first ? pxg * 2.0 * 9 * 64 : 0.0), [&] {
+          return tvs::launch_conv_tc(first ? 2 : 0, in_map[cur], out_map[cur ^ 1], a, first ? &p->conv0 : nullptr,
+                                     grid, st);
+        });
+      }
       cur ^= 1;
     }
     tvs::ConvArgs a = geom(row0 / us, rows / us);
@@ -630,6 +643,7 @@ int tvs_plan_create_ex(int device, int depth, int channels, int out_bands, int m
     if (const char* e = std::getenv("TVS_FUSE_CONV0")) p->unfused_conv0 = std::atoi(e) == 0;
     if (const char* e = std::getenv("TVS_FP32_CUDA")) p->fp32_split = std::atoi(e) == 0;
     if (const char* e = std::getenv("TVS_L2_HINTS")) p->l2_hints = std::atoi(e);
+    if (const char* e = std::getenv("TVS_PAIR2")) p->pair2 = std::atoi(e) != 0;
     if (const char* e = std::getenv("TVS_CONV0_TC")) p->conv0_tc = std::atoi(e);
     if (const char* e = std::getenv("TVS_PAIR")) p->pair_fuse = std::atoi(e) != 0;
     if (const char* e = std::getenv("TVS_STACK")) p->stack = std::atoi(e);
@@ -712,6 +726,11 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
       if (p->tc_path()) {
         TVS_CUDA(tvs::launch_pack_hidden_f16(w_dev[l + 1], dst_scale,
                                              p->wpack + (size_t)l * tvs::conv_wpack_bytes(false), st));
+        if (p->pair2 && p->unshuffle == 1) {
+          if (!p->wpack2) TVS_CUDA(cudaMalloc(&p->wpack2, (size_t)nh * tvs::conv_pair2_wpack_bytes()));
+          TVS_CUDA(tvs::launch_pack_hidden_pair2(w_dev[l + 1], dst_scale,
+                                                 p->wpack2 + (size_t)l * tvs::conv_pair2_wpack_bytes(), st));
+        }
       } else if (p->split_path()) {
         TVS_CUDA(tvs::launch_pack_hidden_split(w_dev[l + 1], dst_scale,
                                                p->wpack + (size_t)l * tvs::conv_wpack_split_bytes(), st));

@@ -427,3 +427,25 @@ def test_conv0_tcgen05_ragged(seeded_state, oracle, shape):
     with torch.no_grad():
         ref = oracle(torch.from_numpy(x)).numpy()
     _check(m, x, ref)
+
+
+@pytest.mark.parametrize("shape", [(2, 1, 48, 160), (3, 1, 64, 256), (1, 1, 5, 130), (2, 1, 1, 512)])
+def test_cta_pair_prototype_bitwise(seeded_state, shape):
+    """TVS_PAIR2=1 (CTA-pair hidden layers, cta_group::2 with M=256 and the B
+    operand split across the pair) gives bitwise the single-CTA result: every
+    output pixel sees the same MMA sequence."""
+    outs = []
+    for env in ("0", "1"):
+        os.environ["TVS_PAIR2"] = env
+        os.environ["TVS_STACK"] = "0"
+        try:
+            m = TVSpecNet().eval()
+            m.load_state_dict(seeded_state)
+            m._plan_for(torch.device("cuda", 0))
+        finally:
+            os.environ.pop("TVS_PAIR2")
+            os.environ.pop("TVS_STACK")
+        outs.append(m)
+    x = torch.rand(*shape, generator=torch.Generator().manual_seed(shape[2])).cuda()
+    with torch.no_grad():
+        assert torch.equal(outs[0](x), outs[1](x))
