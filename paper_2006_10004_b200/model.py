@@ -334,8 +334,12 @@ class TVSpecNet(nn.Module):
                 pipes[idx] = pipe
             h2d, d2h = pipe["h2d"], pipe["d2h"]
             xbuf, bbuf, cbuf = pipe["xbuf"], pipe["bbuf"], pipe["cbuf"]
-            x_free = [torch.cuda.Event() for _ in range(2)]
-            b_free = [torch.cuda.Event() for _ in range(2)]
+            # events are reused across calls (every call ends synchronized)
+            evs = pipe.setdefault("events", [])
+            need = 4 + 2 * len(bounds)
+            while len(evs) < need:
+                evs.append(torch.cuda.Event())
+            x_free, b_free = evs[0:2], evs[2:4]
             for ev in x_free + b_free:
                 ev.record(comp)
             for i, (s, e) in enumerate(bounds):
@@ -343,13 +347,13 @@ class TVSpecNet(nn.Module):
                 h2d.wait_event(x_free[j])
                 with torch.cuda.stream(h2d):
                     xbuf[j][:nb].copy_(x_pin[s:e], non_blocking=True)
-                landed = torch.cuda.Event()
+                landed = evs[4 + 2 * i]
                 landed.record(h2d)
                 comp.wait_event(landed)
                 comp.wait_event(b_free[j])
                 plan.forward(xbuf[j].data_ptr(), bbuf[j].data_ptr(), cbuf[j].data_ptr() if closure else 0,
                              nb, H, W, row0, nrows, comp.cuda_stream)
-                done = torch.cuda.Event()
+                done = evs[5 + 2 * i]
                 done.record(comp)
                 x_free[j].record(comp)
                 d2h.wait_event(done)
