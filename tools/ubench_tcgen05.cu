@@ -9,6 +9,8 @@
 //      collector::a reuse.
 //
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I.. ubench_tcgen05.cu
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cstdio>
 #include <cstdlib>
@@ -101,9 +103,12 @@ __device__ __forceinline__ void bulk_store_g(void* gdst, uint32_t ssrc, uint32_t
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc), "r"(bytes)
                : "memory");
 }
+// 19: as 18 but the stores are TMA TENSOR stores (4D map, 32-px x 64-ch SW128
+// boxes from an swizzled staging tile, as the conv epilogue issues them), and
+// warps 2-3 also write the staging tiles with st.shared
 template <int V>
 __global__ void __launch_bounds__(128, 1)
-k_rate(int iters, long long* cycles, int* err, uint8_t* gbuf) {
+k_rate(int iters, long long* cycles, int* err, uint8_t* gbuf, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
@@ -224,11 +229,19 @@ k_rate(int iters, long long* cycles, int* err, uint8_t* gbuf) {
           bulk_wait_read<0>();
           n += 8192;
         }
+        if constexpr (V == 19) {  // two 4 KB tensor-store boxes per 8 KB buffer
+          const int row = (int)((blockIdx.x * 4 + ln) * 64 + (i % 64)) % 4096;
+          tma_store_4d(&tmap, buf, 0, 0, row, 0);
+          tma_store_4d(&tmap, buf + 4096, 0, 32, row, 0);
+          bulk_commit();
+          bulk_wait_read<0>();
+          n += 8192;
+        }
       }
       bulk_wait<0>();
       moved[ln] = n;
     }
-    if constexpr (V == 18) {
+    if constexpr (V == 18 || V == 19) {
       if (warp >= 2) {
         uint4* region = reinterpret_cast<uint4*>(smem + 104 * 1024) + (warp - 2) * 32 * 4;
         const uint4 v = make_uint4(tid, 1, 2, 3);
@@ -357,15 +370,30 @@ static void run_rate(const char* name, int ctas, double macs_per_iter) {
   CK(cudaMalloc(&dC, 2 * ctas * sizeof(long long))); CK(cudaMalloc(&dErr, 4)); CK(cudaMemset(dErr, 0, 4));
   CK(cudaMemset(dC, 0, 2 * ctas * sizeof(long long)));
   static uint8_t* gbuf = nullptr;
-  if (!gbuf) CK(cudaMalloc(&gbuf, (size_t)2 * 16384 * 8192));
+  static CUtensorMap tmap;
+  if (!gbuf) {
+    CK(cudaMalloc(&gbuf, (size_t)2 * 16384 * 8192));
+    void* fnp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q));
+    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fnp);
+    // [1][4096 rows][64 px][64 ch] fp16, box {64 ch, 32 px, 1, 1}, SW128 (the conv epilogue's store)
+    cuuint64_t dims[4] = {64, 64, 4096, 1};
+    cuuint64_t strides[3] = {128, 64 * 128, (cuuint64_t)4096 * 64 * 128};
+    cuuint32_t box[4] = {64, 32, 1, 1}, estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, gbuf + (size_t)16384 * 8192, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { printf("tensor map encode failed %d\n", (int)r); exit(1); }
+  }
   const int smem = (V >= 16 ? 144 : 112) * 1024 + 1024;
   CK(cudaFuncSetAttribute(k_rate<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int iters = 4096;
-  k_rate<V><<<ctas, 128, smem>>>(64, dC, dErr, gbuf);  // warm
+  k_rate<V><<<ctas, 128, smem>>>(64, dC, dErr, gbuf, tmap);  // warm
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  k_rate<V><<<ctas, 128, smem>>>(iters, dC, dErr, gbuf);
+  k_rate<V><<<ctas, 128, smem>>>(iters, dC, dErr, gbuf, tmap);
   cudaEventRecord(e1);
   CK(cudaDeviceSynchronize());
   float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -411,6 +439,7 @@ int main(int argc, char** argv) {
     run_rate<16>("N192 conv + bulk loads", ctas, 128.0 * 192 * 64);
     run_rate<17>("N192 conv + bulk stores", ctas, 128.0 * 192 * 64);
     run_rate<18>("N192 conv + loads+stores+STS", ctas, 128.0 * 192 * 64);
+    run_rate<19>("N192 conv + TMA tensor st+STS", ctas, 128.0 * 192 * 64);
   }
   printf("DONE\n");
   return 0;
