@@ -136,7 +136,8 @@ struct ItemIter {
 __device__ int g_stack_err;  // set when a row-flag wait times out (results invalid, no hang)
 // TVS_CONV_DBG bit 15 (layer stack): MMA-issuer cycle accounting (sum over CTAs): [0] total,
 // [1] waiting for a free accumulator slot, [2] waiting for the input row,
-// [3] waiting for a layer's weights, [4] general-path rows, [5] fast-path rows
+// [3] waiting for a layer's weights, [4] general-path rows, [5] fast-path rows,
+// [6] elapsed ns (globaltimer), so [0] / [6] is the mean SM clock in GHz
 __device__ unsigned long long g_dbg_cycles[8];
 
 // Producer side of the layer stack: input row r of a layer-j item (j >= 1) is
@@ -501,8 +502,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const uint64_t bdesc0 = make_smem_desc(smem_u32(sW), 0, 1024, kLayoutSW128);
     const bool leader = elect_one();
     const bool domma = !(a.dbg & 64);  // ablation (TVS_CONV_DBG): no MMAs
-    unsigned long long cyc[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long cyc[7] = {0, 0, 0, 0, 0, 0, 0};
     const long long tstart = clock64();
+    unsigned long long gstart = 0;
+    if (Cfg::kStack && (a.dbg & 32768)) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gstart));
     mbar_wait(&wbar, 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -707,7 +710,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     }
     if (Cfg::kStack && (a.dbg & 32768) && leader) {
       cyc[0] = clock64() - tstart;
-      for (int i = 0; i < 6; ++i) atomicAdd(&g_dbg_cycles[i], cyc[i]);
+      unsigned long long gend;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gend));
+      cyc[6] = gend - gstart;  // ns: cyc[0] / cyc[6] = the SM clock in GHz
+      for (int i = 0; i < 7; ++i) atomicAdd(&g_dbg_cycles[i], cyc[i]);
     }
   } else {
     // ------------------------------------------------ epilogue ----

@@ -17,6 +17,7 @@ lib.tvs_debug_cycles.restype = ctypes.c_int
 lib.tvs_debug_cycles.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+extra = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # more TVS_CONV_DBG bits (ablations)
 for stack in ("1",):  # the accounting is compiled into the layer-stack kernel only
     os.environ["TVS_STACK"] = stack
     m = TVSpecNet().eval()
@@ -30,13 +31,14 @@ for stack in ("1",):  # the accounting is compiled into the layer-stack kernel o
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * 8)()
     lib.tvs_debug_cycles(buf, 1)
-    os.environ["TVS_CONV_DBG"] = "32768"
+    os.environ["TVS_CONV_DBG"] = str(32768 | extra)
     with torch.no_grad():
         m(x)
     torch.cuda.synchronize()
     os.environ.pop("TVS_CONV_DBG")
     lib.tvs_debug_cycles(buf, 1)
     tot = buf[0] or 1
-    print(f"stack={stack} config {cfg} x{n}: total {tot / 1e9:.3f} Gcyc (sum over CTAs); "
+    print(f"stack={stack} dbg+{extra} config {cfg} x{n}: total {tot / 1e9:.3f} Gcyc (sum over CTAs); "
           f"slot wait {buf[1] / tot * 100:.1f}%, input-row wait {buf[2] / tot * 100:.1f}%, "
-          f"weights wait {buf[3] / tot * 100:.1f}%, rows general {buf[4]}, fast {buf[5]}", flush=True)
+          f"weights wait {buf[3] / tot * 100:.1f}%, rows general {buf[4]}, fast {buf[5]}, "
+          f"SM clock {buf[0] / max(1, buf[6]):.3f} GHz", flush=True)
