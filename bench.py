@@ -99,16 +99,15 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def _kernel_name(tc, launches, depth, hidden_per_fwd=None):
+def _kernel_name(tc, used_stack, depth):
     """The dominant kernel: the layer-stack launch (all hidden layers, conv_tc.cu
-    mode 8) when each batch chunk took 3 launches (conv0, stack, head), else the
-    per-layer hidden conv; the 128-channel wide variant runs conv_tc.cu modes 5
-    (pair input) / 9 (single)."""
+    mode 8) when the forward ran it, else the per-layer hidden conv; the
+    128-channel wide variant runs conv_tc.cu modes 5 (pair input) / 11 (single)."""
     if tc == "wide":
         return "conv3x3_tc_kernel<5>/<11> (wide hidden layers, 128 ch: pair input on quarters, single on halves)"
     if not tc:
         return "hidden_f32_kernel"
-    if launches == 3 or (hidden_per_fwd is not None and abs(hidden_per_fwd * 3 - launches) < 1e-6):
+    if used_stack:
         return f"conv3x3_tc_kernel<8> (layer stack: {depth - 2} hidden layers per launch)"
     return "conv3x3_tc_kernel<0> (hidden layer)"
 
@@ -141,12 +140,12 @@ def tc_stack_probe(plan, step):
     buf = (ctypes.c_ulonglong * 8)()
     torch.cuda.synchronize()
     lib.tvs_debug_cycles(buf, 1)
-    os.environ["TVS_CONV_DBG"] = "32768"
+    plan.set_option("debug", 32768)  # MMA-issuer cycle accounting (conv_tc.cu)
     try:
         step()
         torch.cuda.synchronize()
     finally:
-        os.environ.pop("TVS_CONV_DBG", None)
+        plan.set_option("debug", 0)
     lib.tvs_debug_cycles(buf, 1)
     if buf[6] == 0:
         return False
@@ -233,10 +232,12 @@ def _flush_l2(buf):
     buf.add_(1.0)
 
 
-def time_steps(fn, steps, warmup, flush):
+def time_steps(fn, steps, warmup, flush, reset=None):
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
+    if reset is not None:
+        reset()
     st = torch.cuda.current_stream()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for a, b in evs:
@@ -300,15 +301,17 @@ def run_ours(args, spec):
             model = TVSpecNet(spec.depth, spec.channels, 5, unshuffle=2).eval()
             model.load_state_dict(build_seeded_state(spec.depth, spec.channels, 5, unshuffle=2))
         else:
-            model = TVSpecNet(spec.depth, spec.channels, 5,
-                              precision="fp32" if prec == "fp32cuda" else prec).eval()
+            model = TVSpecNet(spec.depth, spec.channels, 5, precision="fp32" if prec == "fp32cuda" else prec,
+                              options={"fp32_cuda": 1} if prec == "fp32cuda" else None).eval()
             model.load_state_dict(state)
         bands = torch.empty((B, 5, nrows, W), device=dev)
         clos = torch.empty((B, 1, nrows, W), device=dev)
-        if prec == "fp32cuda":  # the CUDA-core fp32 kernels (read at plan creation)
-            os.environ["TVS_FP32_CUDA"] = "1"
         plan = model._plan_for(dev)
-        os.environ.pop("TVS_FP32_CUDA", None)
+        # timed steps: status words checked once at the end (deferred) instead
+        # of a host synchronisation per forward; hidden-layer kernels record
+        # their own device spans (tvs_profile_span) for the roofline
+        plan.set_option("check", 2)
+        plan.set_option("span", 1)
 
         def step():
             plan.forward(x.data_ptr(), bands.data_ptr(), clos.data_ptr(), B, H, W, row0, nrows,
@@ -324,8 +327,14 @@ def run_ours(args, spec):
             dist.barrier()
         torch.cuda.synchronize()
         with ClockSampler(local) as clk:
-            ms = time_steps(step, steps, warm, flush)
+            plan.profile_span(reset=True)  # drops the warm-up launches inside time_steps below
+            ms = time_steps(step, steps, warm, flush, reset=lambda: plan.profile_span(reset=True))
+        span_ms, span_n = plan.profile_span(reset=True)
+        plan.sync(torch.cuda.current_stream().cuda_stream)  # raises if any timed forward failed
+        plan.set_option("check", 1)
+        plan.set_option("span", 0)
         launches = plan.last_launch_count()
+        used_stack = plan.last_used_stack()
         tot_ms = sum(ms)
         if world > 1:
             t = torch.tensor([tot_ms], device=dev)
@@ -333,17 +342,13 @@ def run_ours(args, spec):
             tot_ms = float(t.item())
         value = total_px * steps / 1e6 / (tot_ms / 1e3)
 
-        # live per-kernel timing of the dominant kernel (hidden conv), separate pass
+        # algorithmic FLOPs of one hidden-layer launch (per-kernel accounting of the plan)
         plan.profile_enable(True)
-        prof_steps = max(1, min(steps, 3))
-        for _ in range(prof_steps):
-            _flush_l2(flush)
-            step()
+        step()
         torch.cuda.synchronize()
-        hid_ms, hid_n, hid_flops = plan.profile_read(1)
-        c0_ms, _, _ = plan.profile_read(0)
-        hd_ms, _, _ = plan.profile_read(2)
+        _, hid_n1, hid_flops1 = plan.profile_read(1)
         plan.profile_enable(False)
+        hid_flops = hid_flops1 / max(1, hid_n1) * span_n
 
         # the SM clock the layer-stack kernel actually ran at (clock64 cycles
         # over globaltimer ns in its MMA thread, TVS_CONV_DBG bit 15): the
@@ -375,8 +380,8 @@ def run_ours(args, spec):
             e2e_s = float(t.item())
         e2e_px = ne * nrows * W * (world if _scaling(spec) == "weak" or band is not None else world)
         results[prec] = dict(value=value, ms=tot_ms / steps, ms_list=ms, launches=launches, steps=steps,
-                             warmup=warm, clocks=clk.summary(), hid_ms=hid_ms, hid_n=hid_n, hid_flops=hid_flops,
-                             c0_ms=c0_ms, hd_ms=hd_ms, e2e=e2e_px / 1e6 / e2e_s, hid_per_fwd=hid_n / prof_steps,
+                             warmup=warm, clocks=clk.summary(), hid_ms=span_ms, hid_n=span_n, hid_flops=hid_flops,
+                             e2e=e2e_px / 1e6 / e2e_s, hid_per_fwd=span_n / steps, used_stack=used_stack,
                              in_kernel_mhz=in_kernel_mhz,
                              e2e_bytes=(xe.numel() * 4, out_host.numel() * 4), e2e_images=ne)
         del model, plan, bands, clos
@@ -420,14 +425,18 @@ def run_ours(args, spec):
         "latency_ms": round(step_ms, 4) if spec.batch == 1 else None,
         "tflops_algorithmic": round(f["value"] * 1e6 * fpx / 1e12 / world, 2),
         "frac_of_bf16_peak": round(f["value"] * 1e6 * fpx / 1e12 / world / peak_tf, 4),
-        "roofline": {"bound": "tensor", "kernel": _kernel_name(tc, f["launches"], spec.depth, f["hid_per_fwd"]),
+        "roofline": {"bound": "tensor", "kernel": _kernel_name(tc, f["used_stack"], spec.depth),
                      "achieved": round(hid_tflops, 2), "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": round(hid_tflops / peak_tf, 4), "peak_kind": f"{peak_kind} bf16 burst",
                      "frac_of_sustained": round(hid_tflops / peak_sus, 4) if peak_sus else None,
                      "avg_launch_ms": round(hid_avg_ms, 5), "launches_timed": f["hid_n"],
+                     "launch_timing": "in-kernel globaltimer span of each launch inside the timed steps "
+                                      "(first CTA past its PDL wait to last CTA exit; tvs_profile_span)",
                      "flop_per_launch": f["hid_flops"] / max(1, f["hid_n"]),
-                     "share_of_step": round(f["hid_ms"] / max(1e-9, f["hid_ms"] + f["c0_ms"] + f["hd_ms"]), 4),
-                     "traffic": _traffic(spec, _kernel_name(tc, f["launches"], spec.depth, f["hid_per_fwd"])), "traffic_unit": "bytes per launch (ncu dram read+write)",
+                     "share_of_step": round(f["hid_ms"] / max(1e-9, step_ms * f["steps"]), 4),
+                     "whole_forward_frac": round(f["value"] * 1e6 * fpx / 1e12 / world / peak_tf, 4),
+                     "traffic": _traffic(spec, _kernel_name(tc, f["used_stack"], spec.depth)),
+                     "traffic_unit": "bytes per launch (ncu dram read+write)",
                      "algorithmic_bytes_per_launch": int(B * H * W * alg_bytes_px)},
         "gpu_launches": f["launches"] * f["steps"],
         "e2e": {"value": round(f["e2e"], 3), "unit": UNIT, "h2d_bytes_per_step": f["e2e_bytes"][0],

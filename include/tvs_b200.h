@@ -10,6 +10,7 @@
  *   tvs_forward           <- TVSpecNet.forward(x) -> (B, out_bands, H, W)      model.py:49-52
  *                            (+ optional closure plane image - sum(bands),     inference.py:34-42)
  *   tvs_forward_host      <- predict_bands(model, image) with CPU in/out       inference.py:25-32
+ *   tvs_plan_sync         <- the point where the reference's synchronous forward has returned
  *   tvs_plan_destroy      <- module teardown
  *
  * Conventions: every function returns 0 on success or a negative TVS_E_*
@@ -27,7 +28,7 @@
 extern "C" {
 #endif
 
-#define TVS_ABI_VERSION 1
+#define TVS_ABI_VERSION 2
 
 /* status codes */
 #define TVS_OK 0
@@ -35,6 +36,7 @@ extern "C" {
 #define TVS_E_UNSUPPORTED (-2) /* valid model, configuration not built (e.g. channels != 64) */
 #define TVS_E_CUDA (-3)        /* CUDA runtime/driver failure */
 #define TVS_E_STATE (-4)       /* forward before set_weights, etc. */
+#define TVS_E_NUMERIC (-5)     /* a finite input produced non-finite bands (fp16-range overflow) */
 
 /* numerics modes */
 #define TVS_MODE_FP32 0 /* fp32-accurate (<= 1e-5): split fp16 hi/lo operands on tcgen05 */
@@ -71,10 +73,34 @@ int tvs_plan_create_ex(int device, int depth, int channels, int out_bands, int m
 int tvs_plan_set_weights(tvs_plan* plan, const float* const* w_dev, const float* const* scale_dev,
                          const float* const* shift_dev, int n_layers, void* stream);
 
+/* Plan options; unknown names or bad values -> TVS_E_INVALID.
+ *   "check"        1 (default): tvs_forward verifies the forward's status words
+ *                  before returning (it synchronises `stream`) and returns
+ *                  TVS_E_CUDA / TVS_E_NUMERIC instead of invalid output.
+ *                  2: deferred - the status is evaluated by a later tvs_forward
+ *                  or tvs_plan_sync (async callers).  0: unchecked.
+ *   "stack"        -1 auto / 0 / 1: the all-hidden-layers-in-one-launch kernel
+ *   "watchdog_ms"  layer-stack row-flag wait limit (default 2000)
+ *   "input_scale"  1 (default): per-image power-of-two activation scale that
+ *                  keeps the fp16-range formats finite for any input magnitude
+ *   "span" (see tvs_profile_span), "conv0_tc", "chunk_mb", "debug"; and, applied by the next
+ *   tvs_plan_set_weights: "fp32_cuda", "wide_cuda", "wide_pair_layers",
+ *   "wide_halves". */
+int tvs_plan_set_option(tvs_plan* plan, const char* name, long long value);
+
+/* Synchronise `stream` and evaluate every outstanding (deferred) status:
+ * returns the first failure of a forward since the last sync. */
+int tvs_plan_sync(tvs_plan* plan, void* stream);
+
 /* x: (B,1,H,W) fp32 NCHW; bands: (B,out_bands,valid_rows,W) fp32 receiving
  * rows [valid_row0, valid_row0+valid_rows) of the full forward; closure (may
  * be NULL): (B,1,valid_rows,W) = x - sum_k bands_k.  valid_rows < 0 means all
- * H rows.  All device pointers, 16-byte aligned. */
+ * H rows.  All device pointers, 16-byte aligned.  With the default "check"
+ * option the call returns once the forward has completed and either the
+ * output is valid (TVS_OK) or an error is returned: a layer-stack watchdog
+ * expiry (TVS_E_CUDA; the next forward is unaffected) or non-finite bands from
+ * a finite input (TVS_E_NUMERIC).  Non-finite inputs propagate as in the
+ * reference's fp32 forward. */
 int tvs_forward(tvs_plan* plan, const float* x, float* bands, float* closure_or_null, int B, int H, int W,
                 int valid_row0, int valid_rows, void* stream);
 
@@ -83,8 +109,10 @@ int tvs_forward(tvs_plan* plan, const float* x, float* bands, float* closure_or_
 int tvs_forward_host(tvs_plan* plan, const float* x_host, float* bands_host, float* closure_host_or_null, int B,
                      int H, int W, void* stream);
 
-/* Number of kernels the last tvs_forward launched (for launch accounting). */
+/* Number of kernels the last tvs_forward launched (for launch accounting),
+ * and whether it ran the layer-stack kernel. */
 int tvs_last_launch_count(const tvs_plan* plan);
+int tvs_last_used_stack(const tvs_plan* plan);
 
 /* Per-kernel CUDA-event timing on the forward's stream (off by default).
  * kind: 0 = conv0 (K1), 1 = hidden conv (K2), 2 = head + closure (K3).
@@ -96,6 +124,13 @@ int tvs_last_launch_count(const tvs_plan* plan);
 #define TVS_KIND_HEAD 2
 int tvs_profile_enable(tvs_plan* plan, int on);
 int tvs_profile_read(tvs_plan* plan, int kind, double* total_ms, long long* launches, double* flops);
+
+/* With plan option "span" = 1, every hidden-layer kernel launch (the layer
+ * stack, or each per-layer conv) records its device duration from inside the
+ * kernel: globaltimer from the first CTA past its PDL wait to the last CTA's
+ * exit, so measuring does not perturb the launch overlap.  Returns the summed
+ * milliseconds and launch count since the last reset (synchronises the device). */
+int tvs_profile_span(tvs_plan* plan, double* total_ms, long long* launches, int reset);
 
 int tvs_plan_destroy(tvs_plan* plan);
 

@@ -17,6 +17,7 @@ TVS_E_INVALID = -1
 TVS_E_UNSUPPORTED = -2
 TVS_E_CUDA = -3
 TVS_E_STATE = -4
+TVS_E_NUMERIC = -5
 
 MODE_FP32 = 0
 MODE_FAST = 1
@@ -27,11 +28,15 @@ EXPORTS = (
     "tvs_plan_create",
     "tvs_plan_create_ex",
     "tvs_plan_set_weights",
+    "tvs_plan_set_option",
+    "tvs_plan_sync",
     "tvs_forward",
     "tvs_forward_host",
     "tvs_last_launch_count",
+    "tvs_last_used_stack",
     "tvs_profile_enable",
     "tvs_profile_read",
+    "tvs_profile_span",
     "tvs_plan_destroy",
     "tvs_band_stats",
     "tvs_tvflow_workspace_bytes",
@@ -72,6 +77,12 @@ def load() -> ctypes.CDLL:
         lib.tvs_plan_create_ex.argtypes = [i, i, i, i, i, i, ctypes.POINTER(P)]
         lib.tvs_plan_set_weights.restype = i
         lib.tvs_plan_set_weights.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), i, P]
+        lib.tvs_plan_set_option.restype = i
+        lib.tvs_plan_set_option.argtypes = [P, ctypes.c_char_p, ctypes.c_longlong]
+        lib.tvs_plan_sync.restype = i
+        lib.tvs_plan_sync.argtypes = [P, P]
+        lib.tvs_last_used_stack.restype = i
+        lib.tvs_last_used_stack.argtypes = [P]
         lib.tvs_forward.restype = i
         lib.tvs_forward.argtypes = [P, P, P, P, i, i, i, i, i, P]
         lib.tvs_forward_host.restype = i
@@ -83,6 +94,8 @@ def load() -> ctypes.CDLL:
         lib.tvs_profile_read.restype = i
         lib.tvs_profile_read.argtypes = [P, i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong),
                                          ctypes.POINTER(ctypes.c_double)]
+        lib.tvs_profile_span.restype = i
+        lib.tvs_profile_span.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong), i]
         lib.tvs_band_stats.restype = i
         lib.tvs_band_stats.argtypes = [P, P, i, i, i, P, P, P]
         lib.tvs_tvflow_workspace_bytes.restype = ctypes.c_size_t
@@ -101,6 +114,8 @@ def check(code: int) -> None:
         msg = load().tvs_last_error().decode(errors="replace")
         if code == TVS_E_INVALID:
             raise ValueError(msg)
+        if code == TVS_E_NUMERIC:
+            raise FloatingPointError(f"libtvsb200: {msg}")
         raise TVSError(code, msg)
 
 
@@ -122,6 +137,17 @@ class Plan:
         S = (ctypes.c_void_p * n)(*[p or None for p in scale_ptrs])
         Bv = (ctypes.c_void_p * n)(*shift_ptrs)
         check(self.lib.tvs_plan_set_weights(self.handle, W, S, Bv, n, ctypes.c_void_p(stream)))
+
+    def set_option(self, name: str, value: int) -> None:
+        """Plan option (include/tvs_b200.h tvs_plan_set_option)."""
+        check(self.lib.tvs_plan_set_option(self.handle, name.encode(), int(value)))
+
+    def sync(self, stream: int) -> None:
+        """Synchronise `stream` and raise any deferred forward failure."""
+        check(self.lib.tvs_plan_sync(self.handle, ctypes.c_void_p(stream)))
+
+    def last_used_stack(self) -> bool:
+        return bool(self.lib.tvs_last_used_stack(self.handle))
 
     def forward(self, x_ptr, bands_ptr, closure_ptr, B, H, W, row0, rows, stream: int) -> None:
         check(
@@ -151,6 +177,13 @@ class Plan:
         ms, n, fl = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_double()
         check(self.lib.tvs_profile_read(self.handle, kind, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(fl)))
         return ms.value, n.value, fl.value
+
+    def profile_span(self, reset: bool = True) -> tuple[float, int]:
+        """(device ms, launches) of the hidden-layer kernels since the last
+        reset, measured inside the kernels (plan option "span")."""
+        ms, n = ctypes.c_double(), ctypes.c_longlong()
+        check(self.lib.tvs_profile_span(self.handle, ctypes.byref(ms), ctypes.byref(n), 1 if reset else 0))
+        return ms.value, n.value
 
     def close(self) -> None:
         if self.handle and self.handle.value:

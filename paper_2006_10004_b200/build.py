@@ -17,7 +17,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtvsb200.so"
-SOURCES = ["tvs_api.cu", "conv_tc.cu", "conv0_tc.cu", "conv_edge.cu", "metrics.cu", "tvflow.cu", "conv_pair.cu"]
+SOURCES = ["tvs_api.cu", "conv_tc.cu", "conv0_tc.cu", "conv_edge.cu", "metrics.cu", "tvflow.cu"]
 HEADERS = ["common.cuh", "sm100.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

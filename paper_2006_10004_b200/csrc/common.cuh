@@ -4,8 +4,23 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <mutex>
 
 namespace tvs {
+
+// Kernel attributes (max dynamic smem, cluster sizes) belong to a device
+// context: run `f` once per device ordinal, thread-safely.
+template <typename F>
+cudaError_t once_per_device(std::mutex& mu, uint64_t& done_mask, F&& f) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && ((done_mask >> dev) & 1ull)) return cudaSuccess;
+  e = f();
+  if (e == cudaSuccess && dev < 64) done_mask |= 1ull << dev;
+  return e;
+}
 
 constexpr int kC = 64;            // hidden feature maps (ARCH_SPEC["channels"], model.py:19-26)
 constexpr int kStripPx = 128;     // output pixels per strip = tcgen05 M
@@ -30,11 +45,22 @@ constexpr int kEpiGroupsPlain = TVS_EPI_GROUPS_PLAIN;  // modes 0 / 8
 constexpr int kStagesPlain = TVS_STAGES_PLAIN;
 static_assert(kStagesPlain <= kStages, "barrier arrays are sized by kStages");
 
+// Device-side duration of a kernel's launches (plan option "span"): every CTA
+// takes the globaltimer after its PDL wait (so spans of dependent launches on
+// one stream never overlap) and at exit; the last CTA to exit adds the launch's
+// [first start, last end] to total_ns and re-arms the record.
+struct KernelSpan {
+  unsigned long long start;  // ~0 when armed
+  unsigned long long end;
+  unsigned long long total_ns;
+  unsigned long long launches;
+  unsigned int done;
+};
+
 struct ConvArgs {
   int B, H, W;
   int strips;            // ceil(W / 128)
   int row0, rows;        // output rows computed: [row0, row0 + rows)
-  int reverse, nsub;     // visit each CTA's range as nsub sub-ranges, last first
   const uint8_t* wpack;  // packed fp16 B operand (SW128)
   const float* shift;    // per output channel (hidden: beta - mu*s; head: conv bias)
   int nshift;
@@ -45,9 +71,6 @@ struct ConvArgs {
   int K;
   // fp32-accurate split hidden layer: output fp16 pair rows [B][H][W][hi 64 | lo 64]
   uint8_t* act_out;
-  // L2 eviction hints of the fast hidden layer (TVS_L2_HINTS): bit 0 = input
-  // rows evict_first (read once), bit 1 = output rows evict_last
-  int l2_hints;
   // layer-stack kernel (conv_tc.cu mode 8): all `nlayers` hidden layers in one
   // persistent launch; wpack / shift hold every layer back to back and
   // rowcnt[(b*strips + s)*H + y] counts the epilogue warps (4 per layer) that
@@ -56,10 +79,36 @@ struct ConvArgs {
   int nlayers;
   int* rowcnt;
   const int2* items;  // work items {image, layer << 16 | strip} in a topological order
-  // TVS_CONV_DBG experiments (results invalid except 8): 1 no stack flag waits,
-  // 8 writer-side proxy fence, 16 epilogue skips its work, 32 no input loads, 64 no MMAs
+  // per-image input exponent e_b (tvs_api.cu, input_scale_kernel): the
+  // activations of image b are computed as 2^-e_b times the model's (exact:
+  // ReLU commutes with powers of two), keeping them inside the fp16 range.
+  // Hidden epilogues scale the BN shift by 2^-e_b, heads rescale by 2^e_b.
+  // Null = no scaling.
+  const int* escale;
+  // per-forward status words (kStat*), reset by the host before each forward
+  int* status;
+  unsigned long long watchdog_ns;  // layer stack: give up a row-flag wait after this long
+  KernelSpan* span;                // null, or accumulate this launch's device duration
+  // TVS_CONV_DBG / plan option "debug" (results invalid except kDbgWithholdFlag,
+  // which exercises the watchdog): 1 no stack flag waits, 16 epilogue skips its
+  // work, 32 no input loads, 64 no MMAs, ... (conv_tc.cu)
   int dbg;
 };
+// status words (ConvArgs::status)
+constexpr int kStatWatchdog = 0;    // a layer-stack row-flag wait expired: that forward's output is invalid
+constexpr int kStatNonFiniteOut = 1;  // a head wrote a NaN / Inf band value
+constexpr int kStatNonFiniteIn = 2;   // the input held NaN / Inf (the reference propagates them)
+constexpr int kStatWords = 4;
+constexpr int kDbgWithholdFlag = 1 << 17;
+constexpr int kDbgNoPdlStack = 1 << 18;     // launch the stack without programmatic serialization  // stack: never publish row 1 of (image 0, strip 0, layer 2)
+// 2^k as an exact fp32 (|k| <= 126)
+__host__ __device__ __forceinline__ float pow2i(int k) {
+  union { unsigned u; float f; } v;
+  v.u = (unsigned)(127 + k) << 23;
+  return v.f;
+}
+// per-image scale factor 2^-e (1 when the plan does not scale)
+__device__ __forceinline__ float image_scale(const int* escale, int b) { return escale ? pow2i(-__ldg(escale + b)) : 1.0f; }
 // Second pair of tensor maps of the layer-stack kernel (layer j reads buffer j&1
 // and writes buffer (j+1)&1; tm_in / tm_out cover buffer 0 input / buffer 1 output)
 struct StackMaps {
@@ -68,25 +117,10 @@ struct StackMaps {
 };
 cudaError_t launch_conv_stack(const CUtensorMap& tm_in0, const CUtensorMap& tm_out1, const StackMaps& sm,
                               const ConvArgs& a, int grid, cudaStream_t st);
-int conv_stack_error(int reset);  // watchdog flag of the stack kernel's row-flag waits
-// CTA-pair (cta_group::2) hidden layer, per-layer form (conv_tc.cu, TVS_PAIR2)
-size_t conv_pair2_wpack_bytes();
-cudaError_t launch_pack_hidden_pair2(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
-cudaError_t launch_conv_pair2(const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a, int grid,
-                              cudaStream_t st);
+// the stack kernel can run on this device: cooperative launch supported and
+// one CTA per SM fits (all `grid` CTAs co-resident)
+bool conv_stack_fits(int num_sms, int grid);
 int debug_cycles(unsigned long long* out, int reset);  // TVS_CONV_DBG bit 15 counters
-
-// two fused hidden layers (conv_pair.cu): cluster of S = ceil(W/128) CTAs
-struct PairArgs {
-  int B, H, W, S;
-  const uint8_t* wpack0;  // layer L pack (conv_tc.cu mode 0 format)
-  const uint8_t* wpack1;  // layer L+1 pack
-  const float* shift0;
-  const float* shift1;
-  uint8_t* act_out;       // fp16 NHWC [B][H][W][64] output of layer L+1
-  int dbg;                // bring-up switches (TVS_PAIR_DBG): 1 no DSMEM halo, 2 no layer-L+1 MMAs, 4 no mid stores
-};
-cudaError_t launch_conv_pair(const CUtensorMap& tm_in, const PairArgs& a, int max_ctas, cudaStream_t st);
 
 // fp32 hidden layer (conv_edge.cu)
 constexpr int kF32TileRows = 4, kF32TilePx = 32, kF32CiChunk = 16;
@@ -102,11 +136,11 @@ size_t conv_wpack_wide_bytes(bool head);  // wide variant (128 ch) on tcgen05: 4
 size_t conv_wpack_unshuf_head_bytes();    // unshuffle = 2 variant: Conv2d(64, 4K) head pack
 cudaError_t launch_pack_head_unshuf(const float* w, int K4, uint8_t* out, cudaStream_t st);
 // unshuffle = 2: Conv2d(4, 64) + ReLU over pixel_unshuffle(x, 2); H, W = half-res grid
-cudaError_t launch_conv0_unshuffle(const float* x, void* act, const float* w, const float* b, int B, int H, int W,
-                                   cudaStream_t st);
+cudaError_t launch_conv0_unshuffle(const float* x, void* act, const float* w, const float* b, const int* escale, int B,
+                                   int H, int W, cudaStream_t st);
 struct Conv0Params;
 cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a,
-                           const Conv0Params* c0, int grid, cudaStream_t st);
+                           int grid, cudaStream_t st);
 cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
 cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
 // parts = 4: output-channel quarters (modes 5 / 9); 2: halves (mode 11)
@@ -120,10 +154,16 @@ struct Conv0Params {  // passed by value: lives in the kernel's constant bank
 };
 // act_fmt: 0 = fp16 NHWC, 1 = fp32 NHWC, 2 = fp16 hi/lo pair NHWC (4*C bytes/px: hi C | lo C)
 constexpr int kActF16 = 0, kActF32 = 1, kActSplit = 2;
-cudaError_t launch_conv0(int act_fmt, int C, const float* x, void* act, const Conv0Params& p, int B, int H,
-                         int W, cudaStream_t st);
+cudaError_t launch_conv0(int act_fmt, int C, const float* x, void* act, const Conv0Params& p, const int* escale,
+                         int B, int H, int W, cudaStream_t st);
+// per-image input exponents: e_b = 0 while the conv0 output bound
+// M_b = max|x_b| * w0_l1 + b0_max lies in [2^-6, 2^6], else round(log2 M_b) - 2;
+// counts non-finite inputs into status[kStatNonFiniteIn]
+cudaError_t launch_input_scale(const float* x, int B, long long px_per_image, float w0_l1, float b0_max, int* escale,
+                               int* status, cudaStream_t st);
 cudaError_t launch_head_f32(int C, const float* act, const float* x, const float* wh, const float* bh, float* bands,
-                            float* closure, int B, int H, int W, int K, int row0, int rows, cudaStream_t st);
+                            float* closure, int B, int H, int W, int K, int row0, int rows, int* status,
+                            cudaStream_t st);
 cudaError_t launch_hidden_f32(int C, const float* in, float* out, const float* w, const float* scale,
                               const float* shift, int B, int H, int W, cudaStream_t st);
 cudaError_t configure_kernels();  // one-time smem opt-ins
@@ -131,8 +171,8 @@ cudaError_t configure_kernels();  // one-time smem opt-ins
 // in_ch = 1 (reference conv0) or 4 (unshuffle = 2 variant, H/W = half-res grid)
 size_t conv0_tc_pack_bytes(int in_ch);
 cudaError_t launch_pack_conv0_tc(const float* w, int in_ch, uint8_t* out, cudaStream_t st);
-cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t* bpack, const float* bias, int B,
-                            int H, int W, int num_sms, cudaStream_t st);
+cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t* bpack, const float* bias,
+                            const int* escale, int B, int H, int W, int num_sms, cudaStream_t st);
 // metrics.cu: per-plane scoring statistics (8 doubles per plane)
 cudaError_t launch_band_stats(const float* gt, const float* pred, int planes, int H, int W,
                               const double* range_override, double* stats, cudaStream_t st);

@@ -102,7 +102,8 @@ __device__ __forceinline__ void conv0_taps(const float* __restrict__ x, long lon
 template <int kKB>
 __global__ void __launch_bounds__(128) conv0_tc_kernel(const float* __restrict__ x, __half* __restrict__ act,
                                                        const uint8_t* __restrict__ bpack,
-                                                       const float* __restrict__ bias, int B, int H, int W) {
+                                                       const float* __restrict__ bias,
+                                                       const int* __restrict__ escale, int B, int H, int W) {
   using Cfg = Conv0TcCfg<kKB>;
   constexpr int n = Cfg::kTaps;
   constexpr int NT = Cfg::kTiles;
@@ -199,6 +200,8 @@ __global__ void __launch_bounds__(128) conv0_tc_kernel(const float* __restrict__
     // in NHWC (per-lane 128 B stores would cost 32 LSU wavefronts each)
 #pragma unroll 1
     for (int i = 0; i < NT; ++i) {
+      // 2^-e of this tile's image (exact; 1 for in-range inputs)
+      const float sc = escale ? pow2i(-__ldg(escale + (int)min((base + i) / strips / H, (long long)B - 1))) : 1.0f;
       uint32_t acc[4][16];
 #pragma unroll
       for (int j = 0; j < 4; ++j) tmem_ld16(tmem + lane_addr + i * 64 + j * 16, acc[j]);
@@ -212,8 +215,8 @@ __global__ void __launch_bounds__(128) conv0_tc_kernel(const float* __restrict__
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int c = c8 * 8 + e * 2;
-          const float f0 = __uint_as_float(acc[c >> 4][c & 15]) + sBias[c];
-          const float f1 = __uint_as_float(acc[c >> 4][(c & 15) + 1]) + sBias[c + 1];
+          const float f0 = (__uint_as_float(acc[c >> 4][c & 15]) + sBias[c]) * sc;
+          const float f1 = (__uint_as_float(acc[c >> 4][(c & 15) + 1]) + sBias[c + 1]) * sc;
           asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[e]) : "f"(f1), "f"(f0));
         }
         st_shared_v4(srow + ((c8 ^ (t & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
@@ -279,18 +282,19 @@ cudaError_t launch_pack_conv0_tc(const float* w, int in_ch, uint8_t* out, cudaSt
   return cudaGetLastError();
 }
 
-cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t* bpack, const float* bias, int B,
-                            int H, int W, int num_sms, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv0_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t* bpack, const float* bias,
+                            const int* escale, int B, int H, int W, int num_sms, cudaStream_t st) {
+  static std::mutex mu;
+  static uint64_t done = 0;
+  cudaError_t e = once_per_device(mu, done, [] {
+    cudaError_t r = cudaFuncSetAttribute(conv0_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)Conv0TcCfg<1>::kSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv0_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(conv0_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)Conv0TcCfg<4>::kSmem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+    return r;
+  });
+  if (e != cudaSuccess) return e;
   const long long tiles = (long long)B * H * ((W + 127) / 128);
   const int nt = in_ch == 1 ? Conv0TcCfg<1>::kTiles : Conv0TcCfg<4>::kTiles;
   const int per_sm = in_ch == 1 ? Conv0TcCfg<1>::kPerSm : Conv0TcCfg<4>::kPerSm;
@@ -298,9 +302,9 @@ cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t*
   // plain launch (no PDL attribute): K1 is a forward's first kernel and has
   // no griddepcontrol.wait, so it must not overlap the previous forward's head
   if (in_ch == 1) {
-    conv0_tc_kernel<1><<<grid, 128, Conv0TcCfg<1>::kSmem, st>>>(x, static_cast<__half*>(act), bpack, bias, B, H, W);
+    conv0_tc_kernel<1><<<grid, 128, Conv0TcCfg<1>::kSmem, st>>>(x, static_cast<__half*>(act), bpack, bias, escale, B, H, W);
   } else {
-    conv0_tc_kernel<4><<<grid, 128, Conv0TcCfg<4>::kSmem, st>>>(x, static_cast<__half*>(act), bpack, bias, B, H, W);
+    conv0_tc_kernel<4><<<grid, 128, Conv0TcCfg<4>::kSmem, st>>>(x, static_cast<__half*>(act), bpack, bias, escale, B, H, W);
   }
   return cudaGetLastError();
 }

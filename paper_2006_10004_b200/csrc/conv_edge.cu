@@ -45,7 +45,8 @@ __device__ __forceinline__ void store_act8<float>(float* dst, const float* v) {
 // memory and written coalesced.
 template <typename T, int C, bool kSplit = false>
 __global__ void __launch_bounds__(128)
-conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params p, int B, int H, int W) {
+conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params p, const int* __restrict__ escale,
+             int B, int H, int W) {
   constexpr int P = (C == 64) ? 128 : 64;  // pixels per block (static smem <= 32 KB)
   constexpr int E = kSplit ? 2 * C : C;    // elements per pixel (split: hi | lo halves)
   __shared__ __align__(16) T stage[P * E];
@@ -60,6 +61,7 @@ conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params
     const int y = (int)(t % H);
     const long long b = t / H;
     const float* img = x + b * (long long)H * W;
+    const float sc = image_scale(escale, (int)b);  // exact 2^-e_b (1 for in-range inputs)
     float in[9];
 #pragma unroll
     for (int ky = 0; ky < 3; ++ky)
@@ -80,7 +82,7 @@ conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params
         Acc acc = 0;
 #pragma unroll
         for (int t9 = 0; t9 < 9; ++t9) acc = fma((Acc)p.w[co * 9 + t9], (Acc)in[t9], acc);
-        v[e] = fmaxf((float)(acc + (Acc)p.b[co]), 0.0f);
+        v[e] = fmaxf((float)(acc + (Acc)p.b[co]), 0.0f) * sc;
       }
       if constexpr (kSplit) {
         float lo[8];
@@ -125,7 +127,7 @@ template <typename T, int C>
 __global__ void __launch_bounds__(128)
 head_kernel(const T* __restrict__ act, const float* __restrict__ x, const float* __restrict__ wh,
             const float* __restrict__ bh, float* __restrict__ bands, float* __restrict__ closure, int B,
-            int H, int W, int K, int row0, int rows) {
+            int H, int W, int K, int row0, int rows, int* __restrict__ status) {
   extern __shared__ float swh[];  // [9][64][K]
   for (int i = threadIdx.x; i < 9 * C * K; i += blockDim.x) {
     const int k = i % K, ci = (i / K) % C, t = i / (K * C);
@@ -170,13 +172,16 @@ head_kernel(const T* __restrict__ act, const float* __restrict__ x, const float*
   float sum = 0.0f;
   const long long plane = (long long)rows * W;
   float* ob = bands + b * K * plane + (long long)rr * W + xw;
+  bool bad = false;
 #pragma unroll
   for (int k = 0; k < kMaxBands; ++k)
     if (k < K) {
       const float o = (float)(acc[k] + (Acc)bh[k]);
       ob[k * plane] = o;
       sum += o;
+      bad |= !isfinite(o);
     }
+  if (bad && status) atomicOr(status + kStatNonFiniteOut, 1);
   if (closure != nullptr) closure[b * plane + (long long)rr * W + xw] = x[(b * H + y) * (long long)W + xw] - sum;
 }
 
@@ -263,26 +268,26 @@ hidden_f32_kernel(const float* __restrict__ in, float* __restrict__ out, const f
   }
 }
 
-cudaError_t launch_conv0(int act_fmt, int C, const float* x, void* act, const Conv0Params& p, int B, int H, int W,
-                         cudaStream_t st) {
+cudaError_t launch_conv0(int act_fmt, int C, const float* x, void* act, const Conv0Params& p, const int* escale,
+                         int B, int H, int W, cudaStream_t st) {
   const long long npx = (long long)B * H * W;
   if (C == 64) {
     const unsigned grid = (unsigned)((npx + 127) / 128);
     if (act_fmt == kActF16)
-      conv0_kernel<__half, 64><<<grid, 128, 0, st>>>(x, static_cast<__half*>(act), p, B, H, W);
+      conv0_kernel<__half, 64><<<grid, 128, 0, st>>>(x, static_cast<__half*>(act), p, escale, B, H, W);
     else if (act_fmt == kActSplit)
-      conv0_kernel<__half, 64, true><<<grid, 128, 0, st>>>(x, static_cast<__half*>(act), p, B, H, W);
+      conv0_kernel<__half, 64, true><<<grid, 128, 0, st>>>(x, static_cast<__half*>(act), p, escale, B, H, W);
     else
-      conv0_kernel<float, 64><<<grid, 128, 0, st>>>(x, static_cast<float*>(act), p, B, H, W);
+      conv0_kernel<float, 64><<<grid, 128, 0, st>>>(x, static_cast<float*>(act), p, escale, B, H, W);
   } else if (C == 128 && act_fmt == kActF32) {
     const unsigned grid = (unsigned)((npx + 63) / 64);
-    conv0_kernel<float, 128><<<grid, 64, 0, st>>>(x, static_cast<float*>(act), p, B, H, W);
+    conv0_kernel<float, 128><<<grid, 64, 0, st>>>(x, static_cast<float*>(act), p, escale, B, H, W);
   } else if (C == 128 && act_fmt == kActF16) {
     const unsigned grid = (unsigned)((npx + 63) / 64);
-    conv0_kernel<__half, 128><<<grid, 64, 0, st>>>(x, static_cast<__half*>(act), p, B, H, W);
+    conv0_kernel<__half, 128><<<grid, 64, 0, st>>>(x, static_cast<__half*>(act), p, escale, B, H, W);
   } else if (C == 128 && act_fmt == kActSplit) {
     const unsigned grid = (unsigned)((npx + 63) / 64);
-    conv0_kernel<__half, 128, true><<<grid, 64, 0, st>>>(x, static_cast<__half*>(act), p, B, H, W);
+    conv0_kernel<__half, 128, true><<<grid, 64, 0, st>>>(x, static_cast<__half*>(act), p, escale, B, H, W);
   } else {
     return cudaErrorInvalidValue;
   }
@@ -298,7 +303,7 @@ cudaError_t launch_conv0(int act_fmt, int C, const float* x, void* act, const Co
 // shared memory, output staged and written coalesced as fp16 NHWC.
 __global__ void __launch_bounds__(128)
 conv0_unshuffle_kernel(const float* __restrict__ x, __half* __restrict__ act, const float* __restrict__ w,
-                       const float* __restrict__ bias, int B, int H, int W) {
+                       const float* __restrict__ bias, const int* __restrict__ escale, int B, int H, int W) {
   constexpr int P = 128, C = 64;
   __shared__ float sw[C * 36];
   __shared__ float sb[C];
@@ -317,6 +322,7 @@ conv0_unshuffle_kernel(const float* __restrict__ x, __half* __restrict__ act, co
     const long long b = t / H;
     const int Wf = 2 * W;
     const float* img = x + b * (long long)(2 * H) * Wf;
+    const float sc = image_scale(escale, (int)b);
     float in[36];  // [c = 2i + j][ky][kx]
 #pragma unroll
     for (int ky = 0; ky < 3; ++ky)
@@ -338,7 +344,7 @@ conv0_unshuffle_kernel(const float* __restrict__ x, __half* __restrict__ act, co
         float acc = 0.0f;
 #pragma unroll
         for (int t36 = 0; t36 < 36; ++t36) acc = fmaf(sw[co * 36 + t36], in[t36], acc);
-        v[e] = fmaxf(acc + sb[co], 0.0f);
+        v[e] = fmaxf(acc + sb[co], 0.0f) * sc;
       }
       store_act8<__half>(dst + c8 * 8, v);
     }
@@ -351,22 +357,24 @@ conv0_unshuffle_kernel(const float* __restrict__ x, __half* __restrict__ act, co
   for (int i = threadIdx.x; i < n16; i += blockDim.x) out[i] = src[i];
 }
 
-cudaError_t launch_conv0_unshuffle(const float* x, void* act, const float* w, const float* b, int B, int H, int W,
-                                   cudaStream_t st) {
+cudaError_t launch_conv0_unshuffle(const float* x, void* act, const float* w, const float* b, const int* escale, int B,
+                                   int H, int W, cudaStream_t st) {
   const long long npx = (long long)B * H * W;
-  conv0_unshuffle_kernel<<<(unsigned)((npx + 127) / 128), 128, 0, st>>>(x, static_cast<__half*>(act), w, b, B, H, W);
+  conv0_unshuffle_kernel<<<(unsigned)((npx + 127) / 128), 128, 0, st>>>(x, static_cast<__half*>(act), w, b, escale,
+                                                                        B, H, W);
   return cudaGetLastError();
 }
 
 cudaError_t launch_head_f32(int C, const float* act, const float* x, const float* wh, const float* bh, float* bands,
-                            float* closure, int B, int H, int W, int K, int row0, int rows, cudaStream_t st) {
+                            float* closure, int B, int H, int W, int K, int row0, int rows, int* status,
+                            cudaStream_t st) {
   const long long nout = (long long)B * rows * W;
   const unsigned grid = (unsigned)((nout + 127) / 128);
   const size_t smem = (size_t)9 * C * K * sizeof(float);
   if (C == 64)
-    head_kernel<float, 64><<<grid, 128, smem, st>>>(act, x, wh, bh, bands, closure, B, H, W, K, row0, rows);
+    head_kernel<float, 64><<<grid, 128, smem, st>>>(act, x, wh, bh, bands, closure, B, H, W, K, row0, rows, status);
   else if (C == 128)
-    head_kernel<float, 128><<<grid, 128, smem, st>>>(act, x, wh, bh, bands, closure, B, H, W, K, row0, rows);
+    head_kernel<float, 128><<<grid, 128, smem, st>>>(act, x, wh, bh, bands, closure, B, H, W, K, row0, rows, status);
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();
@@ -381,6 +389,65 @@ cudaError_t launch_hidden_f32(int C, const float* in, float* out, const float* w
     hidden_f32_kernel<128><<<(unsigned)tiles, 512, f32_smem(128), st>>>(in, out, w, scale, shift, B, H, W);
   else
     return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------ per-image input scale ----
+// One block per image: amax over the plane and a non-finite count.  The
+// exponent keeps the conv0 output bound M = amax * w0_l1 + b0_max (and with
+// it every fp16 activation of a well-conditioned network) near 1: inputs
+// whose M lies in [2^-6, 2^6] (every BASELINE workload) keep e = 0, so their
+// arithmetic is unchanged and bitwise identical across batch/row-band shards.
+__global__ void __launch_bounds__(256)
+input_scale_kernel(const float* __restrict__ x, long long n, float w0_l1, float b0_max, int* __restrict__ escale,
+                   int* __restrict__ status) {
+  const float* img = x + (long long)blockIdx.x * n;
+  float amax = 0.0f;
+  int bad = 0;
+  const bool vec = (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(img) & 15) == 0);
+  if (vec) {
+    const float4* v = reinterpret_cast<const float4*>(img);
+    for (long long i = threadIdx.x; i < n / 4; i += blockDim.x) {
+      const float4 q = __ldg(v + i);
+      const float e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (isfinite(e[k])) amax = fmaxf(amax, fabsf(e[k]));
+        else bad = 1;
+      }
+    }
+  } else {
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+      const float e = __ldg(img + i);
+      if (isfinite(e)) amax = fmaxf(amax, fabsf(e));
+      else bad = 1;
+    }
+  }
+  __shared__ float s_max[8];
+  __shared__ int s_bad[8];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) { s_max[threadIdx.x >> 5] = amax; s_bad[threadIdx.x >> 5] = bad; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) { amax = fmaxf(amax, s_max[w]); bad |= s_bad[w]; }
+    amax = fmaxf(amax, s_max[0]);
+    bad |= s_bad[0];
+    const float m = fmaf(amax, w0_l1, b0_max);
+    int e = 0;
+    if (m > 0.0f && (m < 0.015625f || m > 64.0f)) e = min(60, max(-60, ilogbf(m) - 1));
+    escale[blockIdx.x] = e;
+    if (bad) atomicOr(status + kStatNonFiniteIn, 1);
+  }
+}
+
+cudaError_t launch_input_scale(const float* x, int B, long long px_per_image, float w0_l1, float b0_max, int* escale,
+                               int* status, cudaStream_t st) {
+  if (B <= 0) return cudaSuccess;
+  input_scale_kernel<<<B, 256, 0, st>>>(x, px_per_image, w0_l1, b0_max, escale, status);
   return cudaGetLastError();
 }
 

@@ -49,11 +49,7 @@ struct Segment {
   int layer;  // hidden layer of a layer-stack item (mode 8)
 };
 struct SegIter {
-  // [cur, end) of the current sub-range; sub-ranges are visited last-first
-  // when a.reverse is set, so a layer first reads the rows the previous layer
-  // wrote last (those are still L2-resident).
-  long long lo, hi, cur, end;
-  int sub, nsub;
+  long long cur, end;  // [cur, end): this CTA's strip-rows
   int nh = 1;          // visits per segment (2: once per output-channel half)
   bool pend = false;   // second visit of `last` outstanding
   Segment last;
@@ -62,18 +58,10 @@ struct SegIter {
   TVS_DEV SegIter(const ConvArgs& a, int halves = 1, int parts = 1) : nh(halves) {
     const long long T = (long long)a.B * a.strips * a.rows;
     const long long part = blockIdx.x / parts, nparts = gridDim.x / parts;
-    lo = T * part / nparts;
-    hi = T * (part + 1) / nparts;
-    nsub = a.reverse ? a.nsub : 1;
-    sub = 0;
-    set_sub();
+    cur = T * part / nparts;
+    end = T * (part + 1) / nparts;
   }
   TVS_DEV int first_layer_or0(const ConvArgs&) const { return 0; }
-  TVS_DEV void set_sub() {
-    const int k = nsub - 1 - sub;  // reverse order
-    cur = lo + (hi - lo) * k / nsub;
-    end = lo + (hi - lo) * (k + 1) / nsub;
-  }
   TVS_DEV bool next(const ConvArgs& a, Segment& g) {
     if (pend) {
       g = last;
@@ -81,10 +69,7 @@ struct SegIter {
       pend = false;
       return true;
     }
-    while (cur >= end) {
-      if (++sub >= nsub) return false;
-      set_sub();
-    }
+    if (cur >= end) return false;
     const long long col = cur / a.rows;
     const int y0 = (int)(cur - col * a.rows);
     const int n = (int)min((long long)(a.rows - y0), end - cur);
@@ -133,7 +118,6 @@ struct ItemIter {
   }
 };
 
-__device__ int g_stack_err;  // set when a row-flag wait times out (results invalid, no hang)
 // TVS_CONV_DBG bit 15 (layer stack): MMA-issuer cycle accounting (sum over CTAs): [0] total,
 // [1] waiting for a free accumulator slot, [2] waiting for the input row,
 // [3] waiting for a layer's weights, [4] general-path rows, [5] fast-path rows,
@@ -155,6 +139,7 @@ struct StackGate {
     const int s = g.x0 / kStripPx;
     const int* base = a.rowcnt + (long long)g.b * a.strips * a.H;
     bool refreshed = false;
+    unsigned long long t0 = 0;
     for (uint32_t spins = 0;; ++spins) {
       int v[3][kAhead];
       bool need[3];
@@ -181,11 +166,19 @@ struct StackGate {
         ok = ok && c > 0;
       }
       if (ok) break;
-      if (*(volatile int*)&g_stack_err) return;
+      // watchdog: never hang.  Once any wait of this launch has expired the
+      // output is invalid (the host reports it), so every later wait gives up
+      // at once and the launch drains.
+      if (ld_relaxed_gpu(a.status + kStatWatchdog)) return;
       __nanosleep(32);
-      if (spins > (1u << 26)) {
-        atomicExch(&g_stack_err, 1);
-        return;
+      if ((spins & 63u) == 63u) {
+        const unsigned long long now = globaltimer_ns();
+        if (t0 == 0) {
+          t0 = now;
+        } else if (now - t0 > a.watchdog_ns) {
+          atomicExch(a.status + kStatWatchdog, 1);
+          return;
+        }
       }
     }
     if (refreshed) {  // acquire what the counters published, then hand it to the TMA (async) proxy
@@ -195,9 +188,7 @@ struct StackGate {
   }
 };
 
-// kMode: 0 = hidden layer (TMA producer), 1 = head, 2 = first hidden layer
-// with conv0 fused into its producer (4 warps compute Conv2d(1,64)+ReLU of
-// each input row from the fp32 image straight into the smem ring),
+// kMode: 0 = hidden layer, 1 = head,
 // 3 / 4 = fp32-accurate hidden layer / head on split operands: activations
 // are stored as an fp16 pair (hi = RN(a), lo = RN(a - hi): channels 0-63 and
 // 64-127 of a 256 B/px NHWC row), weights as hi/lo fp16 packs scaled by 2^8
@@ -227,7 +218,6 @@ struct ConvCfg {
   static constexpr bool kSplit = kMode >= 3 && kMode <= 6;
   static constexpr bool kUnshuf = kMode == 7;
   static constexpr bool kHead = kMode == 1 || kMode == 4 || kMode == 6 || kMode == 7 || kMode == 10;
-  static constexpr bool kFirst = kMode == 2;
   static constexpr bool kWide = kMode == 5 || kMode == 6 || kMode == 9 || kMode == 10 || kMode == 11;
   static constexpr bool kQuarters = kMode == 5 || kMode == 9;
   // mode 11: wide single-input layer split into output-channel HALVES (pairs of
@@ -238,15 +228,12 @@ struct ConvCfg {
   static constexpr int kCin = kWide ? 128 : 64;
   static constexpr int kKBlk = kCin / 64;        // 64-channel K blocks (one SW128 row buffer each)
   static constexpr int kKSteps = 4 * kKBlk;      // K16 steps per tap
-  static constexpr int kProdWarps = kFirst ? 4 : 1;
-  static constexpr int kMmaWarp = kProdWarps;
-  static constexpr int kEpiWarp0 = kProdWarps + 1;
-  // 4 more producer warps in mode 2 -> two epilogue groups keep <= 4 warps per
-  // SM sub-partition (register file: 16K regs per SMSP, so 128 regs/thread)
+  static constexpr int kMmaWarp = 1;  // warp 0: TMA producer
+  static constexpr int kEpiWarp0 = 2;
   // plain fp16 hidden layer (modes 0 / 8): epilogue groups and ring depth are
   // build-time knobs (4 groups on a 5-deep ring measured no faster than 3 / 6)
   static constexpr bool kPlain = kMode == 0 || kMode == 8;
-  static constexpr int kGroups = kFirst ? 2 : (kPlain ? kEpiGroupsPlain : kEpiGroups);
+  static constexpr int kGroups = kPlain ? kEpiGroupsPlain : kEpiGroups;
   static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kGroups);
   // split hidden layer: two passes of 32 output channels (TMEM room for three rings)
   static constexpr bool kHalves = kMode == 3;
@@ -316,7 +303,7 @@ constexpr float kMainDebias18 = 1.0f + 0.5f * 0.7213f * 9.0f * 1.1920929e-7f;  /
 template <int kMode>
 __global__ void __launch_bounds__(ConvCfg<kMode>::kThreads, 1)
 conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
-                  const ConvArgs a, const __grid_constant__ Conv0Params c0, const __grid_constant__ StackMaps smaps) {
+                  const ConvArgs a, const __grid_constant__ StackMaps smaps) {
   using Cfg = ConvCfg<kMode>;
   using Iter = std::conditional_t<Cfg::kStack, ItemIter, SegIter>;
   constexpr bool kHead = Cfg::kHead;
@@ -338,7 +325,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < Cfg::kNStages; ++i) { mbar_init(&full[i], Cfg::kProdWarps); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < Cfg::kNStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < kSlots; ++i) { mbar_init(&slot_full[i], 1); mbar_init(&slot_empty[i], 4); }
     mbar_init(&wbar, 1);
     mbar_init(&wfree, 1);
@@ -360,88 +347,12 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   const uint32_t tmem = tmem_base_smem;
   pdl_launch_dependents();  // the next layer may start its prologue on free SMs
   pdl_wait();               // previous layer's activations are complete and visible
+  if (a.span && threadIdx.x == 0) span_open(a.span);
 
-  if (Cfg::kFirst && warp < Cfg::kProdWarps) {
-    // ------------------------------------------- conv0 producer (K1 fused) ----
-    // Input row r of this layer = ReLU(Conv2d(1,64)(x))[row r] at pixels
-    // x0-1 .. x0+128, written as fp16 into the SW128 ring stage; pixels outside
-    // the image are zero (this layer's Conv2d padding).  Thread t (128 threads)
-    // owns strip pixel 1+t (all 64 channels) and keeps its 3x3 input window in
-    // registers, loading one new x row per input row, one row ahead.  The two
-    // halo pixels (0 and 129) are split over all threads: thread t computes
-    // channel t%64 of halo pixel t/64.  Weights come from the parameter block.
-    const int pt = warp * 32 + lane;                 // 0..127
-    const int sp = 1 + pt;                           // strip pixel (ring row)
-    const int hp = (pt >> 6) ? 129 : 0;              // halo pixel of this thread
-    const int hco = pt & 63;                         // its channel
-    int stage = 0;
-    uint32_t phase = 0;
-    SegIter it(a, Cfg::kVisits, Cfg::kParts);
-    Segment g;
-    while (it.next(a, g)) {
-      const float* img = a.x + (long long)g.b * a.H * a.W;
-      const int xg = g.x0 - 1 + sp, xh = g.x0 - 1 + hp;
-      auto ld3 = [&](int yy, int xc, float* v) {  // x[yy][xc-1..xc+1], zero outside the image
-        const bool rowok = yy >= 0 && yy < a.H;
-#pragma unroll
-        for (int kx = 0; kx < 3; ++kx) {
-          const int xx = xc + kx - 1;
-          v[kx] = (rowok && xx >= 0 && xx < a.W) ? __ldg(img + (long long)yy * a.W + xx) : 0.0f;
-        }
-      };
-      const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
-      float win[9], hwin[9], nxt[3], hnxt[3];
-      ld3(r0 - 1, xg, win); ld3(r0, xg, win + 3); ld3(r0 + 1, xg, win + 6);
-      ld3(r0 - 1, xh, hwin); ld3(r0, xh, hwin + 3); ld3(r0 + 1, xh, hwin + 6);
-      for (int r = r0; r <= r1; ++r) {
-        ld3(r + 2, xg, nxt);  // next row's window, in flight during this row's math
-        ld3(r + 2, xh, hnxt);
-        mbar_wait(&empty[stage], phase ^ 1);
-        const uint32_t row_u = smem_u32(sIn + stage * kInRowStride);
-        const bool inside = xg >= 0 && xg < a.W;
-#pragma unroll
-        for (int chunk = 0; chunk < 8; ++chunk) {
-          uint32_t packed[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float v2[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int co = chunk * 8 + e * 2 + h;
-              float acc = 0.0f;
-#pragma unroll
-              for (int t9 = 0; t9 < 9; ++t9) acc = fmaf(c0.w[co * 9 + t9], win[t9], acc);
-              v2[h] = inside ? fmaxf(acc + c0.b[co], 0.0f) : 0.0f;
-            }
-            __half2 hv = __floats2half2_rn(v2[0], v2[1]);
-            packed[e] = *reinterpret_cast<uint32_t*>(&hv);
-          }
-          st_shared_v4(row_u + sp * 128 + ((chunk ^ (sp & 7)) << 4), packed[0], packed[1], packed[2], packed[3]);
-        }
-        {  // one channel of one halo pixel
-          float acc = 0.0f;
-#pragma unroll
-          for (int t9 = 0; t9 < 9; ++t9) acc = fmaf(c0.w[hco * 9 + t9], hwin[t9], acc);
-          const bool hin = xh >= 0 && xh < a.W;
-          const __half hv = __float2half_rn(hin ? fmaxf(acc + c0.b[hco], 0.0f) : 0.0f);
-          const uint32_t addr = row_u + hp * 128 + (((hco >> 3) ^ (hp & 7)) << 4) + ((hco & 7) << 1);
-          asm volatile("st.shared.b16 [%0], %1;" ::"r"(addr), "h"(__half_as_ushort(hv)) : "memory");
-        }
-        fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[stage]);
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
-#pragma unroll
-        for (int i = 0; i < 6; ++i) { win[i] = win[i + 3]; hwin[i] = hwin[i + 3]; }
-#pragma unroll
-        for (int i = 0; i < 3; ++i) { win[6 + i] = nxt[i]; hwin[6 + i] = hnxt[i]; }
-      }
-    }
-  } else if (!Cfg::kFirst && warp == 0) {
+  if (warp == 0) {
     // ------------------------------------------------ TMA producer ----
     if (elect_one()) {
       prefetch_tmap(&tm_in);
-      const uint64_t pol_in = l2_policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
       Iter it(a, Cfg::kVisits, Cfg::kParts);
@@ -478,12 +389,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           mbar_arrive_expect_tx(&full[stage], nbuf * kInRowBytes);
 #pragma unroll
           for (int i = 0; i < nbuf; ++i) {  // buffer i = channels 64i..64i+63 of the pixel row
-            if (a.l2_hints & 1)
-              tma_load_4d_hint(sIn + stage * Cfg::kStageBytes + i * kInRowStride, tmi, &full[stage], 64 * i,
-                               g.x0 - 1, r, g.b, pol_in);
-            else
-              tma_load_4d(sIn + stage * Cfg::kStageBytes + i * kInRowStride, tmi, &full[stage], 64 * i, g.x0 - 1,
-                          r, g.b);
+            tma_load_4d(sIn + stage * Cfg::kStageBytes + i * kInRowStride, tmi, &full[stage], 64 * i, g.x0 - 1, r,
+                        g.b);
           }
           if (++stage == Cfg::kNStages) { stage = 0; phase ^= 1; }
         }
@@ -726,7 +633,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const uint32_t shift_u = smem_u32(sShift);
     if (!kHead && !Cfg::kSplit && !Cfg::kWide && lane == 0) prefetch_tmap(&tm_out);
     uint32_t seq = 0, gsel = 0;  // gsel = seq % kGroups
-    int grp_layer = -1;          // layer stack: layer whose shift sShiftG[grp] holds
+    int grp_key = -1;            // layer stack: (image, layer) whose scaled shift sShiftG[grp] holds
     const uint32_t shift_g = smem_u32(&sShiftG[Cfg::kStack ? grp : 0][0]);
     Iter it(a, Cfg::kVisits, Cfg::kParts);
     Segment g;
@@ -734,14 +641,17 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
       // layer-stack: this item's BN shift and output buffer
       const float4* shg = reinterpret_cast<const float4*>(a.shift + (size_t)g.layer * kC);
       const CUtensorMap* tmo = (Cfg::kStack && (g.layer & 1)) ? &smaps.out0 : &tm_out;
+      // 2^-e_b of this segment's image (exact; 1 for in-range inputs)
+      const float sc = image_scale(a.escale, g.b);
       if constexpr (Cfg::kStack) {
-        if (g.layer != grp_layer && !(a.dbg & 16384)) {
+        const int key = g.b * 4096 + g.layer;
+        if (key != grp_key && !(a.dbg & 16384)) {
           // every warp of the group is past the previous item's last per-row
           // barrier, so nobody still reads the old shift
           const int t = quarter * 32 + lane;
-          if (t < kC) sShiftG[grp][t] = a.shift[(size_t)g.layer * kC + t];
+          if (t < kC) sShiftG[grp][t] = a.shift[(size_t)g.layer * kC + t] * sc;
           named_bar_sync(1 + grp, 128);
-          grp_layer = g.layer;
+          grp_key = key;
         }
       }
       for (int q = g.ya; q < g.yb; ++q, ++seq, gsel = (gsel + 1 == Cfg::kGroups) ? 0 : gsel + 1) {
@@ -773,7 +683,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
               const uint32_t sh_u = shift_u + (uint32_t)(qtr * NB + chunk * 8) * 4;
               const float4 s0 = ld_shared_f4(sh_u);
               const float4 s1 = ld_shared_f4(sh_u + 16);
-              const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+              const float sh[8] = {s0.x * sc, s0.y * sc, s0.z * sc, s0.w * sc, s1.x * sc, s1.y * sc, s1.z * sc,
+                                   s1.w * sc};
               uint32_t hi[4], lo[4];
 #pragma unroll
               for (int t2 = 0; t2 < 4; ++t2) {
@@ -815,7 +726,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
               const uint32_t sh_u = shift_u + (uint32_t)(g.h * 32 + chunk * 8) * 4;
               const float4 s0 = ld_shared_f4(sh_u);
               const float4 s1 = ld_shared_f4(sh_u + 16);
-              const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+              const float sh[8] = {s0.x * sc, s0.y * sc, s0.z * sc, s0.w * sc, s1.x * sc, s1.y * sc, s1.z * sc,
+                                   s1.w * sc};
               uint32_t hi[4], lo[4];
 #pragma unroll
               for (int t2 = 0; t2 < 4; ++t2) {
@@ -873,7 +785,11 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             const float4 s0 = gl ? __ldg(shg + 2 * chunk) : ld_shared_f4((Cfg::kStack ? shift_g : shift_u) + chunk * 32);
             const float4 s1 = gl ? __ldg(shg + 2 * chunk + 1)
                                  : ld_shared_f4((Cfg::kStack ? shift_g : shift_u) + chunk * 32 + 16);
-            const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+            if (!Cfg::kStack && sc != 1.0f) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) sh[i] *= sc;
+            }
             uint32_t packed[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -899,23 +815,24 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           __syncwarp();
           if (a.dbg & 256) continue;  // ablation: no TMA store
           if (lane == 0) {
-            if (a.l2_hints & 2)
-              tma_store_4d_hint(tmo, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b,
-                                l2_policy_evict_last());
-            else
-              tma_store_4d(tmo, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b);
+            tma_store_4d(tmo, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b);
             bulk_commit();
-            if constexpr (Cfg::kStack) bulk_wait<0>();  // this warp's quarter row has landed
+            if constexpr (Cfg::kStack) {
+              // this warp's quarter row has landed (async proxy); order it
+              // before the generic-proxy release below (the reader acquires,
+              // then fences into the async proxy before its TMA load)
+              bulk_wait<0>();
+              fence_proxy_async_global();
+            }
           }
           if constexpr (Cfg::kStack) {
             // publish the row to the next layer's items: the group's 4 warps
             // meet on a named barrier, one thread releases the row counter (+4)
             __syncwarp();
             named_bar_sync(1 + grp, 128);
-            if (quarter == 0 && lane == 0) {
-              if (a.dbg & 8) fence_proxy_async_global();
+            const bool withhold = (a.dbg & kDbgWithholdFlag) && g.b == 0 && g.x0 == 0 && q == 1 && g.layer == 2;
+            if (quarter == 0 && lane == 0 && !withhold)
               red_release_gpu_add(a.rowcnt + ((long long)g.b * a.strips + g.x0 / kStripPx) * a.H + q, 4);
-            }
           }
         } else if constexpr (Cfg::kUnshuf) {
           uint32_t v[4][16];
@@ -933,6 +850,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             const long long planef = (long long)(2 * a.rows) * Wf;
             const long long r0f = 2LL * (q - a.row0);
             float sum[4] = {0.f, 0.f, 0.f, 0.f};
+            const float inv = 1.0f / sc;  // undo the image's 2^-e activation scale (exact)
+            bool bad = false;
 #pragma unroll
             for (int k = 0; k < kMaxBands; ++k) {
               if (k < a.K) {
@@ -943,14 +862,16 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
                   for (int jj = 0; jj < 2; ++jj) {
                     const int o = k * 4 + i * 2 + jj;  // head channel (pixel_shuffle order)
-                    f[jj] = (__uint_as_float(v[o >> 4][o & 15]) + __uint_as_float(v[(32 + o) >> 4][(32 + o) & 15])) +
-                            sShift[o];
+                    f[jj] = (__uint_as_float(v[o >> 4][o & 15]) + __uint_as_float(v[(32 + o) >> 4][(32 + o) & 15])) *
+                                inv + sShift[o];
                     sum[i * 2 + jj] += f[jj];
+                    bad |= !isfinite(f[jj]);
                   }
                   *reinterpret_cast<float2*>(ob + (r0f + i) * Wf + 2 * xg) = make_float2(f[0], f[1]);
                 }
               }
             }
+            if (bad) atomicOr(a.status + kStatNonFiniteOut, 1);
             if (a.closure) {
 #pragma unroll
               for (int i = 0; i < 2; ++i) {
@@ -1006,14 +927,18 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             const long long pix = (long long)(q - a.row0) * a.W + xg;
             float* ob = a.bands + (long long)g.b * a.K * plane + pix;
             float sum = 0.0f;
+            const float inv = 1.0f / sc;  // undo the image's 2^-e activation scale (exact)
+            bool bad = false;
 #pragma unroll
             for (int k = 0; k < kMaxBands; ++k) {
               if (k < a.K) {
-                const float o = (__uint_as_float(v[0][k]) + __uint_as_float(v[1][k])) + sShift[k];
+                const float o = (__uint_as_float(v[0][k]) + __uint_as_float(v[1][k])) * inv + sShift[k];
                 ob[k * plane] = o;
                 sum += o;
+                bad |= !isfinite(o);
               }
             }
+            if (bad) atomicOr(a.status + kStatNonFiniteOut, 1);
             if (a.closure) a.closure[(long long)g.b * plane + pix] = a.x[((long long)g.b * a.H + q) * a.W + xg] - sum;
           }
         }
@@ -1028,6 +953,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     tc_fence_after();
     tmem_dealloc<Cfg::kTmemCols>(tmem);
   }
+  if (a.span && threadIdx.x == 0) span_close(a.span);
 }
 
 // --------------------------------------------------------------------------
@@ -1217,10 +1143,8 @@ size_t conv_wpack_unshuf_head_bytes() { return ConvCfg<7>::kW; }
 // prologue overlaps the previous kernel; griddepcontrol.wait guards all
 // activation reads and writes.
 cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a,
-                           const Conv0Params* c0, int grid, cudaStream_t st) {
-  static const Conv0Params zero{};
+                           int grid, cudaStream_t st) {
   static const StackMaps zs{};
-  const Conv0Params& p0 = c0 ? *c0 : zero;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.stream = st;
@@ -1233,70 +1157,70 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
     case 0:
       cfg.blockDim = dim3(ConvCfg<0>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<0>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<0>, tm_in, tm_out, a, p0, zs);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<0>, tm_in, tm_out, a, zs);
     case 1:
       cfg.blockDim = dim3(ConvCfg<1>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<1>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<1>, tm_in, tm_out, a, p0, zs);
-    case 2:
-      cfg.blockDim = dim3(ConvCfg<2>::kThreads);
-      cfg.dynamicSmemBytes = ConvCfg<2>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<2>, tm_in, tm_out, a, p0, zs);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<1>, tm_in, tm_out, a, zs);
     case 3:
       cfg.blockDim = dim3(ConvCfg<3>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<3>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<3>, tm_in, tm_out, a, p0, zs);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<3>, tm_in, tm_out, a, zs);
     case 4:
       cfg.blockDim = dim3(ConvCfg<4>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<4>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<4>, tm_in, tm_out, a, p0, zs);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<4>, tm_in, tm_out, a, zs);
     case 5:
       cfg.gridDim = dim3(std::max(4, grid & ~3));  // groups of 4 CTAs (output-channel quarters)
       cfg.blockDim = dim3(ConvCfg<5>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<5>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<5>, tm_in, tm_out, a, p0, zs);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<5>, tm_in, tm_out, a, zs);
     case 6:
       cfg.blockDim = dim3(ConvCfg<6>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<6>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<6>, tm_in, tm_out, a, p0, zs);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<6>, tm_in, tm_out, a, zs);
     case 7:
       cfg.blockDim = dim3(ConvCfg<7>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<7>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<7>, tm_in, tm_out, a, p0, zs);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<7>, tm_in, tm_out, a, zs);
     case 9:
       cfg.gridDim = dim3(std::max(4, grid & ~3));  // groups of 4 CTAs (output-channel quarters)
       cfg.blockDim = dim3(ConvCfg<9>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<9>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<9>, tm_in, tm_out, a, p0, zs);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<9>, tm_in, tm_out, a, zs);
     case 11:
       cfg.gridDim = dim3(std::max(2, grid & ~1));  // pairs of CTAs (output-channel halves)
       cfg.blockDim = dim3(ConvCfg<11>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<11>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<11>, tm_in, tm_out, a, p0, zs);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<11>, tm_in, tm_out, a, zs);
     case 10:
       cfg.blockDim = dim3(ConvCfg<10>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<10>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<10>, tm_in, tm_out, a, p0, zs);
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<10>, tm_in, tm_out, a, zs);
   }
   return cudaErrorInvalidValue;
 }
 
-// Layer stack (mode 8): grid <= #SMs so every CTA is co-resident (1 CTA/SM);
-// rowcnt must be zero on entry.
+// Layer stack (mode 8): a cooperative launch, so the driver guarantees that
+// all `grid` CTAs are co-resident (the deadlock-freedom argument of ItemIter
+// needs it) or fails the launch (cudaErrorCooperativeLaunchTooLarge, e.g.
+// under MPS SM limits), in which case the host falls back to the per-layer
+// kernels.  rowcnt and status must be zero on entry.
 cudaError_t launch_conv_stack(const CUtensorMap& tm_in0, const CUtensorMap& tm_out1, const StackMaps& sm,
                               const ConvArgs& a, int grid, cudaStream_t st) {
-  static const Conv0Params zero{};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(ConvCfg<8>::kThreads);
   cfg.dynamicSmemBytes = ConvCfg<8>::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<8>, tm_in0, tm_out1, a, zero, sm);
+  cfg.numAttrs = (a.dbg & kDbgNoPdlStack) ? 1 : 2;
+  return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<8>, tm_in0, tm_out1, a, sm);
 }
 
 int debug_cycles(unsigned long long* out, int reset) {
@@ -1308,14 +1232,14 @@ int debug_cycles(unsigned long long* out, int reset) {
   return 0;
 }
 
-int conv_stack_error(int reset) {
-  int v = 0;
-  if (cudaMemcpyFromSymbol(&v, g_stack_err, sizeof(int)) != cudaSuccess) return -1;
-  if (reset) {
-    const int z = 0;
-    cudaMemcpyToSymbol(g_stack_err, &z, sizeof(int));
-  }
-  return v;
+bool conv_stack_fits(int num_sms, int grid) {
+  int dev = 0, coop = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) != cudaSuccess || !coop) return false;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv3x3_tc_kernel<8>, ConvCfg<8>::kThreads,
+                                                    ConvCfg<8>::kSmem) != cudaSuccess)
+    return false;
+  return (long long)per_sm * num_sms >= grid;
 }
 
 cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* out, cudaStream_t st) {
@@ -1374,9 +1298,6 @@ cudaError_t configure_kernels() {
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<1>::kSmem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(conv3x3_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)ConvCfg<2>::kSmem);
-  if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<3>::kSmem);
   if (e != cudaSuccess) return e;
@@ -1405,431 +1326,6 @@ cudaError_t configure_kernels() {
                            (int)ConvCfg<10>::kSmem);
   if (e != cudaSuccess) return e;
   return configure_edge_kernels();
-}
-
-// --------------------------------------------------------------------------
-// CTA-pair hidden layer (cta_group::2), per-layer form (prototype, TVS_PAIR2).
-//
-// Two CTAs of a cluster take two adjacent 128-px strips of the same rows; the
-// leader issues tcgen05.mma.cta_group::2 with M = 256: each CTA's TMEM gets
-// its own 128 pixels x N columns, and each CTA supplies HALF of the B operand
-// (D columns [0, N/2) from the leader's shared memory, [N/2, N) from the
-// peer's, at the same offset: tools/probe_pair_mma.cu).  Per SM this halves
-// the B bytes read and the MMA instructions per output row.  Because an MMA's
-// N range is split in half across the pair, every dy-range the slot ring can
-// ask for is packed as its own layout: [W(+1)|W(0)|W(-1)], [W(+1)|W(0)],
-// [W(0)|W(-1)], W(+1), W(0), W(-1) (this CTA's half of each: 320 rows x 128 B
-// per dx, 120 KB).  The accumulation per output pixel is the same MMA sequence
-// as the single-CTA kernel, so results are bitwise equal to it.
-//
-// Barriers: the leader's full[stage] counts both CTAs' TMA input rows and its
-// slot_empty[s] both CTAs' epilogue warps (8 arrivals); commits multicast to
-// both CTAs (empty, slot_full).  The weights land on the leader's wbar.
-#ifndef TVS_P2_STAGES
-#define TVS_P2_STAGES 3
-#endif
-#ifndef TVS_P2_GROUPS
-#define TVS_P2_GROUPS 3
-#endif
-constexpr int kP2Stages = TVS_P2_STAGES;
-constexpr int kP2Groups = TVS_P2_GROUPS;
-constexpr int kP2Threads = 32 * (2 + 4 * kP2Groups);
-constexpr int kP2RowsDx = 320;
-constexpr int kP2W = 3 * kP2RowsDx * 128;  // 120 KB per CTA
-constexpr size_t kP2Smem = 1024 + kP2W + kP2Stages * kInRowStride + 4 * kP2Groups * 4096 + 1024;
-static_assert(kP2Smem <= 232448, "pair kernel smem");
-// layout of the dy-range (d0, c): rows [64 d0, 64 (d0 + c)) of [W(+1)|W(0)|W(-1)]
-__host__ __device__ constexpr int p2_layout(int d0, int c) { return c == 3 ? 0 : (c == 2 ? 1 + d0 : 3 + d0); }
-__host__ __device__ constexpr int p2_row0(int L) { return L == 0 ? 0 : (L == 1 ? 96 : (L == 2 ? 160 : 224 + 32 * (L - 3))); }
-
-template <int kColl>  // 0 plain, 1 collector::a::fill, 2 ::use, 3 ::lastuse
-TVS_DEV void mma2(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
-  if constexpr (kColl == 0)
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-                 ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
-  else if constexpr (kColl == 1)
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::2.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n\t}"
-                 ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
-  else if constexpr (kColl == 2)
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::2.kind::f16.collector::a::use [%0], %1, %2, %3, p;\n\t}"
-                 ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
-  else
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}"
-                 ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc) : "memory");
-}
-TVS_DEV void commit2(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-               ::"r"(smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
-}
-// .cta_group::2: the completing mbarrier may live in the peer CTA of the pair
-TVS_DEV void tma_load_4d_to(void* dst, const void* tmap, uint32_t bar_cluster, int c0, int c1, int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2];"
-      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster),
-        "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
-}
-TVS_DEV void bulk_load_to(void* dst, const void* src, uint32_t bytes, uint32_t bar_cluster) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar_cluster) : "memory");
-}
-
-// segments of a pair: strip-pair rows ordered (image, strip pair, row); this
-// CTA's strip is 2 * pair_strip + rank
-struct SegIterP2 {
-  long long lo, hi, cur;
-  int half_strips, rank;
-  TVS_DEV SegIterP2(const ConvArgs& a, int rk) : rank(rk) {
-    half_strips = a.strips / 2;
-    const long long T = (long long)a.B * half_strips * a.rows;
-    const long long part = blockIdx.x / 2, nparts = gridDim.x / 2;
-    lo = T * part / nparts;
-    hi = T * (part + 1) / nparts;
-    cur = lo;
-  }
-  TVS_DEV bool next(const ConvArgs& a, Segment& g) {
-    if (cur >= hi) return false;
-    const long long col = cur / a.rows;
-    const int y0 = (int)(cur - col * a.rows);
-    const int n = (int)min((long long)(a.rows - y0), hi - cur);
-    g.b = (int)(col / half_strips);
-    g.x0 = ((int)(col % half_strips) * 2 + rank) * kStripPx;
-    g.ya = a.row0 + y0;
-    g.yb = g.ya + n;
-    g.h = 0;
-    g.layer = 0;
-    cur += n;
-    return true;
-  }
-};
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
-conv3x3_pair2_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
-                     const ConvArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  __shared__ uint64_t full[kP2Stages], empty[kP2Stages], slot_full[kSlots], slot_empty[kSlots], wbar, wpeer;
-  __shared__ uint32_t tmem_base_smem;
-  __shared__ __align__(16) float sShift[kC];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sW = smem;
-  uint8_t* sIn = sW + kP2W;
-  uint8_t* sOut = sIn + kP2Stages * kInRowStride;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  constexpr int NB = 64;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kP2Stages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < kSlots; ++i) { mbar_init(&slot_full[i], 1); mbar_init(&slot_empty[i], 8); }
-    mbar_init(&wbar, 1);
-    mbar_init(&wpeer, 1);
-    fence_barrier_init();
-  }
-  if (threadIdx.x < kC) sShift[threadIdx.x] = a.shift[threadIdx.x];
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_smem))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();  // peer barriers initialised before any remote arrival
-  tc_fence_after();
-  const uint32_t tmem = tmem_base_smem;
-  if (threadIdx.x == 0) {  // weights (independent of the previous layer): this CTA's half
-    mbar_arrive_expect_tx(&wbar, kP2W);
-    const uint8_t* wsrc = a.wpack + (size_t)rank * kP2W;
-    for (int i = 0; i < 3; ++i) bulk_load(sW + i * (kP2W / 3), wsrc + i * (kP2W / 3), kP2W / 3, &wbar);
-  }
-  if (rank == 1 && warp == 1 && lane == 0) {  // tell the leader once the peer's half has landed
-    mbar_wait(&wbar, 0);
-    mbar_arrive_remote(mapa_shared(smem_u32(&wpeer), 0));
-  }
-  pdl_launch_dependents();
-  pdl_wait();
-
-  if (warp == 0) {
-    // ------------------------------------------------ TMA producer ----
-    if (elect_one()) {
-      prefetch_tmap(&tm_in);
-      int stage = 0;
-      uint32_t phase = 0;
-      SegIterP2 it(a, (int)rank);
-      Segment g;
-      while (it.next(a, g)) {
-        const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
-        for (int r = r0; r <= r1; ++r) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kInRowBytes);
-          tma_load_4d_to(sIn + stage * kInRowStride, &tm_in, mapa_shared(smem_u32(&full[stage]), 0), 0, g.x0 - 1,
-                         r, g.b);
-          if (++stage == kP2Stages) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (leader) ----
-    if (rank == 0) {
-      const uint64_t adesc0 = make_smem_desc(smem_u32(sIn), 0, 1024, kLayoutSW128);
-      const uint64_t bdesc0 = make_smem_desc(smem_u32(sW), 0, 1024, kLayoutSW128);
-      const bool leader = elect_one();
-      mbar_wait(&wbar, 0);
-      mbar_wait(&wpeer, 0);
-      int stage = 0;
-      uint32_t phase = 0, seq = 0;
-      SegIterP2 it(a, 0);
-      Segment g;
-      // one MMA op of the dy-range (d0, c) into TMEM column tcol
-      auto op = [&](uint64_t ad, int dx, int k, int d0, int c, uint32_t tcol, uint32_t acc, int coll) {
-        const int L = p2_layout(d0, c);
-        const uint64_t bd = bdesc0 + (uint64_t)((dx * kP2RowsDx * 128 + p2_row0(L) * 128 + k * 32) >> 4);
-        const uint32_t idesc = make_idesc(256, 64 * c, kFmtF16, kFmtF16);
-        if (coll == 1) mma2<1>(tmem + tcol, ad, bd, idesc, acc);
-        else if (coll == 3) mma2<3>(tmem + tcol, ad, bd, idesc, acc);
-        else mma2<0>(tmem + tcol, ad, bd, idesc, acc);
-      };
-      const uint32_t i64 = make_idesc(256, 64, kFmtF16, kFmtF16), i128 = make_idesc(256, 128, kFmtF16, kFmtF16),
-                     i192 = make_idesc(256, 192, kFmtF16, kFmtF16);
-      auto bdl = [&](int dx, int k, int L) {  // B descriptor of layout L, dx block, K step k
-        return bdesc0 + (uint64_t)((dx * kP2RowsDx * 128 + p2_row0(L) * 128 + k * 32) >> 4);
-      };
-      bool prewaited = false;
-      while (it.next(a, g)) {
-        const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
-        for (int r = r0; r <= r1; ++r) {
-          // ---- fast path: interior input row (targets r-1, r, r+1 in the
-          // segment; r+1 enters its slot): fixed op patterns per slot phase,
-          // split pieces share A through the collector, next row's barriers
-          // probed mid-row (as in the single-CTA kernel)
-          if (r >= 1 && r - 1 >= g.ya && r + 1 <= g.yb - 1) {
-            const uint32_t sq = seq + (uint32_t)(r - 1 - g.ya);
-            const uint32_t sl = sq & (kSlots - 1);
-            const bool next_fast = (r + 2 <= g.yb - 1);
-            const int nstage = (stage + 1 == kP2Stages) ? 0 : stage + 1;
-            const uint32_t nphase = (stage + 1 == kP2Stages) ? (phase ^ 1) : phase;
-            const uint32_t sq2 = sq + 3;
-            bool pre_ok = false;
-            if (leader) {
-              if (!prewaited)
-                mbar_wait2(&slot_empty[(sq + 2) & (kSlots - 1)], (((sq + 2) >> 3) & 1) ^ 1, &full[stage], phase);
-              tc_fence_after();
-              const uint64_t ad_row = adesc0 + (uint64_t)((stage * kInRowStride) >> 4);
-              const uint32_t t0 = tmem + sl * NB;
-#pragma unroll
-              for (int dx = 0; dx < 3; ++dx)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
-                  const bool first = dx == 0 && k == 0;
-                  if (sl + 3 <= (uint32_t)kSlots) {
-                    if (first) {  // enter row r+1 (acc 0), keep r-1, r
-                      mma2<1>(t0 + 2 * NB, ad, bdl(dx, k, 5), i64, 0u);
-                      mma2<3>(t0, ad, bdl(dx, k, 1), i128, 1u);
-                    } else {
-                      mma2<0>(t0, ad, bdl(dx, k, 0), i192, 1u);
-                    }
-                  } else if (sl + 2 == (uint32_t)kSlots) {  // slots 6, 7 | wrap | 0
-                    mma2<1>(tmem, ad, bdl(dx, k, 5), i64, first ? 0u : 1u);
-                    mma2<3>(t0, ad, bdl(dx, k, 1), i128, 1u);
-                  } else {  // slot 7 | wrap | 0, 1
-                    mma2<1>(t0, ad, bdl(dx, k, 3), i64, 1u);
-                    if (first) {
-                      mma2<2>(tmem, ad, bdl(dx, k, 4), i64, 1u);
-                      mma2<3>(tmem + NB, ad, bdl(dx, k, 5), i64, 0u);
-                    } else {
-                      mma2<3>(tmem, ad, bdl(dx, k, 2), i128, 1u);
-                    }
-                  }
-                  if (((dx == 1 && k == 1) || (dx == 2 && k == 2)) && next_fast && !pre_ok)
-                    pre_ok = mbar_test(&slot_empty[sq2 & (kSlots - 1)], ((sq2 >> 3) & 1) ^ 1) &&
-                             mbar_test(&full[nstage], nphase);
-                }
-              commit2(&empty[stage]);
-              commit2(&slot_full[sl]);
-            }
-            __syncwarp();
-            prewaited = next_fast && pre_ok;
-            stage = nstage;
-            phase = nphase;
-            continue;
-          }
-          prewaited = false;
-          const int q_lo = max(r - 1, g.ya), q_hi = min(r + 1, g.yb - 1);
-          const int q_new = (r == 0) ? q_lo : r + 1;
-          for (int q = max(q_new, q_lo); q <= q_hi; ++q) {
-            const uint32_t sq = seq + (uint32_t)(q - g.ya);
-            mbar_wait(&slot_empty[sq & (kSlots - 1)], ((sq >> 3) & 1) ^ 1);
-          }
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          if (leader && q_lo <= q_hi) {
-            // target rows [q_lo, q_hi] -> consecutive slots, split at the ring
-            // wrap; rows >= q_new enter their slot on the first K step (acc 0)
-            const uint32_t s_lo = (seq + (uint32_t)(q_lo - g.ya)) & (kSlots - 1);
-            const int cnt = q_hi - q_lo + 1;
-            const int c0 = min(cnt, kSlots - (int)s_lo), c1 = cnt - c0;
-            const uint64_t ad_row = adesc0 + (uint64_t)((stage * kInRowStride) >> 4);
-#pragma unroll
-            for (int dx = 0; dx < 3; ++dx)
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint64_t ad = ad_row + (uint64_t)((dx * 128 + k * 32) >> 4);
-                const bool first = dx == 0 && k == 0;
-                // pieces: [q_lo, q_lo + c0) at slot s_lo, [q_lo + c0, q_hi] at slot 0; on the
-                // first step each piece splits at q_new (old rows acc 1, new rows acc 0)
-                for (int piece = 0; piece < 2; ++piece) {
-                  const int pa = piece == 0 ? q_lo : q_lo + c0;
-                  const int pb = piece == 0 ? q_lo + c0 - 1 : q_hi;
-                  if (pa > pb) continue;
-                  const uint32_t pslot = piece == 0 ? s_lo : 0u;
-                  if (!first) {
-                    op(ad, dx, k, pa - (r - 1), pb - pa + 1, pslot * NB, 1u, 0);
-                  } else {
-                    const int ae = min(pb, q_new - 1), bb = max(pa, q_new);
-                    if (pa <= ae) op(ad, dx, k, pa - (r - 1), ae - pa + 1, pslot * NB, 1u, 0);
-                    if (bb <= pb) op(ad, dx, k, bb - (r - 1), pb - bb + 1, (pslot + (uint32_t)(bb - pa)) * NB, 0u, 0);
-                  }
-                }
-              }
-            commit2(&empty[stage]);
-            for (int q = q_lo; q <= q_hi; ++q)
-              if (min(q + 1, a.H - 1) == r) commit2(&slot_full[(seq + (uint32_t)(q - g.ya)) & (kSlots - 1)]);
-          } else if (leader) {
-            commit2(&empty[stage]);
-          }
-          __syncwarp();
-          if (++stage == kP2Stages) { stage = 0; phase ^= 1; }
-        }
-        seq += (uint32_t)(g.yb - g.ya);
-      }
-    }
-  } else {
-    // ------------------------------------------------ epilogue (both CTAs) ----
-    const int ew = warp - 2;                   // 0 .. 4*kP2Groups-1
-    const uint32_t grp = (uint32_t)(ew >> 2);
-    const int quarter = warp & 3;
-    const int px = quarter * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-    const int stg = (int)(grp * 4) + quarter;
-    const uint32_t stage_out = smem_u32(sOut + stg * 4096);
-    const uint32_t shift_u = smem_u32(sShift);
-    if (lane == 0) prefetch_tmap(&tm_out);
-    uint32_t seq = 0, gsel = 0;
-    SegIterP2 it(a, (int)rank);
-    Segment g;
-    while (it.next(a, g)) {
-      for (int q = g.ya; q < g.yb; ++q, ++seq, gsel = (gsel + 1 == kP2Groups) ? 0 : gsel + 1) {
-        if (gsel != grp) continue;
-        const uint32_t slot = seq & (kSlots - 1);
-        mbar_wait(&slot_full[slot], (seq >> 3) & 1);
-        tc_fence_after();
-        uint32_t v[4][16];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) tmem_ld16(tmem + lane_addr + slot * NB + j * 16, v[j]);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 4; ++j) reg_fence16(v[j]);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (rank == 0) mbar_arrive(&slot_empty[slot]);
-          else mbar_arrive_remote(mapa_shared(smem_u32(&slot_empty[slot]), 0));
-        }
-        if (lane == 0) bulk_wait_read<0>();
-        __syncwarp();
-        const uint32_t rowp = stage_out + lane * 128;
-#pragma unroll
-        for (int chunk = 0; chunk < 8; ++chunk) {
-          const float4 s0 = ld_shared_f4(shift_u + chunk * 32);
-          const float4 s1 = ld_shared_f4(shift_u + chunk * 32 + 16);
-          const float sh[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-          uint32_t packed[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = chunk * 8 + e * 2;
-            const float2 fs = __fadd2_rn(make_float2(__uint_as_float(v[c >> 4][c & 15]),
-                                                     __uint_as_float(v[c >> 4][(c & 15) + 1])),
-                                         make_float2(sh[2 * e], sh[2 * e + 1]));
-            asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(packed[e]) : "f"(fs.y), "f"(fs.x));
-          }
-          st_shared_v4(rowp + ((chunk ^ (lane & 7)) << 4), packed[0], packed[1], packed[2], packed[3]);
-        }
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_4d(&tm_out, sOut + stg * 4096, 0, g.x0 + quarter * 32, q, g.b);
-          bulk_commit();
-        }
-        (void)px;
-      }
-    }
-    if (lane == 0) bulk_wait<0>();
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();  // remote arrivals and the leader's MMAs into the peer's TMEM are done
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-  }
-}
-
-__global__ void pack_hidden_pair2_kernel(const float* __restrict__ w, const float* __restrict__ scale,
-                                         uint8_t* __restrict__ out) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*64 + ci
-  if (idx >= kC * kC) return;
-  const int co = idx / kC, ci = idx % kC;
-  float wv[9], rn[9];
-#pragma unroll
-  for (int t = 0; t < 9; ++t) wv[t] = w[idx * 9 + t] * scale[co];
-  dc_round9(wv, rn);
-  for (int t = 0; t < 9; ++t) {
-    const int ky = t / 3, kx = t % 3;
-    const int n = (2 - ky) * 64 + co;  // row of [W(+1)|W(0)|W(-1)]
-    const __half v = __float2half_rn(rn[t]);
-    for (int L = 0; L < 6; ++L) {
-      const int d0 = L == 0 ? 0 : (L <= 2 ? L - 1 : L - 3), c = L == 0 ? 3 : (L <= 2 ? 2 : 1);
-      if (n < 64 * d0 || n >= 64 * (d0 + c)) continue;
-      const int local = n - 64 * d0, half = local / (32 * c), r = p2_row0(L) + local % (32 * c);
-      uint8_t* base = out + (size_t)half * kP2W + (size_t)kx * kP2RowsDx * 128;
-      *reinterpret_cast<__half*>(base + r * 128 + (((ci >> 3) ^ (r & 7)) << 4) + (ci & 7) * 2) = v;
-    }
-  }
-}
-
-size_t conv_pair2_wpack_bytes() { return 2 * (size_t)kP2W; }
-
-cudaError_t launch_pack_hidden_pair2(const float* w, const float* scale, uint8_t* out, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(out, 0, 2 * (size_t)kP2W, st);
-  if (e != cudaSuccess) return e;
-  pack_hidden_pair2_kernel<<<(kC * kC + 127) / 128, 128, 0, st>>>(w, scale, out);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_conv_pair2(const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a, int grid,
-                              cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv3x3_pair2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kP2Smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(std::max(2, grid & ~1));
-  cfg.blockDim = dim3(kP2Threads);
-  cfg.dynamicSmemBytes = kP2Smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, conv3x3_pair2_kernel, tm_in, tm_out, a);
 }
 
 }  // namespace tvs

@@ -18,6 +18,7 @@
 
 #include <cfloat>
 #include <cmath>
+#include "common.cuh"
 #include <cstdint>
 
 namespace tvs {
@@ -223,13 +224,13 @@ cudaError_t launch_band_stats(const float* gt, const float* pred, int planes, in
   const int ih = H - 2 * kR, iw = W - 2 * kR;
   if (ih > 0 && iw > 0) {
     const int tx = (iw + kTile - 1) / kTile, ty = (ih + kTile - 1) / kTile;
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(ssim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)band_stats_ssim_smem());
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
+    static std::mutex mu;
+    static uint64_t done = 0;
+    cudaError_t e = once_per_device(mu, done, [] {
+      return cudaFuncSetAttribute(ssim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)band_stats_ssim_smem());
+    });
+    if (e != cudaSuccess) return e;
     ssim_kernel<<<planes * tx * ty, 256, band_stats_ssim_smem(), st>>>(gt, pred, H, W, range_override, stats, tx,
                                                                          ty);
   }

@@ -396,6 +396,30 @@ TVS_DEV int ld_relaxed_gpu(const int* p) {
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+TVS_DEV unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// KernelSpan bookkeeping (common.cuh), called by one thread per CTA
+template <typename Span>
+TVS_DEV void span_open(Span* sp) { atomicMin(&sp->start, globaltimer_ns()); }
+template <typename Span>
+TVS_DEV void span_close(Span* sp) {
+  atomicMax(&sp->end, globaltimer_ns());
+  __threadfence();
+  if (atomicAdd(&sp->done, 1u) == gridDim.x * gridDim.y * gridDim.z - 1) {
+    __threadfence();
+    const unsigned long long s = *(volatile unsigned long long*)&sp->start;
+    const unsigned long long e = *(volatile unsigned long long*)&sp->end;
+    sp->total_ns += e - s;
+    sp->launches += 1;
+    sp->start = ~0ull;
+    sp->end = 0;
+    sp->done = 0;
+    __threadfence();
+  }
+}
 TVS_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 TVS_DEV void red_release_gpu_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

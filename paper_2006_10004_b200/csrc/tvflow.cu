@@ -32,6 +32,7 @@
 // neighbour, exchanged through shared memory.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <mutex>
 
 #include <cfloat>
 #include <cmath>
@@ -638,10 +639,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tvflow_cluster_kernel(const TvF
 namespace {
 constexpr int kTvSmemMax = 224 * 1024;  // dynamic; static (~1 KB) + dynamic <= 227 KB opt-in
 static_assert(kTcMaxPx * 5 * 8 <= kTvSmemMax, "cluster kernel state exceeds shared memory");
-int g_max_cluster = 0;  // largest usable cluster size, probed once
+// largest usable cluster size per device ordinal (attributes and occupancy are
+// per device context), probed once per device under a lock
+std::mutex g_cluster_mu;
+int g_max_cluster[64] = {};
 
 int usable_cluster_max() {
-  if (g_max_cluster) return g_max_cluster;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cluster_mu);
+  if (dev < 64 && g_max_cluster[dev]) return g_max_cluster[dev];
   cudaFuncSetAttribute(tvflow_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTvSmemMax);
   cudaFuncSetAttribute(tvflow_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   int best = 1;
@@ -661,7 +668,7 @@ int usable_cluster_max() {
     if (cudaOccupancyMaxActiveClusters(&n, tvflow_cluster_kernel, &cfg) == cudaSuccess && n > 0) best = g;
     cudaGetLastError();
   }
-  g_max_cluster = best;
+  if (dev < 64) g_max_cluster[dev] = best;
   return best;
 }
 }  // namespace

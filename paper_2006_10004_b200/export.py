@@ -152,22 +152,41 @@ def _predict_planes_batch(model, images: list[np.ndarray], closure: str) -> np.n
 
 
 def _batched_export(model, jobs, batch_images: int, closure: str, io_threads: int) -> int:
-    """jobs: list of (src_path, dst_path, plane_index).  Groups equal shapes,
-    overlaps reads / writes with the GPU forward."""
+    """jobs: list of (src_path, dst_path, plane_index).  Works through the jobs
+    in bounded windows (a few batches of files at a time, so host memory does
+    not grow with the dataset), groups equal shapes inside a window, and
+    overlaps the next window's reads and this window's writes with the GPU
+    forward."""
     if closure not in ("fused", "host"):
         raise ValueError("closure must be 'fused' or 'host'")
+    window = max(1, batch_images) * 4
+
+    def read_plane(job):  # copy the plane out so the rest of the file buffer is freed
+        return np.array(read_tensor(job[0])[job[2]], copy=True)
+
     with ThreadPoolExecutor(max(1, io_threads)) as pool:
-        planes = list(pool.map(lambda j: read_tensor(j[0])[j[2]], jobs))
-        by_shape: dict[tuple, list[int]] = {}
-        for i, p in enumerate(planes):
-            by_shape.setdefault(p.shape, []).append(i)
         writes = []
-        for idx in by_shape.values():
-            for s in range(0, len(idx), batch_images):
-                chunk = idx[s : s + batch_images]
-                out = _predict_planes_batch(model, [planes[i] for i in chunk], closure)
-                for k, i in enumerate(chunk):
-                    writes.append(pool.submit(write_tensor, jobs[i][1], out[k]))
+        nxt = [pool.submit(read_plane, j) for j in jobs[0:window]]
+        for w0 in range(0, len(jobs), window):
+            planes = [f.result() for f in nxt]
+            nxt = [pool.submit(read_plane, j) for j in jobs[w0 + window:w0 + 2 * window]]
+            by_shape: dict[tuple, list[int]] = {}
+            for i, p in enumerate(planes):
+                by_shape.setdefault(p.shape, []).append(i)
+            for idx in by_shape.values():
+                for s in range(0, len(idx), batch_images):
+                    chunk = idx[s : s + batch_images]
+                    out = _predict_planes_batch(model, [planes[i] for i in chunk], closure)
+                    for k, i in enumerate(chunk):
+                        writes.append(pool.submit(write_tensor, jobs[w0 + i][1], out[k]))
+            del planes
+            pending = []
+            for w in writes:  # surface finished writes' errors, keep the rest
+                if w.done():
+                    w.result()
+                else:
+                    pending.append(w)
+            writes = pending
         for w in writes:
             w.result()
     return len(jobs)

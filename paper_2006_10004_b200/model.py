@@ -58,7 +58,7 @@ class TVSpecNet(nn.Module):
     """DnCNN-shaped regressor from an image to its first ``out_bands`` bands."""
 
     def __init__(self, depth: int = 17, channels: int = 64, out_bands: int = 5, *, precision: str = "fast",
-                 unshuffle: int = 1):
+                 unshuffle: int = 1, options: dict | None = None):
         super().__init__()
         if depth < 3:
             raise ValueError("depth must be at least 3 (first, hidden, last)")
@@ -81,6 +81,9 @@ class TVSpecNet(nn.Module):
         if precision not in _PRECISIONS:
             raise ValueError(f"precision must be one of {sorted(_PRECISIONS)}")
         self._precision = precision
+        # C-ABI plan options (include/tvs_b200.h tvs_plan_set_option), applied
+        # to every per-device plan this module creates
+        self._options: dict[str, int] = dict(options or {})
         self._plans: dict[int, tuple[_native.Plan, tuple]] = {}
 
     # ------------------------------------------------------------ config ----
@@ -97,6 +100,16 @@ class TVSpecNet(nn.Module):
         if value != self._precision:
             self._precision = value
             self._drop_plans()
+
+    @property
+    def plan_options(self) -> dict:
+        return dict(self._options)
+
+    def set_plan_option(self, name: str, value: int) -> None:
+        """Set a plan option (e.g. ``stack``, ``check``, ``watchdog_ms``); the
+        per-device plans are rebuilt with it at the next forward."""
+        self._options[name] = int(value)
+        self._drop_plans()
 
     def _drop_plans(self) -> None:
         for plan, _ in self._plans.values():
@@ -152,6 +165,9 @@ class TVSpecNet(nn.Module):
         plan = entry[0] if entry is not None else _native.Plan(
             idx, self.depth, self.channels, self.out_bands, _PRECISIONS[self._precision], self.unshuffle
         )
+        if entry is None:
+            for name, value in self._options.items():
+                plan.set_option(name, value)
         with torch.cuda.device(idx):
             stream = torch.cuda.current_stream(idx)
             dev = torch.device("cuda", idx)
@@ -312,6 +328,20 @@ class TVSpecNet(nn.Module):
                 sms = torch.cuda.get_device_properties(idx).multi_processor_count
                 cache[skey] = self._host_schedule(B, H, W, nrows, closure, sms)
             sizes = cache[skey]
+        # sub-batch forwards report their status at the final plan.sync (one
+        # synchronisation instead of one per sub-batch)
+        if self._options.get("check", 1) == 1:
+            plan.set_option("check", 2)
+            try:
+                return self._pipeline(plan, x_pin, out, cout, sizes, dev, closure, row0, nrows)
+            finally:
+                plan.set_option("check", 1)
+        return self._pipeline(plan, x_pin, out, cout, sizes, dev, closure, row0, nrows)
+
+    def _pipeline(self, plan, x_pin, out, cout, sizes, dev, closure, row0, nrows):
+        B, _, H, W = x_pin.shape
+        K = self.out_bands
+        idx = dev.index
         bounds, s0 = [], 0
         for n in sizes:
             bounds.append((s0, s0 + n))
@@ -363,8 +393,13 @@ class TVSpecNet(nn.Module):
                         cout[s:e].copy_(cbuf[j][:nb], non_blocking=True)
                 b_free[j].record(d2h)
             d2h.synchronize()
-            comp.synchronize()
+            plan.sync(comp.cuda_stream)  # raises a deferred failure of any sub-batch
         return out, cout
+
+    def last_used_stack(self, device: int | None = None) -> bool:
+        """Whether the last forward on that device ran the layer-stack kernel."""
+        idx = torch.cuda.current_device() if device is None else device
+        return self._plans[idx][0].last_used_stack() if idx in self._plans else False
 
     def last_launch_count(self, device: int | None = None) -> int:
         idx = torch.cuda.current_device() if device is None else device

@@ -21,7 +21,7 @@ def test_library_loads_and_exports_all_symbols():
     lib = _native.load()
     for name in _declared():
         assert hasattr(lib, name), name
-    assert lib.tvs_abi_version() == 1
+    assert lib.tvs_abi_version() == 2
 
 
 def test_invalid_arguments_report_errors_without_gpu_work():
@@ -33,3 +33,6 @@ def test_invalid_arguments_report_errors_without_gpu_work():
     assert lib.tvs_plan_create(0, 17, 64, 5, 1, None) == _native.TVS_E_INVALID
     assert lib.tvs_forward(None, None, None, None, 1, 1, 1, 0, -1, None) == _native.TVS_E_INVALID
     assert lib.tvs_plan_destroy(None) == 0
+    assert lib.tvs_plan_set_option(None, b"stack", 1) == _native.TVS_E_INVALID
+    assert lib.tvs_plan_sync(None, None) == _native.TVS_E_INVALID
+    assert lib.tvs_last_used_stack(None) == 0

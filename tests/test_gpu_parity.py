@@ -5,8 +5,6 @@ Tolerances (BASELINE.json north_star), relative L2 per image per band:
   * precision="fast": <= 1e-2, closure (band-sum reconstruction) <= 1e-2
 All calls go through the C ABI (libtvsb200.so) via the drop-in module.
 """
-import os
-
 import numpy as np
 import pytest
 import torch
@@ -247,34 +245,8 @@ def test_nontrivial_batchnorm_stats(oracle):
 def test_launch_accounting(model):
     x = torch.rand(1, 1, 64, 64, device="cuda")
     model(x)
-    assert model.last_launch_count() == model.depth  # conv0 + (depth-2) hidden + head
-
-
-def test_fused_conv0_path(seeded_state, oracle, monkeypatch):
-    """Opt-in K1 fusion (TVS_FUSE_CONV0=1): conv0 computed by the first hidden
-    layer's producer warps; identical numerics contract, one launch fewer."""
-    monkeypatch.setenv("TVS_FUSE_CONV0", "1")
-    m = TVSpecNet().eval()
-    m.load_state_dict(seeded_state)
-    x = np.stack([make_image(CONFIGS[2], i) for i in range(2)])[:, None]
-    with torch.no_grad():
-        ref = oracle(torch.from_numpy(x)).numpy()
-    _check(m, x, ref)
-    assert m.last_launch_count() == m.depth - 1
-    # bitwise equal to the unfused CUDA-core K1 (same fp32 FFMA arithmetic, fp16
-    # rounding); the tcgen05 K1 (TF32 hi/lo split) agrees to fp16 rounding
-    monkeypatch.setenv("TVS_FUSE_CONV0", "0")
-    monkeypatch.setenv("TVS_CONV0_TC", "0")
-    m2 = TVSpecNet().eval()
-    m2.load_state_dict(seeded_state)
-    xd = torch.from_numpy(x).cuda()
-    assert torch.equal(m(xd), m2(xd))
-    monkeypatch.setenv("TVS_CONV0_TC", "1")
-    m3 = TVSpecNet().eval()
-    m3.load_state_dict(seeded_state)
-    _check(m3, x, ref)
-    a, b = m3(xd), m2(xd)  # fp16 rounding flips, amplified over 16 fp16 layers
-    assert (torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(b)).item() < 5e-3
+    # input-scale + conv0 + (depth-2) hidden + head
+    assert model.last_launch_count() == model.depth + 1
 
 
 def test_conv0_tcgen05_matches_fp32_conv0(seeded_state):
@@ -283,14 +255,9 @@ def test_conv0_tcgen05_matches_fp32_conv0(seeded_state):
     activations may differ by one fp16 ulp where the sums differ in the last
     fp32 bits.  Signed inputs of larger magnitude exercise the hi/lo split."""
     outs = []
-    for env in ("1", "0"):
-        os.environ["TVS_CONV0_TC"] = env
-        try:
-            m = TVSpecNet(depth=3).eval()  # conv0 -> 1 hidden -> head: conv0 dominates
-            m.load_state_dict(build_seeded_state(3, 64, 5))
-            m._plan_for(torch.device("cuda", 0))
-        finally:
-            os.environ.pop("TVS_CONV0_TC")
+    for tc in (1, 0):
+        m = TVSpecNet(depth=3, options={"conv0_tc": tc}).eval()  # conv0 -> 1 hidden -> head: conv0 dominates
+        m.load_state_dict(build_seeded_state(3, 64, 5))
         outs.append(m)
     g = torch.Generator().manual_seed(3)
     for x in (torch.rand(2, 1, 40, 300, generator=g), torch.randn(2, 1, 40, 300, generator=g) * 30):
@@ -308,20 +275,19 @@ def test_abi_errors_on_gpu(model):
     y = torch.empty(1, 5, 8, 8, device="cuda")
     with pytest.raises(ValueError):
         plan.forward(x.data_ptr(), y.data_ptr(), 0, 1, 8, 8, 6, 5, 0)  # window past H
-    assert _native.load().tvs_abi_version() == 1
+    assert _native.load().tvs_abi_version() == 2
+    with pytest.raises(ValueError):
+        plan.set_option("no_such_option", 1)
+    with pytest.raises(ValueError):
+        plan.set_option("check", 7)
 
 
 @pytest.mark.gpu
-def test_fp32_cuda_core_kernels(golden, monkeypatch):
-    """The CUDA-core fp32 kernels (TVS_FP32_CUDA=1; the path of the wide variant)
-    on the 64-channel model: same 1e-5 gate as the default tcgen05 fp32 mode."""
-    monkeypatch.setenv("TVS_FP32_CUDA", "1")
-    import torch
-
-    from oracle.tvspecnet_oracle import band_rel_l2, build_seeded_state
-    from paper_2006_10004_b200 import TVSpecNet
-
-    m = TVSpecNet(precision="fp32")
+def test_fp32_cuda_core_kernels(golden):
+    """The CUDA-core fp32 kernels (plan option fp32_cuda=1; the path of the wide
+    variant's fp32 mode) on the 64-channel model: same 1e-5 gate as the default
+    tcgen05 fp32 mode."""
+    m = TVSpecNet(precision="fp32", options={"fp32_cuda": 1})
     m.load_state_dict(build_seeded_state())
     m = m.cuda().eval()
     for case in ("small", "nonsq", "cfg1"):
@@ -330,38 +296,26 @@ def test_fp32_cuda_core_kernels(golden, monkeypatch):
         assert band_rel_l2(out, golden[f"{case}_y"]).max() <= 1e-5, case
 
 
-def _stack_model(seeded_state, monkeypatch, stack):
-    monkeypatch.setenv("TVS_STACK", str(stack))
-    m = TVSpecNet().eval()
+def _stack_model(seeded_state, stack, **opts):
+    m = TVSpecNet(options={"stack": stack, **opts}).eval()
     m.load_state_dict(seeded_state)
-    m._plan_for(torch.device("cuda", 0))  # the plan reads TVS_STACK when it is created
-    monkeypatch.delenv("TVS_STACK")
     return m
 
 
-def _stack_watchdog():
-    import ctypes
-    lib = _native.load()
-    lib.tvs_debug_stack.restype = ctypes.c_int
-    lib.tvs_debug_stack.argtypes = [ctypes.c_int]
-    return lib.tvs_debug_stack(1)
-
-
 @pytest.mark.parametrize("shape", [(2, 48, 160), (1, 37, 300), (3, 64, 128), (1, 5, 7), (2, 1, 130)])
-def test_layer_stack_bitwise(seeded_state, monkeypatch, shape):
+def test_layer_stack_bitwise(seeded_state, shape):
     """The layer-stack kernel (conv_tc.cu mode 8: all hidden layers in one
     persistent launch, layers handed over through L2 under row flags) computes
     every output with the per-layer kernel's exact MMA sequence: bitwise equal,
     including ragged strips (W % 128 != 0), H < 3 and W < 128."""
-    _stack_watchdog()
-    m0 = _stack_model(seeded_state, monkeypatch, 0)
-    m1 = _stack_model(seeded_state, monkeypatch, 1)
+    m0 = _stack_model(seeded_state, 0)
+    m1 = _stack_model(seeded_state, 1)
     x = torch.rand(*shape[:1], 1, *shape[1:], generator=torch.Generator().manual_seed(sum(shape))).cuda()
     with torch.no_grad():
-        y0, y1 = m0(x), m1(x)
+        y0, y1 = m0(x), m1(x)  # the default "check" option raises on a watchdog expiry
     torch.cuda.synchronize()
-    assert _stack_watchdog() == 0
-    assert m0.last_launch_count() == m0.depth and m1.last_launch_count() == 3
+    assert not m0.last_used_stack() and m1.last_used_stack()
+    assert m0.last_launch_count() == m0.depth + 1 and m1.last_launch_count() == 4
     assert torch.equal(y0, y1)
 
 
@@ -371,11 +325,9 @@ def test_layer_stack_auto_config2(seeded_state, oracle):
     m = TVSpecNet().eval()
     m.load_state_dict(seeded_state)
     x = np.stack([make_image(CONFIGS[2], i) for i in range(64)])[:, None]
-    _stack_watchdog()
     bands, clos = m.forward_planes(torch.from_numpy(x).cuda(), closure=True)
     torch.cuda.synchronize()
-    assert _stack_watchdog() == 0
-    assert m.last_launch_count() == 3
+    assert m.last_used_stack() and m.last_launch_count() == 4
     with torch.no_grad():
         ref = oracle(torch.from_numpy(x[[0, 63]])).numpy()
     err = band_rel_l2(bands.cpu().numpy()[[0, 63]], ref)
@@ -384,18 +336,15 @@ def test_layer_stack_auto_config2(seeded_state, oracle):
 
 
 @pytest.mark.parametrize("pairs,tol", [(24, 1e-2), (12, 1e-2), (6, 1.5e-2), (0, 2e-2)])
-def test_wide_pair_schedules(wide_case, monkeypatch, pairs, tol):
+def test_wide_pair_schedules(wide_case, pairs, tol):
     """Wide variant, fast mode: the first `pairs` hidden layers read fp16 hi/lo
     pair activations (conv_tc.cu mode 5), the rest single fp16 (mode 9, head
     mode 10).  24 (all) and 12 (the default) meet the 1e-2 gate; fewer pairs
     trade accuracy for MMA work (tools/emulate_wide.py: 6 -> ~1.06e-2, 0 ->
     1.1-1.3e-2, the plain-fp16 roofline probe)."""
     state, x, y32, _ = wide_case
-    monkeypatch.setenv("TVS_WIDE_PAIR", str(pairs))
-    m = TVSpecNet(26, 128, 5).eval()
+    m = TVSpecNet(26, 128, 5, options={"wide_pair_layers": pairs}).eval()
     m.load_state_dict(state)
-    m._plan_for(torch.device("cuda", 0))
-    monkeypatch.delenv("TVS_WIDE_PAIR")
     out, clos = _run(m, x)
     err = band_rel_l2(out, y32).max()
     assert err <= tol, f"pairs={pairs}: worst band rel-L2 {err:.3e}"
@@ -427,25 +376,3 @@ def test_conv0_tcgen05_ragged(seeded_state, oracle, shape):
     with torch.no_grad():
         ref = oracle(torch.from_numpy(x)).numpy()
     _check(m, x, ref)
-
-
-@pytest.mark.parametrize("shape", [(2, 1, 48, 160), (3, 1, 64, 256), (1, 1, 5, 130), (2, 1, 1, 512)])
-def test_cta_pair_prototype_bitwise(seeded_state, shape):
-    """TVS_PAIR2=1 (CTA-pair hidden layers, cta_group::2 with M=256 and the B
-    operand split across the pair) gives bitwise the single-CTA result: every
-    output pixel sees the same MMA sequence."""
-    outs = []
-    for env in ("0", "1"):
-        os.environ["TVS_PAIR2"] = env
-        os.environ["TVS_STACK"] = "0"
-        try:
-            m = TVSpecNet().eval()
-            m.load_state_dict(seeded_state)
-            m._plan_for(torch.device("cuda", 0))
-        finally:
-            os.environ.pop("TVS_PAIR2")
-            os.environ.pop("TVS_STACK")
-        outs.append(m)
-    x = torch.rand(*shape, generator=torch.Generator().manual_seed(shape[2])).cuda()
-    with torch.no_grad():
-        assert torch.equal(outs[0](x), outs[1](x))

@@ -103,16 +103,18 @@ def test_dataset_crops_match_reference(golden_tv, tmp_path):
 
     ref = json.loads(str(golden_tv["gt_manifest"]))
     paths = make_images(tmp_path / "img")
-    crops, metas = gt._draw_entries([str(p) for p in paths], GT_KW["count"], GT_KW["crop_size"], GT_KW["seed"],
-                                    GT_KW["augment_fraction"])
-    stacked = np.stack(crops)
+    cache = {}
+    specs = gt.plan_crops([str(p) for p in paths], GT_KW["count"], GT_KW["crop_size"], GT_KW["seed"],
+                          GT_KW["augment_fraction"], cache)
+    stacked = np.stack([gt._cut(cache[s.source], s.crop_size, s.row, s.col, s.factor) for s in specs])
     mean, std = float(stacked.mean()), float(stacked.std())
     assert mean == ref["preprocessing"]["mean"] and std == ref["preprocessing"]["std"]
     grids = ((stacked - mean) / std).astype("<f4")
     assert np.array_equal(grids, golden_tv["gt_planes"][:, 0])
-    for m, e in zip(metas, ref["entries"]):
-        assert list(m.crop_offset) == e["crop_offset"] and m.downsample_factor == e["downsample_factor"]
-        assert list(m.crop_size) == e["crop_size"] and m.seed_spawn == e["seed_spawn"]
+    for s, e in zip(specs, ref["entries"]):
+        m = s.manifest_entry(e["solver_warnings"])
+        assert m["crop_offset"] == e["crop_offset"] and m["downsample_factor"] == e["downsample_factor"]
+        assert m["crop_size"] == e["crop_size"] and m["seed_spawn"] == e["seed_spawn"]
     # preprocess() reproduces an entry's input plane (dataset.py:96-110)
     e0 = ref["entries"][1]
     one = gt.preprocess(paths[1], GT_KW["crop_size"], GT_KW["seed"], mean, std, index=1,

@@ -1,4 +1,4 @@
-"""MMA-issuer cycle accounting (TVS_CONV_DBG bit 15): where the single MMA
+"""MMA-issuer cycle accounting (plan option debug, bit 15): where the single MMA
 thread of each CTA spends its time, summed over CTAs, for one forward."""
 import ctypes
 import os
@@ -17,25 +17,23 @@ lib.tvs_debug_cycles.restype = ctypes.c_int
 lib.tvs_debug_cycles.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-extra = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # more TVS_CONV_DBG bits (ablations)
+extra = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # more debug bits (ablations)
 for stack in ("1",):  # the accounting is compiled into the layer-stack kernel only
-    os.environ["TVS_STACK"] = stack
-    m = TVSpecNet().eval()
+    m = TVSpecNet(options={"stack": int(stack)}).eval()
     m.load_state_dict(build_seeded_state())
     m = m.cuda()
-    m._plan_for(torch.device("cuda", 0))
-    os.environ.pop("TVS_STACK")
+    plan = m._plan_for(torch.device("cuda", 0))
     x = torch.from_numpy(make_batch(CONFIGS[cfg], 0, n)).cuda()
     with torch.no_grad():
         m(x)
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * 8)()
     lib.tvs_debug_cycles(buf, 1)
-    os.environ["TVS_CONV_DBG"] = str(32768 | extra)
+    plan.set_option("debug", 32768 | extra)
     with torch.no_grad():
         m(x)
     torch.cuda.synchronize()
-    os.environ.pop("TVS_CONV_DBG")
+    plan.set_option("debug", 0)
     lib.tvs_debug_cycles(buf, 1)
     tot = buf[0] or 1
     print(f"stack={stack} dbg+{extra} config {cfg} x{n}: total {tot / 1e9:.3f} Gcyc (sum over CTAs); "

@@ -1,5 +1,5 @@
 """Worst-band error of the wide variant's fast mode per pair schedule
-(TVS_WIDE_PAIR) on config 5 images 0-1 against the fp32 oracle (GPU)."""
+(plan option wide_pair_layers) on config 5 images 0-1 against the fp32 oracle (GPU)."""
 import os
 import sys
 from pathlib import Path
@@ -19,10 +19,8 @@ x = np.stack([make_image(CONFIGS["5w"], i) for i in range(2)])[:, None]
 with torch.no_grad():
     ref = o(torch.from_numpy(x)).numpy()
 for pairs in (24, 16, 12, 8, 6, 0):
-    os.environ["TVS_WIDE_PAIR"] = str(pairs)
-    m = TVSpecNet(26, 128, 5).eval()
+    m = TVSpecNet(26, 128, 5, options={"wide_pair_layers": pairs}).eval()
     m.load_state_dict(state)
-    m._plan_for(torch.device("cuda", 0))
     with torch.no_grad():
         out = m(torch.from_numpy(x).cuda()).cpu().numpy()
     e = band_rel_l2(out, ref)
