@@ -378,7 +378,7 @@ def run_ours(args, spec):
             t = torch.tensor([e2e_s], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        e2e_px = ne * nrows * W * (world if _scaling(spec) == "weak" or band is not None else world)
+        e2e_px = ne * nrows * W * world  # every rank times its own share (max over ranks below)
         results[prec] = dict(value=value, ms=tot_ms / steps, ms_list=ms, launches=launches, steps=steps,
                              warmup=warm, clocks=clk.summary(), hid_ms=span_ms, hid_n=span_n, hid_flops=hid_flops,
                              e2e=e2e_px / 1e6 / e2e_s, hid_per_fwd=span_n / steps, used_stack=used_stack,

@@ -160,7 +160,7 @@ cudaError_t launch_conv0(int act_fmt, int C, const float* x, void* act, const Co
 // M_b = max|x_b| * w0_l1 + b0_max lies in [2^-6, 2^6], else round(log2 M_b) - 2;
 // counts non-finite inputs into status[kStatNonFiniteIn]
 cudaError_t launch_input_scale(const float* x, int B, long long px_per_image, float w0_l1, float b0_max, int* escale,
-                               int* status, cudaStream_t st);
+                               int* scratch, int* status, cudaStream_t st);
 cudaError_t launch_head_f32(int C, const float* act, const float* x, const float* wh, const float* bh, float* bands,
                             float* closure, int B, int H, int W, int K, int row0, int rows, int* status,
                             cudaStream_t st);

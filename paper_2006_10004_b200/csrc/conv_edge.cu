@@ -14,6 +14,7 @@
 //       sequential fp32 sum over all 576 terms lands at 1.0e-5 from the
 //       reference - too close to the 1e-5 gate; chunked
 //       partials are as good as full fp64 (5.1e-6).
+#include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
@@ -393,35 +394,27 @@ cudaError_t launch_hidden_f32(int C, const float* in, float* out, const float* w
 }
 
 // ------------------------------------------------ per-image input scale ----
-// One block per image: amax over the plane and a non-finite count.  The
-// exponent keeps the conv0 output bound M = amax * w0_l1 + b0_max (and with
-// it every fp16 activation of a well-conditioned network) near 1: inputs
-// whose M lies in [2^-6, 2^6] (every BASELINE workload) keep e = 0, so their
+// Grid (chunks, B): each block reduces one chunk of image b to amax and a
+// non-finite flag, merges them with atomics (amax as order-preserving bits of
+// a non-negative float), and the image's last block turns them into e_b.  The
+// exponent keeps the conv0 output bound M = amax * w0_l1 + b0_max (and with it
+// every fp16 activation of a well-conditioned network) near 1: inputs whose M
+// lies in [2^-6, 2^6] (every BASELINE workload) keep e = 0, so their
 // arithmetic is unchanged and bitwise identical across batch/row-band shards.
+// scratch: 2 * B zeroed ints per forward ([0, B) amax bits, [B, 2B) block count).
 __global__ void __launch_bounds__(256)
 input_scale_kernel(const float* __restrict__ x, long long n, float w0_l1, float b0_max, int* __restrict__ escale,
-                   int* __restrict__ status) {
-  const float* img = x + (long long)blockIdx.x * n;
+                   int* __restrict__ scratch, int* __restrict__ status) {
+  const int b = blockIdx.y, B = gridDim.y;
+  const float* img = x + (long long)b * n;
+  const long long per = (n + gridDim.x - 1) / gridDim.x;
+  const long long lo = per * blockIdx.x, hi = min(n, lo + per);
   float amax = 0.0f;
   int bad = 0;
-  const bool vec = (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(img) & 15) == 0);
-  if (vec) {
-    const float4* v = reinterpret_cast<const float4*>(img);
-    for (long long i = threadIdx.x; i < n / 4; i += blockDim.x) {
-      const float4 q = __ldg(v + i);
-      const float e[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (isfinite(e[k])) amax = fmaxf(amax, fabsf(e[k]));
-        else bad = 1;
-      }
-    }
-  } else {
-    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-      const float e = __ldg(img + i);
-      if (isfinite(e)) amax = fmaxf(amax, fabsf(e));
-      else bad = 1;
-    }
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const float e = __ldg(img + i);
+    if (isfinite(e)) amax = fmaxf(amax, fabsf(e));
+    else bad = 1;
   }
   __shared__ float s_max[8];
   __shared__ int s_bad[8];
@@ -432,22 +425,28 @@ input_scale_kernel(const float* __restrict__ x, long long n, float w0_l1, float 
   }
   if ((threadIdx.x & 31) == 0) { s_max[threadIdx.x >> 5] = amax; s_bad[threadIdx.x >> 5] = bad; }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < 8; ++w) { amax = fmaxf(amax, s_max[w]); bad |= s_bad[w]; }
-    amax = fmaxf(amax, s_max[0]);
-    bad |= s_bad[0];
-    const float m = fmaf(amax, w0_l1, b0_max);
-    int e = 0;
-    if (m > 0.0f && (m < 0.015625f || m > 64.0f)) e = min(60, max(-60, ilogbf(m) - 1));
-    escale[blockIdx.x] = e;
-    if (bad) atomicOr(status + kStatNonFiniteIn, 1);
-  }
+  if (threadIdx.x != 0) return;
+  for (int w = 1; w < 8; ++w) { amax = fmaxf(amax, s_max[w]); bad |= s_bad[w]; }
+  if (bad) atomicOr(status + kStatNonFiniteIn, 1);
+  atomicMax(scratch + b, __float_as_int(amax));
+  __threadfence();
+  if (atomicAdd(scratch + B + b, 1) != (int)gridDim.x - 1) return;
+  __threadfence();
+  const float m = fmaf(__int_as_float(*(volatile int*)(scratch + b)), w0_l1, b0_max);
+  int e = 0;
+  if (m > 0.0f && (m < 0.015625f || m > 64.0f)) e = min(60, max(-60, ilogbf(m) - 1));
+  escale[b] = e;
 }
 
 cudaError_t launch_input_scale(const float* x, int B, long long px_per_image, float w0_l1, float b0_max, int* escale,
-                               int* status, cudaStream_t st) {
+                               int* scratch, int* status, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  input_scale_kernel<<<B, 256, 0, st>>>(x, px_per_image, w0_l1, b0_max, escale, status);
+  cudaError_t e = cudaMemsetAsync(scratch, 0, 2 * (size_t)B * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  // ~4 blocks per SM in total, >= 4096 px per block
+  const long long want = std::max(1LL, std::min((592LL + B - 1) / B, (px_per_image + 4095) / 4096));
+  input_scale_kernel<<<dim3((unsigned)want, (unsigned)B), 256, 0, st>>>(x, px_per_image, w0_l1, b0_max, escale,
+                                                                          scratch, status);
   return cudaGetLastError();
 }
 

@@ -540,10 +540,11 @@ void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int
       if (p->escale) TVS_CUDA(cudaFree(p->escale));
       p->escale = nullptr;
       p->escale_n = 0;
-      TVS_CUDA(cudaMalloc(&p->escale, (size_t)B * sizeof(int)));
+      TVS_CUDA(cudaMalloc(&p->escale, (size_t)B * 3 * sizeof(int)));  // exponents | 2B scratch
       p->escale_n = B;
     }
-    TVS_CUDA(tvs::launch_input_scale(x, B, (long long)H * W, p->w0_l1, p->b0_max, p->escale, p->status, st));
+    TVS_CUDA(tvs::launch_input_scale(x, B, (long long)H * W, p->w0_l1, p->b0_max, p->escale, p->escale + B,
+                                     p->status, st));
     p->last_launches++;
     escale = p->escale;
   }

@@ -162,12 +162,22 @@ class TVSpecNet(nn.Module):
         entry = self._plans.get(idx)
         if entry is not None and entry[1] == key:
             return entry[0]
-        plan = entry[0] if entry is not None else _native.Plan(
-            idx, self.depth, self.channels, self.out_bands, _PRECISIONS[self._precision], self.unshuffle
-        )
-        if entry is None:
-            for name, value in self._options.items():
-                plan.set_option(name, value)
+        plan = entry[0] if entry is not None else self._new_plan(idx)
+        self._load_plan(plan, idx)
+        self._plans[idx] = (plan, key)
+        return plan
+
+    def _new_plan(self, idx: int) -> _native.Plan:
+        """A fresh C-ABI plan on device `idx` with this module's options (no weights)."""
+        plan = _native.Plan(idx, self.depth, self.channels, self.out_bands, _PRECISIONS[self._precision],
+                            self.unshuffle)
+        for name, value in self._options.items():
+            plan.set_option(name, value)
+        return plan
+
+    @torch.no_grad()
+    def _load_plan(self, plan: _native.Plan, idx: int) -> None:
+        """Fold eval BatchNorm on the host side and hand the layers to `plan`."""
         with torch.cuda.device(idx):
             stream = torch.cuda.current_stream(idx)
             dev = torch.device("cuda", idx)
@@ -181,8 +191,6 @@ class TVSpecNet(nn.Module):
                              [b.data_ptr() for _, _, b in staged], stream.cuda_stream)
             # keep the fp32 staging alive until the repack kernels have consumed it
             stream.synchronize()
-        self._plans[idx] = (plan, key)
-        return plan
 
     # ------------------------------------------------------------- forward ----
     def _exec_device(self, x: torch.Tensor) -> torch.device:

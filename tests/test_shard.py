@@ -68,17 +68,19 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, mode, out_q):
+def _worker(rank, world, port, mode, out_q, batch=3):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.set_num_threads(1)
     net = _Shallow()
-    x = torch.from_numpy(np.random.default_rng(1).random((3, 1, 20, 18)).astype(np.float32))
+    x = torch.from_numpy(np.random.default_rng(1).random((batch, 1, 20, 18)).astype(np.float32))
     bands, clos = forward_shard(net, x, rank, world, mode, closure=True)
     dim = 0 if mode == "batch" else 2
     all_b = gather(bands, world, dim)
     all_c = gather(clos, world, dim)
-    if rank == 0:
+    if rank != 0:
+        assert all_b is None and all_c is None  # only the destination rank holds the result
+    else:
         with torch.no_grad():
             full = net(x)
         out_q.put((torch.equal(all_b, full), float((all_b.sum(1, keepdim=True) + all_c - x).abs().max())))
@@ -86,12 +88,13 @@ def _worker(rank, world, port, mode, out_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["batch", "rows"])
-def test_gloo_world2_shard_and_gather(mode):
+@pytest.mark.parametrize("mode,batch", [("batch", 3), ("rows", 3), ("batch", 1)])
+def test_gloo_world2_shard_and_gather(mode, batch):
+    """batch=1 in batch mode leaves rank 1 with an empty shard (nothing sent)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q, batch)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
