@@ -110,3 +110,19 @@ def test_nonfinite_input_propagates(seeded_state):
     y = _model(seeded_state)(x.cuda()).cpu()
     assert torch.isnan(y[0, :, 10, 20]).all()
     assert torch.isfinite(y[0, :, :, :2]).all()  # far from the NaN the receptive field is clean
+
+
+def test_stack_stress_bitwise(seeded_state):
+    """compute-sanitizer is not available on this pool (DESIGN §3 K4), so the
+    row-flag protocol is stressed instead: 40 random shapes (ragged strips,
+    short columns, 1-4 images) through the layer stack, each bitwise equal to
+    the per-layer kernels and raising nothing (the watchdog is armed)."""
+    m0 = _model(seeded_state, stack=0)
+    m1 = _model(seeded_state, stack=1, watchdog_ms=500)
+    rng = np.random.default_rng(123)
+    for i in range(40):
+        b, h, w = int(rng.integers(1, 5)), int(rng.integers(1, 70)), int(rng.integers(1, 420))
+        x = torch.from_numpy(rng.random((b, 1, h, w), dtype=np.float32)).cuda()
+        y0, y1 = m0(x), m1(x)
+        assert m1.last_used_stack()
+        assert torch.equal(y0, y1), (b, h, w)
