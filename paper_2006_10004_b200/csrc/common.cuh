@@ -45,17 +45,16 @@ constexpr int kEpiGroupsPlain = TVS_EPI_GROUPS_PLAIN;  // modes 0 / 8
 constexpr int kStagesPlain = TVS_STAGES_PLAIN;
 static_assert(kStagesPlain <= kStages, "barrier arrays are sized by kStages");
 
-// Device-side duration of a kernel's launches (plan option "span"): every CTA
-// takes the globaltimer after its PDL wait (so spans of dependent launches on
-// one stream never overlap) and at exit; the last CTA to exit adds the launch's
-// [first start, last end] to total_ns and re-arms the record.
+// Device-side duration of one kernel launch (plan option "span"): every CTA
+// reduces the globaltimer after its PDL wait (so spans of dependent launches
+// on one stream never overlap) into `start` and at exit into `end`, with
+// fire-and-forget atomics; the host sums end - start over the launch records.
 struct KernelSpan {
   unsigned long long start;  // ~0 when armed
   unsigned long long end;
-  unsigned long long total_ns;
-  unsigned long long launches;
-  unsigned int done;
 };
+// status flag store (host-mapped memory: plain stores, no system-scope atomics)
+__device__ __forceinline__ void flag_set(int* p) { *(volatile int*)p = 1; }
 
 struct ConvArgs {
   int B, H, W;
@@ -85,8 +84,10 @@ struct ConvArgs {
   // Hidden epilogues scale the BN shift by 2^-e_b, heads rescale by 2^e_b.
   // Null = no scaling.
   const int* escale;
-  // per-forward status words (kStat*), reset by the host before each forward
+  // per-forward status words (kStat*): a slot of pinned, mapped host memory
+  // the host zeroes before the forward (kernels only ever store 1 into it)
   int* status;
+  int* abort;  // layer stack: device word set when a watchdog fired (zeroed with rowcnt)
   unsigned long long watchdog_ns;  // layer stack: give up a row-flag wait after this long
   KernelSpan* span;                // null, or accumulate this launch's device duration
   // TVS_CONV_DBG / plan option "debug" (results invalid except kDbgWithholdFlag,
@@ -161,6 +162,8 @@ cudaError_t launch_conv0(int act_fmt, int C, const float* x, void* act, const Co
 // counts non-finite inputs into status[kStatNonFiniteIn]
 cudaError_t launch_input_scale(const float* x, int B, long long px_per_image, float w0_l1, float b0_max, int* escale,
                                int* scratch, int* status, cudaStream_t st);
+// the input-scale kernel's scratch: 2 * B ints, zero on first use; the kernel
+// leaves it zeroed for the next forward
 cudaError_t launch_head_f32(int C, const float* act, const float* x, const float* wh, const float* bh, float* bands,
                             float* closure, int B, int H, int W, int K, int row0, int rows, int* status,
                             cudaStream_t st);
@@ -171,8 +174,10 @@ cudaError_t configure_kernels();  // one-time smem opt-ins
 // in_ch = 1 (reference conv0) or 4 (unshuffle = 2 variant, H/W = half-res grid)
 size_t conv0_tc_pack_bytes(int in_ch);
 cudaError_t launch_pack_conv0_tc(const float* w, int in_ch, uint8_t* out, cudaStream_t st);
+// pdl: launched programmatically after the input-scale kernel (x may be read
+// before griddepcontrol.wait; escale and the activation writes come after it)
 cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t* bpack, const float* bias,
-                            const int* escale, int B, int H, int W, int num_sms, cudaStream_t st);
+                            const int* escale, int B, int H, int W, int num_sms, bool pdl, cudaStream_t st);
 // metrics.cu: per-plane scoring statistics (8 doubles per plane)
 cudaError_t launch_band_stats(const float* gt, const float* pred, int planes, int H, int W,
                               const double* range_override, double* stats, cudaStream_t st);

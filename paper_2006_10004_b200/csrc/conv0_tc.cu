@@ -147,6 +147,10 @@ __global__ void __launch_bounds__(128) conv0_tc_kernel(const float* __restrict__
   long long base = (long long)blockIdx.x * NT;
 #pragma unroll
   for (int i = 0; i < NT; ++i) conv0_taps<kKB>(x, base + i, tiles, strips, H, W, t, tap[i]);
+  // programmatic launch after the input-scale kernel: the exponents (and the
+  // right to overwrite the activation buffer) come after this wait; x was
+  // complete before that kernel started.  A no-op for a plain launch.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (; base < tiles; base += step) {
     // ---- A rows of this thread's pixel in each tile: taps split hi / lo
 #pragma unroll
@@ -283,7 +287,7 @@ cudaError_t launch_pack_conv0_tc(const float* w, int in_ch, uint8_t* out, cudaSt
 }
 
 cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t* bpack, const float* bias,
-                            const int* escale, int B, int H, int W, int num_sms, cudaStream_t st) {
+                            const int* escale, int B, int H, int W, int num_sms, bool pdl, cudaStream_t st) {
   static std::mutex mu;
   static uint64_t done = 0;
   cudaError_t e = once_per_device(mu, done, [] {
@@ -299,14 +303,25 @@ cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t*
   const int nt = in_ch == 1 ? Conv0TcCfg<1>::kTiles : Conv0TcCfg<4>::kTiles;
   const int per_sm = in_ch == 1 ? Conv0TcCfg<1>::kPerSm : Conv0TcCfg<4>::kPerSm;
   const int grid = (int)std::max(1LL, std::min<long long>((tiles + nt - 1) / nt, (long long)num_sms * per_sm));
-  // plain launch (no PDL attribute): K1 is a forward's first kernel and has
-  // no griddepcontrol.wait, so it must not overlap the previous forward's head
+  // PDL only behind the input-scale kernel (which reads x and nothing else);
+  // as a forward's first kernel K1 is a plain launch, so it cannot overlap
+  // the previous forward's head or whatever produced x
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  __half* out = static_cast<__half*>(act);
   if (in_ch == 1) {
-    conv0_tc_kernel<1><<<grid, 128, Conv0TcCfg<1>::kSmem, st>>>(x, static_cast<__half*>(act), bpack, bias, escale, B, H, W);
-  } else {
-    conv0_tc_kernel<4><<<grid, 128, Conv0TcCfg<4>::kSmem, st>>>(x, static_cast<__half*>(act), bpack, bias, escale, B, H, W);
+    cfg.dynamicSmemBytes = Conv0TcCfg<1>::kSmem;
+    return cudaLaunchKernelEx(&cfg, conv0_tc_kernel<1>, x, out, bpack, bias, escale, B, H, W);
   }
-  return cudaGetLastError();
+  cfg.dynamicSmemBytes = Conv0TcCfg<4>::kSmem;
+  return cudaLaunchKernelEx(&cfg, conv0_tc_kernel<4>, x, out, bpack, bias, escale, B, H, W);
 }
 
 }  // namespace tvs

@@ -182,7 +182,7 @@ head_kernel(const T* __restrict__ act, const float* __restrict__ x, const float*
       sum += o;
       bad |= !isfinite(o);
     }
-  if (bad && status) atomicOr(status + kStatNonFiniteOut, 1);
+  if (bad && status) flag_set(status + kStatNonFiniteOut);
   if (closure != nullptr) closure[b * plane + (long long)rr * W + xw] = x[(b * H + y) * (long long)W + xw] - sum;
 }
 
@@ -405,6 +405,7 @@ cudaError_t launch_hidden_f32(int C, const float* in, float* out, const float* w
 __global__ void __launch_bounds__(256)
 input_scale_kernel(const float* __restrict__ x, long long n, float w0_l1, float b0_max, int* __restrict__ escale,
                    int* __restrict__ scratch, int* __restrict__ status) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // conv0 may start its prologue
   const int b = blockIdx.y, B = gridDim.y;
   const float* img = x + (long long)b * n;
   const long long per = (n + gridDim.x - 1) / gridDim.x;
@@ -427,12 +428,13 @@ input_scale_kernel(const float* __restrict__ x, long long n, float w0_l1, float 
   __syncthreads();
   if (threadIdx.x != 0) return;
   for (int w = 1; w < 8; ++w) { amax = fmaxf(amax, s_max[w]); bad |= s_bad[w]; }
-  if (bad) atomicOr(status + kStatNonFiniteIn, 1);
+  if (bad && status) flag_set(status + kStatNonFiniteIn);
   atomicMax(scratch + b, __float_as_int(amax));
   __threadfence();
   if (atomicAdd(scratch + B + b, 1) != (int)gridDim.x - 1) return;
   __threadfence();
-  const float m = fmaf(__int_as_float(*(volatile int*)(scratch + b)), w0_l1, b0_max);
+  const float m = fmaf(__int_as_float(atomicExch(scratch + b, 0)), w0_l1, b0_max);
+  scratch[B + b] = 0;  // re-armed for the next forward (stream order)
   int e = 0;
   if (m > 0.0f && (m < 0.015625f || m > 64.0f)) e = min(60, max(-60, ilogbf(m) - 1));
   escale[b] = e;
@@ -441,8 +443,6 @@ input_scale_kernel(const float* __restrict__ x, long long n, float w0_l1, float 
 cudaError_t launch_input_scale(const float* x, int B, long long px_per_image, float w0_l1, float b0_max, int* escale,
                                int* scratch, int* status, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(scratch, 0, 2 * (size_t)B * sizeof(int), st);
-  if (e != cudaSuccess) return e;
   // ~4 blocks per SM in total, >= 4096 px per block
   const long long want = std::max(1LL, std::min((592LL + B - 1) / B, (px_per_image + 4095) / 4096));
   input_scale_kernel<<<dim3((unsigned)want, (unsigned)B), 256, 0, st>>>(x, px_per_image, w0_l1, b0_max, escale,

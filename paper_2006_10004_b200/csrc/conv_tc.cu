@@ -169,14 +169,15 @@ struct StackGate {
       // watchdog: never hang.  Once any wait of this launch has expired the
       // output is invalid (the host reports it), so every later wait gives up
       // at once and the launch drains.
-      if (ld_relaxed_gpu(a.status + kStatWatchdog)) return;
+      if (ld_relaxed_gpu(a.abort)) return;
       __nanosleep(32);
       if ((spins & 63u) == 63u) {
         const unsigned long long now = globaltimer_ns();
         if (t0 == 0) {
           t0 = now;
         } else if (now - t0 > a.watchdog_ns) {
-          atomicExch(a.status + kStatWatchdog, 1);
+          atomicExch(a.abort, 1);
+          if (a.status) flag_set(a.status + kStatWatchdog);
           return;
         }
       }
@@ -871,7 +872,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                 }
               }
             }
-            if (bad) atomicOr(a.status + kStatNonFiniteOut, 1);
+            if (bad && a.status) flag_set(a.status + kStatNonFiniteOut);
             if (a.closure) {
 #pragma unroll
               for (int i = 0; i < 2; ++i) {
@@ -938,7 +939,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                 bad |= !isfinite(o);
               }
             }
-            if (bad) atomicOr(a.status + kStatNonFiniteOut, 1);
+            if (bad && a.status) flag_set(a.status + kStatNonFiniteOut);
             if (a.closure) a.closure[(long long)g.b * plane + pix] = a.x[((long long)g.b * a.H + q) * a.W + xg] - sum;
           }
         }
@@ -1205,7 +1206,7 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
 // all `grid` CTAs are co-resident (the deadlock-freedom argument of ItemIter
 // needs it) or fails the launch (cudaErrorCooperativeLaunchTooLarge, e.g.
 // under MPS SM limits), in which case the host falls back to the per-layer
-// kernels.  rowcnt and status must be zero on entry.
+// kernels.  rowcnt and the abort word must be zero on entry.
 cudaError_t launch_conv_stack(const CUtensorMap& tm_in0, const CUtensorMap& tm_out1, const StackMaps& sm,
                               const ConvArgs& a, int grid, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};

@@ -401,24 +401,14 @@ TVS_DEV unsigned long long globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// KernelSpan bookkeeping (common.cuh), called by one thread per CTA
+// KernelSpan bookkeeping (common.cuh), one thread per CTA, no return values
 template <typename Span>
-TVS_DEV void span_open(Span* sp) { atomicMin(&sp->start, globaltimer_ns()); }
+TVS_DEV void span_open(Span* sp) {
+  asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(&sp->start), "l"(globaltimer_ns()) : "memory");
+}
 template <typename Span>
 TVS_DEV void span_close(Span* sp) {
-  atomicMax(&sp->end, globaltimer_ns());
-  __threadfence();
-  if (atomicAdd(&sp->done, 1u) == gridDim.x * gridDim.y * gridDim.z - 1) {
-    __threadfence();
-    const unsigned long long s = *(volatile unsigned long long*)&sp->start;
-    const unsigned long long e = *(volatile unsigned long long*)&sp->end;
-    sp->total_ns += e - s;
-    sp->launches += 1;
-    sp->start = ~0ull;
-    sp->end = 0;
-    sp->done = 0;
-    __threadfence();
-  }
+  asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(&sp->end), "l"(globaltimer_ns()) : "memory");
 }
 TVS_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 TVS_DEV void red_release_gpu_add(int* p, int v) {

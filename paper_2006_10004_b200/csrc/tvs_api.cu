@@ -115,14 +115,18 @@ struct tvs_plan {
   // activation ping-pong scratch
   void* act[2] = {nullptr, nullptr};
   size_t act_bytes = 0;
-  tvs::KernelSpan* span = nullptr;  // device record of the hidden-layer launches (option "span")
+  // device records of the hidden-layer launches (option "span"), one per launch
+  static constexpr int kSpanSlots = 8192;
+  tvs::KernelSpan* span = nullptr;
+  int span_next = 0;
   // per-image input exponents
   int* escale = nullptr;
   size_t escale_n = 0;
-  // per-forward status words (tvs::kStat*): device copy, pinned host ring
+  // per-forward status words (tvs::kStat*): a ring of slots in pinned, mapped
+  // host memory that the kernels write directly (no per-forward memset or copy)
   static constexpr int kRing = 32;
-  int* status = nullptr;
   int* status_host = nullptr;  // kRing x kStatWords
+  int* status_dev = nullptr;   // the same memory, device view
   cudaEvent_t status_ev[kRing] = {};
   int status_next = 0;
   std::deque<int> status_pending;  // deferred mode: slots not yet evaluated
@@ -199,7 +203,7 @@ void free_all(tvs_plan* p) {
     if (e) cudaEventDestroy(e);
   if (p->status_host) cudaFreeHost(p->status_host);
   free_weights(p);
-  void* ptrs[] = {p->act[0], p->act[1], p->dx, p->rowcnt, p->escale, p->status, p->span};
+  void* ptrs[] = {p->act[0], p->act[1], p->dx, p->rowcnt, p->escale, p->span};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -285,7 +289,7 @@ void drain_profile(tvs_plan* p) {
 }
 
 void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B, int H, int W, int row0, int rows,
-               cudaStream_t st, const int* escale) {
+               cudaStream_t st, const int* escale, int* status, bool conv0_pdl) {
   void* const* act = p->act;
   const int max_ctas = p->num_sms;
   const bool fast = p->tc_path();
@@ -307,7 +311,8 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
                                   (double)stack_items_n >= 0.95 * (double)(rounds * p->num_sms));
   }
   if (stack) {
-    const size_t n = (size_t)B * ((W / us + tvs::kStripPx - 1) / tvs::kStripPx) * (H / us);
+    // row flags + the watchdog's abort word, zeroed per launch
+    const size_t n = (size_t)B * ((W / us + tvs::kStripPx - 1) / tvs::kStripPx) * (H / us) + 1;
     if (n > p->rowcnt_n) {
       if (p->rowcnt) TVS_CUDA(cudaFree(p->rowcnt));
       p->rowcnt = nullptr;
@@ -316,6 +321,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       p->rowcnt_n = n;
     }
     TVS_CUDA(cudaMemsetAsync(p->rowcnt, 0, n * sizeof(int), st));
+    conv0_pdl = false;  // the memset sits between the input-scale kernel and K1
   }
   // K1
   // wide fast stack: hidden layer j reads an fp16 hi/lo pair for j < P, single
@@ -327,26 +333,30 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
                        : (split ? tvs::kActSplit : (wide ? (pair_in(0) ? tvs::kActSplit : tvs::kActF16) : tvs::kActF32));
   if (us == 2 && p->opt.conv0_tc)
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C, [&] {
-      return tvs::launch_conv0_tc(4, x, act[0], p->c0pack, p->c0bias, escale, B, H / 2, W / 2, p->num_sms, st);
+      return tvs::launch_conv0_tc(4, x, act[0], p->c0pack, p->c0bias, escale, B, H / 2, W / 2, p->num_sms,
+                                  conv0_pdl, st);
     });
   else if (us == 2)
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
                  [&] { return tvs::launch_conv0_unshuffle(x, act[0], p->w0u, p->b0u, escale, B, H / 2, W / 2, st); });
   else if (fast && p->opt.conv0_tc)
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C, [&] {
-      return tvs::launch_conv0_tc(1, x, act[0], p->c0pack, p->c0bias, escale, B, H, W, p->num_sms, st);
+      return tvs::launch_conv0_tc(1, x, act[0], p->c0pack, p->c0bias, escale, B, H, W, p->num_sms, conv0_pdl, st);
     });
   else
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
                  [&] { return tvs::launch_conv0(fmt, C, x, act[0], p->conv0, escale, B, H, W, st); });
-  tvs::KernelSpan* hidden_span = p->opt.span ? p->span : nullptr;
+  // one span record per hidden-layer launch (option "span")
+  auto next_span = [&]() -> tvs::KernelSpan* {
+    return (p->opt.span && p->span_next < tvs_plan::kSpanSlots) ? p->span + p->span_next++ : nullptr;
+  };
   // common per-launch fields
   auto base_args = [&](int Hg, int Wg, int strips, int r0, int nrows) {
     tvs::ConvArgs a{};
     a.B = B; a.H = Hg; a.W = Wg; a.strips = strips;
     a.row0 = r0; a.rows = nrows;
     a.escale = escale;
-    a.status = p->status;
+    a.status = status;
     a.watchdog_ns = (unsigned long long)std::max(1, p->opt.watchdog_ms) * 1000000ull;
     a.dbg = p->opt.debug;
     return a;
@@ -369,7 +379,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.nshift = C;
       a.act_out = static_cast<uint8_t*>(act[cur ^ 1]);
       a.out_single = pair_in(l + 1) ? 0 : 1;
-      a.span = hidden_span;
+      a.span = next_span();
       const CUtensorMap& m = pair_in(l) ? pair_map[cur] : single_map[cur];
       // 4 (quarters) or 2 (halves) CTAs per strip-row range: size the grid by groups
       const int mode = pair_in(l) ? 5 : (p->packed_halves ? 11 : 9);
@@ -399,7 +409,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.shift = p->bhid + (size_t)l * tvs::kC;
       a.nshift = tvs::kC;
       a.act_out = static_cast<uint8_t*>(act[cur ^ 1]);
-      a.span = hidden_span;
+      a.span = next_span();
       const int grid = conv_grid(max_ctas, a);
       timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64,
                    [&] { return tvs::launch_conv_tc(3, in_map[cur], in_map[cur], a, grid, st); });
@@ -430,8 +440,9 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.nshift = tvs::kC;
       a.nlayers = nh;
       a.rowcnt = p->rowcnt;
+      a.abort = p->rowcnt + (p->rowcnt_n - 1);
       a.items = stack_items(p, B, strips, a.nlayers, st);
-      a.span = hidden_span;
+      a.span = next_span();
       tvs::StackMaps sm{};
       sm.in1 = in_map[1];
       sm.out0 = out_map[0];
@@ -458,7 +469,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.shift = p->bhid + (size_t)l * tvs::kC;
       a.nshift = tvs::kC;
       a.x = x;
-      a.span = hidden_span;
+      a.span = next_span();
       const int grid = conv_grid(max_ctas, a);
       timed_launch(p, st, TVS_KIND_HIDDEN, pxg * 2.0 * 9 * 64 * 64,
                    [&] { return tvs::launch_conv_tc(0, in_map[cur], out_map[cur ^ 1], a, grid, st); });
@@ -483,7 +494,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     }
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * C * p->out_bands, [&] {
       return tvs::launch_head_f32(C, (const float*)act[cur], x, p->wh, p->bh, bands, closure, B, H, W, p->out_bands,
-                                  row0, rows, p->status, st);
+                                  row0, rows, status, st);
     });
   }
 }
@@ -533,7 +544,18 @@ void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int
   const size_t per_img = (size_t)H * W * p->act_px_bytes() / ((size_t)p->unshuffle * p->unshuffle);
   const size_t in_img = (size_t)H * W, out_img = (size_t)rows * W;
   const bool check = p->opt.check != 0;
-  if (check || p->scaled()) TVS_CUDA(cudaMemsetAsync(p->status, 0, tvs::kStatWords * sizeof(int), st));
+  int* status = nullptr;
+  int slot = -1;
+  if (check) {
+    if (p->status_pending.size() >= (size_t)tvs_plan::kRing) {  // deferred ring full: settle the oldest
+      TVS_CUDA(cudaEventSynchronize(p->status_ev[p->status_pending.front()]));
+      drain_status(p, false);
+    }
+    slot = p->status_next;
+    p->status_next = (slot + 1) % tvs_plan::kRing;
+    std::fill(p->status_host + slot * tvs::kStatWords, p->status_host + (slot + 1) * tvs::kStatWords, 0);
+    status = p->status_dev + slot * tvs::kStatWords;
+  }
   const int* escale = nullptr;
   if (p->scaled()) {
     if ((size_t)B > p->escale_n) {
@@ -541,10 +563,11 @@ void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int
       p->escale = nullptr;
       p->escale_n = 0;
       TVS_CUDA(cudaMalloc(&p->escale, (size_t)B * 3 * sizeof(int)));  // exponents | 2B scratch
+      TVS_CUDA(cudaMemsetAsync(p->escale, 0, (size_t)B * 3 * sizeof(int), st));
       p->escale_n = B;
     }
     TVS_CUDA(tvs::launch_input_scale(x, B, (long long)H * W, p->w0_l1, p->b0_max, p->escale, p->escale + B,
-                                     p->status, st));
+                                     status, st));
     p->last_launches++;
     escale = p->escale;
   }
@@ -554,23 +577,14 @@ void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int
   for (int b0 = 0; b0 < B; b0 += cb) {
     const int nb = std::min(cb, B - b0);
     run_chunk(p, x + b0 * in_img, bands + (size_t)b0 * p->out_bands * out_img,
-              closure ? closure + b0 * out_img : nullptr, nb, H, W, row0, rows, st, escale ? escale + b0 : nullptr);
+              closure ? closure + b0 * out_img : nullptr, nb, H, W, row0, rows, st, escale ? escale + b0 : nullptr,
+              status, escale != nullptr && b0 == 0);
   }
   if (!check) return;
-  // status words of this forward -> a pinned host slot
-  if (p->status_pending.size() >= (size_t)tvs_plan::kRing) {  // deferred ring full: evaluate the oldest
-    const int oldest = p->status_pending.front();
-    TVS_CUDA(cudaEventSynchronize(p->status_ev[oldest]));
-    drain_status(p, false);
-  }
-  const int slot = p->status_next;
-  p->status_next = (slot + 1) % tvs_plan::kRing;
-  int* hs = p->status_host + slot * tvs::kStatWords;
-  TVS_CUDA(cudaMemcpyAsync(hs, p->status, tvs::kStatWords * sizeof(int), cudaMemcpyDeviceToHost, st));
   TVS_CUDA(cudaEventRecord(p->status_ev[slot], st));
   if (p->opt.check == 1) {
     TVS_CUDA(cudaEventSynchronize(p->status_ev[slot]));
-    evaluate_status(hs);
+    evaluate_status(p->status_host + slot * tvs::kStatWords);
   } else {
     p->status_pending.push_back(slot);
   }
@@ -634,12 +648,14 @@ int tvs_plan_create_ex(int device, int depth, int channels, int out_bands, int m
     try {
       TVS_CUDA(tvs::configure_kernels());
       p->stack_ok = tvs::conv_stack_fits(p->num_sms, p->num_sms);
-      TVS_CUDA(cudaMalloc(&p->status, tvs::kStatWords * sizeof(int)));
-      TVS_CUDA(cudaMalloc(&p->span, sizeof(tvs::KernelSpan)));
-      TVS_CUDA(cudaMemset(p->span, 0, sizeof(tvs::KernelSpan)));
-      TVS_CUDA(cudaMemset(p->span, 0xff, sizeof(unsigned long long)));  // start = ~0 (armed)
-      TVS_CUDA(cudaMemset(p->status, 0, tvs::kStatWords * sizeof(int)));
-      TVS_CUDA(cudaMallocHost(&p->status_host, tvs_plan::kRing * tvs::kStatWords * sizeof(int)));
+      TVS_CUDA(cudaMalloc(&p->span, tvs_plan::kSpanSlots * sizeof(tvs::KernelSpan)));
+      {
+        std::vector<tvs::KernelSpan> armed(tvs_plan::kSpanSlots, tvs::KernelSpan{~0ull, 0ull});
+        TVS_CUDA(cudaMemcpy(p->span, armed.data(), armed.size() * sizeof(tvs::KernelSpan), cudaMemcpyHostToDevice));
+      }
+      TVS_CUDA(cudaHostAlloc(&p->status_host, tvs_plan::kRing * tvs::kStatWords * sizeof(int), cudaHostAllocMapped));
+      std::fill(p->status_host, p->status_host + tvs_plan::kRing * tvs::kStatWords, 0);
+      TVS_CUDA(cudaHostGetDevicePointer((void**)&p->status_dev, p->status_host, 0));
       for (auto& e : p->status_ev) TVS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     } catch (...) {
       free_all(p);
@@ -872,14 +888,19 @@ int tvs_profile_span(tvs_plan* p, double* total_ms, long long* launches, int res
     if (!p) throw TvsError(TVS_E_INVALID, "null plan");
     DeviceGuard dg(p->device);
     TVS_CUDA(cudaDeviceSynchronize());
-    tvs::KernelSpan h{};
-    TVS_CUDA(cudaMemcpy(&h, p->span, sizeof(h), cudaMemcpyDeviceToHost));
-    if (total_ms) *total_ms = (double)h.total_ns * 1e-6;
-    if (launches) *launches = (long long)h.launches;
-    if (reset) {
-      tvs::KernelSpan z{};
-      z.start = ~0ull;
-      TVS_CUDA(cudaMemcpy(p->span, &z, sizeof(z), cudaMemcpyHostToDevice));
+    const int n = p->span_next;
+    std::vector<tvs::KernelSpan> h(std::max(1, n));
+    if (n) TVS_CUDA(cudaMemcpy(h.data(), p->span, n * sizeof(tvs::KernelSpan), cudaMemcpyDeviceToHost));
+    double ns = 0.0;
+    long long cnt = 0;
+    for (int i = 0; i < n; ++i)
+      if (h[i].end > h[i].start) { ns += (double)(h[i].end - h[i].start); ++cnt; }
+    if (total_ms) *total_ms = ns * 1e-6;
+    if (launches) *launches = cnt;
+    if (reset && n) {
+      std::fill(h.begin(), h.begin() + n, tvs::KernelSpan{~0ull, 0ull});
+      TVS_CUDA(cudaMemcpy(p->span, h.data(), n * sizeof(tvs::KernelSpan), cudaMemcpyHostToDevice));
+      p->span_next = 0;
     }
   });
 }
