@@ -134,6 +134,34 @@ int tvs_profile_span(tvs_plan* plan, double* total_ms, long long* launches, int 
 
 int tvs_plan_destroy(tvs_plan* plan);
 
+/* ---- Training step: replaces the train-mode forward and
+ * the autograd backward of TVSpecNet (model.py:29-52, BatchNorm2d with batch
+ * statistics) inside _epoch_pass (training.py:45-61).  64 channels.
+ *
+ *   tvs_train_create   <- TVSpecNet(depth, out_bands) in train() mode
+ *   tvs_train_forward  <- model(img) with model.training == True
+ *   tvs_train_backward <- loss.backward() through the model
+ *
+ * Forward: w_dev[i] conv weights [cout][cin][3][3] fp32 (i = 0..depth-1),
+ * bias_dev[0] / bias_dev[depth-1] the conv0 / head biases (others ignored),
+ * gamma_dev[j] / beta_dev[j] the BatchNorm affine parameters of hidden layer j
+ * (j = 0..depth-3), all DEVICE pointers that must stay valid until the
+ * matching backward returns.  out: (B,out_bands,H,W) fp32.  mean_out /
+ * var_out: (depth-2) x 64 batch mean and UNBIASED variance per hidden layer
+ * (the caller updates running_mean / running_var with its momentum, as
+ * BatchNorm2d does).  Activations for the backward stay in the train plan: one
+ * forward/backward pair at a time per plan.
+ * Backward: g_out = dL/d(out) (B,out_bands,H,W) fp32; writes dw[i] (conv
+ * weight layout), dbias[0], dbias[depth-1], dgamma[j], dbeta[j], fp32 DEVICE. */
+typedef struct tvs_train tvs_train;
+int tvs_train_create(int device, int depth, int out_bands, tvs_train** out_plan);
+int tvs_train_forward(tvs_train* plan, const float* const* w_dev, const float* const* bias_dev,
+                      const float* const* gamma_dev, const float* const* beta_dev, float eps, const float* x,
+                      float* out, float* mean_out, float* var_out, int B, int H, int W, void* stream);
+int tvs_train_backward(tvs_train* plan, const float* g_out, float* const* dw, float* const* dbias,
+                       float* const* dgamma, float* const* dbeta, void* stream);
+int tvs_train_destroy(tvs_train* plan);
+
 /* Band scoring statistics (spectv metrics.py:28-237), fp64.
  * gt, pred: DEVICE (planes, H, W) fp32.  stats: DEVICE planes x 8 doubles:
  *   [0] sum (gt - pred)^2           -> PSNR / MSE   (metrics.py:28-37)

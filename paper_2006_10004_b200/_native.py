@@ -41,6 +41,10 @@ EXPORTS = (
     "tvs_band_stats",
     "tvs_tvflow_workspace_bytes",
     "tvs_tvflow_analyze",
+    "tvs_train_create",
+    "tvs_train_forward",
+    "tvs_train_backward",
+    "tvs_train_destroy",
 )
 
 _lock = threading.Lock()
@@ -103,6 +107,15 @@ def load() -> ctypes.CDLL:
         d = ctypes.c_double
         lib.tvs_tvflow_analyze.restype = i
         lib.tvs_tvflow_analyze.argtypes = [P, i, i, i, d, i, P, i, i, d, d, d, i, P, P, P, P, P, P]
+        lib.tvs_train_create.restype = i
+        lib.tvs_train_create.argtypes = [i, i, i, ctypes.POINTER(P)]
+        PP = ctypes.POINTER(P)
+        lib.tvs_train_forward.restype = i
+        lib.tvs_train_forward.argtypes = [P, PP, PP, PP, PP, ctypes.c_float, P, P, P, P, i, i, i, P]
+        lib.tvs_train_backward.restype = i
+        lib.tvs_train_backward.argtypes = [P, P, PP, PP, PP, PP, P]
+        lib.tvs_train_destroy.restype = i
+        lib.tvs_train_destroy.argtypes = [P]
         lib.tvs_plan_destroy.restype = i
         lib.tvs_plan_destroy.argtypes = [P]
         _lib = lib
@@ -188,6 +201,41 @@ class Plan:
     def close(self) -> None:
         if self.handle and self.handle.value:
             self.lib.tvs_plan_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _ptrs(seq):
+    return (ctypes.c_void_p * len(seq))(*[p or None for p in seq])
+
+
+class TrainPlan:
+    """RAII owner of one ``tvs_train`` (training step on one device)."""
+
+    def __init__(self, device: int, depth: int, out_bands: int):
+        self.lib = load()
+        self.handle = ctypes.c_void_p()
+        check(self.lib.tvs_train_create(device, depth, out_bands, ctypes.byref(self.handle)))
+        self.device, self.depth, self.out_bands = device, depth, out_bands
+
+    def forward(self, w, bias, gamma, beta, eps, x, out, mean, var, B, H, W, stream: int) -> None:
+        check(self.lib.tvs_train_forward(self.handle, _ptrs(w), _ptrs(bias), _ptrs(gamma), _ptrs(beta),
+                                         ctypes.c_float(eps), ctypes.c_void_p(x), ctypes.c_void_p(out),
+                                         ctypes.c_void_p(mean), ctypes.c_void_p(var), B, H, W,
+                                         ctypes.c_void_p(stream)))
+
+    def backward(self, g_out, dw, dbias, dgamma, dbeta, stream: int) -> None:
+        check(self.lib.tvs_train_backward(self.handle, ctypes.c_void_p(g_out), _ptrs(dw), _ptrs(dbias),
+                                          _ptrs(dgamma), _ptrs(dbeta), ctypes.c_void_p(stream)))
+
+    def close(self) -> None:
+        if self.handle and self.handle.value:
+            self.lib.tvs_train_destroy(self.handle)
             self.handle = ctypes.c_void_p()
 
     def __del__(self):

@@ -17,12 +17,14 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtvsb200.so"
-SOURCES = ["tvs_api.cu", "conv_tc.cu", "conv0_tc.cu", "conv_edge.cu", "metrics.cu", "tvflow.cu"]
-HEADERS = ["common.cuh", "sm100.cuh"]
+SOURCES = ["tvs_api.cu", "conv_tc.cu", "conv0_tc.cu", "conv_edge.cu", "metrics.cu", "tvflow.cu", "train.cu"]
+HEADERS = ["common.cuh", "sm100.cuh", "host_util.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-O2", "-shared"]
+# cuBLAS: the training step's wgrad GEMMs (train.cu); rpath so the .so finds it outside torch too
+LIBS = ["-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
 
 
 def nvcc() -> str:
@@ -44,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, *FLAGS, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
+    cmd = [nvcc(), *ARCH, *FLAGS, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES], *LIBS]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = PKG / "build.log"
     log.write_text(" ".join(cmd) + "\n" + res.stdout + res.stderr)

@@ -88,6 +88,11 @@ struct ConvArgs {
   // the host zeroes before the forward (kernels only ever store 1 into it)
   int* status;
   int* abort;  // layer stack: device word set when a watchdog fired (zeroed with rowcnt)
+  // training (train.cu): modes 0 / 3 write the raw fp32 accumulator (no
+  // shift, no ReLU) as fp32 NHWC [B][H][W][64] to act_out, times 2^-(*out_exp)
+  // when out_exp is set (the dgrad conv undoes its input's gradient scale)
+  int raw_f32;
+  const int* out_exp;
   unsigned long long watchdog_ns;  // layer stack: give up a row-flag wait after this long
   KernelSpan* span;                // null, or accumulate this launch's device duration
   // TVS_CONV_DBG / plan option "debug" (results invalid except kDbgWithholdFlag,
@@ -144,6 +149,7 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
                            int grid, cudaStream_t st);
 cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
 cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
+cudaError_t launch_pack_hidden_f16_t(const float* w, uint8_t* out, cudaStream_t st);  // training dgrad pack
 // parts = 4: output-channel quarters (modes 5 / 9); 2: halves (mode 11)
 cudaError_t launch_pack_hidden_wide(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int parts);
 cudaError_t launch_pack_head_wide(const float* w, int K, uint8_t* out, cudaStream_t st);

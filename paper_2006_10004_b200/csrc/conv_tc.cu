@@ -720,6 +720,25 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
+          if (a.raw_f32) {  // training forward: pre-BatchNorm conv output, fp32
+            if (xg < a.W) {
+              float* dst = reinterpret_cast<float*>(a.act_out) + (((long long)g.b * a.H + q) * a.W + xg) * 64 + g.h * 32;
+#pragma unroll
+              for (int c4 = 0; c4 < 8; ++c4) {
+                float f[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  const int ch = c4 * 4 + t;
+                  const float z = fmaf(__uint_as_float(e[ch >> 4][ch & 15]), kMainDebias18,
+                                       fmaf(__uint_as_float(o[ch >> 4][ch & 15]), kMainDebias18,
+                                            __uint_as_float(c[ch >> 4][ch & 15])));
+                  f[t] = z * (1.0f / kSplitWScale);
+                }
+                *reinterpret_cast<float4*>(dst + c4 * 4) = make_float4(f[0], f[1], f[2], f[3]);
+              }
+            }
+            continue;
+          }
           if (xg < a.W) {
             uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * 256 + g.h * 64;
 #pragma unroll
@@ -767,6 +786,20 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
+          if (!Cfg::kStack && a.raw_f32) {  // training dgrad: raw fp32 accumulator, unscaled
+            if (xg < a.W) {
+              const float m = a.out_exp ? pow2i(-__ldg(a.out_exp)) : 1.0f;
+              float* dst = reinterpret_cast<float*>(a.act_out) + (((long long)g.b * a.H + q) * a.W + xg) * 64;
+#pragma unroll
+              for (int c4 = 0; c4 < 16; ++c4)
+                *reinterpret_cast<float4*>(dst + c4 * 4) =
+                    make_float4(__uint_as_float(v[c4 >> 2][(c4 & 3) * 4]) * m,
+                                __uint_as_float(v[c4 >> 2][(c4 & 3) * 4 + 1]) * m,
+                                __uint_as_float(v[c4 >> 2][(c4 & 3) * 4 + 2]) * m,
+                                __uint_as_float(v[c4 >> 2][(c4 & 3) * 4 + 3]) * m);
+            }
+            continue;
+          }
           if (a.dbg & 128) {  // ablation: TMEM read only (keep the values alive)
             uint32_t acc = 0;
 #pragma unroll
@@ -1031,6 +1064,28 @@ __global__ void pack_hidden_f16_kernel(const float* __restrict__ w, const float*
     const int ky = t / 3, kx = t % 3;
     put_b(out, ConvCfg<0>::kWdx, kx, (2 - ky) * 64 + co, ci, __float2half_rn(rn[t]));
   }
+}
+
+// Training dgrad (mode 0 on gradients): the transposed, flipped filter
+// W'[ci][co][2-ky][2-kx] = W[co][ci][ky][kx] as a mode-0 B pack, plain fp16
+// rounding (the backward tolerates fp16 operands).
+__global__ void pack_hidden_f16_t_kernel(const float* __restrict__ w, uint8_t* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*64 + ci of the forward filter
+  if (idx >= kC * kC) return;
+  const int co = idx / kC, ci = idx % kC;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int ky = t / 3, kx = t % 3;
+    // output channel ci of the dgrad conv at tap (2-ky, 2-kx): B row (2 - (2-ky))*64 + ci = ky*64 + ci
+    put_b(out, ConvCfg<0>::kWdx, 2 - kx, ky * 64 + ci, co, __float2half_rn(w[idx * 9 + t]));
+  }
+}
+
+cudaError_t launch_pack_hidden_f16_t(const float* w, uint8_t* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<0>::kW, st);
+  if (e != cudaSuccess) return e;
+  pack_hidden_f16_t_kernel<<<(kC * kC + 127) / 128, 128, 0, st>>>(w, out);
+  return cudaGetLastError();
 }
 
 // Wide hidden (mode 5): 128x128 filters, DC-compensated fp16, packed per output

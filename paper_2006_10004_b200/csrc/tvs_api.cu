@@ -18,54 +18,21 @@
 
 #include "../../include/tvs_b200.h"
 #include "common.cuh"
+#include "host_util.h"
 
 
-namespace {
-
-thread_local std::string g_last_error;
-
-struct TvsError : std::runtime_error {
-  int code;
-  TvsError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
-
-#define TVS_CUDA(call)                                                                                     \
-  do {                                                                                                     \
-    cudaError_t e_ = (call);                                                                               \
-    if (e_ != cudaSuccess)                                                                                 \
-      throw TvsError(TVS_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + " (" __FILE__ ":" + \
-                                     std::to_string(__LINE__) + ")");                                      \
-  } while (0)
-
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    TVS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-    if (!p || q != cudaDriverEntryPointSuccess) throw TvsError(TVS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
+namespace tvs_host {
+std::string& last_error() {
+  thread_local std::string msg;
+  return msg;
 }
+}  // namespace tvs_host
 
-// fp16 NHWC activation [B][H][W][C] (C = 64, or 128 = a hi|lo pair row) as a
-// 4-D tensor map, SW128, box (64, box_px, 1, 1)
-CUtensorMap make_act_map(void* base, int B, int H, int W, int box_px, int C = 64) {
-  CUtensorMap m;
-  const cuuint64_t rb = (cuuint64_t)C * 2;
-  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
-  cuuint64_t strides[3] = {rb, (cuuint64_t)W * rb, (cuuint64_t)H * W * rb};
-  cuuint32_t box[4] = {64, (cuuint32_t)box_px, 1, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw TvsError(TVS_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-  return m;
-}
-
-}  // namespace
+using tvs_host::DeviceGuard;
+using tvs_host::TvsError;
+using tvs_host::get_encode;
+using tvs_host::guarded;
+using tvs_host::make_act_map;
 
 struct tvs_plan {
   int device = 0, depth = 17, channels = 64, out_bands = 5, mode = TVS_MODE_FAST;
@@ -169,19 +136,6 @@ struct tvs_plan {
 
 namespace {
 
-// Restores the caller's current device on scope exit: the ABI may run on any
-// thread and must not change that thread's device.
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    if (prev != dev) TVS_CUDA(cudaSetDevice(dev));
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
-  }
-};
 
 void free_weights(tvs_plan* p) {
   void* ptrs[] = {p->wh, p->bh, p->wpack, p->hpack, p->whid, p->bhid, p->shid, p->w0u, p->b0u, p->c0pack, p->c0bias};
@@ -590,22 +544,6 @@ void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int
   }
 }
 
-template <typename F>
-int guarded(F&& f) {
-  try {
-    f();
-    return TVS_OK;
-  } catch (const TvsError& e) {
-    g_last_error = e.what();
-    return e.code;
-  } catch (const std::exception& e) {
-    g_last_error = e.what();
-    return TVS_E_CUDA;
-  } catch (...) {
-    g_last_error = "unknown error";
-    return TVS_E_CUDA;
-  }
-}
 
 }  // namespace
 
@@ -613,7 +551,7 @@ extern "C" {
 
 int tvs_abi_version(void) { return TVS_ABI_VERSION; }
 
-const char* tvs_last_error(void) { return g_last_error.c_str(); }
+const char* tvs_last_error(void) { return tvs_host::last_error().c_str(); }
 
 int tvs_plan_create(int device, int depth, int channels, int out_bands, int mode, tvs_plan** out_plan) {
   return tvs_plan_create_ex(device, depth, channels, out_bands, mode, 1, out_plan);

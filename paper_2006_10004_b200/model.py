@@ -17,8 +17,11 @@ parameter versions), hands them to a per-device C-ABI plan (libtvsb200.so), and 
 conv0 -> 15 tcgen05 hidden convs -> head on the GPU.  CPU tensors are copied
 to the execution device and the result copied back, so the reference's CPU
 callers (``predict_bands``, inference.py:25-32) work unchanged.  There is no
-CPU fallback and no train-mode path: ``forward`` raises in ``train()`` mode
-(batch statistics are out of scope) and when no CUDA device is present.
+CPU fallback: ``forward`` raises when no CUDA device is present.  In
+``train()`` mode it runs the B200 training step (train_step.py, csrc/train.cu):
+batch-statistics BatchNorm, an autograd backward on the C ABI, and the
+running-stat updates, so the reference's training loop (training.py:45-61)
+drives the drop-in unchanged.
 
 ``precision`` selects the numerics: ``"fast"`` (default; fp16 tcgen05 hidden
 layers, exact fp32 conv0/head; <= 1e-2 relative L2 per band vs the fp32
@@ -119,7 +122,16 @@ class TVSpecNet(nn.Module):
     def __getstate__(self):
         state = self.__dict__.copy()
         state["_plans"] = {}
+        state["_train_plans"] = {}
         return state
+
+    def _train_plan(self, idx: int):
+        from .train_step import new_train_plan
+
+        plans = self.__dict__.setdefault("_train_plans", {})
+        if idx not in plans:
+            plans[idx] = new_train_plan(self, idx)
+        return plans[idx]
 
     # ------------------------------------------------------ weight folding ----
     def _weight_key(self, device: torch.device) -> tuple:
@@ -208,12 +220,15 @@ class TVSpecNet(nn.Module):
             raise ValueError(f"expected (batch, 1, h, w) input, got {tuple(x.shape)}")
         if x.dtype != torch.float32:
             raise RuntimeError(f"Input type ({x.dtype}) and weight type (torch.float32) should be the same")
-        if self.training:
-            raise RuntimeError("TVSpecNet (B200) implements the eval-mode forward only; call .eval() first")
         if self.unshuffle == 2 and (x.shape[2] % 2 or x.shape[3] % 2):
             raise ValueError(f"unshuffle=2 needs even height and width, got {tuple(x.shape[2:])}")
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if self.training:
+            from .train_step import TrainForward, train_params
+
+            self._check_input(x)
+            return TrainForward.apply(self, x, *train_params(self))
         return self.forward_planes(x)[0]
 
     def forward_planes(self, x: torch.Tensor, closure: bool = False, rows: tuple[int, int] | None = None):
@@ -222,6 +237,8 @@ class TVSpecNet(nn.Module):
         head kernel's epilogue; ``rows=(row0, nrows)`` returns only that row
         window of the full-image forward (row-band sharding)."""
         self._check_input(x)
+        if self.training:
+            raise RuntimeError("forward_planes is the eval-mode (inference) forward; call .eval() first")
         dev = self._exec_device(x)
         plan = self._plan_for(dev)
         B, _, H, W = x.shape

@@ -1,0 +1,121 @@
+"""Train-mode forward and backward of the drop-in TVSpecNet on B200.
+
+The reference trains the module with torch autograd on the CPU
+(/root/reference/pkg/trainer/src/tvsurrogate/training.py:45-61,
+``_epoch_pass``: ``model.train()``, ``compute_loss(model(img), ...)``,
+``value.total.backward()``, ``optimizer.step()``).  The drop-in keeps that
+calling contract: in ``train()`` mode ``TVSpecNet.forward`` runs
+``TrainForward``, an autograd Function whose forward and backward are the
+C-ABI training step (``tvs_train_forward`` / ``tvs_train_backward``,
+csrc/train.cu), so the reference loop, its losses and its Adam optimizer work
+unchanged on the module's parameters (CPU or CUDA).
+
+BatchNorm2d semantics (model.py:41, train mode): normalisation by the batch
+mean and biased variance; running_mean / running_var move towards the batch
+mean and unbiased variance with the layer's momentum; num_batches_tracked
+counts steps.  Those buffer updates happen here, from the statistics the
+kernels return.
+"""
+
+from __future__ import annotations
+
+import torch
+from torch import nn
+
+from . import _native
+
+
+def _layers(model):
+    """(conv0, [(conv_j, bn_j)], head) of the reference body layout."""
+    mods = list(model.body)
+    convs = [m for m in mods if isinstance(m, nn.Conv2d)]
+    bns = [m for m in mods if isinstance(m, nn.BatchNorm2d)]
+    return convs[0], list(zip(convs[1:-1], bns)), convs[-1]
+
+
+def train_params(model) -> list[torch.Tensor]:
+    """The parameters the step differentiates, in a fixed order:
+    conv0.weight, conv0.bias, (conv_j.weight, bn_j.weight, bn_j.bias)*, head.weight, head.bias."""
+    c0, hidden, head = _layers(model)
+    out = [c0.weight, c0.bias]
+    for conv, bn in hidden:
+        out += [conv.weight, bn.weight, bn.bias]
+    return out + [head.weight, head.bias]
+
+
+class TrainForward(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, model, x, *params):
+        dev = model._exec_device(x)
+        idx = dev.index
+        plan = model._train_plan(idx)
+        nh = model.depth - 2
+        with torch.cuda.device(idx):
+            stream = torch.cuda.current_stream(idx)
+            staged = [p.detach().to(dev, torch.float32).contiguous() for p in params]
+            xd = x.detach().to(dev, torch.float32).contiguous()
+            w = [staged[0]] + [staged[2 + 3 * j] for j in range(nh)] + [staged[-2]]
+            bias = [staged[1]] + [None] * nh + [staged[-1]]
+            gamma = [staged[3 + 3 * j] for j in range(nh)]
+            beta = [staged[4 + 3 * j] for j in range(nh)]
+            B, _, H, W = xd.shape
+            out = torch.empty((B, model.out_bands, H, W), device=dev)
+            mean = torch.empty((max(nh, 1), 64), device=dev)
+            var = torch.empty((max(nh, 1), 64), device=dev)
+            _, hidden, _ = _layers(model)
+            eps = hidden[0][1].eps if hidden else 1e-5
+            plan.forward([t.data_ptr() for t in w], [0 if t is None else t.data_ptr() for t in bias],
+                         [t.data_ptr() for t in gamma], [t.data_ptr() for t in beta], eps, xd.data_ptr(),
+                         out.data_ptr(), mean.data_ptr(), var.data_ptr(), B, H, W, stream.cuda_stream)
+            model._train_step_id = getattr(model, "_train_step_id", 0) + 1
+            ctx.step_id = model._train_step_id
+        _update_running_stats(model, mean, var)
+        ctx.model, ctx.plan, ctx.dev = model, plan, dev
+        ctx.keep = (staged, xd, w, gamma, beta)  # the plan reads these device pointers in backward
+        ctx.param_devices = [(p.device, p.dtype) for p in params]
+        ctx.shapes = [p.shape for p in params]
+        return out if x.is_cuda else out.to(x.device)
+
+    @staticmethod
+    def backward(ctx, g_out):
+        model, plan, dev = ctx.model, ctx.plan, ctx.dev
+        if getattr(model, "_train_step_id", None) != ctx.step_id:
+            raise RuntimeError("TVSpecNet (B200) training: backward of an older forward; the train plan keeps "
+                               "one step's activations (run forward and backward in pairs)")
+        nh = model.depth - 2
+        idx = dev.index
+        with torch.cuda.device(idx):
+            stream = torch.cuda.current_stream(idx)
+            g = g_out.detach().to(dev, torch.float32).contiguous()
+            grads = [torch.empty(s, device=dev, dtype=torch.float32) for s in ctx.shapes]
+            dw = [grads[0]] + [grads[2 + 3 * j] for j in range(nh)] + [grads[-2]]
+            dbias = [grads[1]] + [None] * nh + [grads[-1]]
+            dgamma = [grads[3 + 3 * j] for j in range(nh)]
+            dbeta = [grads[4 + 3 * j] for j in range(nh)]
+            plan.backward(g.data_ptr(), [t.data_ptr() for t in dw], [0 if t is None else t.data_ptr() for t in dbias],
+                          [t.data_ptr() for t in dgamma], [t.data_ptr() for t in dbeta], stream.cuda_stream)
+        out = [gr.to(d, dt) for gr, (d, dt) in zip(grads, ctx.param_devices)]
+        ctx.keep = None
+        return (None, None, *out)
+
+
+@torch.no_grad()
+def _update_running_stats(model, mean: torch.Tensor, var: torch.Tensor) -> None:
+    """BatchNorm2d train-mode buffer updates (torch semantics: momentum, or the
+    cumulative average when momentum is None)."""
+    _, hidden, _ = _layers(model)
+    for j, (_, bn) in enumerate(hidden):
+        if not bn.track_running_stats:
+            continue
+        bn.num_batches_tracked.add_(1)
+        m = bn.momentum if bn.momentum is not None else 1.0 / float(bn.num_batches_tracked.item())
+        rm = mean[j].to(bn.running_mean.device, bn.running_mean.dtype)
+        rv = var[j].to(bn.running_var.device, bn.running_var.dtype)
+        bn.running_mean.mul_(1.0 - m).add_(rm, alpha=m)
+        bn.running_var.mul_(1.0 - m).add_(rv, alpha=m)
+
+
+def new_train_plan(model, idx: int) -> _native.TrainPlan:
+    if model.channels != 64 or model.unshuffle != 1:
+        raise NotImplementedError("the B200 training step is built for the reference architecture (64 channels)")
+    return _native.TrainPlan(idx, model.depth, model.out_bands)

@@ -72,10 +72,11 @@ def test_layer_params_fold_matches_eval_bn():
     torch.testing.assert_close(y, ref, rtol=1e-12, atol=1e-12)
 
 
-def test_train_mode_and_dtype_rejected():
+def test_no_cpu_fallback_and_dtype_rejected():
     m = TVSpecNet()
-    with pytest.raises(RuntimeError):
-        m(torch.zeros(1, 1, 8, 8))  # train mode: no batch-statistics path
+    if not torch.cuda.is_available():
+        with pytest.raises(RuntimeError):
+            m(torch.zeros(1, 1, 8, 8))  # train mode needs the B200 training step: no CPU fallback
     m.eval()
     with pytest.raises(RuntimeError):
         m(torch.zeros(1, 1, 8, 8, dtype=torch.float64))
