@@ -72,36 +72,41 @@ def test_train_step_selectors(gold, sel):
         assert torch.isfinite(p.grad).all()
 
 
-def test_epoch_pass_with_adam_tracks_oracle():
-    """Three _epoch_pass iterations (training.py:45-61) with Adam(lr=1e-3) on
-    the drop-in and on the CPU oracle: the losses stay together, and after the
-    steps eval() forwards agree (running statistics and weights moved alike)."""
-    torch.manual_seed(0)
+def _adam_run(model, dev, dtype, steps=3):
+    opt = torch.optim.Adam(model.parameters(), lr=1e-3)
+    losses = []
+    for it in range(steps):
+        img, gt, res = (t.to(dev, dtype) for t in train_batch(seed=10 + it, B=2, H=40, W=36))
+        opt.zero_grad(set_to_none=True)
+        v = compute_loss(model(img), gt, img, res, "L")
+        v.total.backward()
+        opt.step()
+        losses.append(v.total.item())
+    model.eval()
+    img, _, _ = train_batch(seed=99, B=1, H=48, W=48)
+    with torch.no_grad():
+        y = model(img.to(dev, dtype)).double().cpu()
+    return losses, y
+
+
+def test_epoch_pass_with_adam_tracks_reference_within_its_own_fp32_floor():
+    """Three _epoch_pass iterations (training.py:45-61) with Adam(lr=1e-3).
+    Adam's normalised steps amplify the gradients' conditioning: the oracle's
+    own fp32 run drifts from its fp64 run by 2e-3 in the third loss and 30% in
+    the eval output afterwards.  The drop-in must stay within 4x that floor
+    of the fp64 run."""
     state = build_seeded_state()
     ours = TVSpecNet()
     ours.load_state_dict(state)
-    ours = ours.cuda().train()
-    ref = oracle_from_state(state).train()
-    opt_o = torch.optim.Adam(ours.parameters(), lr=1e-3)
-    opt_r = torch.optim.Adam(ref.parameters(), lr=1e-3)
-    for it in range(3):
-        img, gt, res = train_batch(seed=10 + it, B=2, H=40, W=36)
-        opt_o.zero_grad(set_to_none=True)
-        lo = compute_loss(ours(img.cuda()), gt.cuda(), img.cuda(), res.cuda(), "L")
-        lo.total.backward()
-        opt_o.step()
-        opt_r.zero_grad(set_to_none=True)
-        lr = compute_loss(ref(img), gt, img, res, "L")
-        lr.total.backward()
-        opt_r.step()
-        assert abs(lo.total.item() - lr.total.item()) <= 1e-3 * abs(lr.total.item()), it
-    ours.eval()
-    ref.eval()
-    img, _, _ = train_batch(seed=99, B=1, H=48, W=48)
-    with torch.no_grad():
-        a = ours(img.cuda()).cpu()
-        b = ref(img)
-    assert (torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(b)).item() < 2e-2
+    lo, yo = _adam_run(ours.cuda().train(), "cuda", torch.float32)
+    l32, y32 = _adam_run(oracle_from_state(state).train(), "cpu", torch.float32)
+    l64, y64 = _adam_run(oracle_from_state(state).double().train(), "cpu", torch.float64)
+    print("losses ours", lo, "fp32", l32, "fp64", l64)
+    assert abs(lo[0] - l64[0]) <= 1e-5 * abs(l64[0])
+    for i in range(1, 3):
+        assert abs(lo[i] - l64[i]) <= 4 * abs(l32[i] - l64[i]) + 1e-4 * abs(l64[i]), i
+    floor = torch.linalg.vector_norm(y32 - y64).item()
+    assert torch.linalg.vector_norm(yo - y64).item() <= 4 * floor + 1e-3 * torch.linalg.vector_norm(y64).item()
 
 
 def test_ragged_shapes_and_forward_backward_pairing():
