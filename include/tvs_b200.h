@@ -104,6 +104,18 @@ int tvs_plan_sync(tvs_plan* plan, void* stream);
 int tvs_forward(tvs_plan* plan, const float* x, float* bands, float* closure_or_null, int B, int H, int W,
                 int valid_row0, int valid_rows, void* stream);
 
+/* tvs_forward with the fused band-sum reconstruction check (north_star item 3;
+ * the closure identity of inference.py:34-42, tested by the reference at
+ * pkg/trainer/tests/test_inference.py:31-38).  `closure` is required.  The
+ * head kernel's epilogue evaluates r = x - (sum_k bands_k + closure) from the
+ * fp32 values it stores and accumulates, per image b over the row window,
+ *   recon[2b]   = sum r^2,   recon[2b+1] = sum x^2     (fp64)
+ * into `recon`, a caller-owned DEVICE buffer of 2*B doubles (zeroed by the
+ * call, stream-ordered).  sqrt(recon[2b] / recon[2b+1]) is the image's
+ * relative reconstruction error. */
+int tvs_forward_checked(tvs_plan* plan, const float* x, float* bands, float* closure, double* recon, int B, int H,
+                        int W, int valid_row0, int valid_rows, void* stream);
+
 /* Same contract with HOST buffers: copies in, runs, copies out, and
  * synchronises `stream` before returning. */
 int tvs_forward_host(tvs_plan* plan, const float* x_host, float* bands_host, float* closure_host_or_null, int B,

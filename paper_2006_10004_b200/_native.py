@@ -31,6 +31,7 @@ EXPORTS = (
     "tvs_plan_set_option",
     "tvs_plan_sync",
     "tvs_forward",
+    "tvs_forward_checked",
     "tvs_forward_host",
     "tvs_last_launch_count",
     "tvs_last_used_stack",
@@ -89,6 +90,8 @@ def load() -> ctypes.CDLL:
         lib.tvs_last_used_stack.argtypes = [P]
         lib.tvs_forward.restype = i
         lib.tvs_forward.argtypes = [P, P, P, P, i, i, i, i, i, P]
+        lib.tvs_forward_checked.restype = i
+        lib.tvs_forward_checked.argtypes = [P, P, P, P, P, i, i, i, i, i, P]
         lib.tvs_forward_host.restype = i
         lib.tvs_forward_host.argtypes = [P, P, P, P, i, i, i, P]
         lib.tvs_last_launch_count.restype = i
@@ -168,6 +171,16 @@ class Plan:
                 self.handle, ctypes.c_void_p(x_ptr), ctypes.c_void_p(bands_ptr),
                 ctypes.c_void_p(closure_ptr) if closure_ptr else None,
                 B, H, W, row0, rows, ctypes.c_void_p(stream),
+            )
+        )
+
+    def forward_checked(self, x_ptr, bands_ptr, closure_ptr, recon_ptr, B, H, W, row0, rows, stream: int) -> None:
+        """tvs_forward_checked: the forward plus the fused band-sum
+        reconstruction check sums (recon: device float64 (B, 2))."""
+        check(
+            self.lib.tvs_forward_checked(
+                self.handle, ctypes.c_void_p(x_ptr), ctypes.c_void_p(bands_ptr), ctypes.c_void_p(closure_ptr),
+                ctypes.c_void_p(recon_ptr), B, H, W, row0, rows, ctypes.c_void_p(stream),
             )
         )
 

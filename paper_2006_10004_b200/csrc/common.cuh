@@ -56,6 +56,25 @@ struct KernelSpan {
 // status flag store (host-mapped memory: plain stores, no system-scope atomics)
 __device__ __forceinline__ void flag_set(int* p) { *(volatile int*)p = 1; }
 
+// Fused band-sum reconstruction check (north_star item 3; the closure identity
+// of inference.py:34-42 / pkg/trainer/tests/test_inference.py:31-38): every
+// head epilogue that writes the closure plane c = x - sum_k b_k also evaluates
+// r = x - (sum_k b_k + c) from the values it stores and adds r^2 and x^2 (fp64)
+// to recon[2b], recon[2b+1].  Called by all 32 lanes of a warp (lanes without
+// a pixel pass r = x = 0); one pair of atomics per warp and row.
+__device__ __forceinline__ void recon_accumulate(double* recon, int b, float r, float x) {
+  double r2 = (double)r * (double)r, x2 = (double)x * (double)x;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(recon + 2 * b, r2);
+    atomicAdd(recon + 2 * b + 1, x2);
+  }
+}
+
 struct ConvArgs {
   int B, H, W;
   int strips;            // ceil(W / 128)
@@ -67,6 +86,7 @@ struct ConvArgs {
   const float* x;        // (B,1,H,W) input plane for the closure
   float* bands;          // (B,K,rows,W)
   float* closure;        // (B,1,rows,W) or null
+  double* recon;         // null, or (B,2) fused reconstruction check sums (recon_accumulate)
   int K;
   // fp32-accurate split hidden layer: output fp16 pair rows [B][H][W][hi 64 | lo 64]
   uint8_t* act_out;
@@ -77,7 +97,10 @@ struct ConvArgs {
   int out_single;  // wide hidden (modes 5 / 9): write single fp16 output instead of the hi/lo pair
   int nlayers;
   int* rowcnt;
-  const int2* items;  // work items {image, layer << 16 | strip} in a topological order
+  // work items {image, layer << 16 | strip, first row, end row} (image -1:
+  // padding, skipped) in a topological order, CTA i taking entries i, i+G, ...
+  const int4* items;
+  int nitems;
   // per-image input exponent e_b (tvs_api.cu, input_scale_kernel): the
   // activations of image b are computed as 2^-e_b times the model's (exact:
   // ReLU commutes with powers of two), keeping them inside the fp16 range.
@@ -106,6 +129,7 @@ constexpr int kStatNonFiniteOut = 1;  // a head wrote a NaN / Inf band value
 constexpr int kStatNonFiniteIn = 2;   // the input held NaN / Inf (the reference propagates them)
 constexpr int kStatWords = 4;
 constexpr int kDbgWithholdFlag = 1 << 17;
+constexpr int kDbgTrace = 1 << 19;  // stack: globaltimer per row of image 0 strip 0 (g_trace, tvs_debug_trace)
 constexpr int kDbgNoPdlStack = 1 << 18;     // launch the stack without programmatic serialization  // stack: never publish row 1 of (image 0, strip 0, layer 2)
 // 2^k as an exact fp32 (|k| <= 126)
 __host__ __device__ __forceinline__ float pow2i(int k) {
@@ -127,6 +151,7 @@ cudaError_t launch_conv_stack(const CUtensorMap& tm_in0, const CUtensorMap& tm_o
 // one CTA per SM fits (all `grid` CTAs co-resident)
 bool conv_stack_fits(int num_sms, int grid);
 int debug_cycles(unsigned long long* out, int reset);  // TVS_CONV_DBG bit 15 counters
+int debug_trace(unsigned long long* out, int reset);   // kDbgTrace row timeline
 
 // fp32 hidden layer (conv_edge.cu)
 constexpr int kF32TileRows = 4, kF32TilePx = 32, kF32CiChunk = 16;
@@ -171,6 +196,7 @@ cudaError_t launch_input_scale(const float* x, int B, long long px_per_image, fl
 // the input-scale kernel's scratch: 2 * B ints, zero on first use; the kernel
 // leaves it zeroed for the next forward
 cudaError_t launch_head_f32(int C, const float* act, const float* x, const float* wh, const float* bh, float* bands,
+                            double* recon,
                             float* closure, int B, int H, int W, int K, int row0, int rows, int* status,
                             cudaStream_t st);
 cudaError_t launch_hidden_f32(int C, const float* in, float* out, const float* w, const float* scale,

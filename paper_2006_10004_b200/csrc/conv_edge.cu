@@ -127,8 +127,8 @@ __device__ __forceinline__ void load_act8<float>(const float* src, float* v) {
 template <typename T, int C>
 __global__ void __launch_bounds__(128)
 head_kernel(const T* __restrict__ act, const float* __restrict__ x, const float* __restrict__ wh,
-            const float* __restrict__ bh, float* __restrict__ bands, float* __restrict__ closure, int B,
-            int H, int W, int K, int row0, int rows, int* __restrict__ status) {
+            const float* __restrict__ bh, float* __restrict__ bands, float* __restrict__ closure,
+            double* __restrict__ recon, int B, int H, int W, int K, int row0, int rows, int* __restrict__ status) {
   extern __shared__ float swh[];  // [9][64][K]
   for (int i = threadIdx.x; i < 9 * C * K; i += blockDim.x) {
     const int k = i % K, ci = (i / K) % C, t = i / (K * C);
@@ -136,8 +136,10 @@ head_kernel(const T* __restrict__ act, const float* __restrict__ x, const float*
   }
   __syncthreads();
   const long long nout = (long long)B * rows * W;
-  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= nout) return;
+  const long long p0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = p0 < nout;
+  if (!live && !recon) return;
+  const long long p = live ? p0 : nout - 1;  // dead lanes of the last warp only feed zeros to recon
   const int xw = (int)(p % W);
   const long long t = p / W;
   const int rr = (int)(t % rows);
@@ -178,12 +180,27 @@ head_kernel(const T* __restrict__ act, const float* __restrict__ x, const float*
   for (int k = 0; k < kMaxBands; ++k)
     if (k < K) {
       const float o = (float)(acc[k] + (Acc)bh[k]);
-      ob[k * plane] = o;
+      if (live) ob[k * plane] = o;
       sum += o;
       bad |= !isfinite(o);
     }
   if (bad && status) flag_set(status + kStatNonFiniteOut);
-  if (closure != nullptr) closure[b * plane + (long long)rr * W + xw] = x[(b * H + y) * (long long)W + xw] - sum;
+  const float xv = x[(b * H + y) * (long long)W + xw];
+  const float c = xv - sum;
+  if (closure != nullptr && live) closure[b * plane + (long long)rr * W + xw] = c;
+  if (recon) {
+    // warps of this kernel straddle images when rows*W % 32 != 0: one atomic
+    // pair per lane-image run would need segmented reduction, so use per-lane
+    // atomics there (the CUDA-core fp32 path is the slow reference path)
+    const float r = live ? xv - (sum + c) : 0.0f, xx = live ? xv : 0.0f;
+    const long long b0 = __shfl_sync(0xffffffffu, b, 0);
+    if (__all_sync(0xffffffffu, b == b0)) {
+      recon_accumulate(recon, (int)b0, r, xx);
+    } else if (live) {
+      atomicAdd(recon + 2 * b, (double)r * r);
+      atomicAdd(recon + 2 * b + 1, (double)xx * xx);
+    }
+  }
 }
 
 // --------------------------------------------------- fp32 hidden layer ----
@@ -367,15 +384,16 @@ cudaError_t launch_conv0_unshuffle(const float* x, void* act, const float* w, co
 }
 
 cudaError_t launch_head_f32(int C, const float* act, const float* x, const float* wh, const float* bh, float* bands,
+                            double* recon,
                             float* closure, int B, int H, int W, int K, int row0, int rows, int* status,
                             cudaStream_t st) {
   const long long nout = (long long)B * rows * W;
   const unsigned grid = (unsigned)((nout + 127) / 128);
   const size_t smem = (size_t)9 * C * K * sizeof(float);
   if (C == 64)
-    head_kernel<float, 64><<<grid, 128, smem, st>>>(act, x, wh, bh, bands, closure, B, H, W, K, row0, rows, status);
+    head_kernel<float, 64><<<grid, 128, smem, st>>>(act, x, wh, bh, bands, closure, recon, B, H, W, K, row0, rows, status);
   else if (C == 128)
-    head_kernel<float, 128><<<grid, 128, smem, st>>>(act, x, wh, bh, bands, closure, B, H, W, K, row0, rows, status);
+    head_kernel<float, 128><<<grid, 128, smem, st>>>(act, x, wh, bh, bands, closure, recon, B, H, W, K, row0, rows, status);
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();

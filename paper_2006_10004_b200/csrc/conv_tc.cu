@@ -88,30 +88,34 @@ struct SegIter {
   }
 };
 
-// Layer-stack work items (mode 8): item k = (image b, hidden layer j, strip s),
-// ordered image-major, then layer, then strip, so an item only depends on items
-// with smaller k (layer j-1 of the same image, strips s-1..s+1).  CTA i takes
-// items i, i+G, i+2G, ... (equal-length columns of all H rows); the minimal
-// unfinished item always has its inputs complete, so the persistent grid
-// cannot deadlock as long as all G CTAs are co-resident (G <= #SMs, 1 CTA/SM).
-// The item list itself (a.items, built by the host: tvs_api.cu stack_items)
-// is any topological order; the default is image-major.
+// Layer-stack work items (mode 8): item = output rows [ya, yb) of one strip of
+// one hidden layer of one image (whole columns for big batches, row bands for
+// small ones).  An item depends only on layer j-1 rows ya-1..yb of its image
+// (strips s-1..s+1), so any order listing an image's layer j-1 items before
+// its layer j items is topological.  CTA i walks entries i, i+G, i+2G, ... of
+// the host-built table (stack_items in tvs_api.cu), which keeps every CTA's
+// own sequence topologically sorted; then the minimal unfinished item is
+// always the one its CTA is working on and has its inputs, so the persistent
+// grid cannot deadlock while all G CTAs are co-resident (cooperative launch,
+// 1 CTA/SM).  Entries with image -1 pad the table.
 struct ItemIter {
   long long k, n;
   TVS_DEV ItemIter(const ConvArgs& a, int = 1, int = 1) {
     k = blockIdx.x;
-    n = (long long)a.B * a.strips * a.nlayers;
+    n = a.nitems;
+    while (k < n && a.items[k].x < 0) k += gridDim.x;
   }
   TVS_DEV int first_layer_or0(const ConvArgs& a) const { return first_layer(a); }
   TVS_DEV int first_layer(const ConvArgs& a) const { return k < n ? a.items[k].y >> 16 : 0; }
   TVS_DEV bool next(const ConvArgs& a, Segment& g) {
+    while (k < n && a.items[k].x < 0) k += gridDim.x;
     if (k >= n) return false;
-    const int2 it = a.items[k];
+    const int4 it = a.items[k];
     g.b = it.x;
     g.layer = it.y >> 16;
     g.x0 = (it.y & 0xffff) * kStripPx;
-    g.ya = 0;
-    g.yb = a.H;
+    g.ya = it.z;
+    g.yb = it.w;
     g.h = 0;
     k += gridDim.x;
     return true;
@@ -123,6 +127,16 @@ struct ItemIter {
 // [3] waiting for a layer's weights, [4] general-path rows, [5] fast-path rows,
 // [6] elapsed ns (globaltimer), so [0] / [6] is the mean SM clock in GHz
 __device__ unsigned long long g_dbg_cycles[8];
+// kDbgTrace (layer stack, image 0, strip 0, rows < kTraceRows): [0][layer][row]
+// gate passed (producer), [1][layer][row] input row landed (MMA issuer),
+// [2][layer][row] output row published (epilogue), [3] accumulator ready
+// (epilogue warp quarter 0), [4] TMA store issued; globaltimer ns
+constexpr int kTraceKinds = 5, kTraceRows = 1024, kTraceLayers = 32;
+__device__ unsigned long long g_trace[kTraceKinds][kTraceLayers][kTraceRows];
+TVS_DEV void trace_mark(const ConvArgs& a, int kind, const Segment& g, int row) {
+  if ((a.dbg & kDbgTrace) && g.b == 0 && g.x0 == 0 && row >= 0 && row < kTraceRows && g.layer < kTraceLayers)
+    g_trace[kind][g.layer][row] = globaltimer_ns();
+}
 
 // Producer side of the layer stack: input row r of a layer-j item (j >= 1) is
 // layer j-1's output row r of strips s-1..s+1 (the 130-px halo box reaches one
@@ -381,6 +395,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (Cfg::kStack)
             if (g.layer > 0 && !(a.dbg & 1)) gate.wait(a, g, r);
+          if constexpr (Cfg::kStack) trace_mark(a, 0, g, r);
           constexpr int nbuf = (Cfg::kSplit ? 2 : 1) * Cfg::kKBlk;  // [hi blocks][lo blocks]
           if (a.dbg & 32) {  // ablation (TVS_CONV_DBG): no input loads
             mbar_arrive(&full[stage]);
@@ -464,6 +479,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             } else if (!prewaited)
               mbar_wait2(&slot_empty[(sq + 2) & Cfg::kRingMask], (((sq + 2) >> Cfg::kRingLog) & 1) ^ 1, &full[stage],
                          phase);
+            if constexpr (Cfg::kStack) trace_mark(a, 1, g, r);
             tc_fence_after();
             const uint64_t ad_row = adesc0 + (uint64_t)((stage * Cfg::kStageBytes) >> 4);
             const uint32_t t0s = s * NB;  // slot column offset inside a ring
@@ -582,6 +598,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         const uint32_t Ct = R1t, Cb = R1b, Ci = idesc_of(C_e - s1b + 1);
         const uint32_t Dt = R1t + (uint32_t)(D_b - s1b) * NB, Db = brow16(D_b), Di = idesc_of(q_hi - D_b + 1);
         mbar_wait(&full[stage], phase);
+        if constexpr (Cfg::kStack) if (leader) trace_mark(a, 1, g, r);
         if (Cfg::kStack && (a.dbg & 32768)) { cyc[1] += tg1 - tg0; cyc[2] += clock64() - tg1; ++cyc[4]; }
         tc_fence_after();
         if (leader) {
@@ -659,6 +676,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         if (gsel != grp) continue;
         const uint32_t slot = seq & Cfg::kRingMask;
         mbar_wait(&slot_full[slot], (seq >> Cfg::kRingLog) & 1);
+        if constexpr (Cfg::kStack) if (quarter == 0 && lane == 0) trace_mark(a, 3, g, q);
         tc_fence_after();
         const int xg = g.x0 + px;
         if constexpr (Cfg::kPartsW) {
@@ -852,6 +870,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             tma_store_4d(tmo, sOut + ew * Cfg::kStageOut, 0, g.x0 + quarter * 32, q, g.b);
             bulk_commit();
             if constexpr (Cfg::kStack) {
+              if (quarter == 0) trace_mark(a, 4, g, q);
               // this warp's quarter row has landed (async proxy); order it
               // before the generic-proxy release below (the reader acquires,
               // then fences into the async proxy before its TMA load)
@@ -865,8 +884,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             __syncwarp();
             named_bar_sync(1 + grp, 128);
             const bool withhold = (a.dbg & kDbgWithholdFlag) && g.b == 0 && g.x0 == 0 && q == 1 && g.layer == 2;
-            if (quarter == 0 && lane == 0 && !withhold)
+            if (quarter == 0 && lane == 0 && !withhold) {
               red_release_gpu_add(a.rowcnt + ((long long)g.b * a.strips + g.x0 / kStripPx) * a.H + q, 4);
+              trace_mark(a, 2, g, q);
+            }
           }
         } else if constexpr (Cfg::kUnshuf) {
           uint32_t v[4][16];
@@ -878,6 +899,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
+          double rr2 = 0.0, rx2 = 0.0;  // reconstruction check (recon_accumulate, pre-squared)
           if (xg < a.W) {
             // half-res pixel (q, xg) -> full-res 2x2 block at rows 2q+i, cols 2xg+j
             const int Wf = 2 * a.W;
@@ -911,9 +933,23 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
               for (int i = 0; i < 2; ++i) {
                 const float2 xi =
                     *reinterpret_cast<const float2*>(a.x + ((long long)g.b * 2 * a.H + 2 * q + i) * Wf + 2 * xg);
-                *reinterpret_cast<float2*>(a.closure + (long long)g.b * planef + (r0f + i) * Wf + 2 * xg) =
-                    make_float2(xi.x - sum[i * 2], xi.y - sum[i * 2 + 1]);
+                const float2 c = make_float2(xi.x - sum[i * 2], xi.y - sum[i * 2 + 1]);
+                *reinterpret_cast<float2*>(a.closure + (long long)g.b * planef + (r0f + i) * Wf + 2 * xg) = c;
+                const float r0 = xi.x - (sum[i * 2] + c.x), r1 = xi.y - (sum[i * 2 + 1] + c.y);
+                rr2 += (double)r0 * r0 + (double)r1 * r1;
+                rx2 += (double)xi.x * xi.x + (double)xi.y * xi.y;
               }
+            }
+          }
+          if (a.recon) {  // four full-res pixels per lane: pre-squared sums
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              rr2 += __shfl_xor_sync(0xffffffffu, rr2, o);
+              rx2 += __shfl_xor_sync(0xffffffffu, rx2, o);
+            }
+            if (lane == 0) {
+              atomicAdd(a.recon + 2 * g.b, rr2);
+              atomicAdd(a.recon + 2 * g.b + 1, rx2);
             }
           }
         } else {
@@ -956,6 +992,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
+          float rr = 0.0f, rx = 0.0f;  // reconstruction-check residual and input of this lane's pixel
           if (xg < a.W) {
             const long long plane = (long long)a.rows * a.W;
             const long long pix = (long long)(q - a.row0) * a.W + xg;
@@ -973,8 +1010,15 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
               }
             }
             if (bad && a.status) flag_set(a.status + kStatNonFiniteOut);
-            if (a.closure) a.closure[(long long)g.b * plane + pix] = a.x[((long long)g.b * a.H + q) * a.W + xg] - sum;
+            if (a.closure) {
+              const float xv = a.x[((long long)g.b * a.H + q) * a.W + xg];
+              const float c = xv - sum;
+              a.closure[(long long)g.b * plane + pix] = c;
+              rr = xv - (sum + c);
+              rx = xv;
+            }
           }
+          if (a.recon) recon_accumulate(a.recon, g.b, rr, rx);  // warp-uniform; every lane arrives
         }
       }
     }
@@ -1277,6 +1321,15 @@ cudaError_t launch_conv_stack(const CUtensorMap& tm_in0, const CUtensorMap& tm_o
   cfg.attrs = attr;
   cfg.numAttrs = (a.dbg & kDbgNoPdlStack) ? 1 : 2;
   return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<8>, tm_in0, tm_out1, a, sm);
+}
+
+int debug_trace(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)) != cudaSuccess) return -1;
+  if (reset) {
+    static unsigned long long z[kTraceKinds * kTraceLayers * kTraceRows];
+    cudaMemcpyToSymbol(g_trace, z, sizeof(z));
+  }
+  return 0;
 }
 
 int debug_cycles(unsigned long long* out, int reset) {

@@ -45,6 +45,8 @@ struct tvs_plan {
   // the next tvs_plan_set_weights.
   struct Options {
     int stack = -1;             // layer stack K4: -1 auto (item-rich chunks), 0 off, 1 whenever legal
+    int stack_band_rows = 0;    // layer-stack item height: 0 auto, R > 0 rows per item (>= H: whole columns)
+    int stack_skew = 1;         // layer-stack row bands: layer j's band edges sit at j*skew mod R
     int conv0_tc = 1;           // K1 on tcgen05 (TF32 hi/lo) instead of the CUDA-core K1
     int wide_pair_layers = 12;  // (pack) wide variant: leading hidden layers on fp16 hi/lo pairs
     int wide_halves = 1;        // (pack) wide single-input layers on output-channel halves (mode 11)
@@ -114,11 +116,16 @@ struct tvs_plan {
   // occupancy); cleared if the driver ever refuses the cooperative launch
   bool stack_ok = false;
   static constexpr int kStackMinItems = 6;
+  // row-band stack items (auto): images at least kStackMinBandH tall whose
+  // per-layer launches give each SM at most kBandMaxRowsPerSm strip-rows
+  static constexpr int kStackMinBandH = 128;
+  static constexpr double kBandMaxRowsPerSm = 8.0;
+  static constexpr int kStackBandRows = 6;
   int* rowcnt = nullptr;  // row flags (B*strips*H ints), zeroed per chunk
   size_t rowcnt_n = 0;
-  // work-item tables per (B, strips, layers), uploaded once and never
-  // overwritten (a running stack kernel may be reading an older one)
-  struct Items { long long key[3]; int2* dev; int2* host; };
+  // work-item tables per (B, strips, layers, bands, order), uploaded once and
+  // never overwritten (a running stack kernel may be reading an older one)
+  struct Items { long long key[6]; int4* dev; int4* host; size_t n; };
   std::vector<Items> items;
 
   int n_hidden() const { return depth - 2; }
@@ -173,26 +180,48 @@ void ensure_act(tvs_plan* p, size_t bytes) {
   p->act_bytes = bytes;
 }
 
-// Work items of the layer-stack kernel for (B, strips, layers) in a
-// topological order: image-major, then layer, then strip (an item only
-// depends on layer j-1 items of its image, which sort before it).
-const int2* stack_items(tvs_plan* p, int B, int strips, int L, cudaStream_t st) {
-  const long long key[3] = {B, strips, L};
+// Work items of the layer-stack kernel (conv_tc.cu ItemIter) for a chunk of B
+// images, `strips` strips, L hidden layers and H rows, image-major, then
+// layer, then row band, then strip: an item only depends on layer j-1 items of
+// its image, which sort before it.  CTA i runs entries i, i+G, ... in table
+// order, so every CTA's sequence is topologically sorted too.
+//
+// Row bands (R < H) are skewed: layer j's band edges sit at rows congruent to
+// j*skew (mod R).  A band [a, a+R) of layer j then reads rows a-1 .. a+R of
+// layer j-1, which are rows skew-1 and skew of two layer j-1 bands: both are
+// produced early in those items, so every layer trails the one before it by a
+// few rows.  With aligned edges (skew 0) row a-1 is the LAST row of the band
+// above, and band k of layer j could only start once band k-1 of layer j-1 had
+// finished: a diagonal wavefront costing a whole band per layer
+// (tools/stack_trace.py).
+const int4* stack_items(tvs_plan* p, int B, int strips, int L, int H, int R, int skew, cudaStream_t st,
+                        size_t* n_out) {
+  const long long key[6] = {B, strips, L, H, R, skew};
   for (auto& it : p->items)
-    if (std::equal(key, key + 3, it.key)) return it.dev;
-  const size_t n = (size_t)B * strips * L;
-  tvs_plan::Items it{{key[0], key[1], key[2]}, nullptr, nullptr};
-  TVS_CUDA(cudaMallocHost(&it.host, n * sizeof(int2)));
-  size_t k = 0;
+    if (std::equal(key, key + 6, it.key)) {
+      *n_out = it.n;
+      return it.dev;
+    }
+  std::vector<int4> v;
   for (int i = 0; i < B; ++i)
-    for (int j = 0; j < L; ++j)
-      for (int s = 0; s < strips; ++s) it.host[k++] = make_int2(i, j << 16 | s);
-  if (cudaMalloc(&it.dev, n * sizeof(int2)) != cudaSuccess) {
+    for (int j = 0; j < L; ++j) {
+      const int s0 = R < H ? (int)(((long long)j * skew) % R) : 0;  // first band edge below row 0
+      for (int ya = 0; ya < H;) {
+        const int yb = std::min(H, ya == 0 && s0 > 0 ? s0 : ya + R);
+        for (int s = 0; s < strips; ++s) v.push_back(make_int4(i, j << 16 | s, ya, yb));
+        ya = yb;
+      }
+    }
+  tvs_plan::Items it{{key[0], key[1], key[2], key[3], key[4], key[5]}, nullptr, nullptr, v.size()};
+  TVS_CUDA(cudaMallocHost(&it.host, v.size() * sizeof(int4)));
+  std::copy(v.begin(), v.end(), it.host);
+  if (cudaMalloc(&it.dev, v.size() * sizeof(int4)) != cudaSuccess) {
     cudaFreeHost(it.host);
     throw TvsError(TVS_E_CUDA, "cudaMalloc of the layer-stack item table failed");
   }
-  TVS_CUDA(cudaMemcpyAsync(it.dev, it.host, n * sizeof(int2), cudaMemcpyHostToDevice, st));
+  TVS_CUDA(cudaMemcpyAsync(it.dev, it.host, v.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
   p->items.push_back(it);
+  *n_out = it.n;
   return it.dev;
 }
 
@@ -243,7 +272,7 @@ void drain_profile(tvs_plan* p) {
 }
 
 void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B, int H, int W, int row0, int rows,
-               cudaStream_t st, const int* escale, int* status, bool conv0_pdl) {
+               cudaStream_t st, const int* escale, int* status, bool conv0_pdl, double* recon) {
   void* const* act = p->act;
   const int max_ctas = p->num_sms;
   const bool fast = p->tc_path();
@@ -255,15 +284,33 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
   // layer stack (FAST path): all CTAs of the persistent grid co-resident
   // (cooperative launch, verified at plan creation)
   bool stack = false;
-  const long long stack_items_n = (long long)B * ((W / us + tvs::kStripPx - 1) / tvs::kStripPx) * p->n_hidden();
-  const int stack_grid = (int)std::min<long long>(p->num_sms, stack_items_n);
-  if (fast && p->opt.stack != 0 && p->stack_ok) {
-    // auto: enough items per SM, and a last round that is nearly full (the
-    // items are equal-length columns, a partial round idles SMs)
-    const long long rounds = (stack_items_n + p->num_sms - 1) / p->num_sms;
-    stack = p->opt.stack == 1 || (stack_items_n >= (long long)tvs_plan::kStackMinItems * p->num_sms &&
-                                  (double)stack_items_n >= 0.95 * (double)(rounds * p->num_sms));
+  const int Hs = H / us, strips_s = (W / us + tvs::kStripPx - 1) / tvs::kStripPx;
+  const long long stack_cols = (long long)B * strips_s * p->n_hidden();  // whole-column items
+  int band_rows = Hs;  // rows per stack item
+  if (fast && p->opt.stack != 0 && p->stack_ok && strips_s < 65536 && p->n_hidden() < 32768) {
+    // auto: enough whole-column items per SM with a nearly full last round
+    // (equal-length items; a partial round idles SMs), else row-band items
+    // when the image is tall enough to cut (batch-1 latency: the reference's
+    // own calling pattern, inference.py:25-32)
+    const long long rounds = (stack_cols + p->num_sms - 1) / p->num_sms;
+    const bool columns = stack_cols >= (long long)tvs_plan::kStackMinItems * p->num_sms &&
+                         (double)stack_cols >= 0.95 * (double)(rounds * p->num_sms);
+    // row bands: when the per-layer kernels would give each SM only a few
+    // strip-rows per layer (batch 1 at 256^2: 3.5), the 15 launches are
+    // latency-bound and a row-band stack wins (tools/stack_sweep.py: 4-8-row
+    // bands with skew 1 best on config 1, 6% under the per-layer kernels;
+    // config 3 at 55 rows per SM per layer is faster per layer)
+    const double rows_per_sm = (double)B * strips_s * Hs / p->num_sms;
+    const bool few_rows = rows_per_sm <= tvs_plan::kBandMaxRowsPerSm && Hs >= tvs_plan::kStackMinBandH;
+    if (p->opt.stack_band_rows > 0)
+      band_rows = std::min(Hs, p->opt.stack_band_rows);
+    else if (!columns && (few_rows || p->opt.stack == 1) && Hs > tvs_plan::kStackBandRows)
+      band_rows = tvs_plan::kStackBandRows;
+    const bool banded = band_rows < Hs;
+    stack = p->opt.stack == 1 || columns || (banded && few_rows);
   }
+  const int stack_nbands = (Hs + band_rows - 1) / band_rows + (band_rows < Hs ? 1 : 0);
+  const int stack_grid = (int)std::min<long long>(p->num_sms, stack_cols * stack_nbands);
   if (stack) {
     // row flags + the watchdog's abort word, zeroed per launch
     const size_t n = (size_t)B * ((W / us + tvs::kStripPx - 1) / tvs::kStripPx) * (H / us) + 1;
@@ -347,7 +394,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     a.wpack = p->hpack;
     a.shift = p->bh;
     a.nshift = p->out_bands;
-    a.x = x; a.bands = bands; a.closure = closure; a.K = p->out_bands;
+    a.x = x; a.bands = bands; a.closure = closure; a.recon = recon; a.K = p->out_bands;
     const int grid = conv_grid(max_ctas, a);
     const CUtensorMap& mh = pair_in(nh) ? pair_map[cur] : single_map[cur];
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * C * p->out_bands,
@@ -373,7 +420,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     a.wpack = p->hpack;
     a.shift = p->bh;
     a.nshift = p->out_bands;
-    a.x = x; a.bands = bands; a.closure = closure; a.K = p->out_bands;
+    a.x = x; a.bands = bands; a.closure = closure; a.recon = recon; a.K = p->out_bands;
     const int grid = conv_grid(max_ctas, a);
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands,
                  [&] { return tvs::launch_conv_tc(4, in_map[cur], in_map[cur], a, grid, st); });
@@ -395,7 +442,9 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.nlayers = nh;
       a.rowcnt = p->rowcnt;
       a.abort = p->rowcnt + (p->rowcnt_n - 1);
-      a.items = stack_items(p, B, strips, a.nlayers, st);
+      size_t nitems = 0;
+      a.items = stack_items(p, B, strips, a.nlayers, Hg, band_rows, p->opt.stack_skew, st, &nitems);
+      a.nitems = (int)nitems;
       a.span = next_span();
       tvs::StackMaps sm{};
       sm.in1 = in_map[1];
@@ -433,7 +482,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     a.wpack = p->hpack;
     a.shift = p->bh;
     a.nshift = p->out_bands * us * us;
-    a.x = x; a.bands = bands; a.closure = closure; a.K = p->out_bands;
+    a.x = x; a.bands = bands; a.closure = closure; a.recon = recon; a.K = p->out_bands;
     const int grid = conv_grid(max_ctas, a);
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands,
                  [&] { return tvs::launch_conv_tc(us == 2 ? 7 : 1, in_map[cur], in_map[cur], a, grid, st); });
@@ -447,7 +496,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       cur ^= 1;
     }
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * C * p->out_bands, [&] {
-      return tvs::launch_head_f32(C, (const float*)act[cur], x, p->wh, p->bh, bands, closure, B, H, W, p->out_bands,
+      return tvs::launch_head_f32(C, (const float*)act[cur], x, p->wh, p->bh, bands, recon, closure, B, H, W, p->out_bands,
                                   row0, rows, status, st);
     });
   }
@@ -482,7 +531,7 @@ void drain_status(tvs_plan* p, bool wait) {
 }
 
 void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int B, int H, int W, int row0, int rows,
-                  cudaStream_t st) {
+                  cudaStream_t st, double* recon = nullptr) {
   if (!p->weights_ready) throw TvsError(TVS_E_STATE, "tvs_forward before tvs_plan_set_weights");
   if (!x || !bands) throw TvsError(TVS_E_INVALID, "null x/bands pointer");
   if (B < 0 || H < 1 || W < 1) throw TvsError(TVS_E_INVALID, "bad shape B/H/W");
@@ -490,6 +539,7 @@ void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int
   if (row0 < 0 || rows < 1 || row0 + rows > H) throw TvsError(TVS_E_INVALID, "bad valid row window");
   if (p->unshuffle == 2 && (H % 2 || W % 2 || row0 % 2 || rows % 2))
     throw TvsError(TVS_E_INVALID, "unshuffle = 2 needs even H, W and an even row window");
+  if (recon && !closure) throw TvsError(TVS_E_INVALID, "the reconstruction check needs the closure plane");
   p->last_launches = 0;
   p->last_stack = 0;
   if (B == 0) return;
@@ -510,6 +560,7 @@ void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int
     std::fill(p->status_host + slot * tvs::kStatWords, p->status_host + (slot + 1) * tvs::kStatWords, 0);
     status = p->status_dev + slot * tvs::kStatWords;
   }
+  if (recon) TVS_CUDA(cudaMemsetAsync(recon, 0, (size_t)B * 2 * sizeof(double), st));
   const int* escale = nullptr;
   if (p->scaled()) {
     if ((size_t)B > p->escale_n) {
@@ -532,7 +583,7 @@ void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int
     const int nb = std::min(cb, B - b0);
     run_chunk(p, x + b0 * in_img, bands + (size_t)b0 * p->out_bands * out_img,
               closure ? closure + b0 * out_img : nullptr, nb, H, W, row0, rows, st, escale ? escale + b0 : nullptr,
-              status, escale != nullptr && b0 == 0);
+              status, escale != nullptr && b0 == 0, recon ? recon + 2 * b0 : nullptr);
   }
   if (!check) return;
   TVS_CUDA(cudaEventRecord(p->status_ev[slot], st));
@@ -613,6 +664,12 @@ int tvs_plan_set_option(tvs_plan* p, const char* name, long long value) {
     if (k == "stack") {
       if (value < -1 || value > 1) throw TvsError(TVS_E_INVALID, "stack takes -1 (auto), 0 or 1");
       o.stack = (int)value;
+    } else if (k == "stack_band_rows") {
+      if (value < 0 || value > (1 << 20)) throw TvsError(TVS_E_INVALID, "stack_band_rows out of range");
+      o.stack_band_rows = (int)value;
+    } else if (k == "stack_skew") {
+      if (value < 0 || value > 64) throw TvsError(TVS_E_INVALID, "stack_skew takes 0..64");
+      o.stack_skew = (int)value;
     } else if (k == "conv0_tc") flag(o.conv0_tc);
     else if (k == "wide_pair_layers") {
       if (value < 0 || value > 1024) throw TvsError(TVS_E_INVALID, "wide_pair_layers out of range");
@@ -770,6 +827,17 @@ int tvs_forward(tvs_plan* p, const float* x, float* bands, float* closure_or_nul
   });
 }
 
+int tvs_forward_checked(tvs_plan* p, const float* x, float* bands, float* closure, double* recon, int B, int H, int W,
+                        int valid_row0, int valid_rows, void* stream) {
+  return guarded([&] {
+    if (!p || !closure || !recon) throw TvsError(TVS_E_INVALID, "null plan/closure/recon");
+    if (p->weights_ready && (p->packed_tc != p->tc_path() || p->packed_split != p->split_path() ||
+                             p->packed_wide != p->wide_path()))
+      throw TvsError(TVS_E_STATE, "plan options changed the weight layout: call tvs_plan_set_weights again");
+    forward_impl(p, x, bands, closure, B, H, W, valid_row0, valid_rows, (cudaStream_t)stream, recon);
+  });
+}
+
 int tvs_forward_host(tvs_plan* p, const float* x_host, float* bands_host, float* closure_host_or_null, int B, int H,
                      int W, void* stream) {
   return guarded([&] {
@@ -906,6 +974,8 @@ int tvs_tvflow_analyze(const double* f, int N, int H, int W, double dt, int n_st
 
 // diagnostics (not part of the public ABI): stack MMA-issuer cycle counters
 int tvs_debug_cycles(unsigned long long* out, int reset) { return tvs::debug_cycles(out, reset); }
+// diagnostics: the kDbgTrace row timeline, 5 x 32 x 1024 globaltimer stamps (conv_tc.cu g_trace)
+int tvs_debug_trace(unsigned long long* out, int reset) { return tvs::debug_trace(out, reset); }
 
 int tvs_plan_destroy(tvs_plan* p) {
   return guarded([&] {

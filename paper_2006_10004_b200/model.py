@@ -231,11 +231,18 @@ class TVSpecNet(nn.Module):
             return TrainForward.apply(self, x, *train_params(self))
         return self.forward_planes(x)[0]
 
-    def forward_planes(self, x: torch.Tensor, closure: bool = False, rows: tuple[int, int] | None = None):
+    def forward_planes(self, x: torch.Tensor, closure: bool = False, rows: tuple[int, int] | None = None,
+                       check_reconstruction: bool = False):
         """(bands, closure-or-None).  ``closure`` adds the band-sum
         reconstruction plane image - sum(bands) (inference.py:34-42) from the
         head kernel's epilogue; ``rows=(row0, nrows)`` returns only that row
-        window of the full-image forward (row-band sharding)."""
+        window of the full-image forward (row-band sharding).
+
+        ``check_reconstruction`` (implies ``closure``; CUDA tensors) returns
+        (bands, closure, rel) with rel[b] = ||x - sum(bands) - closure|| /
+        ||x|| over the row window, evaluated by the head epilogue from the
+        stored values (tvs_forward_checked) - the identity the reference tests
+        at 1e-5 (pkg/trainer/tests/test_inference.py:31-38)."""
         self._check_input(x)
         if self.training:
             raise RuntimeError("forward_planes is the eval-mode (inference) forward; call .eval() first")
@@ -247,13 +254,22 @@ class TVSpecNet(nn.Module):
             raise ValueError(f"bad row window {rows} for height {H}")
         if self.unshuffle == 2 and (row0 % 2 or nrows % 2):
             raise ValueError(f"unshuffle=2 needs an even row window, got {rows}")
+        if check_reconstruction and not x.is_cuda:
+            raise ValueError("check_reconstruction needs a CUDA input (device-side check sums)")
         if not x.is_cuda:
             return self._forward_host(plan, x, dev, closure, row0, nrows)
+        closure = closure or check_reconstruction
         with torch.cuda.device(dev):
             stream = torch.cuda.current_stream(dev)
             xd = x.contiguous()
             bands = torch.empty((B, self.out_bands, nrows, W), device=dev, dtype=torch.float32)
             clos = torch.empty((B, 1, nrows, W), device=dev, dtype=torch.float32) if closure else None
+            if check_reconstruction:
+                recon = torch.empty((B, 2), device=dev, dtype=torch.float64)
+                plan.forward_checked(xd.data_ptr(), bands.data_ptr(), clos.data_ptr(), recon.data_ptr(), B, H, W,
+                                     row0, nrows, stream.cuda_stream)
+                rel = torch.sqrt(recon[:, 0] / recon[:, 1].clamp_min(torch.finfo(torch.float64).tiny))
+                return bands, clos, rel
             plan.forward(xd.data_ptr(), bands.data_ptr(), clos.data_ptr() if closure else 0, B, H, W, row0, nrows,
                          stream.cuda_stream)
         return bands, clos

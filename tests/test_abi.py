@@ -32,6 +32,7 @@ def test_invalid_arguments_report_errors_without_gpu_work():
     assert lib.tvs_plan_create(0, 17, 96, 5, 1, ctypes.byref(plan)) == _native.TVS_E_UNSUPPORTED
     assert lib.tvs_plan_create(0, 17, 64, 5, 1, None) == _native.TVS_E_INVALID
     assert lib.tvs_forward(None, None, None, None, 1, 1, 1, 0, -1, None) == _native.TVS_E_INVALID
+    assert lib.tvs_forward_checked(None, None, None, None, None, 1, 1, 1, 0, -1, None) == _native.TVS_E_INVALID
     assert lib.tvs_plan_destroy(None) == 0
     assert lib.tvs_plan_set_option(None, b"stack", 1) == _native.TVS_E_INVALID
     assert lib.tvs_plan_sync(None, None) == _native.TVS_E_INVALID

@@ -376,3 +376,89 @@ def test_conv0_tcgen05_ragged(seeded_state, oracle, shape):
     with torch.no_grad():
         ref = oracle(torch.from_numpy(x)).numpy()
     _check(m, x, ref)
+
+
+@pytest.mark.parametrize("band_rows,skew", [(1, 0), (2, 1), (3, 2), (5, 0), (8, 2), (16, 3), (16, 0), (17, 2)])
+@pytest.mark.parametrize("shape", [(1, 48, 160), (2, 37, 300), (1, 64, 256)])
+def test_layer_stack_row_bands_bitwise(seeded_state, shape, band_rows, skew):
+    """Row-band stack items (an item = R rows of one strip of one layer, band
+    edges of layer j at rows = j*skew mod R; the batch-1 path): a band edge is
+    a segment edge of the per-layer kernel too, so the outputs stay bitwise
+    equal, for band heights down to one row, with and without skew."""
+    m0 = _stack_model(seeded_state, 0)
+    m1 = _stack_model(seeded_state, 1, stack_band_rows=band_rows, stack_skew=skew, watchdog_ms=500)
+    x = torch.rand(*shape[:1], 1, *shape[1:], generator=torch.Generator().manual_seed(band_rows + sum(shape))).cuda()
+    with torch.no_grad():
+        y0, y1 = m0(x), m1(x)
+    torch.cuda.synchronize()
+    assert m1.last_used_stack()
+    assert torch.equal(y0, y1)
+
+
+def test_layer_stack_auto_batch1(seeded_state, oracle, golden):
+    """Config 1 (one 256^2 image, 30 whole-column items) selects the row-band
+    layer stack by default; parity against the reference-generated fixture."""
+    m = TVSpecNet().eval()
+    m.load_state_dict(seeded_state)
+    with torch.no_grad():
+        out = m(torch.from_numpy(golden["cfg1_x"]).cuda()).cpu().numpy()
+    assert m.last_used_stack() and m.last_launch_count() == 4
+    assert band_rel_l2(out, golden["cfg1_y"]).max() <= TOL["fast"]
+
+
+def _recon_host(x, bands, clos):
+    """The check's definition evaluated on the host from the returned planes:
+    r = x - (sequential fp32 band sum + closure), sums of r^2 and x^2 in fp64."""
+    s = bands[:, 0]
+    for k in range(1, bands.shape[1]):
+        s = s + bands[:, k]
+    r = (x[:, 0] - (s + clos[:, 0])).double()
+    return (r * r).sum((1, 2)), (x[:, 0].double() ** 2).sum((1, 2))
+
+
+@pytest.mark.parametrize("variant", ["fast", "fast_stack", "fast_bands", "fp32", "fp32_cuda", "wide", "unshuffle"])
+def test_fused_reconstruction_check(seeded_state, variant):
+    """tvs_forward_checked (north_star item 3): the head epilogue's residual
+    sums equal the same check evaluated on the host from the stored planes,
+    and the closure identity holds at the reference's 1e-5
+    (pkg/trainer/tests/test_inference.py:31-38) for every head kernel."""
+    from oracle.tvspecnet_oracle import build_seeded_state as bss
+
+    opts, arch, state = {}, {}, seeded_state
+    if variant == "fast_stack":
+        opts = {"stack": 1}
+    elif variant == "fast_bands":
+        opts = {"stack": 1, "stack_band_rows": 8}
+    elif variant == "fp32_cuda":
+        opts = {"fp32_cuda": 1}
+    elif variant == "wide":
+        arch = dict(depth=26, channels=128)
+        state = bss(**arch)
+    elif variant == "unshuffle":
+        arch = dict(unshuffle=2)
+        state = bss(17, 64, 5, unshuffle=2)
+    prec = "fp32" if variant.startswith("fp32") else "fast"
+    m = TVSpecNet(**arch, precision=prec, options=opts).eval()
+    m.load_state_dict(state)
+    x = torch.rand(3, 1, 40, 300, generator=torch.Generator().manual_seed(11)).cuda() * 3.0
+    bands, clos, rel = m.forward_planes(x, check_reconstruction=True)
+    torch.cuda.synchronize()
+    if variant in ("fast_stack", "fast_bands"):
+        assert m.last_used_stack()
+    r2, x2 = _recon_host(x, bands, clos)
+    got = torch.sqrt(r2 / x2)
+    assert torch.allclose(rel, got.to(rel.device), rtol=1e-9, atol=1e-15), (rel, got)
+    assert float(rel.max()) <= 1e-6
+    np.testing.assert_allclose((bands.sum(1, keepdim=True) + clos).cpu().numpy(), x.cpu().numpy(), atol=1e-5)
+    # a row window: the sums cover only the window's rows
+    b2, c2, rel2 = m.forward_planes(x, rows=(8, 16), check_reconstruction=True)
+    r2w, x2w = _recon_host(x[:, :, 8:24], b2, c2)
+    assert torch.allclose(rel2, torch.sqrt(r2w / x2w).to(rel2.device), rtol=1e-9, atol=1e-15)
+
+
+def test_predict_planes_reconstruction_gate(model):
+    """predict_planes runs the fused check and returns [input, bands, closure]."""
+    x = torch.rand(2, 1, 32, 48, generator=torch.Generator().manual_seed(3)).cuda()
+    planes = predict_planes(model, x)
+    assert planes.shape == (2, 7, 32, 48)
+    np.testing.assert_allclose(planes[:, 1:].sum(1).cpu().numpy(), x[:, 0].cpu().numpy(), atol=1e-5)

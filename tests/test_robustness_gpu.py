@@ -123,6 +123,11 @@ def test_stack_stress_bitwise(seeded_state):
     for i in range(40):
         b, h, w = int(rng.integers(1, 5)), int(rng.integers(1, 70)), int(rng.integers(1, 420))
         x = torch.from_numpy(rng.random((b, 1, h, w), dtype=np.float32)).cuda()
+        if i % 2:  # row-band items of a random height and skew
+            m1.set_plan_option("stack_band_rows", int(rng.integers(1, max(2, h))))
+            m1.set_plan_option("stack_skew", int(rng.integers(0, 4)))
+        else:
+            m1.set_plan_option("stack_band_rows", 0)
         y0, y1 = m0(x), m1(x)
         assert m1.last_used_stack()
-        assert torch.equal(y0, y1), (b, h, w)
+        assert torch.equal(y0, y1), (b, h, w, m1.plan_options)
