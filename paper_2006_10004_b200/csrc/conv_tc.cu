@@ -363,6 +363,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   pdl_launch_dependents();  // the next layer may start its prologue on free SMs
   pdl_wait();               // previous layer's activations are complete and visible
   if (a.span && threadIdx.x == 0) span_open(a.span);
+  // kDbgTrace: per-CTA start / end stamps in the unused layer slot 31
+  if (Cfg::kStack && (a.dbg & kDbgTrace) && threadIdx.x == 0 && blockIdx.x < kTraceRows)
+    g_trace[0][kTraceLayers - 1][blockIdx.x] = globaltimer_ns();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer ----
@@ -1032,6 +1035,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     tmem_dealloc<Cfg::kTmemCols>(tmem);
   }
   if (a.span && threadIdx.x == 0) span_close(a.span);
+  if (Cfg::kStack && (a.dbg & kDbgTrace) && threadIdx.x == 0 && blockIdx.x < kTraceRows)
+    g_trace[1][kTraceLayers - 1][blockIdx.x] = globaltimer_ns();
 }
 
 // --------------------------------------------------------------------------

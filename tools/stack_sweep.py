@@ -25,7 +25,7 @@ nimg = int(flags.get("--imgs", CONFIGS[cfg].batch))
 reps = int(flags.get("--reps", 30))
 rows = [int(r) for r in flags.get("--rows", "0,8,16,32").split(",")]
 skews = [int(o) for o in flags.get("--skews", "1").split(",")]
-directs = [None]
+chunk = int(flags.get("--chunk-mb", "0"))
 state = build_seeded_state()
 x = torch.from_numpy(make_batch(CONFIGS[cfg], 0, nimg)).cuda()
 flush = torch.empty(256 << 20 >> 2, device="cuda")
@@ -62,6 +62,8 @@ def timed(m):
 
 
 def model(opts):
+    if chunk:
+        opts = dict(opts, chunk_mb=chunk)
     m = TVSpecNet(options=opts).eval()
     m.load_state_dict(state)
     return m.cuda()
@@ -72,7 +74,7 @@ y0, t0 = timed(m0)
 px = x.shape[0] * x.shape[2] * x.shape[3]
 print(json.dumps({"config": cfg, "imgs": nimg, "variant": "per-layer", "median_ms": round(statistics.median(t0), 4),
                   "min_ms": round(min(t0), 4), "mp_s": round(px / 1e3 / statistics.median(t0), 2)}), flush=True)
-for d in directs:
+for _ in [0]:
   for o in skews:
     for r in rows:
         m = model({"stack": 1, "stack_band_rows": r, "stack_skew": o})
