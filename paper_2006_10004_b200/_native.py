@@ -7,10 +7,13 @@ fails loudly if the .so is missing (run ``__graft_entry__.build()``).
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libtvsb200.so"
+if os.environ.get("TVS_LIB"):  # diagnostics builds only (e.g. libtvsb200_trace.so, build.py --trace)
+    LIB_PATH = Path(os.environ["TVS_LIB"]).resolve()
 
 TVS_OK = 0
 TVS_E_INVALID = -1
@@ -90,8 +93,9 @@ def load() -> ctypes.CDLL:
         lib.tvs_last_used_stack.argtypes = [P]
         lib.tvs_forward.restype = i
         lib.tvs_forward.argtypes = [P, P, P, P, i, i, i, i, i, P]
-        lib.tvs_forward_checked.restype = i
-        lib.tvs_forward_checked.argtypes = [P, P, P, P, P, i, i, i, i, i, P]
+        if hasattr(lib, "tvs_forward_checked"):  # (absent only in older diagnostics builds, TVS_LIB)
+            lib.tvs_forward_checked.restype = i
+            lib.tvs_forward_checked.argtypes = [P, P, P, P, P, i, i, i, i, i, P]
         lib.tvs_forward_host.restype = i
         lib.tvs_forward_host.argtypes = [P, P, P, P, i, i, i, P]
         lib.tvs_last_launch_count.restype = i

@@ -17,6 +17,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtvsb200.so"
+# diagnostics build (--trace): the layer-stack row timeline compiled in
+# (conv_tc.cu TVS_STACK_TRACE); tools/stack_trace.py loads it via TVS_LIB
+TRACE_LIB = PKG / "libtvsb200_trace.so"
 SOURCES = ["tvs_api.cu", "conv_tc.cu", "conv0_tc.cu", "conv_edge.cu", "metrics.cu", "tvflow.cu", "train.cu"]
 HEADERS = ["common.cuh", "sm100.cuh", "host_util.h"]
 
@@ -34,19 +37,21 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+def _stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     deps = [CSRC / s for s in SOURCES + HEADERS] + [PKG.parent / "include" / "tvs_b200.h", Path(__file__)]
     return any(d.stat().st_mtime > t for d in deps if d.exists())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, *FLAGS, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES], *LIBS]
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Path:
+    lib = TRACE_LIB if trace else LIB
+    if not force and not _stale(lib):
+        return lib
+    tmp = lib.with_suffix(".so.tmp")
+    extra = ["-DTVS_STACK_TRACE"] if trace else []
+    cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES], *LIBS]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = PKG / "build.log"
     log.write_text(" ".join(cmd) + "\n" + res.stdout + res.stderr)
@@ -55,9 +60,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv))

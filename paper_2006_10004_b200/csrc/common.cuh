@@ -101,6 +101,11 @@ struct ConvArgs {
   // padding, skipped) in a topological order, CTA i taking entries i, i+G, ...
   const int4* items;
   int nitems;
+  // head after a layer stack (mode 1): > 0 = gate every input row on the
+  // stack's row flags (rowcnt >= gate_target) instead of waiting for the
+  // whole stack grid (griddepcontrol.wait), so the head runs on the SMs the
+  // stack's CTAs free at its tail
+  int gate_target;
   // per-image input exponent e_b (tvs_api.cu, input_scale_kernel): the
   // activations of image b are computed as 2^-e_b times the model's (exact:
   // ReLU commutes with powers of two), keeping them inside the fp16 range.

@@ -133,9 +133,20 @@ __device__ unsigned long long g_dbg_cycles[8];
 // (epilogue warp quarter 0), [4] TMA store issued; globaltimer ns
 constexpr int kTraceKinds = 5, kTraceRows = 1024, kTraceLayers = 32;
 __device__ unsigned long long g_trace[kTraceKinds][kTraceLayers][kTraceRows];
+// Compiled in only by the diagnostics build (build.py --trace: -DTVS_STACK_TRACE,
+// libtvsb200_trace.so): even untaken, the checks cost the issue-bound MMA
+// thread ~2% of the config-2 stack (3.31 vs 3.25 ms, same box).
 TVS_DEV void trace_mark(const ConvArgs& a, int kind, const Segment& g, int row) {
+#ifdef TVS_STACK_TRACE
   if ((a.dbg & kDbgTrace) && g.b == 0 && g.x0 == 0 && row >= 0 && row < kTraceRows && g.layer < kTraceLayers)
     g_trace[kind][g.layer][row] = globaltimer_ns();
+#endif
+}
+TVS_DEV void trace_cta(const ConvArgs& a, int kind) {
+#ifdef TVS_STACK_TRACE
+  if ((a.dbg & kDbgTrace) && threadIdx.x == 0 && blockIdx.x < kTraceRows)
+    g_trace[kind][kTraceLayers - 1][blockIdx.x] = globaltimer_ns();
+#endif
 }
 
 // Producer side of the layer stack: input row r of a layer-j item (j >= 1) is
@@ -148,8 +159,8 @@ struct StackGate {
   static constexpr int kAhead = 8;
   int ready[3];  // last row known complete in strips s-1, s, s+1
   TVS_DEV void reset() { ready[0] = ready[1] = ready[2] = -1; }
-  TVS_DEV void wait(const ConvArgs& a, const Segment& g, int r) {
-    const int target = 4 * g.layer;
+  TVS_DEV void wait(const ConvArgs& a, const Segment& g, int r) { wait(a, g, r, 4 * g.layer); }
+  TVS_DEV void wait(const ConvArgs& a, const Segment& g, int r, const int target) {
     const int s = g.x0 / kStripPx;
     const int* base = a.rowcnt + (long long)g.b * a.strips * a.H;
     bool refreshed = false;
@@ -361,11 +372,12 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   tc_fence_after();
   const uint32_t tmem = tmem_base_smem;
   pdl_launch_dependents();  // the next layer may start its prologue on free SMs
-  pdl_wait();               // previous layer's activations are complete and visible
+  // previous layer's activations are complete and visible (a head gated on
+  // the stack's row flags acquires them row by row instead)
+  if (!(kMode == 1 && a.gate_target)) pdl_wait();
   if (a.span && threadIdx.x == 0) span_open(a.span);
   // kDbgTrace: per-CTA start / end stamps in the unused layer slot 31
-  if (Cfg::kStack && (a.dbg & kDbgTrace) && threadIdx.x == 0 && blockIdx.x < kTraceRows)
-    g_trace[0][kTraceLayers - 1][blockIdx.x] = globaltimer_ns();
+  if constexpr (Cfg::kStack) trace_cta(a, 0);
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer ----
@@ -393,11 +405,14 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           tmi = (g.layer & 1) ? &smaps.in1 : &tm_in;
           gate.reset();
         }
+        if constexpr (kMode == 1) gate.reset();
         const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
         for (int r = r0; r <= r1; ++r) {
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (Cfg::kStack)
             if (g.layer > 0 && !(a.dbg & 1)) gate.wait(a, g, r);
+          if constexpr (kMode == 1)
+            if (a.gate_target) gate.wait(a, g, r, a.gate_target);
           if constexpr (Cfg::kStack) trace_mark(a, 0, g, r);
           constexpr int nbuf = (Cfg::kSplit ? 2 : 1) * Cfg::kKBlk;  // [hi blocks][lo blocks]
           if (a.dbg & 32) {  // ablation (TVS_CONV_DBG): no input loads
@@ -1035,8 +1050,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     tmem_dealloc<Cfg::kTmemCols>(tmem);
   }
   if (a.span && threadIdx.x == 0) span_close(a.span);
-  if (Cfg::kStack && (a.dbg & kDbgTrace) && threadIdx.x == 0 && blockIdx.x < kTraceRows)
-    g_trace[1][kTraceLayers - 1][blockIdx.x] = globaltimer_ns();
+  if constexpr (Cfg::kStack) trace_cta(a, 1);
 }
 
 // --------------------------------------------------------------------------

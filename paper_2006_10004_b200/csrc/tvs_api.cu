@@ -47,6 +47,8 @@ struct tvs_plan {
     int stack = -1;             // layer stack K4: -1 auto (item-rich chunks), 0 off, 1 whenever legal
     int stack_band_rows = 0;    // layer-stack item height: 0 auto, R > 0 rows per item (>= H: whole columns)
     int stack_skew = 1;         // layer-stack row bands: layer j's band edges sit at j*skew mod R
+    int head_gate = 1;          // head after a stack: gate rows on the stack's flags (runs in the stack's tail)
+    int head_grid = 4;          // gated head: CTAs per SM of its grid (tools/ab.py: 4 best, -1.5%)
     int conv0_tc = 1;           // K1 on tcgen05 (TF32 hi/lo) instead of the CUDA-core K1
     int wide_pair_layers = 12;  // (pack) wide variant: leading hidden layers on fp16 hi/lo pairs
     int wide_halves = 1;        // (pack) wide single-input layers on output-channel halves (mode 11)
@@ -482,8 +484,17 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     a.wpack = p->hpack;
     a.shift = p->bh;
     a.nshift = p->out_bands * us * us;
+    if (l0 == nh && nh > 0 && us == 1 && p->opt.head_gate) {
+      // the head starts on the SMs the stack's CTAs free and acquires layer
+      // nh-1's rows through the stack's row flags (conv_tc.cu gate_target)
+      a.rowcnt = p->rowcnt;
+      a.abort = p->rowcnt + (p->rowcnt_n - 1);
+      a.gate_target = 4 * nh;
+    }
     a.x = x; a.bands = bands; a.closure = closure; a.recon = recon; a.K = p->out_bands;
-    const int grid = conv_grid(max_ctas, a);
+    // a gated head gets more, shorter CTAs: the block scheduler hands them to
+    // the SMs in the order the stack's CTAs free them (dynamic balance)
+    const int grid = a.gate_target ? conv_grid(max_ctas * std::max(1, p->opt.head_grid), a) : conv_grid(max_ctas, a);
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands,
                  [&] { return tvs::launch_conv_tc(us == 2 ? 7 : 1, in_map[cur], in_map[cur], a, grid, st); });
   } else {
@@ -667,7 +678,12 @@ int tvs_plan_set_option(tvs_plan* p, const char* name, long long value) {
     } else if (k == "stack_band_rows") {
       if (value < 0 || value > (1 << 20)) throw TvsError(TVS_E_INVALID, "stack_band_rows out of range");
       o.stack_band_rows = (int)value;
-    } else if (k == "stack_skew") {
+    } else if (k == "head_gate") flag(o.head_gate);
+    else if (k == "head_grid") {
+      if (value < 1 || value > 64) throw TvsError(TVS_E_INVALID, "head_grid takes 1..64");
+      o.head_grid = (int)value;
+    }
+    else if (k == "stack_skew") {
       if (value < 0 || value > 64) throw TvsError(TVS_E_INVALID, "stack_skew takes 0..64");
       o.stack_skew = (int)value;
     } else if (k == "conv0_tc") flag(o.conv0_tc);

@@ -462,3 +462,19 @@ def test_predict_planes_reconstruction_gate(model):
     planes = predict_planes(model, x)
     assert planes.shape == (2, 7, 32, 48)
     np.testing.assert_allclose(planes[:, 1:].sum(1).cpu().numpy(), x[:, 0].cpu().numpy(), atol=1e-5)
+
+
+@pytest.mark.parametrize("rows", [None, (5, 9)])
+def test_head_gated_on_stack_flags_bitwise(seeded_state, rows):
+    """The head launched after a layer stack acquires layer 14's rows through
+    the stack's row flags (no grid-wide wait, it runs in the stack's tail);
+    its output is bitwise the same as with the grid-wide dependency."""
+    x = torch.rand(64, 1, 16, 256, generator=torch.Generator().manual_seed(8)).cuda()
+    outs = []
+    for gate in (0, 1):
+        m = _stack_model(seeded_state, -1, head_gate=gate)
+        b, c = m.forward_planes(x, closure=True, rows=rows)
+        torch.cuda.synchronize()
+        assert m.last_used_stack()
+        outs.append((b, c))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])

@@ -4,6 +4,7 @@ BASELINE config: how long SMs idle at the launch's tail.
     python tools/stack_cta_spread.py --config 2 [--imgs 64]
 """
 import ctypes
+import os
 import json
 import sys
 from pathlib import Path
@@ -12,6 +13,9 @@ import numpy as np
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2006_10004_b200 import build as _build  # noqa: E402
+
+os.environ["TVS_LIB"] = str(_build.build(trace=True))  # the row timeline is compiled in only here
 from oracle.tvspecnet_oracle import build_seeded_state  # noqa: E402
 from paper_2006_10004_b200 import TVSpecNet, _native  # noqa: E402
 from paper_2006_10004_b200.workloads import CONFIGS, make_batch  # noqa: E402
