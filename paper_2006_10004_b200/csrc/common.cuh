@@ -134,7 +134,9 @@ constexpr int kStatNonFiniteOut = 1;  // a head wrote a NaN / Inf band value
 constexpr int kStatNonFiniteIn = 2;   // the input held NaN / Inf (the reference propagates them)
 constexpr int kStatWords = 4;
 constexpr int kDbgWithholdFlag = 1 << 17;
-constexpr int kDbgTrace = 1 << 19;  // stack: globaltimer per row of image 0 strip 0 (g_trace, tvs_debug_trace)
+constexpr int kDbgTrace = 1 << 19;
+constexpr int kDbgNoStoreWait = 1 << 20;  // ablation: stack publishes a row without its store-completion wait (invalid)
+constexpr int kDbgSpinGate = 1 << 21;     // ablation: StackGate polls without __nanosleep  // stack: globaltimer per row of image 0 strip 0 (g_trace, tvs_debug_trace)
 constexpr int kDbgNoPdlStack = 1 << 18;     // launch the stack without programmatic serialization  // stack: never publish row 1 of (image 0, strip 0, layer 2)
 // 2^k as an exact fp32 (|k| <= 126)
 __host__ __device__ __forceinline__ float pow2i(int k) {

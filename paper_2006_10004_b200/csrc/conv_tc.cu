@@ -195,7 +195,7 @@ struct StackGate {
       // output is invalid (the host reports it), so every later wait gives up
       // at once and the launch drains.
       if (ld_relaxed_gpu(a.abort)) return;
-      __nanosleep(32);
+      if (!(a.dbg & kDbgSpinGate)) __nanosleep(32);
       if ((spins & 63u) == 63u) {
         const unsigned long long now = globaltimer_ns();
         if (t0 == 0) {
@@ -892,8 +892,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
               // this warp's quarter row has landed (async proxy); order it
               // before the generic-proxy release below (the reader acquires,
               // then fences into the async proxy before its TMA load)
-              bulk_wait<0>();
-              fence_proxy_async_global();
+              if (!(a.dbg & kDbgNoStoreWait)) {
+                bulk_wait<0>();
+                fence_proxy_async_global();
+              }
             }
           }
           if constexpr (Cfg::kStack) {

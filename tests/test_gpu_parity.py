@@ -100,6 +100,29 @@ def test_wide_variant(golden, wide_case, prec):
     assert band_rel_l2(out, y32).max() <= 1.5e-5
 
 
+@pytest.mark.parametrize("img", [1, 2, 3])
+def test_wide_fp32_standing_exception_more_images(img):
+    """The wide variant's fp32 mode vs the 1e-5 gate on more config-5 images
+    (128x128 crops): the fp32 reference is itself >= ~1e-5 from the exact
+    result on this 26-layer model, so the standing exception is checked as
+    (a) <= 1e-5 against fp64 and (b) against the fp32 oracle no further than
+    the oracle's own fp64 distance plus 1e-5."""
+    state = build_seeded_state(26, 128, 5)
+    x = make_image(CONFIGS["5w"], img)[None, None, 96:224, 160:288].copy()
+    o32 = oracle_from_state(state, 26, 128, 5)
+    o64 = oracle_from_state(state, 26, 128, 5).double()
+    with torch.no_grad():
+        y32 = o32(torch.from_numpy(x)).numpy()
+        y64 = o64(torch.from_numpy(x).double()).numpy()
+    m = TVSpecNet(26, 128, 5, precision="fp32").eval()
+    m.load_state_dict(state)
+    out, _ = _run(m, x)
+    e64, e32, floor = band_rel_l2(out, y64).max(), band_rel_l2(out, y32).max(), band_rel_l2(y32, y64).max()
+    print(f"wide fp32 img {img}: vs fp64 {e64:.3e}, vs fp32 oracle {e32:.3e}, oracle vs fp64 {floor:.3e}")
+    assert e64 <= 1e-5
+    assert e32 <= floor + 1e-5
+
+
 @pytest.mark.parametrize("cfg,count", [(2, 4), (3, 1), (5, 2)])
 def test_configs_vs_oracle(model, oracle, cfg, count):
     spec = CONFIGS[cfg]
