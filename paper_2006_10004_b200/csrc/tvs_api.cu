@@ -54,7 +54,7 @@ struct tvs_plan {
     int wide_halves = 1;        // (pack) wide single-input layers on output-channel halves (mode 11)
     int fp32_cuda = 0;          // (pack) fp32 mode on the CUDA-core fp32 kernels
     int wide_cuda = 0;          // (pack) wide variant on the CUDA-core fp32 kernels
-    long long chunk_mb = 2048;  // activation budget per batch chunk
+    long long chunk_mb = 16384;  // activation budget per batch chunk (x2 ping-pong); lazily sized to the batch
     int check = 1;              // per-forward status: 0 off, 1 synchronous, 2 deferred (tvs_plan_sync)
     int watchdog_ms = 2000;     // layer-stack row-flag wait limit
     int input_scale = 1;        // per-image power-of-two activation scale (fp16 range guard)
@@ -118,6 +118,7 @@ struct tvs_plan {
   // occupancy); cleared if the driver ever refuses the cooperative launch
   bool stack_ok = false;
   static constexpr int kStackMinItems = 6;
+  static constexpr int kStackMaxColH = 1024;
   // row-band stack items (auto): images at least kStackMinBandH tall whose
   // per-layer launches give each SM at most kBandMaxRowsPerSm strip-rows
   static constexpr int kStackMinBandH = 128;
@@ -295,8 +296,11 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     // when the image is tall enough to cut (batch-1 latency: the reference's
     // own calling pattern, inference.py:25-32)
     const long long rounds = (stack_cols + p->num_sms - 1) / p->num_sms;
+    // (columns taller than kStackMaxColH keep the per-layer kernels: with
+    // 2160-row columns the layers drift apart and the hand-off misses L2;
+    // config 4 measured 945 vs 965 MP/s, tools/ab.py chunk_mb=120000)
     const bool columns = stack_cols >= (long long)tvs_plan::kStackMinItems * p->num_sms &&
-                         (double)stack_cols >= 0.95 * (double)(rounds * p->num_sms);
+                         (double)stack_cols >= 0.95 * (double)(rounds * p->num_sms) && Hs <= tvs_plan::kStackMaxColH;
     // row bands: when the per-layer kernels would give each SM only a few
     // strip-rows per layer (batch 1 at 256^2: 3.5), the 15 launches are
     // latency-bound and a row-band stack wins (tools/stack_sweep.py: 4-8-row

@@ -67,12 +67,12 @@ def test_deferred_check_reports_at_sync(seeded_state):
 @pytest.mark.parametrize("precision", ["fast", "fp32"])
 @pytest.mark.parametrize("stack", [0, 1])
 def test_input_scale_sweep(seeded_state, oracle, precision, stack):
-    """Inputs scaled by 1e-4 .. 1e4 against the fp32 oracle on the same input."""
+    """Inputs scaled by 1e-4 .. 1e6 against the fp32 oracle on the same input."""
     if precision == "fp32" and stack == 1:
         pytest.skip("the layer stack is the fast path")
     m = _model(seeded_state, precision, stack=stack)
     base = np.random.default_rng(11).random((2, 1, 40, 150)).astype(np.float32)
-    for scale in (1e-4, 1e-3, 1e-2, 1e-1, 1.0, 1e1, 1e2, 1e3, 1e4):
+    for scale in (1e-4, 1e-3, 1e-2, 1e-1, 1.0, 1e1, 1e2, 1e3, 1e4, 1e6):
         x = (base * np.float32(scale)).astype(np.float32)
         with torch.no_grad():
             ref = oracle(torch.from_numpy(x)).numpy()

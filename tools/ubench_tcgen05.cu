@@ -139,6 +139,12 @@ k_rate(int iters, long long* cycles, int* err, uint8_t* gbuf, const __grid_const
           mma_tf32_ss(tmem, ad, bd, idesc, 1);
         } else if constexpr (V == 5) {
           mma_f8_ss(tmem, ad, bd, make_idesc(128, 64, kFmtE4M3, kFmtE4M3), 1);
+        } else if constexpr (V == 30) {  // the wide quarter kernels' shape: N=96 (32 co x 3 dy)
+          mma_f16_ss(tmem, ad, bd, make_idesc(128, 96, kFmtF16, kFmtF16), 1);
+        } else if constexpr (V == 31) {  // N=96 with e4m3 operands (the fp8 lo-product candidate)
+          mma_f8_ss(tmem, ad, bd, make_idesc(128, 96, kFmtE4M3, kFmtE4M3), 1);
+        } else if constexpr (V == 32) {
+          mma_f8_ss(tmem, ad, bd, make_idesc(128, 192, kFmtE4M3, kFmtE4M3), 1);
         } else if constexpr (V == 6) {
           uint64_t bd1 = make_smem_desc(b0 + 8192 + k * 32, 0, 1024, kLayoutSW128);
           uint64_t bd2 = make_smem_desc(b0 + 16384 + k * 32, 0, 1024, kLayoutSW128);
@@ -148,7 +154,7 @@ k_rate(int iters, long long* cycles, int* err, uint8_t* gbuf, const __grid_const
                        ::"r"(tmem + 64), "l"(ad), "l"(bd1), "r"(idesc) : "memory");
           asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::lastuse [%0], %1, %2, %3, 1;"
                        ::"r"(tmem + 128), "l"(ad), "l"(bd2), "r"(idesc) : "memory");
-        } else if constexpr (V == 8 || V == 9 || V == 11 || V == 12 || V >= 16) {
+        } else if constexpr (V == 8 || V == 9 || V == 11 || V == 12 || (V >= 16 && V < 30)) {
           // conv row pattern: A shifted by dx*128 B (V=8) or aligned (V=9), B = N192 block of dx
           const int dx = it % 3;
           const uint32_t ash = (V == 9) ? 0u : (uint32_t)dx * 128u;
@@ -198,9 +204,9 @@ k_rate(int iters, long long* cycles, int* err, uint8_t* gbuf, const __grid_const
     long long t1 = clock64();
     if (!ok) atomicAdd(err, 1);
     cycles[blockIdx.x] = t1 - t0;
-    if constexpr (V == 11 || V == 12 || V >= 16) *reinterpret_cast<volatile uint32_t*>(smem + 110 * 1024) = 1;
+    if constexpr (V == 11 || V == 12 || (V >= 16 && V < 30)) *reinterpret_cast<volatile uint32_t*>(smem + 110 * 1024) = 1;
   }
-  if constexpr (V >= 16) {
+  if constexpr (V >= 16 && V < 30) {
     // warp 1, lanes 0-3: bulk traffic, each lane through its own 8 KB buffer
     // at 112 + 8*lane KB (4 copies in flight)
     volatile uint32_t* flag = reinterpret_cast<volatile uint32_t*>(smem + 110 * 1024);
@@ -386,7 +392,7 @@ static void run_rate(const char* name, int ctas, double macs_per_iter) {
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { printf("tensor map encode failed %d\n", (int)r); exit(1); }
   }
-  const int smem = (V >= 16 ? 144 : 112) * 1024 + 1024;
+  const int smem = ((V >= 16 && V < 30) ? 144 : 112) * 1024 + 1024;
   CK(cudaFuncSetAttribute(k_rate<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int iters = 4096;
   k_rate<V><<<ctas, 128, smem>>>(64, dC, dErr, gbuf, tmap);  // warm
@@ -426,6 +432,9 @@ int main(int argc, char** argv) {
     run_rate<3>("f16 M128 N256 K64", ctas, 128.0 * 256 * 64);
     run_rate<4>("tf32 M128 N64 K32", ctas, 128.0 * 64 * 32);
     run_rate<5>("e4m3 M128 N64 K128", ctas, 128.0 * 64 * 128);
+    run_rate<30>("f16 M128 N96 K64", ctas, 128.0 * 96 * 64);
+    run_rate<31>("e4m3 M128 N96 K128", ctas, 128.0 * 96 * 128);
+    run_rate<32>("e4m3 M128 N192 K128", ctas, 128.0 * 192 * 128);
     run_rate<6>("f16 N64 x3 collector::a", ctas, 3 * 128.0 * 64 * 64);
     run_rate<7>("f16 N64 noswz shifted A", ctas, 128.0 * 64 * 64);
     run_rate<8>("f16 N192 conv dx-shifted A", ctas, 128.0 * 192 * 64);
