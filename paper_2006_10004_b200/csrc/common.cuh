@@ -215,8 +215,9 @@ size_t conv0_tc_pack_bytes(int in_ch);
 cudaError_t launch_pack_conv0_tc(const float* w, int in_ch, uint8_t* out, cudaStream_t st);
 // pdl: launched programmatically after the input-scale kernel (x may be read
 // before griddepcontrol.wait; escale and the activation writes come after it)
-cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t* bpack, const float* bias,
-                            const int* escale, int B, int H, int W, int num_sms, bool pdl, cudaStream_t st);
+cudaError_t launch_conv0_tc(int in_ch, const float* x, const CUtensorMap& out_map, const uint8_t* bpack,
+                            const float* bias, const int* escale, int B, int H, int W, int num_sms, bool pdl,
+                            cudaStream_t st);
 // metrics.cu: per-plane scoring statistics (8 doubles per plane)
 cudaError_t launch_band_stats(const float* gt, const float* pred, int planes, int H, int W,
                               const double* range_override, double* stats, cudaStream_t st);

@@ -62,17 +62,22 @@ __device__ __forceinline__ uint32_t sw128_off(int row, int kk, int rows_per_bloc
   return (uint32_t)(kb * rows_per_block * 128 + row * 128 + ((c ^ (row & 7)) << 4) + (kk & 3) * 4);
 }
 
-// taps of pixel px (strip row `tile`); zero outside the image
+// (image, row, first pixel) of strip row `tile` (32-bit: tiles < 2^31)
+struct TileXY {
+  int b, y, x0;
+};
+__device__ __forceinline__ TileXY tile_xy(int tile, int strips, int H) {
+  const int by = tile / strips;
+  return {by / H, by - (by / H) * H, (tile - by * strips) * 128};
+}
+
+// taps of pixel x0 + t of strip row `c`; zero outside the image
 template <int kKB>
-__device__ __forceinline__ void conv0_taps(const float* __restrict__ x, long long tile, long long tiles, int strips,
-                                           int H, int W, int t, float (&tap)[Conv0TcCfg<kKB>::kTaps]) {
-  if (tile >= tiles) tile = tiles - 1;  // past the end: any valid row (result unused)
-  const int px = (int)(tile % strips) * 128 + t;
-  const long long by = tile / strips;
-  const int y = (int)(by % H);
-  const long long b = by / H;
+__device__ __forceinline__ void conv0_taps(const float* __restrict__ x, TileXY c, int H, int W, int t,
+                                           float (&tap)[Conv0TcCfg<kKB>::kTaps]) {
+  const int px = c.x0 + t, y = c.y;
   if constexpr (kKB == 1) {
-    const float* img = x + b * (long long)H * W;
+    const float* img = x + (long long)c.b * H * W;
 #pragma unroll
     for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
@@ -81,7 +86,7 @@ __device__ __forceinline__ void conv0_taps(const float* __restrict__ x, long lon
         tap[ky * 3 + kx] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(img + (long long)yy * W + xx) : 0.0f;
       }
   } else {  // half-res grid (H, W); full-res plane (2H, 2W)
-    const float* img = x + b * (long long)(2 * H) * (2 * W);
+    const float* img = x + (long long)c.b * (2 * H) * (2 * W);
 #pragma unroll
     for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
@@ -100,7 +105,8 @@ __device__ __forceinline__ void conv0_taps(const float* __restrict__ x, long lon
 }
 
 template <int kKB>
-__global__ void __launch_bounds__(128) conv0_tc_kernel(const float* __restrict__ x, __half* __restrict__ act,
+__global__ void __launch_bounds__(128) conv0_tc_kernel(const float* __restrict__ x,
+                                                       const __grid_constant__ CUtensorMap out_map,
                                                        const uint8_t* __restrict__ bpack,
                                                        const float* __restrict__ bias,
                                                        const int* __restrict__ escale, int B, int H, int W) {
@@ -138,15 +144,16 @@ __global__ void __launch_bounds__(128) conv0_tc_kernel(const float* __restrict__
   const uint64_t bdesc0 = make_smem_desc(smem_u32(sB), 0, 1024, kLayoutSW128);
   const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
   const int strips = (W + 127) / 128;
-  const long long tiles = (long long)B * H * strips;
-  const long long step = (long long)gridDim.x * NT;
+  const int tiles = B * H * strips;  // < 2^31 (launch_conv0_tc)
+  const int step = gridDim.x * NT;
   uint32_t phase = 0;
   // tiles blockIdx.x*NT + i of each round; the next round's taps are loaded
-  // while this round's MMAs and epilogue run
+  // while this round's MMAs and epilogue run (past the end: any valid row,
+  // result unused)
   float tap[NT][n];
-  long long base = (long long)blockIdx.x * NT;
+  int base = blockIdx.x * NT;
 #pragma unroll
-  for (int i = 0; i < NT; ++i) conv0_taps<kKB>(x, base + i, tiles, strips, H, W, t, tap[i]);
+  for (int i = 0; i < NT; ++i) conv0_taps<kKB>(x, tile_xy(min(base + i, tiles - 1), strips, H), H, W, t, tap[i]);
   // programmatic launch after the input-scale kernel: the exponents (and the
   // right to overwrite the activation buffer) come after this wait; x was
   // complete before that kernel started.  A no-op for a plain launch.
@@ -194,18 +201,20 @@ __global__ void __launch_bounds__(128) conv0_tc_kernel(const float* __restrict__
     }
     // next round's taps (global loads in flight during the MMAs and the epilogue)
 #pragma unroll
-    for (int i = 0; i < NT; ++i) conv0_taps<kKB>(x, base + step + i, tiles, strips, H, W, t, tap[i]);
+    for (int i = 0; i < NT; ++i)
+      conv0_taps<kKB>(x, tile_xy(min(base + step + i, tiles - 1), strips, H), H, W, t, tap[i]);
     mbar_wait(&mma_done, phase);
     phase ^= 1;
     tc_fence_after();
     // ---- epilogue: lane quarter `warp` = pixels 32*warp .. +31 of each tile,
-    // staged through the (now free) A tile in an XOR-swizzled layout, then
-    // copied out coalesced: the strip row's 128 pixels are 16 KB contiguous
-    // in NHWC (per-lane 128 B stores would cost 32 LSU wavefronts each)
+    // staged through the (now free) A tile in the SW128 layout, then written
+    // by one TMA tensor store per strip row (box 64 ch x 128 px; the tensor
+    // map clips a partial last strip)
 #pragma unroll 1
     for (int i = 0; i < NT; ++i) {
       // 2^-e of this tile's image (exact; 1 for in-range inputs)
-      const float sc = escale ? pow2i(-__ldg(escale + (int)min((base + i) / strips / H, (long long)B - 1))) : 1.0f;
+      const int ti = min(base + i, tiles - 1);
+      const float sc = escale ? pow2i(-__ldg(escale + tile_xy(ti, strips, H).b)) : 1.0f;
       uint32_t acc[4][16];
 #pragma unroll
       for (int j = 0; j < 4; ++j) tmem_ld16(tmem + lane_addr + i * 64 + j * 16, acc[j]);
@@ -213,46 +222,39 @@ __global__ void __launch_bounds__(128) conv0_tc_kernel(const float* __restrict__
 #pragma unroll
       for (int j = 0; j < 4; ++j) reg_fence16(acc[j]);
       const uint32_t srow = smem_u32(sA + i * Cfg::kTileA) + t * 128;
+      const float2 sc2 = make_float2(sc, sc);
 #pragma unroll
       for (int c8 = 0; c8 < 8; ++c8) {
         uint32_t pk[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int c = c8 * 8 + e * 2;
-          const float f0 = (__uint_as_float(acc[c >> 4][c & 15]) + sBias[c]) * sc;
-          const float f1 = (__uint_as_float(acc[c >> 4][(c & 15) + 1]) + sBias[c + 1]) * sc;
-          asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[e]) : "f"(f1), "f"(f0));
+          // (acc + bias) * 2^-e, packed fp32x2 (FADD2 / FMUL2)
+          float2 f = __fadd2_rn(make_float2(__uint_as_float(acc[c >> 4][c & 15]),
+                                            __uint_as_float(acc[c >> 4][(c & 15) + 1])),
+                                make_float2(sBias[c], sBias[c + 1]));
+          if (sc != 1.0f) f = __fmul2_rn(f, sc2);
+          asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(pk[e]) : "f"(f.y), "f"(f.x));
         }
         st_shared_v4(srow + ((c8 ^ (t & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
       }
     }
+    fence_async_smem();  // staging (generic proxy) -> the TMA store (async proxy)
     tc_fence_before();
     __syncthreads();
+    if (t == 0) {
 #pragma unroll 1
-    for (int i = 0; i < NT; ++i) {
-      const long long tile = base + i;
-      if (tile >= tiles) break;
-      const int x0 = (int)(tile % strips) * 128;
-      const long long by = tile / strips;
-      const int nvalid = min(128, W - x0);
-      uint4* dst = reinterpret_cast<uint4*>(act + (by * W + x0) * 64);
-      // thread t moves chunk c = t % 8 of rows r0 + 16k (r0 = t / 8): the
-      // swizzle term r & 7 == r0 & 7 is fixed per thread
-      const int c = t & 7, r0 = t >> 3;
-      const uint32_t stg = smem_u32(sA + i * Cfg::kTileA) + (uint32_t)(r0 * 128 + ((c ^ (r0 & 7)) << 4));
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int r = r0 + 16 * k;
-        if (r < nvalid) {
-          uint4 v;
-          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(stg + k * 16 * 128));
-          dst[r * 8 + c] = v;
-        }
+      for (int i = 0; i < NT; ++i) {
+        if (base + i >= tiles) break;
+        const TileXY c = tile_xy(base + i, strips, H);
+        tma_store_4d(&out_map, sA + i * Cfg::kTileA, 0, c.x0, c.y, c.b);
       }
+      bulk_commit();
+      bulk_wait_read<0>();  // the staging tiles are the next round's A tiles
     }
-    __syncthreads();  // staging read before the next round's A rows overwrite it
+    __syncthreads();
   }
+  if (t == 0) bulk_wait<0>();  // stores complete before the grid ends (PDL dependents read them)
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -286,8 +288,9 @@ cudaError_t launch_pack_conv0_tc(const float* w, int in_ch, uint8_t* out, cudaSt
   return cudaGetLastError();
 }
 
-cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t* bpack, const float* bias,
-                            const int* escale, int B, int H, int W, int num_sms, bool pdl, cudaStream_t st) {
+cudaError_t launch_conv0_tc(int in_ch, const float* x, const CUtensorMap& out_map, const uint8_t* bpack,
+                            const float* bias, const int* escale, int B, int H, int W, int num_sms, bool pdl,
+                            cudaStream_t st) {
   static std::mutex mu;
   static uint64_t done = 0;
   cudaError_t e = once_per_device(mu, done, [] {
@@ -300,6 +303,7 @@ cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t*
   });
   if (e != cudaSuccess) return e;
   const long long tiles = (long long)B * H * ((W + 127) / 128);
+  if (tiles >= (1LL << 31) - 1024) return cudaErrorInvalidValue;  // 32-bit tile indices
   const int nt = in_ch == 1 ? Conv0TcCfg<1>::kTiles : Conv0TcCfg<4>::kTiles;
   const int per_sm = in_ch == 1 ? Conv0TcCfg<1>::kPerSm : Conv0TcCfg<4>::kPerSm;
   const int grid = (int)std::max(1LL, std::min<long long>((tiles + nt - 1) / nt, (long long)num_sms * per_sm));
@@ -315,13 +319,12 @@ cudaError_t launch_conv0_tc(int in_ch, const float* x, void* act, const uint8_t*
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  __half* out = static_cast<__half*>(act);
   if (in_ch == 1) {
     cfg.dynamicSmemBytes = Conv0TcCfg<1>::kSmem;
-    return cudaLaunchKernelEx(&cfg, conv0_tc_kernel<1>, x, out, bpack, bias, escale, B, H, W);
+    return cudaLaunchKernelEx(&cfg, conv0_tc_kernel<1>, x, out_map, bpack, bias, escale, B, H, W);
   }
   cfg.dynamicSmemBytes = Conv0TcCfg<4>::kSmem;
-  return cudaLaunchKernelEx(&cfg, conv0_tc_kernel<4>, x, out, bpack, bias, escale, B, H, W);
+  return cudaLaunchKernelEx(&cfg, conv0_tc_kernel<4>, x, out_map, bpack, bias, escale, B, H, W);
 }
 
 }  // namespace tvs

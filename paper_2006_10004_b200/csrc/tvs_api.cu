@@ -340,7 +340,8 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
                        : (split ? tvs::kActSplit : (wide ? (pair_in(0) ? tvs::kActSplit : tvs::kActF16) : tvs::kActF32));
   if (us == 2 && p->opt.conv0_tc)
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C, [&] {
-      return tvs::launch_conv0_tc(4, x, act[0], p->c0pack, p->c0bias, escale, B, H / 2, W / 2, p->num_sms,
+      return tvs::launch_conv0_tc(4, x, make_act_map(act[0], B, H / 2, W / 2, 128), p->c0pack, p->c0bias, escale, B,
+                                  H / 2, W / 2, p->num_sms,
                                   conv0_pdl, st);
     });
   else if (us == 2)
@@ -348,7 +349,8 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
                  [&] { return tvs::launch_conv0_unshuffle(x, act[0], p->w0u, p->b0u, escale, B, H / 2, W / 2, st); });
   else if (fast && p->opt.conv0_tc)
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C, [&] {
-      return tvs::launch_conv0_tc(1, x, act[0], p->c0pack, p->c0bias, escale, B, H, W, p->num_sms, conv0_pdl, st);
+      return tvs::launch_conv0_tc(1, x, make_act_map(act[0], B, H, W, 128), p->c0pack, p->c0bias, escale, B, H, W,
+                                  p->num_sms, conv0_pdl, st);
     });
   else
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
