@@ -183,7 +183,8 @@ cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* 
 cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
 cudaError_t launch_pack_hidden_f16_t(const float* w, uint8_t* out, cudaStream_t st);  // training dgrad pack
 // parts = 4: output-channel quarters (modes 5 / 9); 2: halves (mode 11)
-cudaError_t launch_pack_hidden_wide(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int parts);
+cudaError_t launch_pack_hidden_wide(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int parts,
+                                    bool lo8);
 cudaError_t launch_pack_head_wide(const float* w, int K, uint8_t* out, cudaStream_t st);
 cudaError_t launch_pack_head_f16(const float* w, int K, uint8_t* out, cudaStream_t st);
 cudaError_t launch_fill(float* dst, float v, int n, cudaStream_t st);

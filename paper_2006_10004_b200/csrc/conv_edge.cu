@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <type_traits>
 
+#include <cuda_fp8.h>
+
 #include "common.cuh"
 
 namespace tvs {
@@ -49,8 +51,11 @@ __global__ void __launch_bounds__(128)
 conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params p, const int* __restrict__ escale,
              int B, int H, int W) {
   constexpr int P = (C == 64) ? 128 : 64;  // pixels per block (static smem <= 32 KB)
-  constexpr int E = kSplit ? 2 * C : C;    // elements per pixel (split: hi | lo halves)
-  __shared__ __align__(16) T stage[P * E];
+  // bytes per pixel: split 64-ch = [hi 64 | lo 64] fp16 (fp32 mode); split
+  // 128-ch = the wide pair format [hi 128 fp16 | lo 128 e4m3 x 2^11]
+  constexpr bool kLo8 = kSplit && C == 128;
+  constexpr int kPxB = kLo8 ? 3 * C : (kSplit ? 2 : 1) * C * (int)sizeof(T);
+  __shared__ __align__(16) uint8_t stage_b[P * kPxB];
   // PDL: the first hidden layer may start its prologue (it waits for this grid's completion)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long npx = (long long)B * H * W;
@@ -71,21 +76,33 @@ conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params
         const int yy = y + ky - 1, xx = xw + kx - 1;
         in[ky * 3 + kx] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(img + (long long)yy * W + xx) : 0.0f;
       }
-    T* dst = stage + threadIdx.x * E;
+    T* dst = reinterpret_cast<T*>(stage_b + threadIdx.x * kPxB);
 #pragma unroll
     for (int c8 = 0; c8 < C / 8; ++c8) {
       float v[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int co = c8 * 8 + e;
-        // fp64 accumulation in the fp32-accurate formats
-        using Acc = std::conditional_t<std::is_same_v<T, float> || kSplit, double, float>;
+        // fp64 accumulation in the fp32-accurate formats; the wide fast mode's
+        // pair (fp16 hi + e4m3 lo, ~15 significant bits) needs no more than fp32
+        using Acc = std::conditional_t<std::is_same_v<T, float> || (kSplit && !kLo8), double, float>;
         Acc acc = 0;
 #pragma unroll
         for (int t9 = 0; t9 < 9; ++t9) acc = fma((Acc)p.w[co * 9 + t9], (Acc)in[t9], acc);
         v[e] = fmaxf((float)(acc + (Acc)p.b[co]), 0.0f) * sc;
       }
-      if constexpr (kSplit) {
+      if constexpr (kLo8) {
+        uint32_t lo8[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float l0 = (v[2 * e] - __half2float(__float2half_rn(v[2 * e]))) * (float)(1 << 11);
+          const float l1 = (v[2 * e + 1] - __half2float(__float2half_rn(v[2 * e + 1]))) * (float)(1 << 11);
+          lo8[e] = __nv_cvt_float2_to_fp8x2(make_float2(l0, l1), __NV_SATFINITE, __NV_E4M3);
+        }
+        store_act8<T>(dst + c8 * 8, v);
+        *reinterpret_cast<uint2*>(stage_b + threadIdx.x * kPxB + 2 * C + c8 * 8) =
+            make_uint2(lo8[0] | (lo8[1] << 16), lo8[2] | (lo8[3] << 16));
+      } else if constexpr (kSplit) {
         float lo[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) lo[e] = v[e] - __half2float(__float2half_rn(v[e]));
@@ -99,9 +116,9 @@ conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params
   __syncthreads();
   // coalesced copy of the staged block (valid pixels only)
   const long long nvalid = min((long long)P, npx - p0);
-  const int n16 = (int)(nvalid * E * sizeof(T) / 16);
-  const uint4* src = reinterpret_cast<const uint4*>(stage);
-  uint4* out = reinterpret_cast<uint4*>(act + p0 * E);
+  const int n16 = (int)(nvalid * kPxB / 16);
+  const uint4* src = reinterpret_cast<const uint4*>(stage_b);
+  uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(act) + p0 * kPxB);
   for (int i = threadIdx.x; i < n16; i += blockDim.x) out[i] = src[i];
 }
 

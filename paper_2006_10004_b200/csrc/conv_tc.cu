@@ -33,6 +33,8 @@
 #include <algorithm>
 #include <type_traits>
 
+#include <cuda_fp8.h>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -270,21 +272,37 @@ struct ConvCfg {
   static constexpr int kWdx = kKBlk * kWdxBlk;        // B bytes per dx
   static constexpr int kWhalf = 3 * kWdx;             // one channel half (all dx)
   static constexpr int kW1 = kWhalf * (kHalves ? 2 : 1);  // one weight pack
-  static constexpr int kW = kHalves ? 2 * kW1 : kW1;  // fp32 hidden: hi pack | lo pack
+  // wide pair-input layer (mode 5): the activation pair is [hi fp16 | lo e4m3
+  // x 2^kLo8ActExp] (384 B/px) and the lo pass runs on kind::f8f6f4 against an
+  // e4m3 copy of the weights x 2^kLo8WExp (36 KB per quarter after the fp16
+  // pack), accumulating into its own ring (kCorrCol); the epilogue adds it back
+  // scaled by 2^-(kLo8ActExp + kLo8WExp).  A K=32 e4m3 MMA costs an N=96 K=16 f16
+  // one (tools/ubench_tcgen05.cu), so the lo pass takes half the MMAs.
+  static constexpr bool kLo8 = kMode == 5;
+  static constexpr int kWdxLo = 3 * NB * 128;         // e4m3 B bytes per dx (3 dy x NB rows x 128 ci)
+  static constexpr int kW = kHalves ? 2 * kW1 : (kLo8 ? kW1 + 3 * kWdxLo : kW1);  // fp32 hidden: hi | lo
+  static constexpr int kWChunk = kLo8 ? kWdxLo : kWdx;  // bulk-load granularity of the pack
   static constexpr int kPasses = kMode == 3 ? 3 : (kSplit ? 2 : 1);
+  // K steps of pass p (the e4m3 lo pass: K = 32 per MMA over the 128-byte lo row)
+  static constexpr int ksteps(int p) { return (kLo8 && p == 1) ? 4 : kKSteps; }
+  static constexpr bool f8(int p) { return kLo8 && p == 1; }
   static constexpr int kNStages =
       kSplit ? ((kMode == 4) ? 5 : 2)
              : (kPlain ? kStagesPlain : (kWideHalves ? 2 : (kWide ? 4 : kStages)));  // input-row ring depth
   // one stage: [hi K blocks][lo K blocks], one 17 KB SW128 row buffer each
-  static constexpr int kStageBytes = (kSplit ? 2 : 1) * kKBlk * kInRowStride;
+  static constexpr int kStageBytes = (kLo8 ? 3 : (kSplit ? 2 : 1) * kKBlk) * kInRowStride;
   static constexpr int kStageOut = (kHead || kSplit || kWide) ? 0 : 32 * 128;  // per-warp TMA-store staging
   static constexpr size_t kSmem = 1024 + kW + kNStages * kStageBytes + 4 * kGroups * kStageOut + 1024;
   // A / B descriptor offsets (bytes) of pass p, K step k (within-block k%4 added by the caller)
   static constexpr uint32_t a_off(int p, int k) {
     return ((kSplit && p == 1) ? kKBlk * kInRowStride : 0) + (k / 4) * kInRowStride;
   }
-  static constexpr uint32_t b_off(int p) { return (kHalves && p == 2) ? kW1 : 0; }
+  static constexpr uint32_t b_off(int p) { return (kHalves && p == 2) ? kW1 : ((kLo8 && p == 1) ? kW1 : 0); }
   static constexpr uint32_t b_koff(int k) { return (k / 4) * kWdxBlk + (k % 4) * 32; }
+  // B byte offset of (pass p, dx tap, K step k) inside the pack (dy block 0)
+  static constexpr uint32_t b_at(int p, int dx, int k) {
+    return f8(p) ? kW1 + dx * kWdxLo + k * 32 : b_off(p) + dx * kWdx + b_koff(k);
+  }
   // TMEM accumulator rings.  tcgen05 f16 MMAs add their products exactly and
   // truncate the fp32 accumulator toward zero once per MMA
   // (tools/probe_mma_rounding.cu), so every MMA into an accumulator costs it
@@ -300,31 +318,49 @@ struct ConvCfg {
   // truncations), plus the correction ring.
   static constexpr bool kTwoRings = kMode == 3 || kMode == 4;  // the fp32-accurate modes
   static constexpr int kRing = kTwoRings ? (kHead ? 8 : 4) : kSlots;
-  static constexpr int kTmemCols = kTwoRings ? 512 : kSlots * NB;  // 512 / 256
+  static constexpr int kTmemCols = (kTwoRings || kLo8) ? 512 : kSlots * NB;  // 512 / 256
   static constexpr uint32_t kRingMask = kRing - 1;
   static constexpr int kRingLog = kRing == 4 ? 2 : 3;
   static constexpr uint32_t kOddCol = kRing * NB;                      // split hidden: 2nd main ring
   static constexpr uint32_t kCorrCol = kHalves ? 2 * kRing * NB : kRing * NB;
   // TMEM ring of pass p, K step k; whether (p, k) (at dx 0) is the first MMA into that ring
   static constexpr uint32_t ring_col(int p, int k) {
-    return !kTwoRings ? 0 : (kHalves ? (p == 0 ? (k < 2 ? 0 : kOddCol) : kCorrCol) : (p > 0 ? kCorrCol : 0));
+    return !(kTwoRings || kLo8) ? 0 : (kHalves ? (p == 0 ? (k < 2 ? 0 : kOddCol) : kCorrCol) : (p > 0 ? kCorrCol : 0));
   }
   static constexpr bool enters(int p, int k) {
     return kHalves ? ((p == 0 && (k == 0 || k == 2)) || (p == 1 && k == 0))
-                   : (k == 0 && (p == 0 || (kTwoRings && p == 1)));
+                   : (k == 0 && (p == 0 || ((kTwoRings || kLo8) && p == 1)));
   }
   static constexpr int kParts = kQuarters ? 4 : (kWideHalves ? 2 : 1);  // SegIter grid partition
   static constexpr int kVisits = kHalves ? 2 : 1;    // SegIter visits per segment
   static constexpr int kPxBytes = kSplit ? 4 * kCin : 2 * kCin;  // activation bytes per pixel
 };
-static_assert(ConvCfg<9>::kSmem <= 232448 && ConvCfg<10>::kSmem <= 232448 && ConvCfg<11>::kSmem <= 232448,
+static_assert(ConvCfg<5>::kSmem <= 232448 && ConvCfg<9>::kSmem <= 232448 && ConvCfg<10>::kSmem <= 232448 &&
+                  ConvCfg<11>::kSmem <= 232448,
               "wide single-input smem");
 constexpr float kSplitWScale = 256.0f;  // split hidden weights are packed x 2^8
+constexpr int kLo8ActExp = 11, kLo8WExp = 10;  // wide pair layers: lo activations x 2^11, e4m3 weights x 2^10
 // 1 + E[truncation loss] of the main accumulator: 36 MMAs, each losing 0.5 ulp of
 // a partial sum that grows ~linearly to the result, E[ulp(x)/|x|] = 0.7213 * 2^-23
 // over a binade (tools/emulate_split_accum.py: 1.2e-5 -> 5.1e-6 worst band)
 constexpr float kMainDebias = 1.0f + 0.5f * 0.7213f * 18.0f * 1.1920929e-7f;
 constexpr float kMainDebias18 = 1.0f + 0.5f * 0.7213f * 9.0f * 1.1920929e-7f;  // a ring of 18 MMAs
+
+// an f16 or (the wide pair layers' lo pass) e4m3 MMA; `f8` is a compile-time
+// constant at every call site once the pass loop is unrolled
+__device__ __forceinline__ void mma_any(bool f8, uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  if (f8) mma_f8_ss(d, a, b, id, acc); else mma_f16_ss(d, a, b, id, acc);
+}
+__device__ __forceinline__ void mma_any_fill(bool f8, uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  if (f8) mma_f8_ss_fill(d, a, b, id, acc); else mma_f16_ss_fill(d, a, b, id, acc);
+}
+__device__ __forceinline__ void mma_any_use(bool f8, uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  if (f8) mma_f8_ss_use(d, a, b, id, acc); else mma_f16_ss_use(d, a, b, id, acc);
+}
+__device__ __forceinline__ void mma_any_lastuse(bool f8, uint32_t d, uint64_t a, uint64_t b, uint32_t id,
+                                                uint32_t acc) {
+  if (f8) mma_f8_ss_lastuse(d, a, b, id, acc); else mma_f16_ss_lastuse(d, a, b, id, acc);
+}
 
 template <int kMode>
 __global__ void __launch_bounds__(ConvCfg<kMode>::kThreads, 1)
@@ -365,7 +401,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     mbar_arrive_expect_tx(&wbar, Cfg::kW);
     const uint8_t* wsrc = a.wpack + (Cfg::kPartsW ? (blockIdx.x % Cfg::kParts) * Cfg::kW : 0) +
                           (size_t)Iter(a).first_layer_or0(a) * Cfg::kW;
-    for (int i = 0; i < Cfg::kW / Cfg::kWdx; ++i) bulk_load(sW + i * Cfg::kWdx, wsrc + i * Cfg::kWdx, Cfg::kWdx, &wbar);
+    for (int i = 0; i < Cfg::kW / Cfg::kWChunk; ++i)
+      bulk_load(sW + i * Cfg::kWChunk, wsrc + i * Cfg::kWChunk, Cfg::kWChunk, &wbar);
   }
   tc_fence_before();
   __syncthreads();
@@ -398,8 +435,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             ++nreload;
             mbar_arrive_expect_tx(&wbar, Cfg::kW);
             const uint8_t* wsrc = a.wpack + (size_t)g.layer * Cfg::kW;
-            for (int i = 0; i < Cfg::kW / Cfg::kWdx; ++i)
-              bulk_load(sW + i * Cfg::kWdx, wsrc + i * Cfg::kWdx, Cfg::kWdx, &wbar);
+            for (int i = 0; i < Cfg::kW / Cfg::kWChunk; ++i)
+              bulk_load(sW + i * Cfg::kWChunk, wsrc + i * Cfg::kWChunk, Cfg::kWChunk, &wbar);
             cur_layer = g.layer;
           }
           tmi = (g.layer & 1) ? &smaps.in1 : &tm_in;
@@ -414,7 +451,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           if constexpr (kMode == 1)
             if (a.gate_target) gate.wait(a, g, r, a.gate_target);
           if constexpr (Cfg::kStack) trace_mark(a, 0, g, r);
-          constexpr int nbuf = (Cfg::kSplit ? 2 : 1) * Cfg::kKBlk;  // [hi blocks][lo blocks]
+          // [hi blocks][lo blocks]; the wide pair layer's lo half is one 128-byte e4m3 block
+          constexpr int nbuf = Cfg::kLo8 ? 3 : (Cfg::kSplit ? 2 : 1) * Cfg::kKBlk;
           if (a.dbg & 32) {  // ablation (TVS_CONV_DBG): no input loads
             mbar_arrive(&full[stage]);
             if (++stage == Cfg::kNStages) { stage = 0; phase ^= 1; }
@@ -508,7 +546,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             // the next input row is late, draining the tensor-core queue.
             auto prewait = [&](int p, int dx, int k) {
               if (((p == Cfg::kPasses / 2 && dx == 1 && k == 1) ||
-                   (p == Cfg::kPasses - 1 && dx == 2 && k == Cfg::kKSteps - 2)) &&
+                   (p == Cfg::kPasses - 1 && dx == 2 && k == Cfg::ksteps(p) - 2)) &&
                   next_fast && !pre_ok && !(a.dbg & 2048))
                 pre_ok = mbar_test(&slot_empty[sq2 & Cfg::kRingMask], ((sq2 >> Cfg::kRingLog) & 1) ^ 1) &&
                          mbar_test(&full[nstage], nphase);
@@ -526,15 +564,17 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
               for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
                 for (int k = 0; k < Cfg::kKSteps; ++k) {
+                  if (k >= Cfg::ksteps(p)) continue;  // (the e4m3 lo pass has 4)
+                  const bool f8p = Cfg::f8(p);
                   const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p, k) + dx * 128 + (k % 4) * 32) >> 4);
-                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + Cfg::b_koff(k)) >> 4);
+                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_at(p, dx, k) + hoff) >> 4);
                   const bool first_k = Cfg::enters(p, k) && dx == 0 && !nosplit;
                   const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + (nowrap ? 0u : t0s);
                   if (first_k) {  // enter row r+1 (acc=0), keep r-1, r
-                    if (domma) mma_f16_ss_fill(t0 + 2 * NB, ad, bd + b2, idesc1, 0u);
-                    if (domma) mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
+                    if (domma) mma_any_fill(f8p, t0 + 2 * NB, ad, bd + b2, idesc1, 0u);
+                    if (domma) mma_any_lastuse(f8p, t0, ad, bd, idesc2, 1u);
                   } else {
-                    if (domma) mma_f16_ss(t0, ad, bd, idesc3, 1u);
+                    if (domma) mma_any(f8p, t0, ad, bd, idesc3, 1u);
                   }
                   prewait(p, dx, k);
                 }
@@ -545,12 +585,14 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
               for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
                 for (int k = 0; k < Cfg::kKSteps; ++k) {
+                  if (k >= Cfg::ksteps(p)) continue;  // (the e4m3 lo pass has 4)
+                  const bool f8p = Cfg::f8(p);
                   const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p, k) + dx * 128 + (k % 4) * 32) >> 4);
-                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + Cfg::b_koff(k)) >> 4);
+                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_at(p, dx, k) + hoff) >> 4);
                   const bool first_k = Cfg::enters(p, k) && dx == 0;
                   const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + t0s;
-                  if (domma) mma_f16_ss_fill(rb, ad, bd + b2, idesc1, first_k ? 0u : 1u);
-                  if (domma) mma_f16_ss_lastuse(t0, ad, bd, idesc2, 1u);
+                  if (domma) mma_any_fill(f8p, rb, ad, bd + b2, idesc1, first_k ? 0u : 1u);
+                  if (domma) mma_any_lastuse(f8p, t0, ad, bd, idesc2, 1u);
                   prewait(p, dx, k);
                 }
             } else {  // slot R-1 | wrap | 0, 1
@@ -560,16 +602,18 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
               for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
                 for (int k = 0; k < Cfg::kKSteps; ++k) {
+                  if (k >= Cfg::ksteps(p)) continue;  // (the e4m3 lo pass has 4)
+                  const bool f8p = Cfg::f8(p);
                   const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p, k) + dx * 128 + (k % 4) * 32) >> 4);
-                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + hoff + dx * Cfg::kWdx + Cfg::b_koff(k)) >> 4);
+                  const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_at(p, dx, k) + hoff) >> 4);
                   const bool first_k = Cfg::enters(p, k) && dx == 0;
                   const uint32_t rb = tmem + Cfg::ring_col(p, k), t0 = rb + t0s;
-                  if (domma) mma_f16_ss_fill(t0, ad, bd, idesc1, 1u);
+                  if (domma) mma_any_fill(f8p, t0, ad, bd, idesc1, 1u);
                   if (first_k) {
-                    if (domma) mma_f16_ss_use(rb, ad, bd + b1, idesc1, 1u);
-                    if (domma) mma_f16_ss_lastuse(rb + NB, ad, bd + b2, idesc1, 0u);
+                    if (domma) mma_any_use(f8p, rb, ad, bd + b1, idesc1, 1u);
+                    if (domma) mma_any_lastuse(f8p, rb + NB, ad, bd + b2, idesc1, 0u);
                   } else {
-                    if (domma) mma_f16_ss_lastuse(rb, ad, bd + b1, idesc2, 1u);
+                    if (domma) mma_any_lastuse(f8p, rb, ad, bd + b1, idesc2, 1u);
                   }
                   prewait(p, dx, k);
                 }
@@ -627,18 +671,19 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
             for (int k = 0; k < Cfg::kKSteps; ++k) {
+                  if (k >= Cfg::ksteps(p)) continue;  // (the e4m3 lo pass has 4)
+                  const bool f8p = Cfg::f8(p);
               const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p, k) + dx * 128 + (k % 4) * 32) >> 4);
-              const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_off(p) + (uint32_t)g.h * Cfg::kWhalf +
-                                                       dx * Cfg::kWdx + Cfg::b_koff(k)) >> 4);
+              const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_at(p, dx, k) + (uint32_t)g.h * Cfg::kWhalf) >> 4);
               const uint32_t rb = tmem + Cfg::ring_col(p, k);
               if (Cfg::enters(p, k) && dx == 0) {
-                if (vA) if (domma) mma_f16_ss(rb + At, ad, bd + Ab, Ai, 1u);
-                if (vB) if (domma) mma_f16_ss(rb + Bt, ad, bd + Bb, Bi, 0u);
-                if (vC) if (domma) mma_f16_ss(rb + Ct, ad, bd + Cb, Ci, 1u);
-                if (vD) if (domma) mma_f16_ss(rb + Dt, ad, bd + Db, Di, 0u);
+                if (vA) if (domma) mma_any(f8p, rb + At, ad, bd + Ab, Ai, 1u);
+                if (vB) if (domma) mma_any(f8p, rb + Bt, ad, bd + Bb, Bi, 0u);
+                if (vC) if (domma) mma_any(f8p, rb + Ct, ad, bd + Cb, Ci, 1u);
+                if (vD) if (domma) mma_any(f8p, rb + Dt, ad, bd + Db, Di, 0u);
               } else {
-                if (domma) mma_f16_ss(rb + R0t, ad, bd + R0b, R0i, 1u);
-                if (c1 > 0) if (domma) mma_f16_ss(rb + R1t, ad, bd + R1b, R1i, 1u);
+                if (domma) mma_any(f8p, rb + R0t, ad, bd + R0b, R0i, 1u);
+                if (c1 > 0) if (domma) mma_any(f8p, rb + R1t, ad, bd + R1b, R1i, 1u);
               }
             }
           }
@@ -705,16 +750,33 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           uint32_t v[NB / 16][16];
 #pragma unroll
           for (int j = 0; j < NB / 16; ++j) tmem_ld16(tmem + lane_addr + slot * NB + j * 16, v[j]);
-          tmem_ld_wait();
+          if constexpr (Cfg::kLo8) {  // + the e4m3 lo pass's ring, unscaled (exact: a power of two)
+            uint32_t w[NB / 16][16];
 #pragma unroll
-          for (int j = 0; j < NB / 16; ++j) reg_fence16(v[j]);
+            for (int j = 0; j < NB / 16; ++j) tmem_ld16(tmem + lane_addr + Cfg::kCorrCol + slot * NB + j * 16, w[j]);
+            tmem_ld_wait();
+            constexpr float kUn = 1.0f / (float)(1 << (kLo8ActExp + kLo8WExp));
+#pragma unroll
+            for (int j = 0; j < NB / 16; ++j) {
+              reg_fence16(v[j]);
+              reg_fence16(w[j]);
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                v[j][i] = __float_as_uint(fmaf(__uint_as_float(w[j][i]), kUn, __uint_as_float(v[j][i])));
+            }
+          } else {
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < NB / 16; ++j) reg_fence16(v[j]);
+          }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
           if (xg < a.W) {
-            // output pixel stride: pair 4*C bytes (hi C | lo C), single 2*C
-            const int opx = a.out_single ? 2 * Cfg::kCin : 4 * Cfg::kCin;
+            // output pixel stride: pair 3*C bytes (hi C fp16 | lo C e4m3), single 2*C
+            const int opx = a.out_single ? 2 * Cfg::kCin : 3 * Cfg::kCin;
             uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * opx + qtr * NB * 2;
+            uint8_t* dst_lo = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * opx + 2 * Cfg::kCin + qtr * NB;
 #pragma unroll
             for (int chunk = 0; chunk < NB / 8; ++chunk) {
               const uint32_t sh_u = shift_u + (uint32_t)(qtr * NB + chunk * 8) * 4;
@@ -722,7 +784,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
               const float4 s1 = ld_shared_f4(sh_u + 16);
               const float sh[8] = {s0.x * sc, s0.y * sc, s0.z * sc, s0.w * sc, s1.x * sc, s1.y * sc, s1.z * sc,
                                    s1.w * sc};
-              uint32_t hi[4], lo[4];
+              uint32_t hi[4];
+              uint16_t lo8[4];
 #pragma unroll
               for (int t2 = 0; t2 < 4; ++t2) {
                 const int ch = chunk * 8 + t2 * 2;
@@ -730,13 +793,16 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                 const float f1 = fmaxf(__uint_as_float(v[ch >> 4][(ch & 15) + 1]) + sh[t2 * 2 + 1], 0.0f);
                 const __half2 hh = __floats2half2_rn(f0, f1);
                 const float2 hf = __half22float2(hh);
-                const __half2 ll = __floats2half2_rn(f0 - hf.x, f1 - hf.y);
                 hi[t2] = *reinterpret_cast<const uint32_t*>(&hh);
-                lo[t2] = *reinterpret_cast<const uint32_t*>(&ll);
+                // lo = (f - hi) x 2^11 as e4m3 (the pair format of the next pair layer)
+                lo8[t2] = __nv_cvt_float2_to_fp8x2(make_float2((f0 - hf.x) * (float)(1 << kLo8ActExp),
+                                                               (f1 - hf.y) * (float)(1 << kLo8ActExp)),
+                                                   __NV_SATFINITE, __NV_E4M3);
               }
               *reinterpret_cast<uint4*>(dst + chunk * 16) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
               if (!a.out_single)
-                *reinterpret_cast<uint4*>(dst + 2 * Cfg::kCin + chunk * 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                *reinterpret_cast<uint2*>(dst_lo + chunk * 8) =
+                    make_uint2((uint32_t)lo8[0] | ((uint32_t)lo8[1] << 16), (uint32_t)lo8[2] | ((uint32_t)lo8[3] << 16));
             }
           }
         } else if constexpr (Cfg::kHalves) {
@@ -1156,7 +1222,7 @@ cudaError_t launch_pack_hidden_f16_t(const float* w, uint8_t* out, cudaStream_t 
 // Wide hidden (mode 5): 128x128 filters, DC-compensated fp16, packed per output
 // quarter qtr = co/32: [qtr][dx][K block ci/64][3 dy x 32 rows x 128 B]
 __global__ void pack_hidden_wide_kernel(const float* __restrict__ w, const float* __restrict__ scale,
-                                        uint8_t* __restrict__ out, int parts) {
+                                        uint8_t* __restrict__ out, int parts, int lo8) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*128 + ci
   if (idx >= 128 * 128) return;
   const int co = idx / 128, ci = idx % 128;
@@ -1166,7 +1232,9 @@ __global__ void pack_hidden_wide_kernel(const float* __restrict__ w, const float
   dc_round9(wv, rn);
   // quarters (modes 5 / 9): 4 packs of 32 output channels; halves (mode 11): 2 of 64
   const int nbp = 128 / parts;
-  const size_t wpart = parts == 4 ? ConvCfg<5>::kW : ConvCfg<11>::kW;
+  // per-part stride: quarters of a pair-input layer (mode 5) carry the e4m3
+  // copy after the fp16 pack; single-input quarters (mode 9) / halves (mode 11) do not
+  const size_t wpart = parts == 4 ? (lo8 ? ConvCfg<5>::kW : ConvCfg<9>::kW) : ConvCfg<11>::kW;
   const int wdxblk = 3 * nbp * 128, wdx = 2 * wdxblk;
   uint8_t* base = out + (co / nbp) * wpart + (ci >> 6) * wdxblk;
 #pragma unroll
@@ -1174,14 +1242,25 @@ __global__ void pack_hidden_wide_kernel(const float* __restrict__ w, const float
     const int ky = t / 3, kx = t % 3;
     put_b(base, wdx, kx, (2 - ky) * nbp + (co % nbp), ci & 63, __float2half_rn(rn[t]));
   }
+  if (lo8) {  // mode 5 lo pass: e4m3(W s 2^kLo8WExp), [dx][3 dy x 32 rows x 128 ci bytes], SW128
+    uint8_t* lob = out + (co / nbp) * wpart + ConvCfg<5>::kW1;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const int ky = t / 3, kx = t % 3;
+      const int n = (2 - ky) * nbp + (co % nbp);
+      const uint32_t off = (uint32_t)kx * ConvCfg<5>::kWdxLo + (uint32_t)n * 128u +
+                           (uint32_t)(((ci >> 4) ^ (n & 7)) << 4) + (uint32_t)(ci & 15);
+      lob[off] = (uint8_t)__nv_cvt_float_to_fp8(wv[t] * (float)(1 << kLo8WExp), __NV_SATFINITE, __NV_E4M3);
+    }
+  }
 }
 
-// Wide head (mode 6): W = W_hi + W_lo over 128 input channels, [dx][K block][96 rows]
+// Wide head (mode 10): W = W_hi + W_lo over 128 input channels, [dx][K block][96 rows]
 __global__ void pack_head_wide_kernel(const float* __restrict__ w, int K, uint8_t* __restrict__ out) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // k*128 + ci
   if (idx >= K * 128) return;
   const int k = idx / 128, ci = idx % 128;
-  using C6 = ConvCfg<6>;
+  using C6 = ConvCfg<10>;
   uint8_t* base = out + (ci >> 6) * C6::kWdxBlk;
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
@@ -1257,7 +1336,7 @@ __global__ void fill_kernel(float* dst, float v, int n) {
 
 size_t conv_wpack_bytes(bool head) { return head ? ConvCfg<1>::kW : ConvCfg<0>::kW; }
 size_t conv_wpack_split_bytes() { return ConvCfg<3>::kW; }
-size_t conv_wpack_wide_bytes(bool head) { return head ? ConvCfg<6>::kW : 4 * ConvCfg<5>::kW; }
+size_t conv_wpack_wide_bytes(bool head) { return head ? ConvCfg<10>::kW : 4 * ConvCfg<5>::kW; }
 size_t conv_wpack_unshuf_head_bytes() { return ConvCfg<7>::kW; }
 
 // Launched with programmatic stream serialization (PDL): the kernel's
@@ -1296,10 +1375,6 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
       cfg.blockDim = dim3(ConvCfg<5>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<5>::kSmem;
       return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<5>, tm_in, tm_out, a, zs);
-    case 6:
-      cfg.blockDim = dim3(ConvCfg<6>::kThreads);
-      cfg.dynamicSmemBytes = ConvCfg<6>::kSmem;
-      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<6>, tm_in, tm_out, a, zs);
     case 7:
       cfg.blockDim = dim3(ConvCfg<7>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<7>::kSmem;
@@ -1386,16 +1461,21 @@ cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_hidden_wide(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int parts) {
-  static_assert(4 * ConvCfg<5>::kW == 2 * ConvCfg<11>::kW, "quarter and half packs share the layer stride");
+// one wide hidden layer's pack inside its conv_wpack_wide_bytes(false) slot:
+// quarters of a pair-input layer (mode 5, lo8: fp16 + e4m3 copies), or
+// single-input quarters (mode 9) / halves (mode 11)
+cudaError_t launch_pack_hidden_wide(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int parts,
+                                    bool lo8) {
+  static_assert(4 * ConvCfg<9>::kW == 2 * ConvCfg<11>::kW && 4 * ConvCfg<5>::kW >= 2 * ConvCfg<11>::kW,
+                "every wide pack fits the layer stride");
   cudaError_t e = cudaMemsetAsync(out, 0, 4 * ConvCfg<5>::kW, st);
   if (e != cudaSuccess) return e;
-  pack_hidden_wide_kernel<<<(128 * 128 + 127) / 128, 128, 0, st>>>(w, scale, out, parts);
+  pack_hidden_wide_kernel<<<(128 * 128 + 127) / 128, 128, 0, st>>>(w, scale, out, parts, lo8 ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pack_head_wide(const float* w, int K, uint8_t* out, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<6>::kW, st);
+  cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<10>::kW, st);
   if (e != cudaSuccess) return e;
   pack_head_wide_kernel<<<(K * 128 + 127) / 128, 128, 0, st>>>(w, K, out);
   return cudaGetLastError();
@@ -1437,8 +1517,6 @@ cudaError_t configure_kernels() {
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<5>::kSmem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(conv3x3_tc_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)ConvCfg<6>::kSmem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<7>::kSmem);

@@ -255,6 +255,44 @@ TVS_DEV void mma_f8_ss(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t
       "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
       ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
 }
+// kind::f8f6f4 with the A-operand collector (the wide pair layers' e4m3 lo pass)
+TVS_DEV void mma_f8_ss_fill(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4.collector::a::fill [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+TVS_DEV void mma_f8_ss_use(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4.collector::a::use [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+TVS_DEV void mma_f8_ss_lastuse(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+// one MMA of pass kind F8 (kind::f8f6f4) or f16; Q: 0 plain, 1 fill, 2 use, 3 lastuse
+template <bool F8, int Q>
+TVS_DEV void mma_ss(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  if constexpr (F8) {
+    if constexpr (Q == 0) mma_f8_ss(d_tmem, adesc, bdesc, idesc, accumulate);
+    else if constexpr (Q == 1) mma_f8_ss_fill(d_tmem, adesc, bdesc, idesc, accumulate);
+    else if constexpr (Q == 2) mma_f8_ss_use(d_tmem, adesc, bdesc, idesc, accumulate);
+    else mma_f8_ss_lastuse(d_tmem, adesc, bdesc, idesc, accumulate);
+  } else {
+    if constexpr (Q == 0) mma_f16_ss(d_tmem, adesc, bdesc, idesc, accumulate);
+    else if constexpr (Q == 1) mma_f16_ss_fill(d_tmem, adesc, bdesc, idesc, accumulate);
+    else if constexpr (Q == 2) mma_f16_ss_use(d_tmem, adesc, bdesc, idesc, accumulate);
+    else mma_f16_ss_lastuse(d_tmem, adesc, bdesc, idesc, accumulate);
+  }
+}
 // Warp-converged issue: every lane executes these, elect.sync picks the one
 // lane that issues (no divergent branch around the MMA sequence).
 #define TVS_MMA_ELECT(QUAL)                                                                              \

@@ -331,11 +331,11 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     conv0_pdl = false;  // the memset sits between the input-scale kernel and K1
   }
   // K1
-  // wide fast stack: hidden layer j reads an fp16 hi/lo pair for j < P, single
-  // fp16 after (j == n_hidden is the head); P = n_hidden keeps every layer paired
+  // wide fast stack: hidden layer j reads an fp16 hi / e4m3 lo pair for j < P,
+  // single fp16 after; the head (j == n_hidden) always reads single fp16
   const int nh = p->n_hidden();
   const int P = std::max(0, std::min(p->packed_pairs, nh));
-  auto pair_in = [&](int j) { return j < P || P >= nh; };
+  auto pair_in = [&](int j) { return j < P && j < nh; };
   const int fmt = fast ? tvs::kActF16
                        : (split ? tvs::kActSplit : (wide ? (pair_in(0) ? tvs::kActSplit : tvs::kActF16) : tvs::kActF32));
   if (us == 2 && p->opt.conv0_tc)
@@ -378,7 +378,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
     CUtensorMap pair_map[2], single_map[2];
     for (int i = 0; i < 2; ++i) {
-      pair_map[i] = make_act_map(act[i], B, H, W, tvs::kHaloPx, 256);
+      pair_map[i] = make_act_map(act[i], B, H, W, tvs::kHaloPx, 192);  // [hi 128 fp16 | lo 128 e4m3] = 192 fp16 units
       single_map[i] = make_act_map(act[i], B, H, W, tvs::kHaloPx, 128);
     }
     for (int l = 0; l < nh; ++l) {
@@ -404,9 +404,9 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     a.nshift = p->out_bands;
     a.x = x; a.bands = bands; a.closure = closure; a.recon = recon; a.K = p->out_bands;
     const int grid = conv_grid(max_ctas, a);
-    const CUtensorMap& mh = pair_in(nh) ? pair_map[cur] : single_map[cur];
+    const CUtensorMap& mh = single_map[cur];
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * C * p->out_bands,
-                 [&] { return tvs::launch_conv_tc(pair_in(nh) ? 6 : 10, mh, mh, a, grid, st); });
+                 [&] { return tvs::launch_conv_tc(10, mh, mh, a, grid, st); });
   } else if (split) {
     // fp32-accurate: split-operand tcgen05 layers on fp16 hi|lo pair rows
     const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
@@ -819,7 +819,7 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
         const bool pair_in = l < P || P >= nh;
         TVS_CUDA(tvs::launch_pack_hidden_wide(w_dev[l + 1], dst_scale,
                                               p->wpack + (size_t)l * tvs::conv_wpack_wide_bytes(false), st,
-                                              pair_in || !p->packed_halves ? 4 : 2));
+                                              pair_in || !p->packed_halves ? 4 : 2, pair_in));
       } else {
         TVS_CUDA(cudaMemcpyAsync(p->whid + (size_t)l * C * C * 9, w_dev[l + 1], (size_t)C * C * 9 * 4,
                                  cudaMemcpyDeviceToDevice, st));
