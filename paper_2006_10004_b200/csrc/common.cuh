@@ -106,6 +106,7 @@ struct ConvArgs {
   // whole stack grid (griddepcontrol.wait), so the head runs on the SMs the
   // stack's CTAs free at its tail
   int gate_target;
+  int watcher;  // layer stack: a dedicated warp polls the row flags (conv_tc.cu StackWatcher)
   // per-image input exponent e_b (tvs_api.cu, input_scale_kernel): the
   // activations of image b are computed as 2^-e_b times the model's (exact:
   // ReLU commutes with powers of two), keeping them inside the fp16 range.

@@ -216,6 +216,47 @@ struct StackGate {
   }
 };
 
+// Flag watcher of the layer stack (plan option stack_watcher, default on): a
+// dedicated warp walks the CTA's items like the producer and keeps polling
+// the row flags of the rows the producer will load next (StackGate's refresh,
+// 8 rows x 3 strips per round trip), publishing progress in shared memory as
+// (item ordinal << 32 | last ready row + 1) with a CTA-scope release after its
+// gpu-scope acquire.  The TMA producer then only spins on shared memory, so a
+// flag round trip is no longer serialised with every row it issues: when a
+// layer runs right behind the one before it (batch 1, row bands) the
+// producer's row rate was bounded by the poll latency and each layer trailed
+// the previous one a little more (tools/stack_trace.py).
+struct StackWatcher {
+  TVS_DEV static void run(const ConvArgs& a, unsigned long long* ready) {
+    ItemIter it(a);
+    Segment g;
+    StackGate gate;
+    unsigned long long ord = 0;
+    bool gave_up = false;
+    while (it.next(a, g)) {
+      const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
+      if (g.layer > 0 && !(a.dbg & 1) && !gave_up) {
+        gate.reset();
+        for (int r = r0; r <= r1;) {
+          gate.wait(a, g, r);  // gpu-scope acquire: row r (and what the refresh saw after it) is ready
+          if (ld_relaxed_gpu(a.abort)) { gave_up = true; break; }
+          const int s = g.x0 / kStripPx;
+          int last = r1;
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+            if (s - 1 + d >= 0 && s - 1 + d < a.strips) last = min(last, gate.ready[d]);
+          last = max(last, r);
+          st_release_cta_shared(ready, (ord << 32) | (unsigned long long)(last + 1));
+          r = last + 1;
+        }
+      }
+      // item done (or ungated): everything of it is ready
+      ++ord;
+      st_release_cta_shared(ready, ord << 32);
+    }
+  }
+};
+
 // kMode: 0 = hidden layer, 1 = head,
 // 3 / 4 = fp32-accurate hidden layer / head on split operands: activations
 // are stored as an fp16 pair (hi = RN(a), lo = RN(a - hi): channels 0-63 and
@@ -262,7 +303,9 @@ struct ConvCfg {
   // build-time knobs (4 groups on a 5-deep ring measured no faster than 3 / 6)
   static constexpr bool kPlain = kMode == 0 || kMode == 8;
   static constexpr int kGroups = kPlain ? kEpiGroupsPlain : kEpiGroups;
-  static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kGroups);
+  // layer stack: one more warp watches the row flags (StackWatcher)
+  static constexpr int kWatchWarp = kEpiWarp0 + 4 * kGroups;
+  static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kGroups + (kStack ? 1 : 0));
   // split hidden layer: two passes of 32 output channels (TMEM room for three rings)
   static constexpr bool kHalves = kMode == 3;
   // TMEM cols per row; the 64-channel heads (modes 1 / 4) use 8 hi + 8 lo
@@ -373,6 +416,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t full[kStages], empty[kStages], slot_full[kSlots], slot_empty[kSlots], wbar, wfree;
   __shared__ uint32_t tmem_base_smem;
+  __shared__ unsigned long long sFlagsReady;  // layer stack: StackWatcher progress (item ordinal << 32 | row + 1)
   __shared__ __align__(16) float sShift[kMaxC];
   // layer stack: each epilogue group's copy of its current layer's BN shift
   // (a per-row __ldg of the shift missed L1 every row: the store-completion
@@ -387,6 +431,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
+    sFlagsReady = 0;
     for (int i = 0; i < Cfg::kNStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < kSlots; ++i) { mbar_init(&slot_full[i], 1); mbar_init(&slot_empty[i], 4); }
     mbar_init(&wbar, 1);
@@ -428,7 +473,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
       const CUtensorMap* tmi = &tm_in;
       StackGate gate;
       Segment g;
+      unsigned long long item_ord = ~0ull, seen = 0;  // stack: this item's ordinal; watcher progress seen
       while (it.next(a, g)) {
+        ++item_ord;
         if constexpr (Cfg::kStack) {
           if (g.layer != cur_layer) {  // MMAs of the previous item done -> load this layer's weights
             mbar_wait(&wfree, nreload & 1);
@@ -446,8 +493,19 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
         const int r0 = max(g.ya - 1, 0), r1 = min(g.yb, a.H - 1);
         for (int r = r0; r <= r1; ++r) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if constexpr (Cfg::kStack)
-            if (g.layer > 0 && !(a.dbg & 1)) gate.wait(a, g, r);
+          if constexpr (Cfg::kStack) {
+            if (g.layer > 0 && !(a.dbg & 1)) {
+              if (a.watcher) {  // the watcher warp acquired the flags; acquire its progress (CTA scope)
+                const unsigned long long want = (item_ord << 32) | (unsigned long long)(r + 1);
+                if (seen < want) {
+                  while ((seen = ld_acquire_cta_shared(&sFlagsReady)) < want) __nanosleep(20);
+                  fence_proxy_async_global();  // generic-proxy view -> this thread's TMA loads
+                }
+              } else {
+                gate.wait(a, g, r);
+              }
+            }
+          }
           if constexpr (kMode == 1)
             if (a.gate_target) gate.wait(a, g, r, a.gate_target);
           if constexpr (Cfg::kStack) trace_mark(a, 0, g, r);
@@ -703,6 +761,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
       cyc[6] = gend - gstart;  // ns: cyc[0] / cyc[6] = the SM clock in GHz
       for (int i = 0; i < 7; ++i) atomicAdd(&g_dbg_cycles[i], cyc[i]);
     }
+  } else if (Cfg::kStack && warp == Cfg::kWatchWarp) {
+    // ------------------------------------------------ flag watcher ----
+    if (a.watcher && lane == 0) StackWatcher::run(a, &sFlagsReady);
   } else {
     // ------------------------------------------------ epilogue ----
     const int ew = warp - Cfg::kEpiWarp0;     // 0 .. 4*kEpiGroups-1

@@ -49,6 +49,7 @@ struct tvs_plan {
     int stack_skew = 1;         // layer-stack row bands: layer j's band edges sit at j*skew mod R
     int head_gate = 1;          // head after a stack: gate rows on the stack's flags (runs in the stack's tail)
     int head_grid = 4;          // gated head: CTAs per SM of its grid (tools/ab.py: 4 best, -1.5%)
+    int stack_watcher = 1;      // layer stack: a dedicated warp polls the row flags
     int conv0_tc = 1;           // K1 on tcgen05 (TF32 hi/lo) instead of the CUDA-core K1
     int wide_pair_layers = 12;  // (pack) wide variant: leading hidden layers on fp16 hi/lo pairs
     int wide_halves = 1;        // (pack) wide single-input layers on output-channel halves (mode 11)
@@ -452,6 +453,7 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.abort = p->rowcnt + (p->rowcnt_n - 1);
       size_t nitems = 0;
       a.items = stack_items(p, B, strips, a.nlayers, Hg, band_rows, p->opt.stack_skew, st, &nitems);
+      a.watcher = p->opt.stack_watcher;
       a.nitems = (int)nitems;
       a.span = next_span();
       tvs::StackMaps sm{};
@@ -685,6 +687,7 @@ int tvs_plan_set_option(tvs_plan* p, const char* name, long long value) {
       if (value < 0 || value > (1 << 20)) throw TvsError(TVS_E_INVALID, "stack_band_rows out of range");
       o.stack_band_rows = (int)value;
     } else if (k == "head_gate") flag(o.head_gate);
+    else if (k == "stack_watcher") flag(o.stack_watcher);
     else if (k == "head_grid") {
       if (value < 1 || value > 64) throw TvsError(TVS_E_INVALID, "head_grid takes 1..64");
       o.head_grid = (int)value;
