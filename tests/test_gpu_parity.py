@@ -501,3 +501,17 @@ def test_head_gated_on_stack_flags_bitwise(seeded_state, rows):
         assert m.last_used_stack()
         outs.append((b, c))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("shape", [(64, 16, 256), (2, 37, 300), (1, 64, 256)])
+def test_stack_flag_watcher_bitwise(seeded_state, shape):
+    """The flag-watcher warp (plan option stack_watcher) only changes who polls
+    the row flags: outputs are bitwise those of the producer-polled stack."""
+    x = torch.rand(shape[0], 1, *shape[1:], generator=torch.Generator().manual_seed(sum(shape))).cuda()
+    outs = []
+    for w in (0, 1):
+        m = _stack_model(seeded_state, 1, stack_watcher=w, watchdog_ms=500)
+        with torch.no_grad():
+            outs.append(m(x))
+        assert m.last_used_stack()
+    assert torch.equal(outs[0], outs[1])
