@@ -142,8 +142,14 @@ def _predict_planes_batch(model, images: list[np.ndarray], closure: str) -> np.n
     """(n, h, w) input planes -> (n, 2+K, h, w) float32 [input, bands, closure]."""
     x = torch.from_numpy(np.stack([np.asarray(im, dtype=np.float32) for im in images])[:, None])
     if closure == "fused":
-        bands, clos = model.forward_planes(x, closure=True)
-        bands, clos = bands.numpy(), clos.numpy()
+        # the head epilogue writes the closure plane and checks the band-sum
+        # identity of every entry (tvs_forward_checked); 1e-5 is the tolerance
+        # of the reference's closure test (test_inference.py:31-38)
+        bands, clos, rel = model.forward_planes(x.pin_memory().cuda(non_blocking=True), check_reconstruction=True)
+        worst = float(rel.max())
+        if not worst <= 1e-5:
+            raise ArithmeticError(f"band-sum reconstruction check failed: relative residual {worst:.3e}")
+        bands, clos = bands.cpu().numpy(), clos.cpu().numpy()
     else:  # reference semantics: closure in float64 from the float64 image (inference.py:41)
         bands = model.forward_planes(x)[0].numpy()
         img64 = np.stack([np.asarray(im, dtype=np.float64) for im in images])[:, None]
