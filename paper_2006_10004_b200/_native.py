@@ -12,8 +12,12 @@ import threading
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libtvsb200.so"
-if os.environ.get("TVS_LIB"):  # diagnostics builds only (e.g. libtvsb200_trace.so, build.py --trace)
-    LIB_PATH = Path(os.environ["TVS_LIB"]).resolve()
+
+
+def _lib_path() -> Path:
+    """The product library, or a diagnostics build named by TVS_LIB (e.g.
+    libtvsb200_trace.so from build.py --trace), read when the library loads."""
+    return Path(os.environ["TVS_LIB"]).resolve() if os.environ.get("TVS_LIB") else LIB_PATH
 
 TVS_OK = 0
 TVS_E_INVALID = -1
@@ -67,12 +71,13 @@ def load() -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        if not LIB_PATH.exists():
+        path = _lib_path()
+        if not path.exists():
             raise RuntimeError(
-                f"{LIB_PATH} is missing: the TVSpecNET B200 path has no CPU fallback; "
+                f"{path} is missing: the TVSpecNET B200 path has no CPU fallback; "
                 "build it with `python -c 'import __graft_entry__ as g; g.build()'`"
             )
-        lib = ctypes.CDLL(str(LIB_PATH))
+        lib = ctypes.CDLL(str(path))
         P = ctypes.c_void_p
         i = ctypes.c_int
         lib.tvs_abi_version.restype = i
