@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+
+#include <nvtx3/nvToolsExt.h>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -246,8 +248,20 @@ cudaEvent_t pool_event(tvs_plan* p) {
 }
 
 // Launch `f` bracketed by events when profiling is on.
+// NVTX ranges (SURVEY §5 tracing): one host range per forward and per kernel
+// launch, visible in Nsight Systems / ncu --nvtx; no-ops without a tool
+// attached (NVTX v3 is header-only and injection-based).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+const char* kind_name(int kind) {
+  return kind == TVS_KIND_CONV0 ? "tvs.conv0" : (kind == TVS_KIND_HIDDEN ? "tvs.hidden" : "tvs.head");
+}
+
 template <typename F>
 void timed_launch(tvs_plan* p, cudaStream_t st, int kind, double flops, F&& f) {
+  NvtxRange nr(kind_name(kind));
   if (!p->profiling) {
     TVS_CUDA(f());
     p->last_launches++;
@@ -562,6 +576,7 @@ void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int
   p->last_launches = 0;
   p->last_stack = 0;
   if (B == 0) return;
+  NvtxRange nr("tvs_forward");
   DeviceGuard dg(p->device);
   drain_status(p, false);  // report a finished earlier forward's failure (deferred mode)
   const size_t per_img = (size_t)H * W * p->act_px_bytes() / ((size_t)p->unshuffle * p->unshuffle);
