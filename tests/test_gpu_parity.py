@@ -515,3 +515,15 @@ def test_stack_flag_watcher_bitwise(seeded_state, shape):
             outs.append(m(x))
         assert m.last_used_stack()
     assert torch.equal(outs[0], outs[1])
+
+
+def test_reconstruction_check_across_chunks(seeded_state):
+    """The per-image check sums land at the right offsets when the batch is
+    cut into activation chunks (plan option chunk_mb)."""
+    m = TVSpecNet(options={"chunk_mb": 1}).eval()  # 40x300 fp16 activations: one image per chunk
+    m.load_state_dict(seeded_state)
+    x = torch.rand(3, 1, 40, 300, generator=torch.Generator().manual_seed(12)).cuda()
+    x[1] *= 4.0
+    bands, clos, rel = m.forward_planes(x, check_reconstruction=True)
+    r2, x2 = _recon_host(x, bands, clos)
+    assert torch.allclose(rel, torch.sqrt(r2 / x2).to(rel.device), rtol=1e-9, atol=1e-15)
