@@ -371,13 +371,38 @@ class TVSpecNet(nn.Module):
             sizes = cache[skey]
         # sub-batch forwards report their status at the final plan.sync (one
         # synchronisation instead of one per sub-batch)
+        run = self._single if len(sizes) == 1 else self._pipeline
         if self._options.get("check", 1) == 1:
             plan.set_option("check", 2)
             try:
-                return self._pipeline(plan, x_pin, out, cout, sizes, dev, closure, row0, nrows)
+                return run(plan, x_pin, out, cout, sizes, dev, closure, row0, nrows)
             finally:
                 plan.set_option("check", 1)
-        return self._pipeline(plan, x_pin, out, cout, sizes, dev, closure, row0, nrows)
+        return run(plan, x_pin, out, cout, sizes, dev, closure, row0, nrows)
+
+    def _single(self, plan, x_pin, out, cout, sizes, dev, closure, row0, nrows):
+        """One sub-batch (batch 1, the reference's predict_bands pattern): H2D,
+        forward and D2H in order on the current stream with cached device
+        buffers, one synchronisation - no copy streams or events to order."""
+        B, _, H, W = x_pin.shape
+        K = self.out_bands
+        with torch.cuda.device(dev):
+            comp = torch.cuda.current_stream(dev)
+            bufs = self.__dict__.setdefault("_single_bufs", {})
+            bkey = (dev.index, B, H, W, nrows, closure)
+            if bkey not in bufs:
+                bufs.clear()  # one shape at a time (the host pipeline caches likewise)
+                bufs[bkey] = (torch.empty((B, 1, H, W), device=dev), torch.empty((B, K, nrows, W), device=dev),
+                              torch.empty((B, 1, nrows, W), device=dev) if closure else None)
+            xd, bd, cd = bufs[bkey]
+            xd.copy_(x_pin, non_blocking=True)
+            plan.forward(xd.data_ptr(), bd.data_ptr(), cd.data_ptr() if closure else 0, B, H, W, row0, nrows,
+                         comp.cuda_stream)
+            out.copy_(bd, non_blocking=True)
+            if closure:
+                cout.copy_(cd, non_blocking=True)
+            plan.sync(comp.cuda_stream)  # synchronises the stream; raises a failed forward
+        return out, cout
 
     def _pipeline(self, plan, x_pin, out, cout, sizes, dev, closure, row0, nrows):
         B, _, H, W = x_pin.shape
