@@ -10,10 +10,12 @@
 //   A[px] = [x_hi(t) | x_lo(t) | x_hi(t) | 0]    B[co] = [W_hi | W_hi | W_lo | 0]
 //
 // so one K chain sums x_hi*W_hi + x_lo*W_hi + x_hi*W_lo (x_lo*W_lo ~ 2^-22 is
-// dropped).  hi = RNA_tf32(v), lo = RNA_tf32(v - hi): 22 significant bits of
-// each operand, fp32 range (an fp16 split would overflow past 65504).  The
-// tf32 products are exact in the fp32 accumulator, so the pre-activation
-// matches the fp32 FFMA sum to a few fp32 ulps before the fp16 rounding.
+// dropped).  Weights: hi = RNA_tf32(w), lo = RNA_tf32(w - hi); inputs: hi =
+// the tensor core's truncation of x, lo = x - trunc(x) (see the A build):
+// 21-22 significant bits of each operand, fp32 range (an fp16 split would
+// overflow past 65504).  The tf32 products are exact in the fp32 accumulator,
+// so the pre-activation matches the fp32 FFMA sum to a few fp32 ulps before
+// the fp16 rounding.
 //
 // kKB = 1: full-resolution conv0, 9 taps -> K = 27 of one 32-element SW128
 //          block (128 B per pixel row).
@@ -169,14 +171,19 @@ __global__ void __launch_bounds__(128) conv0_tc_kernel(const float* __restrict__
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int kk = c4 * 4 + e;
+          // the tensor core reads a tf32 operand as the top 19 bits of the fp32
+          // container (the low 13 mantissa bits are ignored), so x itself is
+          // x_hi = trunc(x) and x_lo = x - trunc(x) (exact) is the rest,
+          // itself used to 10 bits: 2 instructions per tap instead of four
+          // explicit RNA conversions (3 instructions each on sm_100)
           float r = 0.0f;
           if (kk < n) {
-            r = tf32_rna(tap[i][kk]);
+            r = tap[i][kk];
           } else if (kk < 2 * n) {
-            const float h = tf32_rna(tap[i][kk - n]);
-            r = tf32_rna(tap[i][kk - n] - h);
+            const float xv = tap[i][kk - n];
+            r = xv - __uint_as_float(__float_as_uint(xv) & 0xffffe000u);
           } else if (kk < 3 * n) {
-            r = tf32_rna(tap[i][kk - 2 * n]);
+            r = tap[i][kk - 2 * n];
           }
           v[e] = r;
         }
