@@ -284,7 +284,13 @@ struct StackWatcher {
 template <int kMode>
 struct ConvCfg {
   static constexpr bool kStack = kMode == 8;
-  static constexpr bool kSplit = kMode >= 3 && kMode <= 6;
+  static constexpr bool kSplit = (kMode >= 3 && kMode <= 6) || kMode == 12;
+  // 12 = the fp32-accurate hidden layer on CTA PAIRS (a cluster of 2): each CTA
+  // computes one 32-channel half of the same strip-rows, the input rows are
+  // TMA-multicast to both (each CTA loads one of the hi / lo boxes), and each
+  // CTA keeps only its half's weights, so the ring is 4 deep instead of 2 and no
+  // row is read twice (mode 3 visits every segment once per half)
+  static constexpr bool kPairH = kMode == 12;
   static constexpr bool kUnshuf = kMode == 7;
   static constexpr bool kHead = kMode == 1 || kMode == 4 || kMode == 6 || kMode == 7 || kMode == 10;
   static constexpr bool kWide = kMode == 5 || kMode == 6 || kMode == 9 || kMode == 10 || kMode == 11;
@@ -307,7 +313,7 @@ struct ConvCfg {
   static constexpr int kWatchWarp = kEpiWarp0 + 4 * kGroups;
   static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kGroups + (kStack ? 1 : 0));
   // split hidden layer: two passes of 32 output channels (TMEM room for three rings)
-  static constexpr bool kHalves = kMode == 3;
+  static constexpr bool kHalves = kMode == 3 || kMode == 12;
   // TMEM cols per row; the 64-channel heads (modes 1 / 4) use 8 hi + 8 lo
   // weight columns per dy (K <= kMaxBands = 8): N = 48 per MMA instead of 96
   static constexpr int NB = kUnshuf ? 64 : ((kMode == 1 || kMode == 4) ? 16 : ((kHead || kHalves || kQuarters) ? 32 : 64));
@@ -323,14 +329,14 @@ struct ConvCfg {
   // one (tools/ubench_tcgen05.cu), so the lo pass takes half the MMAs.
   static constexpr bool kLo8 = kMode == 5;
   static constexpr int kWdxLo = 3 * NB * 128;         // e4m3 B bytes per dx (3 dy x NB rows x 128 ci)
-  static constexpr int kW = kHalves ? 2 * kW1 : (kLo8 ? kW1 + 3 * kWdxLo : kW1);  // fp32 hidden: hi | lo
+  static constexpr int kW = kPairH ? 2 * kWhalf : (kHalves ? 2 * kW1 : (kLo8 ? kW1 + 3 * kWdxLo : kW1));  // fp32: hi | lo
   static constexpr int kWChunk = kLo8 ? kWdxLo : kWdx;  // bulk-load granularity of the pack
-  static constexpr int kPasses = kMode == 3 ? 3 : (kSplit ? 2 : 1);
+  static constexpr int kPasses = kHalves ? 3 : (kSplit ? 2 : 1);
   // K steps of pass p (the e4m3 lo pass: K = 32 per MMA over the 128-byte lo row)
   static constexpr int ksteps(int p) { return (kLo8 && p == 1) ? 4 : kKSteps; }
   static constexpr bool f8(int p) { return kLo8 && p == 1; }
   static constexpr int kNStages =
-      kSplit ? ((kMode == 4) ? 5 : 2)
+      kSplit ? ((kMode == 4) ? 5 : (kPairH ? 4 : 2))
              : (kPlain ? kStagesPlain : (kWideHalves ? 2 : (kWide ? 4 : kStages)));  // input-row ring depth
   // one stage: [hi K blocks][lo K blocks], one 17 KB SW128 row buffer each
   static constexpr int kStageBytes = (kLo8 ? 3 : (kSplit ? 2 : 1) * kKBlk) * kInRowStride;
@@ -340,7 +346,9 @@ struct ConvCfg {
   static constexpr uint32_t a_off(int p, int k) {
     return ((kSplit && p == 1) ? kKBlk * kInRowStride : 0) + (k / 4) * kInRowStride;
   }
-  static constexpr uint32_t b_off(int p) { return (kHalves && p == 2) ? kW1 : ((kLo8 && p == 1) ? kW1 : 0); }
+  static constexpr uint32_t b_off(int p) {
+    return (kHalves && p == 2) ? (kPairH ? kWhalf : kW1) : ((kLo8 && p == 1) ? kW1 : 0);
+  }
   static constexpr uint32_t b_koff(int k) { return (k / 4) * kWdxBlk + (k % 4) * 32; }
   // B byte offset of (pass p, dx tap, K step k) inside the pack (dy block 0)
   static constexpr uint32_t b_at(int p, int dx, int k) {
@@ -359,7 +367,7 @@ struct ConvCfg {
   // room for the hi*hi products of input channels 0-31 and 32-63 in two
   // separate rings (18 MMAs each: half the accumulated magnitude, half the
   // truncations), plus the correction ring.
-  static constexpr bool kTwoRings = kMode == 3 || kMode == 4;  // the fp32-accurate modes
+  static constexpr bool kTwoRings = kMode == 3 || kMode == 4 || kMode == 12;  // the fp32-accurate modes
   static constexpr int kRing = kTwoRings ? (kHead ? 8 : 4) : kSlots;
   static constexpr int kTmemCols = (kTwoRings || kLo8) ? 512 : kSlots * NB;  // 512 / 256
   static constexpr uint32_t kRingMask = kRing - 1;
@@ -374,8 +382,8 @@ struct ConvCfg {
     return kHalves ? ((p == 0 && (k == 0 || k == 2)) || (p == 1 && k == 0))
                    : (k == 0 && (p == 0 || ((kTwoRings || kLo8) && p == 1)));
   }
-  static constexpr int kParts = kQuarters ? 4 : (kWideHalves ? 2 : 1);  // SegIter grid partition
-  static constexpr int kVisits = kHalves ? 2 : 1;    // SegIter visits per segment
+  static constexpr int kParts = kQuarters ? 4 : ((kWideHalves || kPairH) ? 2 : 1);  // SegIter grid partition
+  static constexpr int kVisits = (kHalves && !kPairH) ? 2 : 1;    // SegIter visits per segment
   static constexpr int kPxBytes = kSplit ? 4 * kCin : 2 * kCin;  // activation bytes per pixel
 };
 static_assert(ConvCfg<5>::kSmem <= 232448 && ConvCfg<9>::kSmem <= 232448 && ConvCfg<10>::kSmem <= 232448 &&
@@ -432,7 +440,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 
   if (threadIdx.x == 0) {
     sFlagsReady = 0;
-    for (int i = 0; i < Cfg::kNStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    // (CTA pairs: a stage is free once BOTH CTAs' MMAs read it - the rows are
+    // multicast into both - so each empty barrier takes two commits)
+    for (int i = 0; i < Cfg::kNStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], Cfg::kPairH ? 2 : 1); }
     for (int i = 0; i < kSlots; ++i) { mbar_init(&slot_full[i], 1); mbar_init(&slot_empty[i], 4); }
     mbar_init(&wbar, 1);
     mbar_init(&wfree, 1);
@@ -442,16 +452,24 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   if (warp == Cfg::kMmaWarp) tmem_alloc<Cfg::kTmemCols>(&tmem_base_smem);
   // weights do not depend on the previous layer: start their load before the
   // PDL wait so it overlaps the previous kernel's tail
+  // CTA pairs (mode 12): this CTA's output-channel half
+  const uint32_t pair_rank = Cfg::kPairH ? cluster_ctarank() : 0u;
   if (threadIdx.x == 0) {
     mbar_arrive_expect_tx(&wbar, Cfg::kW);
-    const uint8_t* wsrc = a.wpack + (Cfg::kPartsW ? (blockIdx.x % Cfg::kParts) * Cfg::kW : 0) +
-                          (size_t)Iter(a).first_layer_or0(a) * Cfg::kW;
-    for (int i = 0; i < Cfg::kW / Cfg::kWChunk; ++i)
-      bulk_load(sW + i * Cfg::kWChunk, wsrc + i * Cfg::kWChunk, Cfg::kWChunk, &wbar);
+    if constexpr (Cfg::kPairH) {  // its half of the split pack: [W_hi half | W_lo half]
+      bulk_load(sW, a.wpack + pair_rank * Cfg::kWhalf, Cfg::kWhalf, &wbar);
+      bulk_load(sW + Cfg::kWhalf, a.wpack + Cfg::kW1 + pair_rank * Cfg::kWhalf, Cfg::kWhalf, &wbar);
+    } else {
+      const uint8_t* wsrc = a.wpack + (Cfg::kPartsW ? (blockIdx.x % Cfg::kParts) * Cfg::kW : 0) +
+                            (size_t)Iter(a).first_layer_or0(a) * Cfg::kW;
+      for (int i = 0; i < Cfg::kW / Cfg::kWChunk; ++i)
+        bulk_load(sW + i * Cfg::kWChunk, wsrc + i * Cfg::kWChunk, Cfg::kWChunk, &wbar);
+    }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (Cfg::kPairH) cluster_sync_all();  // the peer's barriers exist before any multicast lands
   const uint32_t tmem = tmem_base_smem;
   pdl_launch_dependents();  // the next layer may start its prologue on free SMs
   // previous layer's activations are complete and visible (a head gated on
@@ -517,6 +535,12 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             continue;
           }
           mbar_arrive_expect_tx(&full[stage], nbuf * kInRowBytes);
+          if constexpr (Cfg::kPairH) {  // this CTA's box (hi or lo) to both CTAs of the pair
+            tma_load_4d_mc(sIn + stage * Cfg::kStageBytes + pair_rank * kInRowStride, tmi, &full[stage],
+                           64 * (int)pair_rank, g.x0 - 1, r, g.b, (uint16_t)0x3);
+            if (++stage == Cfg::kNStages) { stage = 0; phase ^= 1; }
+            continue;
+          }
 #pragma unroll
           for (int i = 0; i < nbuf; ++i) {  // buffer i = channels 64i..64i+63 of the pixel row
             tma_load_4d(sIn + stage * Cfg::kStageBytes + i * kInRowStride, tmi, &full[stage], 64 * i, g.x0 - 1, r,
@@ -597,7 +621,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             tc_fence_after();
             const uint64_t ad_row = adesc0 + (uint64_t)((stage * Cfg::kStageBytes) >> 4);
             const uint32_t t0s = s * NB;  // slot column offset inside a ring
-            const uint32_t hoff = (uint32_t)g.h * Cfg::kWhalf;  // B offset of the channel half
+            const uint32_t hoff = Cfg::kPairH ? 0u : (uint32_t)g.h * Cfg::kWhalf;  // B offset of the channel half
             constexpr uint32_t b1 = NB * 128 / 16, b2 = 2 * NB * 128 / 16;  // W(dy=0), W(dy=-1) blocks
             // Non-blocking probes (mid-row and near the row's end): a blocking
             // wait here would hold back the rest of this row's MMAs whenever
@@ -676,7 +700,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                   prewait(p, dx, k);
                 }
             }
-            mma_commit(&empty[stage]);
+            if constexpr (Cfg::kPairH) mma_commit_mc(&empty[stage], 0x3); else mma_commit(&empty[stage]);
             mma_commit(&slot_full[s]);
           }
           __syncwarp();
@@ -732,7 +756,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                   if (k >= Cfg::ksteps(p)) continue;  // (the e4m3 lo pass has 4)
                   const bool f8p = Cfg::f8(p);
               const uint64_t ad = ad_row + (uint64_t)((Cfg::a_off(p, k) + dx * 128 + (k % 4) * 32) >> 4);
-              const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_at(p, dx, k) + (uint32_t)g.h * Cfg::kWhalf) >> 4);
+              const uint64_t bd = bdesc0 + (uint64_t)((Cfg::b_at(p, dx, k) +
+                                                       (Cfg::kPairH ? 0u : (uint32_t)g.h * Cfg::kWhalf)) >> 4);
               const uint32_t rb = tmem + Cfg::ring_col(p, k);
               if (Cfg::enters(p, k) && dx == 0) {
                 if (vA) if (domma) mma_any(f8p, rb + At, ad, bd + Ab, Ai, 1u);
@@ -745,7 +770,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
               }
             }
           }
-          mma_commit(&empty[stage]);
+          if constexpr (Cfg::kPairH) mma_commit_mc(&empty[stage], 0x3); else mma_commit(&empty[stage]);
           for (int q = q_lo; q <= q_hi; ++q)
             if (min(q + 1, a.H - 1) == r) mma_commit(&slot_full[(seq + (uint32_t)(q - g.ya)) & Cfg::kRingMask]);
         }
@@ -873,6 +898,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             }
           }
         } else if constexpr (Cfg::kHalves) {
+          const int hh = Cfg::kPairH ? (int)pair_rank : g.h;  // this output-channel half
           // channels 32h..32h+31: z = (E + O) debiased + corrections (x 2^-8) +
           // shift, ReLU, re-split into an fp16 pair; one pixel per lane, 64 B hi
           // + 64 B lo straight to global
@@ -891,7 +917,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
           if (a.raw_f32) {  // training forward: pre-BatchNorm conv output, fp32
             if (xg < a.W) {
-              float* dst = reinterpret_cast<float*>(a.act_out) + (((long long)g.b * a.H + q) * a.W + xg) * 64 + g.h * 32;
+              float* dst = reinterpret_cast<float*>(a.act_out) + (((long long)g.b * a.H + q) * a.W + xg) * 64 + hh * 32;
 #pragma unroll
               for (int c4 = 0; c4 < 8; ++c4) {
                 float f[4];
@@ -909,10 +935,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             continue;
           }
           if (xg < a.W) {
-            uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * 256 + g.h * 64;
+            uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * 256 + hh * 64;
 #pragma unroll
             for (int chunk = 0; chunk < 4; ++chunk) {
-              const uint32_t sh_u = shift_u + (uint32_t)(g.h * 32 + chunk * 8) * 4;
+              const uint32_t sh_u = shift_u + (uint32_t)(hh * 32 + chunk * 8) * 4;
               const float4 s0 = ld_shared_f4(sh_u);
               const float4 s1 = ld_shared_f4(sh_u + 16);
               const float sh[8] = {s0.x * sc, s0.y * sc, s0.z * sc, s0.w * sc, s1.x * sc, s1.y * sc, s1.z * sc,
@@ -1184,6 +1210,9 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     tc_fence_after();
     tmem_dealloc<Cfg::kTmemCols>(tmem);
   }
+  // CTA pairs: no CTA leaves while its peer may still multicast into it or
+  // commit to its barriers
+  if constexpr (Cfg::kPairH) cluster_sync_all();
   if (a.span && threadIdx.x == 0) span_close(a.span);
   if constexpr (Cfg::kStack) trace_cta(a, 1);
 }
@@ -1415,12 +1444,22 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   switch (mode) {
+    case 12:  // fp32-accurate hidden layer on CTA pairs: clusters of 2 (one output-channel half each)
+      attr[1].id = cudaLaunchAttributeClusterDimension;
+      attr[1].val.clusterDim.x = 2;
+      attr[1].val.clusterDim.y = 1;
+      attr[1].val.clusterDim.z = 1;
+      cfg.numAttrs = 2;
+      cfg.gridDim = dim3(std::max(2, grid & ~1));
+      cfg.blockDim = dim3(ConvCfg<12>::kThreads);
+      cfg.dynamicSmemBytes = ConvCfg<12>::kSmem;
+      return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<12>, tm_in, tm_out, a, zs);
     case 0:
       cfg.blockDim = dim3(ConvCfg<0>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<0>::kSmem;
@@ -1577,6 +1616,9 @@ cudaError_t configure_kernels() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<3>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<12>::kSmem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<4>::kSmem);

@@ -113,6 +113,16 @@ TVS_DEV void tma_load_4d(void* dst, const void* tmap, uint64_t* bar, int c0, int
       ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)),
         "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
 }
+// multicast: the box lands at the same shared-memory offset in every CTA of
+// `mask` and completes its bytes on each one's barrier at `bar`'s offset
+TVS_DEV void tma_load_4d_mc(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2, int c3,
+                            uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3), "h"(mask) : "memory");
+}
 // L2 eviction-priority policies and hinted TMA variants
 TVS_DEV uint64_t l2_policy_evict_first() {
   uint64_t p;
@@ -320,6 +330,11 @@ TVS_DEV void wmma_commit(uint64_t* bar) {
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
       ::"r"(smem_u32(bar)) : "memory");
+}
+// tcgen05.commit arriving on the barrier at `bar`'s offset in every CTA of `mask`
+TVS_DEV void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread
 // complete (implies tcgen05.fence::before_thread_sync).

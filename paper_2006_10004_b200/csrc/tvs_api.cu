@@ -52,6 +52,7 @@ struct tvs_plan {
     int head_gate = 1;          // head after a stack: gate rows on the stack's flags (runs in the stack's tail)
     int head_grid = 4;          // gated head: CTAs per SM of its grid (tools/ab.py: 4 best, -1.5%)
     int stack_watcher = 1;      // layer stack: a dedicated warp polls the row flags
+    int fp32_pairs = 1;         // fp32-accurate hidden layers on CTA pairs (mode 12) instead of mode 3
     int conv0_tc = 1;           // K1 on tcgen05 (TF32 hi/lo) instead of the CUDA-core K1
     int wide_pair_layers = 12;  // (pack) wide variant: leading hidden layers on fp16 hi/lo pairs
     int wide_halves = 1;        // (pack) wide single-input layers on output-channel halves (mode 11)
@@ -434,9 +435,13 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       a.nshift = tvs::kC;
       a.act_out = static_cast<uint8_t*>(act[cur ^ 1]);
       a.span = next_span();
-      const int grid = conv_grid(max_ctas, a);
+      // CTA pairs (mode 12): both output-channel halves of a strip-row range at
+      // once, input rows multicast to the pair; a pair covers what one mode-3
+      // CTA covers in two visits, so the grid counts pairs of CTAs
+      const int mode = p->opt.fp32_pairs ? 12 : 3;
+      const int grid = mode == 12 ? 2 * conv_grid(max_ctas / 2, a) : conv_grid(max_ctas, a);
       timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64,
-                   [&] { return tvs::launch_conv_tc(3, in_map[cur], in_map[cur], a, grid, st); });
+                   [&] { return tvs::launch_conv_tc(mode, in_map[cur], in_map[cur], a, grid, st); });
       cur ^= 1;
     }
     tvs::ConvArgs a = base_args(H, W, strips, row0, rows);
@@ -703,6 +708,7 @@ int tvs_plan_set_option(tvs_plan* p, const char* name, long long value) {
       o.stack_band_rows = (int)value;
     } else if (k == "head_gate") flag(o.head_gate);
     else if (k == "stack_watcher") flag(o.stack_watcher);
+    else if (k == "fp32_pairs") flag(o.fp32_pairs);
     else if (k == "head_grid") {
       if (value < 1 || value > 64) throw TvsError(TVS_E_INVALID, "head_grid takes 1..64");
       o.head_grid = (int)value;

@@ -527,3 +527,18 @@ def test_reconstruction_check_across_chunks(seeded_state):
     bands, clos, rel = m.forward_planes(x, check_reconstruction=True)
     r2, x2 = _recon_host(x, bands, clos)
     assert torch.allclose(rel, torch.sqrt(r2 / x2).to(rel.device), rtol=1e-9, atol=1e-15)
+
+
+@pytest.mark.parametrize("shape", [(2, 48, 300), (1, 1, 129), (3, 37, 256), (1, 130, 1)])
+def test_fp32_cta_pairs_bitwise(seeded_state, shape):
+    """The fp32-accurate hidden layer on CTA pairs (mode 12: both output-channel
+    halves at once, input rows multicast to the pair) runs each output's MMA
+    sequence of mode 3: bitwise equal."""
+    x = torch.rand(shape[0], 1, *shape[1:], generator=torch.Generator().manual_seed(sum(shape))).cuda()
+    outs = []
+    for pr in (0, 1):
+        m = TVSpecNet(precision="fp32", options={"fp32_pairs": pr}).eval()
+        m.load_state_dict(seeded_state)
+        with torch.no_grad():
+            outs.append(m(x))
+    assert torch.equal(outs[0], outs[1])
