@@ -38,6 +38,9 @@ constexpr int kEpiGroups = 3;          // epilogue row groups (output row seq % 
 #ifndef TVS_EPI_GROUPS_PLAIN
 #define TVS_EPI_GROUPS_PLAIN 3
 #endif
+#ifndef TVS_WIDE_MCAST
+#define TVS_WIDE_MCAST 0
+#endif
 #ifndef TVS_STAGES_PLAIN
 #define TVS_STAGES_PLAIN 6
 #endif

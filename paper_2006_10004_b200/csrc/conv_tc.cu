@@ -291,6 +291,13 @@ struct ConvCfg {
   // CTA keeps only its half's weights, so the ring is 4 deep instead of 2 and no
   // row is read twice (mode 3 visits every segment once per half)
   static constexpr bool kPairH = kMode == 12;
+  // CTAs per cluster: mode 12 pairs; the wide pair-input layer (mode 5) runs
+  // its 4 output-channel quarters of a strip-row range as one cluster, each
+  // input row TMA-multicast to all four (CTAs 0-2 load one of its 3 boxes)
+  // instead of each CTA fetching it from L2 (build knob TVS_WIDE_MCAST, off:
+  // the cluster runs the four CTAs in lockstep per input row, config 5-wide
+  // 91 vs 119 MP/s)
+  static constexpr int kCluster = kPairH ? 2 : ((kMode == 5 && TVS_WIDE_MCAST) ? 4 : 1);
   static constexpr bool kUnshuf = kMode == 7;
   static constexpr bool kHead = kMode == 1 || kMode == 4 || kMode == 6 || kMode == 7 || kMode == 10;
   static constexpr bool kWide = kMode == 5 || kMode == 6 || kMode == 9 || kMode == 10 || kMode == 11;
@@ -442,7 +449,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     sFlagsReady = 0;
     // (CTA pairs: a stage is free once BOTH CTAs' MMAs read it - the rows are
     // multicast into both - so each empty barrier takes two commits)
-    for (int i = 0; i < Cfg::kNStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], Cfg::kPairH ? 2 : 1); }
+    for (int i = 0; i < Cfg::kNStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], Cfg::kCluster); }
     for (int i = 0; i < kSlots; ++i) { mbar_init(&slot_full[i], 1); mbar_init(&slot_empty[i], 4); }
     mbar_init(&wbar, 1);
     mbar_init(&wfree, 1);
@@ -453,7 +460,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   // weights do not depend on the previous layer: start their load before the
   // PDL wait so it overlaps the previous kernel's tail
   // CTA pairs (mode 12): this CTA's output-channel half
-  const uint32_t pair_rank = Cfg::kPairH ? cluster_ctarank() : 0u;
+  const uint32_t pair_rank = Cfg::kCluster > 1 ? cluster_ctarank() : 0u;
   if (threadIdx.x == 0) {
     mbar_arrive_expect_tx(&wbar, Cfg::kW);
     if constexpr (Cfg::kPairH) {  // its half of the split pack: [W_hi half | W_lo half]
@@ -469,7 +476,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if constexpr (Cfg::kPairH) cluster_sync_all();  // the peer's barriers exist before any multicast lands
+  if constexpr (Cfg::kCluster > 1) cluster_sync_all();  // the peers' barriers exist before any multicast lands
   const uint32_t tmem = tmem_base_smem;
   pdl_launch_dependents();  // the next layer may start its prologue on free SMs
   // previous layer's activations are complete and visible (a head gated on
@@ -535,9 +542,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             continue;
           }
           mbar_arrive_expect_tx(&full[stage], nbuf * kInRowBytes);
-          if constexpr (Cfg::kPairH) {  // this CTA's box (hi or lo) to both CTAs of the pair
-            tma_load_4d_mc(sIn + stage * Cfg::kStageBytes + pair_rank * kInRowStride, tmi, &full[stage],
-                           64 * (int)pair_rank, g.x0 - 1, r, g.b, (uint16_t)0x3);
+          if constexpr (Cfg::kCluster > 1) {  // this CTA's box (if any) to every CTA of the cluster
+            if ((int)pair_rank < nbuf)
+              tma_load_4d_mc(sIn + stage * Cfg::kStageBytes + pair_rank * kInRowStride, tmi, &full[stage],
+                             64 * (int)pair_rank, g.x0 - 1, r, g.b, (uint16_t)((1u << Cfg::kCluster) - 1u));
             if (++stage == Cfg::kNStages) { stage = 0; phase ^= 1; }
             continue;
           }
@@ -700,7 +708,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
                   prewait(p, dx, k);
                 }
             }
-            if constexpr (Cfg::kPairH) mma_commit_mc(&empty[stage], 0x3); else mma_commit(&empty[stage]);
+            if constexpr (Cfg::kCluster > 1) mma_commit_mc(&empty[stage], (uint16_t)((1u << Cfg::kCluster) - 1u)); else mma_commit(&empty[stage]);
             mma_commit(&slot_full[s]);
           }
           __syncwarp();
@@ -770,7 +778,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
               }
             }
           }
-          if constexpr (Cfg::kPairH) mma_commit_mc(&empty[stage], 0x3); else mma_commit(&empty[stage]);
+          if constexpr (Cfg::kCluster > 1) mma_commit_mc(&empty[stage], (uint16_t)((1u << Cfg::kCluster) - 1u)); else mma_commit(&empty[stage]);
           for (int q = q_lo; q <= q_hi; ++q)
             if (min(q + 1, a.H - 1) == r) mma_commit(&slot_full[(seq + (uint32_t)(q - g.ya)) & Cfg::kRingMask]);
         }
@@ -1212,7 +1220,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
   }
   // CTA pairs: no CTA leaves while its peer may still multicast into it or
   // commit to its barriers
-  if constexpr (Cfg::kPairH) cluster_sync_all();
+  if constexpr (Cfg::kCluster > 1) cluster_sync_all();
   if (a.span && threadIdx.x == 0) span_close(a.span);
   if constexpr (Cfg::kStack) trace_cta(a, 1);
 }
@@ -1478,6 +1486,13 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
       return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<4>, tm_in, tm_out, a, zs);
     case 5:
       cfg.gridDim = dim3(std::max(4, grid & ~3));  // groups of 4 CTAs (output-channel quarters)
+      if (ConvCfg<5>::kCluster > 1) {  // ... as clusters (input rows multicast)
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = ConvCfg<5>::kCluster;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = 1;
+        cfg.numAttrs = 2;
+      }
       cfg.blockDim = dim3(ConvCfg<5>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<5>::kSmem;
       return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<5>, tm_in, tm_out, a, zs);
