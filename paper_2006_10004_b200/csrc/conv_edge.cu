@@ -83,9 +83,10 @@ conv0_kernel(const float* __restrict__ x, T* __restrict__ act, const Conv0Params
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int co = c8 * 8 + e;
-        // fp64 accumulation in the fp32-accurate formats; the wide fast mode's
-        // pair (fp16 hi + e4m3 lo, ~15 significant bits) needs no more than fp32
-        using Acc = std::conditional_t<std::is_same_v<T, float> || (kSplit && !kLo8), double, float>;
+        // fp32 accumulation of the 9 taps (a few ulps, the reference's own
+        // fp32 conv class) for the split formats: fp64 cost the fp32 mode
+        // 700 us per config-2 forward; the CUDA-core fp32 path keeps fp64
+        using Acc = std::conditional_t<std::is_same_v<T, float>, double, float>;
         Acc acc = 0;
 #pragma unroll
         for (int t9 = 0; t9 < 9; ++t9) acc = fma((Acc)p.w[co * 9 + t9], (Acc)in[t9], acc);
