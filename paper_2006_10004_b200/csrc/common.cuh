@@ -125,6 +125,13 @@ struct ConvArgs {
   // when out_exp is set (the dgrad conv undoes its input's gradient scale)
   int raw_f32;
   const int* out_exp;
+  // wide fp32-accurate mode (tvs_api.cu, 128 channels as 2 x 2 blocks of the
+  // 64-channel split kernels): a hidden launch on the second input block adds
+  // the first block's raw fp32 partial sums acc_in [B][H][W][64] before the
+  // shift and ReLU; a head launch with acc_bands adds the bands already in
+  // `bands` (the first block's partial output)
+  const float* acc_in;
+  int acc_bands;
   unsigned long long watchdog_ns;  // layer stack: give up a row-flag wait after this long
   KernelSpan* span;                // null, or accumulate this launch's device duration
   // TVS_CONV_DBG / plan option "debug" (results invalid except kDbgWithholdFlag,
@@ -184,13 +191,16 @@ struct Conv0Params;
 cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap& tm_out, const ConvArgs& a,
                            int grid, cudaStream_t st);
 cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
-cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t* out, cudaStream_t st);
+// (cin, co0, ci0): pack the 64 x 64 block at output channel co0, input channel
+// ci0 of a [Cout][cin][3][3] weight (the wide fp32 mode's 2 x 2 blocks)
+cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int cin = 64,
+                                     int co0 = 0, int ci0 = 0);
 cudaError_t launch_pack_hidden_f16_t(const float* w, uint8_t* out, cudaStream_t st);  // training dgrad pack
 // parts = 4: output-channel quarters (modes 5 / 9); 2: halves (mode 11)
 cudaError_t launch_pack_hidden_wide(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int parts,
                                     bool lo8);
 cudaError_t launch_pack_head_wide(const float* w, int K, uint8_t* out, cudaStream_t st);
-cudaError_t launch_pack_head_f16(const float* w, int K, uint8_t* out, cudaStream_t st);
+cudaError_t launch_pack_head_f16(const float* w, int K, uint8_t* out, cudaStream_t st, int cin = 64, int ci0 = 0);
 cudaError_t launch_fill(float* dst, float v, int n, cudaStream_t st);
 struct Conv0Params {  // passed by value: lives in the kernel's constant bank
   float w[kMaxC * 9];  // [co][ky*3+kx]

@@ -923,6 +923,10 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
+          // rows at the image's top / bottom edge have 2 (or 1) dy taps inside the
+          // image: 12 (6) MMAs per main ring instead of 18, so less truncation to undo
+          const int ndy = (q > 0 ? 1 : 0) + 1 + (q + 1 < a.H ? 1 : 0);
+          const float kDb = 1.0f + 0.5f * 0.7213f * 3.0f * 1.1920929e-7f * (float)ndy;
           if (a.raw_f32) {  // training forward: pre-BatchNorm conv output, fp32
             if (xg < a.W) {
               float* dst = reinterpret_cast<float*>(a.act_out) + (((long long)g.b * a.H + q) * a.W + xg) * 64 + hh * 32;
@@ -932,8 +936,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                   const int ch = c4 * 4 + t;
-                  const float z = fmaf(__uint_as_float(e[ch >> 4][ch & 15]), kMainDebias18,
-                                       fmaf(__uint_as_float(o[ch >> 4][ch & 15]), kMainDebias18,
+                  const float z = fmaf(__uint_as_float(e[ch >> 4][ch & 15]), kDb,
+                                       fmaf(__uint_as_float(o[ch >> 4][ch & 15]), kDb,
                                             __uint_as_float(c[ch >> 4][ch & 15])));
                   f[t] = z * (1.0f / kSplitWScale);
                 }
@@ -944,13 +948,21 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           }
           if (xg < a.W) {
             uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * 256 + hh * 64;
+            // wide fp32 mode: the other input block's raw partial sums of this pixel
+            const float* accp =
+                a.acc_in ? a.acc_in + (((long long)g.b * a.H + q) * a.W + xg) * 64 + hh * 32 : nullptr;
 #pragma unroll
             for (int chunk = 0; chunk < 4; ++chunk) {
               const uint32_t sh_u = shift_u + (uint32_t)(hh * 32 + chunk * 8) * 4;
               const float4 s0 = ld_shared_f4(sh_u);
               const float4 s1 = ld_shared_f4(sh_u + 16);
-              const float sh[8] = {s0.x * sc, s0.y * sc, s0.z * sc, s0.w * sc, s1.x * sc, s1.y * sc, s1.z * sc,
-                                   s1.w * sc};
+              float sh[8] = {s0.x * sc, s0.y * sc, s0.z * sc, s0.w * sc, s1.x * sc, s1.y * sc, s1.z * sc, s1.w * sc};
+              if (accp) {
+                const float4 a0 = *reinterpret_cast<const float4*>(accp + chunk * 8);
+                const float4 a1 = *reinterpret_cast<const float4*>(accp + chunk * 8 + 4);
+                sh[0] += a0.x; sh[1] += a0.y; sh[2] += a0.z; sh[3] += a0.w;
+                sh[4] += a1.x; sh[5] += a1.y; sh[6] += a1.z; sh[7] += a1.w;
+              }
               uint32_t hi[4], lo[4];
 #pragma unroll
               for (int t2 = 0; t2 < 4; ++t2) {
@@ -958,8 +970,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
                   const int ch = chunk * 8 + t2 * 2 + t;  // channel within the half
-                  const float z = fmaf(__uint_as_float(e[ch >> 4][ch & 15]), kMainDebias18,
-                                       fmaf(__uint_as_float(o[ch >> 4][ch & 15]), kMainDebias18,
+                  const float z = fmaf(__uint_as_float(e[ch >> 4][ch & 15]), kDb,
+                                       fmaf(__uint_as_float(o[ch >> 4][ch & 15]), kDb,
                                             __uint_as_float(c[ch >> 4][ch & 15])));
                   f[t] = fmaxf(fmaf(z, 1.0f / kSplitWScale, sh[t2 * 2 + t]), 0.0f);
                 }
@@ -1190,7 +1202,8 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
 #pragma unroll
             for (int k = 0; k < kMaxBands; ++k) {
               if (k < a.K) {
-                const float o = (__uint_as_float(v[0][k]) + __uint_as_float(v[1][k])) * inv + sShift[k];
+                float o = (__uint_as_float(v[0][k]) + __uint_as_float(v[1][k])) * inv + sShift[k];
+                if (a.acc_bands) o += ob[k * plane];  // wide fp32 mode: + the first input block's partial
                 ob[k * plane] = o;
                 sum += o;
                 bad |= !isfinite(o);
@@ -1381,14 +1394,15 @@ __global__ void pack_head_wide_kernel(const float* __restrict__ w, int K, uint8_
 // fp32-accurate hidden pack: W' = W*s (BatchNorm fold, fp32) x 2^8 split into
 // hi = RN16(W'), lo = RN16(W' - hi); pack 0 = hi, pack 1 = lo.
 __global__ void pack_hidden_split_kernel(const float* __restrict__ w, const float* __restrict__ scale,
-                                         uint8_t* __restrict__ out) {
+                                         uint8_t* __restrict__ out, int cin, int co0, int ci0) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*64 + ci
   if (idx >= kC * kC) return;
   const int co = idx / kC, ci = idx % kC;
+  const float* wsrc = w + ((size_t)(co0 + co) * cin + ci0 + ci) * 9;
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
     const int ky = t / 3, kx = t % 3;
-    const float wv = (w[idx * 9 + t] * scale[co]) * kSplitWScale;
+    const float wv = (wsrc[t] * scale[co0 + co]) * kSplitWScale;
     const __half hi = __float2half_rn(wv);
     const __half lo = __float2half_rn(wv - __half2float(hi));
     // channel half h = co / 32: rows (2-ky)*32 + co%32 of that half's dx block
@@ -1398,14 +1412,15 @@ __global__ void pack_hidden_split_kernel(const float* __restrict__ w, const floa
   }
 }
 
-__global__ void pack_head_f16_kernel(const float* __restrict__ w, int K, uint8_t* __restrict__ out) {
+__global__ void pack_head_f16_kernel(const float* __restrict__ w, int K, uint8_t* __restrict__ out, int cin,
+                                     int ci0) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // k*64 + ci
   if (idx >= K * kC) return;
   const int k = idx / kC, ci = idx % kC;
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
     const int ky = t / 3, kx = t % 3;
-    const float wf = w[idx * 9 + t];
+    const float wf = w[((size_t)k * cin + ci0 + ci) * 9 + t];
     const __half hi = __float2half_rn(wf);
     const __half lo = __float2half_rn(wf - __half2float(hi));
     const int nb = (2 - ky) * ConvCfg<1>::NB;  // per dy: 8 hi rows, then 8 lo rows
@@ -1575,10 +1590,11 @@ cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* 
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t* out, cudaStream_t st) {
+cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int cin,
+                                     int co0, int ci0) {
   cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<3>::kW, st);
   if (e != cudaSuccess) return e;
-  pack_hidden_split_kernel<<<(kC * kC + 127) / 128, 128, 0, st>>>(w, scale, out);
+  pack_hidden_split_kernel<<<(kC * kC + 127) / 128, 128, 0, st>>>(w, scale, out, cin, co0, ci0);
   return cudaGetLastError();
 }
 
@@ -1609,10 +1625,10 @@ cudaError_t launch_pack_head_unshuf(const float* w, int K4, uint8_t* out, cudaSt
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_head_f16(const float* w, int K, uint8_t* out, cudaStream_t st) {
+cudaError_t launch_pack_head_f16(const float* w, int K, uint8_t* out, cudaStream_t st, int cin, int ci0) {
   cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<1>::kW, st);
   if (e != cudaSuccess) return e;
-  pack_head_f16_kernel<<<(K * kC + 127) / 128, 128, 0, st>>>(w, K, out);
+  pack_head_f16_kernel<<<(K * kC + 127) / 128, 128, 0, st>>>(w, K, out, cin, ci0);
   return cudaGetLastError();
 }
 

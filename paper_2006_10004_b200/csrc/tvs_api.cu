@@ -68,6 +68,7 @@ struct tvs_plan {
 
   // conv0 [64][1][3][3] + bias, head [K][64][3][3] + bias (fp32, folded)
   tvs::Conv0Params conv0{};  // host copy, passed by value to the CUDA-core K1
+  tvs::Conv0Params conv0_blk[2]{};  // wide fp32 mode: the two 64-output-channel blocks of conv0
   float w0_l1 = 0.f, b0_max = 0.f;  // input-scale bound: max_co sum|W0|, max|b0|
   float* wh = nullptr;
   float* bh = nullptr;
@@ -84,12 +85,15 @@ struct tvs_plan {
   uint8_t* c0pack = nullptr;  // K1 on tcgen05: packed TF32 hi/lo B operand
   float* c0bias = nullptr;
   // the path the packed weights were built for (options may change later)
-  bool packed_tc = false, packed_split = false, packed_wide = false;
+  bool packed_tc = false, packed_split = false, packed_wide = false, packed_wide_split = false;
   int packed_pairs = 12, packed_halves = 1;
 
   // activation ping-pong scratch
   void* act[2] = {nullptr, nullptr};
   size_t act_bytes = 0;
+  // wide fp32 mode: raw fp32 partial sums of one 64-channel output block
+  void* act_raw = nullptr;
+  size_t act_raw_bytes = 0;
   // device records of the hidden-layer launches (option "span"), one per launch
   static constexpr int kSpanSlots = 8192;
   tvs::KernelSpan* span = nullptr;
@@ -142,10 +146,18 @@ struct tvs_plan {
   bool split_path() const { return mode == TVS_MODE_FP32 && channels == 64 && !opt.fp32_cuda; }
   // wide variant (128 channels) fast mode on tcgen05 (modes 5/6/9/10/11)
   bool wide_path() const { return mode == TVS_MODE_FAST && channels == 128 && !opt.wide_cuda; }
+  // wide variant, fp32-accurate mode on tcgen05: every 128 -> 128 layer as 2 x 2
+  // blocks of the 64-channel split kernels (modes 12 / 3 / 4), activations as two
+  // 64-channel hi|lo pair planes
+  bool wide_split_path() const {
+    return mode == TVS_MODE_FP32 && channels == 128 && !opt.fp32_cuda && !opt.wide_cuda;
+  }
   size_t act_px_bytes() const { return tc_path() ? 128 : (size_t)channels * 4; }
   // the power-of-two input scale guards the fp16-range formats (fast, split,
   // wide); the CUDA-core fp32 kernels compute at fp32 range and do not need it
-  bool scaled() const { return opt.input_scale && (tc_path() || split_path() || wide_path()); }
+  bool scaled() const {
+    return opt.input_scale && (tc_path() || split_path() || wide_path() || wide_split_path());
+  }
 };
 
 namespace {
@@ -171,7 +183,7 @@ void free_all(tvs_plan* p) {
     if (e) cudaEventDestroy(e);
   if (p->status_host) cudaFreeHost(p->status_host);
   free_weights(p);
-  void* ptrs[] = {p->act[0], p->act[1], p->dx, p->rowcnt, p->escale, p->span};
+  void* ptrs[] = {p->act[0], p->act[1], p->act_raw, p->dx, p->rowcnt, p->escale, p->span};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -185,6 +197,15 @@ void ensure_act(tvs_plan* p, size_t bytes) {
   p->act_bytes = 0;
   for (int i = 0; i < 2; ++i) TVS_CUDA(cudaMalloc(&p->act[i], bytes));
   p->act_bytes = bytes;
+}
+
+void ensure_raw(tvs_plan* p, size_t bytes) {
+  if (bytes <= p->act_raw_bytes) return;
+  if (p->act_raw) TVS_CUDA(cudaFree(p->act_raw));
+  p->act_raw = nullptr;
+  p->act_raw_bytes = 0;
+  TVS_CUDA(cudaMalloc(&p->act_raw, bytes));
+  p->act_raw_bytes = bytes;
 }
 
 // Work items of the layer-stack kernel (conv_tc.cu ItemIter) for a chunk of B
@@ -297,8 +318,12 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
   const bool fast = p->tc_path();
   const bool split = p->split_path();
   const bool wide = p->wide_path();
+  const bool wsplit = p->wide_split_path();
   const int C = p->channels;
   const double px = (double)B * H * W;
+  // wide fp32 mode: act[i] holds two 64-channel pair planes of the chunk
+  const size_t plane_bytes = (size_t)B * H * W * 256;
+  auto plane = [&](int buf, int blk) { return static_cast<uint8_t*>(act[buf]) + (size_t)blk * plane_bytes; };
   const int us = p->unshuffle;  // 2: the layer stack runs on the (H/2, W/2) grid
   // layer stack (FAST path): all CTAs of the persistent grid co-resident
   // (cooperative launch, verified at plan creation)
@@ -368,6 +393,11 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
       return tvs::launch_conv0_tc(1, x, make_act_map(act[0], B, H, W, 128), p->c0pack, p->c0bias, escale, B, H, W,
                                   p->num_sms, conv0_pdl, st);
     });
+  else if (wsplit)
+    for (int o = 0; o < 2; ++o)
+      timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * 64, [&] {
+        return tvs::launch_conv0(tvs::kActSplit, 64, x, plane(0, o), p->conv0_blk[o], escale, B, H, W, st);
+      });
   else
     timed_launch(p, st, TVS_KIND_CONV0, px * 2.0 * 9 * C,
                  [&] { return tvs::launch_conv0(fmt, C, x, act[0], p->conv0, escale, B, H, W, st); });
@@ -423,6 +453,51 @@ void run_chunk(tvs_plan* p, const float* x, float* bands, float* closure, int B,
     const CUtensorMap& mh = single_map[cur];
     timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * C * p->out_bands,
                  [&] { return tvs::launch_conv_tc(10, mh, mh, a, grid, st); });
+  } else if (wsplit) {
+    // wide fp32-accurate mode: out_o = ReLU(conv(P0, W[o][0]) + conv(P1, W[o][1]) + shift_o),
+    // each block conv on the 64-channel split kernel; the first writes its raw
+    // fp32 sums, the second adds them in its epilogue (ConvArgs::acc_in)
+    const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
+    CUtensorMap in_map[2][2];
+    for (int i = 0; i < 2; ++i)
+      for (int k = 0; k < 2; ++k) in_map[i][k] = make_act_map(plane(i, k), B, H, W, tvs::kHaloPx, 128);
+    const int mode = p->opt.fp32_pairs ? 12 : 3;
+    for (int l = 0; l < nh; ++l) {
+      for (int o = 0; o < 2; ++o)
+        for (int k = 0; k < 2; ++k) {
+          tvs::ConvArgs a = base_args(H, W, strips, 0, H);
+          a.wpack = p->wpack + ((size_t)(l * 2 + o) * 2 + k) * tvs::conv_wpack_split_bytes();
+          a.shift = p->bhid + (size_t)l * C + o * 64;
+          a.nshift = 64;
+          if (k == 0) {
+            a.act_out = static_cast<uint8_t*>(p->act_raw);
+            a.raw_f32 = 1;
+          } else {
+            a.act_out = plane(cur ^ 1, o);
+            a.acc_in = static_cast<const float*>(p->act_raw);
+          }
+          a.span = next_span();
+          const int grid = mode == 12 ? 2 * conv_grid(max_ctas / 2, a) : conv_grid(max_ctas, a);
+          timed_launch(p, st, TVS_KIND_HIDDEN, px * 2.0 * 9 * 64 * 64,
+                       [&] { return tvs::launch_conv_tc(mode, in_map[cur][k], in_map[cur][k], a, grid, st); });
+        }
+      cur ^= 1;
+    }
+    for (int k = 0; k < 2; ++k) {
+      tvs::ConvArgs a = base_args(H, W, strips, row0, rows);
+      a.wpack = p->hpack + (size_t)k * tvs::conv_wpack_bytes(true);
+      a.K = p->out_bands;
+      a.x = x; a.bands = bands;
+      if (k == 1) {  // + block 0's partial bands, bias, closure, checks
+        a.shift = p->bh;
+        a.nshift = p->out_bands;
+        a.acc_bands = 1;
+        a.closure = closure; a.recon = recon;
+      }
+      const int grid = conv_grid(max_ctas, a);
+      timed_launch(p, st, TVS_KIND_HEAD, (double)B * rows * W * 2.0 * 9 * 64 * p->out_bands,
+                   [&] { return tvs::launch_conv_tc(4, in_map[cur][k], in_map[cur][k], a, grid, st); });
+    }
   } else if (split) {
     // fp32-accurate: split-operand tcgen05 layers on fp16 hi|lo pair rows
     const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
@@ -618,6 +693,7 @@ void forward_impl(tvs_plan* p, const float* x, float* bands, float* closure, int
   int cb = (int)std::max<size_t>(1, (size_t)(p->opt.chunk_mb << 20) / std::max<size_t>(per_img, 1));
   cb = std::min(cb, B);
   ensure_act(p, per_img * cb);
+  if (p->wide_split_path()) ensure_raw(p, (size_t)H * W * 256 * cb);
   for (int b0 = 0; b0 < B; b0 += cb) {
     const int nb = std::min(cb, B - b0);
     run_chunk(p, x + b0 * in_img, bands + (size_t)b0 * p->out_bands * out_img,
@@ -790,6 +866,9 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
     } else if (p->wide_path()) {
       TVS_CUDA(cudaMalloc(&p->wpack, (size_t)nh * tvs::conv_wpack_wide_bytes(false)));
       TVS_CUDA(cudaMalloc(&p->hpack, tvs::conv_wpack_wide_bytes(true)));
+    } else if (p->wide_split_path()) {  // 2 x 2 blocks per hidden layer, 2 head blocks
+      TVS_CUDA(cudaMalloc(&p->wpack, (size_t)nh * 4 * tvs::conv_wpack_split_bytes()));
+      TVS_CUDA(cudaMalloc(&p->hpack, 2 * tvs::conv_wpack_bytes(true)));
     } else {
       TVS_CUDA(cudaMalloc(&p->whid, (size_t)nh * C * C * 9 * 4));
     }
@@ -813,6 +892,11 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
     } else {
       std::copy(w0.begin(), w0.end(), p->conv0.w);
       std::copy(b0.begin(), b0.end(), p->conv0.b);
+      if (C == 128)
+        for (int o = 0; o < 2; ++o) {
+          std::copy(w0.begin() + o * 64 * 9, w0.begin() + (o + 1) * 64 * 9, p->conv0_blk[o].w);
+          std::copy(b0.begin() + o * 64, b0.begin() + (o + 1) * 64, p->conv0_blk[o].b);
+        }
       TVS_CUDA(cudaMemcpyAsync(p->wh, w_dev[p->depth - 1], (size_t)p->out_bands * C * 9 * 4,
                                cudaMemcpyDeviceToDevice, st));
     }
@@ -839,6 +923,12 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
       } else if (p->split_path()) {
         TVS_CUDA(tvs::launch_pack_hidden_split(w_dev[l + 1], dst_scale,
                                                p->wpack + (size_t)l * tvs::conv_wpack_split_bytes(), st));
+      } else if (p->wide_split_path()) {
+        for (int o = 0; o < 2; ++o)
+          for (int k = 0; k < 2; ++k)
+            TVS_CUDA(tvs::launch_pack_hidden_split(
+                w_dev[l + 1], dst_scale, p->wpack + ((size_t)(l * 2 + o) * 2 + k) * tvs::conv_wpack_split_bytes(), st,
+                128, o * 64, k * 64));
       } else if (p->wide_path()) {  // pair-input layers: quarters (mode 5); single-input: halves (mode 11)
         const bool pair_in = l < P || P >= nh;
         TVS_CUDA(tvs::launch_pack_hidden_wide(w_dev[l + 1], dst_scale,
@@ -855,9 +945,14 @@ int tvs_plan_set_weights(tvs_plan* p, const float* const* w_dev, const float* co
       TVS_CUDA(tvs::launch_pack_head_f16(w_dev[p->depth - 1], p->out_bands, p->hpack, st));
     }
     if (p->wide_path()) TVS_CUDA(tvs::launch_pack_head_wide(w_dev[p->depth - 1], p->out_bands, p->hpack, st));
+    if (p->wide_split_path())
+      for (int k = 0; k < 2; ++k)
+        TVS_CUDA(tvs::launch_pack_head_f16(w_dev[p->depth - 1], p->out_bands,
+                                           p->hpack + (size_t)k * tvs::conv_wpack_bytes(true), st, 128, k * 64));
     p->packed_tc = p->tc_path();
     p->packed_split = p->split_path();
     p->packed_wide = p->wide_path();
+    p->packed_wide_split = p->wide_split_path();
     p->weights_ready = true;
   });
 }
@@ -867,7 +962,7 @@ int tvs_forward(tvs_plan* p, const float* x, float* bands, float* closure_or_nul
   return guarded([&] {
     if (!p) throw TvsError(TVS_E_INVALID, "null plan");
     if (p->weights_ready && (p->packed_tc != p->tc_path() || p->packed_split != p->split_path() ||
-                             p->packed_wide != p->wide_path()))
+                             p->packed_wide != p->wide_path() || p->packed_wide_split != p->wide_split_path()))
       throw TvsError(TVS_E_STATE, "plan options changed the weight layout: call tvs_plan_set_weights again");
     forward_impl(p, x, bands, closure_or_null, B, H, W, valid_row0, valid_rows, (cudaStream_t)stream);
   });
@@ -878,7 +973,7 @@ int tvs_forward_checked(tvs_plan* p, const float* x, float* bands, float* closur
   return guarded([&] {
     if (!p || !closure || !recon) throw TvsError(TVS_E_INVALID, "null plan/closure/recon");
     if (p->weights_ready && (p->packed_tc != p->tc_path() || p->packed_split != p->split_path() ||
-                             p->packed_wide != p->wide_path()))
+                             p->packed_wide != p->wide_path() || p->packed_wide_split != p->wide_split_path()))
       throw TvsError(TVS_E_STATE, "plan options changed the weight layout: call tvs_plan_set_weights again");
     forward_impl(p, x, bands, closure, B, H, W, valid_row0, valid_rows, (cudaStream_t)stream, recon);
   });

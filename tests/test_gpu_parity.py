@@ -100,6 +100,35 @@ def test_wide_variant(golden, wide_case, prec):
     assert band_rel_l2(out, y32).max() <= 1.5e-5
 
 
+@pytest.mark.parametrize("shape", [(2, 37, 300), (1, 130, 1), (3, 64, 128), (1, 1, 129)])
+def test_wide_fp32_tcgen05_blocks(shape):
+    """The wide variant's fp32-accurate mode on tcgen05 (every 128 -> 128 layer as
+    2 x 2 blocks of the 64-channel split kernels, partial sums handed over in
+    fp32) against the CUDA-core fp32 kernels (plan option wide_cuda=1: fp32 FFMA
+    chunks combined in fp64) on ragged shapes, with a row window, the closure
+    and both CTA layouts of the block kernel (modes 12 and 3, bitwise equal)."""
+    state = build_seeded_state(26, 128, 5)
+    x = torch.rand(*shape[:1], 1, *shape[1:], generator=torch.Generator().manual_seed(5)).cuda()
+    outs = {}
+    for name, opts in (("tc", {}), ("tc3", {"fp32_pairs": 0}), ("cuda", {"wide_cuda": 1})):
+        m = TVSpecNet(26, 128, 5, precision="fp32", options=opts).eval()
+        m.load_state_dict(state)
+        bands, clos = m.forward_planes(x, closure=True)
+        outs[name] = bands
+        assert m.last_launch_count() == (26 if name == "cuda" else 1 + 2 + 24 * 4 + 2)
+        np.testing.assert_allclose((bands.sum(1, keepdim=True) + clos).cpu().numpy(), x.cpu().numpy(), atol=1e-5)
+        if shape[1] >= 30:
+            b2, c2 = m.forward_planes(x, closure=True, rows=(9, 13))
+            assert torch.equal(b2, bands[:, :, 9:22])
+            assert torch.equal(c2, clos[:, :, 9:22])
+    assert torch.equal(outs["tc"], outs["tc3"])
+    err = band_rel_l2(outs["tc"].cpu().numpy(), outs["cuda"].cpu().numpy()).max()
+    print(f"wide fp32 {shape}: tcgen05 blocks vs CUDA-core kernels {err:.3e}")
+    # two fp32-class computations of the same 26 layers: each is within ~1e-5
+    # of the exact result (tools/wide_fp32_probe.py), so of each other
+    assert err <= 2e-5
+
+
 @pytest.mark.parametrize("img", [1, 2, 3])
 def test_wide_fp32_standing_exception_more_images(img):
     """The wide variant's fp32 mode vs the 1e-5 gate on more config-5 images
@@ -439,7 +468,8 @@ def _recon_host(x, bands, clos):
     return (r * r).sum((1, 2)), (x[:, 0].double() ** 2).sum((1, 2))
 
 
-@pytest.mark.parametrize("variant", ["fast", "fast_stack", "fast_bands", "fp32", "fp32_cuda", "wide", "unshuffle"])
+@pytest.mark.parametrize(
+    "variant", ["fast", "fast_stack", "fast_bands", "fp32", "fp32_cuda", "wide", "wide_fp32", "unshuffle"])
 def test_fused_reconstruction_check(seeded_state, variant):
     """tvs_forward_checked (north_star item 3): the head epilogue's residual
     sums equal the same check evaluated on the host from the stored planes,
@@ -454,13 +484,13 @@ def test_fused_reconstruction_check(seeded_state, variant):
         opts = {"stack": 1, "stack_band_rows": 8}
     elif variant == "fp32_cuda":
         opts = {"fp32_cuda": 1}
-    elif variant == "wide":
+    elif variant in ("wide", "wide_fp32"):
         arch = dict(depth=26, channels=128)
         state = bss(**arch)
     elif variant == "unshuffle":
         arch = dict(unshuffle=2)
         state = bss(17, 64, 5, unshuffle=2)
-    prec = "fp32" if variant.startswith("fp32") else "fast"
+    prec = "fp32" if "fp32" in variant else "fast"
     m = TVSpecNet(**arch, precision=prec, options=opts).eval()
     m.load_state_dict(state)
     x = torch.rand(3, 1, 40, 300, generator=torch.Generator().manual_seed(11)).cuda() * 3.0
