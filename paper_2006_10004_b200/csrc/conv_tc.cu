@@ -284,13 +284,18 @@ struct StackWatcher {
 template <int kMode>
 struct ConvCfg {
   static constexpr bool kStack = kMode == 8;
-  static constexpr bool kSplit = (kMode >= 3 && kMode <= 6) || kMode == 12;
+  static constexpr bool kSplit = (kMode >= 3 && kMode <= 6) || kMode == 12 || kMode == 13;
   // 12 = the fp32-accurate hidden layer on CTA PAIRS (a cluster of 2): each CTA
   // computes one 32-channel half of the same strip-rows, the input rows are
   // TMA-multicast to both (each CTA loads one of the hi / lo boxes), and each
   // CTA keeps only its half's weights, so the ring is 4 deep instead of 2 and no
   // row is read twice (mode 3 visits every segment once per half)
-  static constexpr bool kPairH = kMode == 12;
+  static constexpr bool kPairH = kMode == 12 || kMode == 13;
+  // 13 = mode 12 with the auxiliary epilogue paths compiled in (raw fp32 output,
+  // a second input block's partial sums added: the wide fp32 mode's 2 x 2 blocks).
+  // Carrying them as run-time branches cost the plain mode 12 epilogue 11%
+  // (825 vs 742 us per config-2 layer), so the plain mode compiles them out.
+  static constexpr bool kAux = kMode != 12;
   // CTAs per cluster: mode 12 pairs; the wide pair-input layer (mode 5) runs
   // its 4 output-channel quarters of a strip-row range as one cluster, each
   // input row TMA-multicast to all four (CTAs 0-2 load one of its 3 boxes)
@@ -320,7 +325,7 @@ struct ConvCfg {
   static constexpr int kWatchWarp = kEpiWarp0 + 4 * kGroups;
   static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kGroups + (kStack ? 1 : 0));
   // split hidden layer: two passes of 32 output channels (TMEM room for three rings)
-  static constexpr bool kHalves = kMode == 3 || kMode == 12;
+  static constexpr bool kHalves = kMode == 3 || kPairH;
   // TMEM cols per row; the 64-channel heads (modes 1 / 4) use 8 hi + 8 lo
   // weight columns per dy (K <= kMaxBands = 8): N = 48 per MMA instead of 96
   static constexpr int NB = kUnshuf ? 64 : ((kMode == 1 || kMode == 4) ? 16 : ((kHead || kHalves || kQuarters) ? 32 : 64));
@@ -374,7 +379,7 @@ struct ConvCfg {
   // room for the hi*hi products of input channels 0-31 and 32-63 in two
   // separate rings (18 MMAs each: half the accumulated magnitude, half the
   // truncations), plus the correction ring.
-  static constexpr bool kTwoRings = kMode == 3 || kMode == 4 || kMode == 12;  // the fp32-accurate modes
+  static constexpr bool kTwoRings = kMode == 3 || kMode == 4 || kPairH;  // the fp32-accurate modes
   static constexpr int kRing = kTwoRings ? (kHead ? 8 : 4) : kSlots;
   static constexpr int kTmemCols = (kTwoRings || kLo8) ? 512 : kSlots * NB;  // 512 / 256
   static constexpr uint32_t kRingMask = kRing - 1;
@@ -927,7 +932,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           // image: 12 (6) MMAs per main ring instead of 18, so less truncation to undo
           const int ndy = (q > 0 ? 1 : 0) + 1 + (q + 1 < a.H ? 1 : 0);
           const float kDb = 1.0f + 0.5f * 0.7213f * 3.0f * 1.1920929e-7f * (float)ndy;
-          if (a.raw_f32) {  // training forward: pre-BatchNorm conv output, fp32
+          if (Cfg::kAux && a.raw_f32) {  // training forward: pre-BatchNorm conv output, fp32
             if (xg < a.W) {
               float* dst = reinterpret_cast<float*>(a.act_out) + (((long long)g.b * a.H + q) * a.W + xg) * 64 + hh * 32;
 #pragma unroll
@@ -950,14 +955,14 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
             uint8_t* dst = a.act_out + (((long long)g.b * a.H + q) * a.W + xg) * 256 + hh * 64;
             // wide fp32 mode: the other input block's raw partial sums of this pixel
             const float* accp =
-                a.acc_in ? a.acc_in + (((long long)g.b * a.H + q) * a.W + xg) * 64 + hh * 32 : nullptr;
+                (Cfg::kAux && a.acc_in) ? a.acc_in + (((long long)g.b * a.H + q) * a.W + xg) * 64 + hh * 32 : nullptr;
 #pragma unroll
             for (int chunk = 0; chunk < 4; ++chunk) {
               const uint32_t sh_u = shift_u + (uint32_t)(hh * 32 + chunk * 8) * 4;
               const float4 s0 = ld_shared_f4(sh_u);
               const float4 s1 = ld_shared_f4(sh_u + 16);
               float sh[8] = {s0.x * sc, s0.y * sc, s0.z * sc, s0.w * sc, s1.x * sc, s1.y * sc, s1.z * sc, s1.w * sc};
-              if (accp) {
+              if (Cfg::kAux && accp) {
                 const float4 a0 = *reinterpret_cast<const float4*>(accp + chunk * 8);
                 const float4 a1 = *reinterpret_cast<const float4*>(accp + chunk * 8 + 4);
                 sh[0] += a0.x; sh[1] += a0.y; sh[2] += a0.z; sh[3] += a0.w;
@@ -1482,6 +1487,8 @@ cudaError_t launch_conv_tc(int mode, const CUtensorMap& tm_in, const CUtensorMap
       cfg.gridDim = dim3(std::max(2, grid & ~1));
       cfg.blockDim = dim3(ConvCfg<12>::kThreads);
       cfg.dynamicSmemBytes = ConvCfg<12>::kSmem;
+      if (a.raw_f32 || a.acc_in)  // auxiliary epilogue paths: their own instantiation
+        return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<13>, tm_in, tm_out, a, zs);
       return cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel<12>, tm_in, tm_out, a, zs);
     case 0:
       cfg.blockDim = dim3(ConvCfg<0>::kThreads);
@@ -1650,6 +1657,9 @@ cudaError_t configure_kernels() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<12>::kSmem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(conv3x3_tc_kernel<13>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ConvCfg<13>::kSmem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(conv3x3_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)ConvCfg<4>::kSmem);
