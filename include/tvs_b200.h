@@ -172,6 +172,10 @@ int tvs_train_forward(tvs_train* plan, const float* const* w_dev, const float* c
                       float* out, float* mean_out, float* var_out, int B, int H, int W, void* stream);
 int tvs_train_backward(tvs_train* plan, const float* g_out, float* const* dw, float* const* dbias,
                        float* const* dgamma, float* const* dbeta, void* stream);
+/* Training options (the train-plan counterpart of tvs_plan_set_option):
+ *   "wgrad_tc"  1 (default) weight gradients on the tcgen05 kernel (wgrad_tc.cu),
+ *               0 one cuBLAS split-K GEMM per filter tap. */
+int tvs_train_set_option(tvs_train* plan, const char* name, int value);
 int tvs_train_destroy(tvs_train* plan);
 
 /* Band scoring statistics (spectv metrics.py:28-237), fp64.

@@ -52,6 +52,7 @@ EXPORTS = (
     "tvs_train_create",
     "tvs_train_forward",
     "tvs_train_backward",
+    "tvs_train_set_option",
     "tvs_train_destroy",
 )
 
@@ -126,6 +127,8 @@ def load() -> ctypes.CDLL:
         lib.tvs_train_forward.argtypes = [P, PP, PP, PP, PP, ctypes.c_float, P, P, P, P, i, i, i, P]
         lib.tvs_train_backward.restype = i
         lib.tvs_train_backward.argtypes = [P, P, PP, PP, PP, PP, P]
+        lib.tvs_train_set_option.restype = i
+        lib.tvs_train_set_option.argtypes = [P, ctypes.c_char_p, ctypes.c_int]
         lib.tvs_train_destroy.restype = i
         lib.tvs_train_destroy.argtypes = [P]
         lib.tvs_plan_destroy.restype = i
@@ -254,6 +257,9 @@ class TrainPlan:
     def backward(self, g_out, dw, dbias, dgamma, dbeta, stream: int) -> None:
         check(self.lib.tvs_train_backward(self.handle, ctypes.c_void_p(g_out), _ptrs(dw), _ptrs(dbias),
                                           _ptrs(dgamma), _ptrs(dbeta), ctypes.c_void_p(stream)))
+
+    def set_option(self, name: str, value: int) -> None:
+        check(self.lib.tvs_train_set_option(self.handle, name.encode(), int(value)))
 
     def close(self) -> None:
         if self.handle and self.handle.value:

@@ -196,6 +196,13 @@ cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* 
 cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int cin = 64,
                                      int co0 = 0, int ci0 = 0);
 cudaError_t launch_pack_hidden_f16_t(const float* w, uint8_t* out, cudaStream_t st);  // training dgrad pack
+// training wgrad on tcgen05 (wgrad_tc.cu): dW = alpha * sum_p G[p] (x) A[p + tap offset] over the
+// zero-bordered pixel list; `part` holds wgrad_part_bytes(num_sms) of split-K partials
+size_t wgrad_part_bytes(int num_sms);
+CUtensorMap make_wgrad_gmap(const void* base, long long rows);  // [rows][64] fp16 gradient operand
+CUtensorMap make_wgrad_amap(const void* base, long long rows);  // [rows][128] fp16 pair activations (hi half read)
+cudaError_t launch_wgrad_tc(const CUtensorMap& gmap, const CUtensorMap& amap, long long PP, int guard, int W,
+                            int rows, const float* alpha, float* part, float* dw, int num_sms, cudaStream_t st);
 // parts = 4: output-channel quarters (modes 5 / 9); 2: halves (mode 11)
 cudaError_t launch_pack_hidden_wide(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int parts,
                                     bool lo8);

@@ -440,18 +440,38 @@ cudaError_t launch_hidden_f32(int C, const float* in, float* out, const float* w
 // scratch: 2 * B zeroed ints per forward ([0, B) amax bits, [B, 2B) block count).
 __global__ void __launch_bounds__(256)
 input_scale_kernel(const float* __restrict__ x, long long n, float w0_l1, float b0_max, int* __restrict__ escale,
-                   int* __restrict__ scratch, int* __restrict__ status) {
+                   int* __restrict__ scratch, int* __restrict__ status, int vec4) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // conv0 may start its prologue
   const int b = blockIdx.y, B = gridDim.y;
   const float* img = x + (long long)b * n;
-  const long long per = (n + gridDim.x - 1) / gridDim.x;
-  const long long lo = per * blockIdx.x, hi = min(n, lo + per);
+  const long long per = ((n + gridDim.x - 1) / gridDim.x + 3) & ~3LL;  // a multiple of 4 px
+  const long long lo = min(n, per * blockIdx.x), hi = min(n, lo + per);
   float amax = 0.0f;
   int bad = 0;
-  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const float e = __ldg(img + i);
-    if (isfinite(e)) amax = fmaxf(amax, fabsf(e));
-    else bad = 1;
+  // max and the non-finite flag are order-independent, so the vector path
+  // (block ranges are multiples of 4 px; taken when the image is 16 B aligned)
+  // gives the same bits: independent 16 B loads instead of a chain of 4 B ones
+  if (vec4) {
+    const float4* img4 = reinterpret_cast<const float4*>(img);
+    for (long long i = lo / 4 + threadIdx.x; i < hi / 4; i += blockDim.x) {
+      const float4 e = __ldg(img4 + i);
+      const float m4 = fmaxf(fmaxf(fabsf(e.x), fabsf(e.y)), fmaxf(fabsf(e.z), fabsf(e.w)));
+      if (isfinite(e.x) && isfinite(e.y) && isfinite(e.z) && isfinite(e.w)) {
+        amax = fmaxf(amax, m4);
+      } else {
+        bad = 1;
+        if (isfinite(e.x)) amax = fmaxf(amax, fabsf(e.x));
+        if (isfinite(e.y)) amax = fmaxf(amax, fabsf(e.y));
+        if (isfinite(e.z)) amax = fmaxf(amax, fabsf(e.z));
+        if (isfinite(e.w)) amax = fmaxf(amax, fabsf(e.w));
+      }
+    }
+  } else {
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      const float e = __ldg(img + i);
+      if (isfinite(e)) amax = fmaxf(amax, fabsf(e));
+      else bad = 1;
+    }
   }
   __shared__ float s_max[8];
   __shared__ int s_bad[8];
@@ -479,10 +499,12 @@ input_scale_kernel(const float* __restrict__ x, long long n, float w0_l1, float 
 cudaError_t launch_input_scale(const float* x, int B, long long px_per_image, float w0_l1, float b0_max, int* escale,
                                int* scratch, int* status, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  // ~4 blocks per SM in total, >= 4096 px per block
-  const long long want = std::max(1LL, std::min((592LL + B - 1) / B, (px_per_image + 4095) / 4096));
+  // ~4 blocks per SM in total, >= 1024 px per block (one 16 B load per thread:
+  // a batch-1 256 x 256 image took 8 us with 16 dependent 4 B loads per thread)
+  const long long want = std::max(1LL, std::min((592LL + B - 1) / B, (px_per_image + 1023) / 1024));
+  const int vec4 = (px_per_image % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
   input_scale_kernel<<<dim3((unsigned)want, (unsigned)B), 256, 0, st>>>(x, px_per_image, w0_l1, b0_max, escale,
-                                                                          scratch, status);
+                                                                          scratch, status, vec4);
   return cudaGetLastError();
 }
 

@@ -319,11 +319,13 @@ head_bwd_reduce_kernel(const float* __restrict__ gout, int B, int K, long long H
   if ((threadIdx.x & 31) == 0) atomicMax(amax_bits, __float_as_int(m));
 }
 
-// Head backward, pass 2: g_out as fp16 * 2^s into [B][H+2][W+2][8] (bands
-// padded to 8 channels), the wgrad GEMM operand; exports s and 2^-s.
+// Head backward, pass 2: g_out as fp16 * 2^s into [B][H+2][W+2][cs] (bands
+// padded with zero channels to cs = 8 for the cuBLAS wgrad, or to cs = 64 in
+// the hidden layers' gradient buffer for the tcgen05 wgrad), the wgrad
+// operand; exports s and 2^-s.
 __global__ void __launch_bounds__(kTB)
 head_bwd_pack_kernel(const float* __restrict__ gout, int B, int K, int H, int W, const int* amax_bits,
-                     __half* __restrict__ gpad8, int* gexp, float* ginv) {
+                     __half* __restrict__ gpadc, int cs, int* gexp, float* ginv) {
   const float m = __int_as_float(amax_bits[0]);
   const int e = m > 0.0f ? min(100, max(-100, 10 - (ilogbf(m) + 1))) : 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -340,8 +342,9 @@ head_bwd_pack_kernel(const float* __restrict__ gout, int B, int K, int H, int W,
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       v[k] = __float2half_rn(k < K ? __ldg(gout + (((long long)bi * K + k) * H + yy) * W + xw) * sc : 0.0f);
-    *reinterpret_cast<uint4*>(gpad8 + (((long long)bi * (H + 2) + yy + 1) * (W + 2) + xw + 1) * 8) =
-        *reinterpret_cast<const uint4*>(v);
+    uint4* dst = reinterpret_cast<uint4*>(gpadc + (((long long)bi * (H + 2) + yy + 1) * (W + 2) + xw + 1) * cs);
+    dst[0] = *reinterpret_cast<const uint4*>(v);
+    for (int c8 = 1; c8 < cs / 8; ++c8) dst[c8] = make_uint4(0u, 0u, 0u, 0u);
   }
 }
 
@@ -479,6 +482,12 @@ struct tvs_train {
   float* ginv = nullptr;     // 2^-s per layer (device scalars for cuBLAS alpha)
   float* fzero = nullptr;
   float* c9 = nullptr;       // 9 x 64 x 64 wgrad GEMM outputs
+  // wgrad on tcgen05 (wgrad_tc.cu; option "wgrad_tc", default on): split-K
+  // partials and the 2-D tensor maps of the gradient / activation buffers
+  int wgrad_tc = 1;
+  float* wpart = nullptr;
+  CUtensorMap gmap;
+  std::vector<CUtensorMap> amaps;
   float eps = 1e-5f;
   bool have_forward = false;
   std::vector<const float*> wv, biasv, gammav, betav;
@@ -533,6 +542,17 @@ void train_ensure_ws(tvs_train* t, int B, int H, int W) {
   TVS_CUDA(cudaMalloc(&t->gpad8, PP * 16));
   TVS_CUDA(cudaMemset(t->gpad8, 0, PP * 16));
   for (int i = 0; i < 2; ++i) TVS_CUDA(cudaMalloc(&t->ga[i], P * 256));
+  t->gmap = tvs::make_wgrad_gmap(t->gpad, (long long)PP);
+  t->amaps.clear();
+  for (int j = 0; j <= nh; ++j) t->amaps.push_back(tvs::make_wgrad_amap(t->apad[j], (long long)PP));
+}
+
+// dW of one conv (rows = its output channels) from the gradient operand in
+// t->gpad and the pair activations a_j (hi halves)
+void wgrad_tc(tvs_train* t, int j, int rows, const float* alpha, float* dw, cudaStream_t st) {
+  const long long PP = (long long)t->B * (t->H + 2) * (t->W + 2);
+  TVS_CUDA(tvs::launch_wgrad_tc(t->gmap, t->amaps[j], PP, (int)t->guard, t->W, rows, alpha, t->wpart, dw, t->num_sms,
+                                st));
 }
 
 int grid_for(long long work, int per_block, int num_sms) {
@@ -594,6 +614,7 @@ int tvs_train_create(int device, int depth, int out_bands, tvs_train** out) {
       TVS_CUDA(cudaMalloc(&t->fzero, sizeof(float)));
       TVS_CUDA(cudaMemset(t->fzero, 0, sizeof(float)));
       TVS_CUDA(cudaMalloc(&t->c9, 9 * 64 * 64 * sizeof(float)));
+      TVS_CUDA(cudaMalloc(&t->wpart, tvs::wgrad_part_bytes(t->num_sms)));
       TVS_CUDA(cudaDeviceSynchronize());
     } catch (...) {
       if (t->blas) cublasDestroy(t->blas);
@@ -694,13 +715,22 @@ int tvs_train_backward(tvs_train* t, const float* g_out, float* const* dw, float
     tvs::head_bwd_reduce_kernel<<<dim3(grid_for((long long)H * W, tvs::kTB * 4, t->num_sms / K + 1), K), tvs::kTB, 0,
                                   st>>>(g_out, B, K, (long long)H * W, t->red + 128, t->amax);
     TVS_CUDA(cudaGetLastError());
-    tvs::head_bwd_pack_kernel<<<grid_for(P, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
-        g_out, B, K, H, W, t->amax, padded0<__half>(t->gpad8, t, 8), t->gexp + nh, t->ginv + nh);
-    TVS_CUDA(cudaGetLastError());
-    wgrad_gemms(t, padded0<__half>(t->gpad8, t, 8), 8, 8, t->apad[nh], t->ginv + nh, st);
-    // the GEMM's M = 8 rows hold bands 0..K-1 (the rest are zero channels)
-    tvs::wgrad_scatter_kernel<<<(K * 64 * 9 + 255) / 256, 256, 0, st>>>(t->c9, 8, K, dw[t->depth - 1]);
-    TVS_CUDA(cudaGetLastError());
+    if (t->wgrad_tc) {
+      // bands as channels 0..K-1 of the 64-channel gradient buffer (zero above;
+      // the hidden layers overwrite its whole interior afterwards)
+      tvs::head_bwd_pack_kernel<<<grid_for(P, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
+          g_out, B, K, H, W, t->amax, padded0<__half>(t->gpad, t, 64), 64, t->gexp + nh, t->ginv + nh);
+      TVS_CUDA(cudaGetLastError());
+      wgrad_tc(t, nh, K, t->ginv + nh, dw[t->depth - 1], st);
+    } else {
+      tvs::head_bwd_pack_kernel<<<grid_for(P, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
+          g_out, B, K, H, W, t->amax, padded0<__half>(t->gpad8, t, 8), 8, t->gexp + nh, t->ginv + nh);
+      TVS_CUDA(cudaGetLastError());
+      wgrad_gemms(t, padded0<__half>(t->gpad8, t, 8), 8, 8, t->apad[nh], t->ginv + nh, st);
+      // the GEMM's M = 8 rows hold bands 0..K-1 (the rest are zero channels)
+      tvs::wgrad_scatter_kernel<<<(K * 64 * 9 + 255) / 256, 256, 0, st>>>(t->c9, 8, K, dw[t->depth - 1]);
+      TVS_CUDA(cudaGetLastError());
+    }
     tvs::head_bias_finish_kernel<<<1, 32, 0, st>>>(t->red + 128, K, dbias[t->depth - 1]);
     tvs::head_dgrad_kernel<<<grid_for(P * 8, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
         g_out, t->wv[t->depth - 1], B, K, H, W, t->ga[0]);
@@ -718,9 +748,13 @@ int tvs_train_backward(tvs_train* t, const float* g_out, float* const* dw, float
           padded0<__half>(t->gpad, t, 64), t->gexp + j, t->ginv + j, dgamma[j], dbeta[j]);
       TVS_CUDA(cudaGetLastError());
       // wgrad: dW_j = sum g_y (x) a_j-1 (hi halves), unscaled by alpha = 2^-s
-      wgrad_gemms(t, padded0<__half>(t->gpad, t, 64), 64, 64, t->apad[j], t->ginv + j, st);
-      tvs::wgrad_scatter_kernel<<<(64 * 64 * 9 + 255) / 256, 256, 0, st>>>(t->c9, 64, 64, dw[j + 1]);
-      TVS_CUDA(cudaGetLastError());
+      if (t->wgrad_tc) {
+        wgrad_tc(t, j, 64, t->ginv + j, dw[j + 1], st);
+      } else {
+        wgrad_gemms(t, padded0<__half>(t->gpad, t, 64), 64, 64, t->apad[j], t->ginv + j, st);
+        tvs::wgrad_scatter_kernel<<<(64 * 64 * 9 + 255) / 256, 256, 0, st>>>(t->c9, 64, 64, dw[j + 1]);
+        TVS_CUDA(cudaGetLastError());
+      }
       // dgrad: g_a_{j-1} = conv(g_y, W^T flipped) on tcgen05, raw fp32 out * 2^-s
       const CUtensorMap m = make_act_map(interior<__half>(t->gpad, t, 64), B, H, W, tvs::kHaloPx, 64, 1);
       tvs::ConvArgs a{};
@@ -747,6 +781,15 @@ int tvs_train_backward(tvs_train* t, const float* g_out, float* const* dw, float
   });
 }
 
+int tvs_train_set_option(tvs_train* t, const char* name, int value) {
+  return guarded([&] {
+    if (!t || !name) throw TvsError(TVS_E_INVALID, "null argument");
+    const std::string k(name);
+    if (k == "wgrad_tc") t->wgrad_tc = value != 0;  // 0: the cuBLAS split-K GEMMs (one per tap)
+    else throw TvsError(TVS_E_INVALID, "unknown training option: " + k);
+  });
+}
+
 int tvs_train_destroy(tvs_train* t) {
   return guarded([&] {
     if (!t) return;
@@ -755,7 +798,7 @@ int tvs_train_destroy(tvs_train* t) {
     train_free_ws(t);
     if (t->blas) cublasDestroy(t->blas);
     void* ptrs[] = {t->wsplit, t->wt, t->hpack, t->ones, t->zero_shift, t->sums, t->red,
-                    t->amax, t->gexp, t->ginv, t->fzero, t->c9};
+                    t->amax, t->gexp, t->ginv, t->fzero, t->c9, t->wpart};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     delete t;

@@ -129,3 +129,25 @@ def test_ragged_shapes_and_forward_backward_pairing():
     m(torch.randn(1, 1, 8, 8, device="cuda"))  # a second forward replaces the plan's saved activations
     with pytest.raises(RuntimeError, match="older forward"):
         out1.sum().backward()
+
+
+@pytest.mark.parametrize("shape", [(2, 32, 32), (3, 37, 150), (1, 5, 7)])
+def test_wgrad_tcgen05_matches_cublas(shape):
+    """The tcgen05 weight-gradient kernel (csrc/wgrad_tc.cu, MN-major operands
+    straight from the pixel-major buffers) against one cuBLAS split-K GEMM per
+    tap (train option wgrad_tc=0): same fp16 operands and fp32 accumulation,
+    only the summation order differs (and tcgen05 truncates its fp32 accumulator
+    once per MMA, tools/probe_mma_rounding.cu): measured <= 2.2e-5, gated at 1e-4."""
+    B, H, W = shape
+    grads = {}
+    for tc in (1, 0):
+        m = TVSpecNet()
+        m.load_state_dict(build_seeded_state())
+        m = m.cuda().train()
+        m._train_plan(0).set_option("wgrad_tc", tc)
+        img, gt, res = (t.cuda() for t in train_batch(seed=7, B=B, H=H, W=W))
+        compute_loss(m(img), gt, img, res, "L").total.backward()
+        grads[tc] = {n: p.grad.detach().cpu().numpy() for n, p in m.named_parameters()}
+    for n, g in grads[1].items():
+        assert np.isfinite(g).all(), n
+        assert _rel(g, grads[0][n]) <= 1e-4, (n, _rel(g, grads[0][n]))
