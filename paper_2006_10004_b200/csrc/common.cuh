@@ -196,6 +196,10 @@ cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* 
 cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int cin = 64,
                                      int co0 = 0, int ci0 = 0);
 cudaError_t launch_pack_hidden_f16_t(const float* w, uint8_t* out, cudaStream_t st);  // training dgrad pack
+// training step: split (forward) + transposed fp16 (dgrad) packs of n hidden layers, one launch per 32 layers
+constexpr int kTrainPackLayers = 32;
+struct TrainPackPtrs { const float* w[kTrainPackLayers]; };
+cudaError_t launch_train_pack_hidden(const float* const* w_dev, int n, uint8_t* wsplit, uint8_t* wt, cudaStream_t st);
 // training wgrad on tcgen05 (wgrad_tc.cu): dW = alpha * sum_p G[p] (x) A[p + tap offset] over the
 // zero-bordered pixel list; `part` holds wgrad_part_bytes(num_sms) of split-K partials
 size_t wgrad_part_bytes(int num_sms);

@@ -1322,16 +1322,18 @@ __global__ void pack_hidden_f16_kernel(const float* __restrict__ w, const float*
 // Training dgrad (mode 0 on gradients): the transposed, flipped filter
 // W'[ci][co][2-ky][2-kx] = W[co][ci][ky][kx] as a mode-0 B pack, plain fp16
 // rounding (the backward tolerates fp16 operands).
-__global__ void pack_hidden_f16_t_kernel(const float* __restrict__ w, uint8_t* __restrict__ out) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*64 + ci of the forward filter
-  if (idx >= kC * kC) return;
-  const int co = idx / kC, ci = idx % kC;
+__device__ __forceinline__ void pack_f16_t_elem(const float* __restrict__ w, uint8_t* __restrict__ out, int idx) {
+  const int co = idx / kC, ci = idx % kC;  // co*64 + ci of the forward filter
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
     const int ky = t / 3, kx = t % 3;
     // output channel ci of the dgrad conv at tap (2-ky, 2-kx): B row (2 - (2-ky))*64 + ci = ky*64 + ci
     put_b(out, ConvCfg<0>::kWdx, 2 - kx, ky * 64 + ci, co, __float2half_rn(w[idx * 9 + t]));
   }
+}
+__global__ void pack_hidden_f16_t_kernel(const float* __restrict__ w, uint8_t* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < kC * kC) pack_f16_t_elem(w, out, idx);
 }
 
 cudaError_t launch_pack_hidden_f16_t(const float* w, uint8_t* out, cudaStream_t st) {
@@ -1398,16 +1400,15 @@ __global__ void pack_head_wide_kernel(const float* __restrict__ w, int K, uint8_
 
 // fp32-accurate hidden pack: W' = W*s (BatchNorm fold, fp32) x 2^8 split into
 // hi = RN16(W'), lo = RN16(W' - hi); pack 0 = hi, pack 1 = lo.
-__global__ void pack_hidden_split_kernel(const float* __restrict__ w, const float* __restrict__ scale,
-                                         uint8_t* __restrict__ out, int cin, int co0, int ci0) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*64 + ci
-  if (idx >= kC * kC) return;
+__device__ __forceinline__ void pack_split_elem(const float* __restrict__ w, const float* __restrict__ scale,
+                                                uint8_t* __restrict__ out, int idx, int cin, int co0, int ci0) {
   const int co = idx / kC, ci = idx % kC;
   const float* wsrc = w + ((size_t)(co0 + co) * cin + ci0 + ci) * 9;
+  const float sc = scale ? scale[co0 + co] : 1.0f;
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
     const int ky = t / 3, kx = t % 3;
-    const float wv = (wsrc[t] * scale[co0 + co]) * kSplitWScale;
+    const float wv = (wsrc[t] * sc) * kSplitWScale;
     const __half hi = __float2half_rn(wv);
     const __half lo = __float2half_rn(wv - __half2float(hi));
     // channel half h = co / 32: rows (2-ky)*32 + co%32 of that half's dx block
@@ -1415,6 +1416,37 @@ __global__ void pack_hidden_split_kernel(const float* __restrict__ w, const floa
     put_b(base, ConvCfg<3>::kWdx, kx, (2 - ky) * 32 + (co & 31), ci, hi);
     put_b(base + ConvCfg<3>::kW1, ConvCfg<3>::kWdx, kx, (2 - ky) * 32 + (co & 31), ci, lo);
   }
+}
+__global__ void pack_hidden_split_kernel(const float* __restrict__ w, const float* __restrict__ scale,
+                                         uint8_t* __restrict__ out, int cin, int co0, int ci0) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*64 + ci
+  if (idx < kC * kC) pack_split_elem(w, scale, out, idx, cin, co0, ci0);
+}
+
+// Training step: the split (forward) and transposed fp16 (dgrad) packs of up
+// to kTrainPackLayers hidden layers in ONE launch (blockIdx.y = layer): 60
+// launches per step became 1 (the step is host-bound at small batches).
+__global__ void train_pack_hidden_kernel(TrainPackPtrs ptrs, uint8_t* __restrict__ wsplit,
+                                         uint8_t* __restrict__ wt) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= kC * kC) return;
+  const float* w = ptrs.w[blockIdx.y];
+  pack_split_elem(w, nullptr, wsplit + (size_t)blockIdx.y * ConvCfg<3>::kW, idx, kC, 0, 0);
+  pack_f16_t_elem(w, wt + (size_t)blockIdx.y * ConvCfg<0>::kW, idx);
+}
+
+cudaError_t launch_train_pack_hidden(const float* const* w_dev, int n, uint8_t* wsplit, uint8_t* wt, cudaStream_t st) {
+  // both packs are written completely (every (co, ci, tap) has its own slot)
+  for (int l0 = 0; l0 < n; l0 += kTrainPackLayers) {
+    TrainPackPtrs ptrs{};
+    const int cnt = std::min(kTrainPackLayers, n - l0);
+    for (int i = 0; i < cnt; ++i) ptrs.w[i] = w_dev[l0 + i];
+    train_pack_hidden_kernel<<<dim3((kC * kC + 127) / 128, cnt), 128, 0, st>>>(
+        ptrs, wsplit + (size_t)l0 * ConvCfg<3>::kW, wt + (size_t)l0 * ConvCfg<0>::kW);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 __global__ void pack_head_f16_kernel(const float* __restrict__ w, int K, uint8_t* __restrict__ out, int cin,

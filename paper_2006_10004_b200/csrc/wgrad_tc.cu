@@ -167,28 +167,32 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap gmap, const __grid_constant_
 }
 
 // dW[co][ci][tap] = alpha * sum_cta part[cta][pair][half*64 + ci][co] for co < rows
-// (tap -> (pair, half): 0-7 -> (tap / 2, tap % 2), 8 -> (4, 1)); one thread per
-// (tap, ci, co), co fastest so the partial reads coalesce.
+// (tap -> (pair, half): 0-7 -> (tap / 2, tap % 2), 8 -> (4, 1)).  A block of
+// 256 threads = 64 output channels (co fastest: the partial reads coalesce) x 4
+// slices of the CTA list; the slices are summed in a fixed order (deterministic).
 __global__ void __launch_bounds__(256)
 wgrad_reduce_kernel(const float* __restrict__ part, int nctas, int rows, const float* __restrict__ alpha,
                     float* __restrict__ dw) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 9 * 64 * 64) return;
-  const int co = i & 63, ci = (i >> 6) & 63, tap = i >> 12;
-  if (co >= rows) return;
+  const int co = threadIdx.x & 63, slice = threadIdx.x >> 6;
+  const int ci = blockIdx.x & 63, tap = blockIdx.x >> 6;
   const int pair = tap < 8 ? tap >> 1 : 4, half = tap < 8 ? (tap & 1) : 1;
   const float* p = part + ((size_t)pair * 128 + half * 64 + ci) * 64 + co;
   const size_t stride = (size_t)wg::kPairs * 128 * 64;
-  float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;  // fixed order: deterministic
-  int c = 0;
-  for (; c + 4 <= nctas; c += 4) {
+  const int per = (nctas + 3) / 4, c0 = slice * per, c1 = min(nctas, c0 + per);
+  float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
+  int c = c0;
+  for (; c + 4 <= c1; c += 4) {
     s0 += p[(size_t)c * stride];
     s1 += p[(size_t)(c + 1) * stride];
     s2 += p[(size_t)(c + 2) * stride];
     s3 += p[(size_t)(c + 3) * stride];
   }
-  for (; c < nctas; ++c) s0 += p[(size_t)c * stride];
-  dw[((size_t)co * 64 + ci) * 9 + tap] = ((s0 + s1) + (s2 + s3)) * __ldg(alpha);
+  for (; c < c1; ++c) s0 += p[(size_t)c * stride];
+  __shared__ float sh[4][64];
+  sh[slice][co] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (slice == 0 && co < rows)
+    dw[((size_t)co * 64 + ci) * 9 + tap] = ((sh[0][co] + sh[1][co]) + (sh[2][co] + sh[3][co])) * __ldg(alpha);
 }
 
 size_t wgrad_part_bytes(int num_sms) { return (size_t)num_sms * wg::kPairs * 128 * 64 * sizeof(float); }
@@ -223,7 +227,7 @@ cudaError_t launch_wgrad_tc(const CUtensorMap& gmap, const CUtensorMap& amap, lo
   wgrad_tc_kernel<<<grid, wg::kThreads, wg::kSmem, st>>>(gmap, amap, PP, guard, W + 2, part);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  wgrad_reduce_kernel<<<(9 * 64 * 64 + 255) / 256, 256, 0, st>>>(part, grid, rows, alpha, dw);
+  wgrad_reduce_kernel<<<9 * 64, 256, 0, st>>>(part, grid, rows, alpha, dw);
   return cudaGetLastError();
 }
 
