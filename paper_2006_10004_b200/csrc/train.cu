@@ -103,24 +103,24 @@ __global__ void __launch_bounds__(kTB) bn_stats_kernel(const float* __restrict__
   const int c4 = threadIdx.x & 15, lane = threadIdx.x >> 4;
   double s1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0};
   const long long step = (long long)gridDim.x * kRedPx;
-  for (long long p0 = (long long)blockIdx.x * kRedPx + lane; p0 < P; p0 += 8 * step) {
+  auto add = [&](const float4& q) {
+    const float e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double d = e[k];
+      s1[k] += d;
+      s2[k] += d * d;
+    }
+  };
+  long long p0 = (long long)blockIdx.x * kRedPx + lane;
+  for (; p0 + 7 * step < P; p0 += 8 * step) {  // eight unpredicated loads in flight
     float4 v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const long long p = p0 + u * step;
-      v[u] = p < P ? __ldg(reinterpret_cast<const float4*>(y + p * 64) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(y + (p0 + u * step) * 64) + c4);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double d = e[k];
-        s1[k] += d;
-        s2[k] += d * d;
-      }
-    }
+    for (int u = 0; u < 8; ++u) add(v[u]);
   }
+  for (; p0 < P; p0 += step) add(__ldg(reinterpret_cast<const float4*>(y + p0 * 64) + c4));
   __shared__ double sh[2][kRedPx][64];
 #pragma unroll
   for (int k = 0; k < 4; ++k) { sh[0][lane][c4 * 4 + k] = s1[k]; sh[1][lane][c4 * 4 + k] = s2[k]; }
@@ -273,7 +273,7 @@ bn_bwd_apply_kernel(const float* __restrict__ ga, const float* __restrict__ y, i
                     const double* sums, const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
                     const double* red, const int* amax_bits, __half* __restrict__ gpad, int* gexp, float* ginv,
                     float* dgamma, float* dbeta) {
-  __shared__ float s_sa[64], s_sb[64], s_k[64], s_m1[64], s_m2[64], s_mean[64], s_rstd[64];
+  __shared__ __align__(16) float s_sa[64], s_sb[64], s_k[64], s_m1[64], s_m2[64], s_mean[64], s_rstd[64];
   __shared__ float s_scale;
   const double n = (double)B * H * W;
   if (threadIdx.x < 64) {
@@ -309,36 +309,37 @@ bn_bwd_apply_kernel(const float* __restrict__ ga, const float* __restrict__ y, i
   __syncthreads();
   const float sc = s_scale;
   const long long P = (long long)B * H * W;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P * 8; i += (long long)gridDim.x * blockDim.x) {
-    const long long p = i >> 3;
-    const int c8 = (int)(i & 7);
-    uint32_t pk[4];
-    const float4 y0 = __ldg(reinterpret_cast<const float4*>(y + p * 64 + c8 * 8));
-    const float4 y1 = __ldg(reinterpret_cast<const float4*>(y + p * 64 + c8 * 8 + 4));
-    const float4 g0 = __ldg(reinterpret_cast<const float4*>(ga + p * 64 + c8 * 8));
-    const float4 g1 = __ldg(reinterpret_cast<const float4*>(ga + p * 64 + c8 * 8 + 4));
-    const float yv[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
-    const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+  // thread = (pixel, 4 channels), as bn_apply_kernel; the channel constants stay in registers
+  const int c4 = threadIdx.x & 15;
+  float csa[4], csb[4], ck[4], cm1[4], cm2[4], cmean[4], crstd[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      float f[2];
+  for (int k = 0; k < 4; ++k) {
+    const int c = c4 * 4 + k;
+    csa[k] = s_sa[c]; csb[k] = s_sb[c]; ck[k] = s_k[c]; cm1[k] = s_m1[c];
+    cm2[k] = s_m2[c]; cmean[k] = s_mean[c]; crstd[k] = s_rstd[c];
+  }
+  for (long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4; p < P;
+       p += ((long long)gridDim.x * blockDim.x) >> 4) {
+    const float4 y4 = __ldg(reinterpret_cast<const float4*>(y + p * 64) + c4);
+    const float4 g4 = __ldg(reinterpret_cast<const float4*>(ga + p * 64) + c4);
+    const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
+    const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+    float f[4];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int c = c8 * 8 + e * 2 + u;
-        const float v = yv[e * 2 + u];
-        const float z = fmaf(s_sa[c], v, s_sb[c]);
-        const float gz = z > 0.0f ? gv[e * 2 + u] : 0.0f;
-        const float yh = (v - s_mean[c]) * s_rstd[c];
-        f[u] = s_k[c] * (gz - s_m1[c] - yh * s_m2[c]) * sc;
-      }
-      const __half2 hh = __floats2half2_rn(f[0], f[1]);
-      pk[e] = *reinterpret_cast<const uint32_t*>(&hh);
+    for (int k = 0; k < 4; ++k) {
+      const float v = yv[k];
+      const float z = fmaf(csa[k], v, csb[k]);
+      const float gz = z > 0.0f ? gv[k] : 0.0f;
+      const float yh = (v - cmean[k]) * crstd[k];
+      f[k] = ck[k] * (gz - cm1[k] - yh * cm2[k]) * sc;
     }
+    const __half2 h01 = __floats2half2_rn(f[0], f[1]), h23 = __floats2half2_rn(f[2], f[3]);
     const int xw = (int)(p % W);
     const long long t = p / W;
     const int yy = (int)(t % H), bi = (int)(t / H);
-    __half* dst = gpad + (((long long)bi * (H + 2) + yy + 1) * (W + 2) + xw + 1) * 64 + c8 * 8;
-    *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    __half* dst = gpad + (((long long)bi * (H + 2) + yy + 1) * (W + 2) + xw + 1) * 64 + c4 * 4;
+    *reinterpret_cast<uint2*>(dst) =
+        make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
   }
 }
 
@@ -403,8 +404,14 @@ head_bwd_pack_kernel(const float* __restrict__ gout, int B, int K, int H, int W,
 __global__ void __launch_bounds__(kTB)
 head_dgrad_kernel(const float* __restrict__ gout, const float* __restrict__ wh, int B, int K, int H, int W,
                   float* __restrict__ ga) {
-  __shared__ float sw[kMaxBands * 64 * 9];
-  for (int i = threadIdx.x; i < K * 64 * 9; i += blockDim.x) sw[i] = wh[i];
+  // [k][tap][ci]: a thread's 8 channels are two 16 B shared loads per (k, tap)
+  // (the [k][ci][tap] global order read 8 scalars at stride 9 with 2-way bank
+  // conflicts: 104 us for 8 x 128 x 128, shared-memory bound)
+  __shared__ __align__(16) float sw[kMaxBands * 9 * 64];
+  for (int i = threadIdx.x; i < K * 64 * 9; i += blockDim.x) {
+    const int tap = i % 9, ci = (i / 9) % 64, k = i / (9 * 64);
+    sw[(k * 9 + tap) * 64 + ci] = wh[i];
+  }
   __syncthreads();
   const long long P = (long long)B * H * W;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P * 8; i += (long long)gridDim.x * blockDim.x) {
@@ -425,8 +432,12 @@ head_dgrad_kernel(const float* __restrict__ gout, const float* __restrict__ wh, 
           const int sx = xw + 1 - kx;
           if (sx < 0 || sx >= W) continue;
           const float gv = __ldg(g + (long long)sy * W + sx);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc[e] = fmaf(sw[(k * 64 + c8 * 8 + e) * 9 + ky * 3 + kx], gv, acc[e]);
+          const float4 w0 = *reinterpret_cast<const float4*>(&sw[(k * 9 + ky * 3 + kx) * 64 + c8 * 8]);
+          const float4 w1 = *reinterpret_cast<const float4*>(&sw[(k * 9 + ky * 3 + kx) * 64 + c8 * 8 + 4]);
+          acc[0] = fmaf(w0.x, gv, acc[0]); acc[1] = fmaf(w0.y, gv, acc[1]);
+          acc[2] = fmaf(w0.z, gv, acc[2]); acc[3] = fmaf(w0.w, gv, acc[3]);
+          acc[4] = fmaf(w1.x, gv, acc[4]); acc[5] = fmaf(w1.y, gv, acc[5]);
+          acc[6] = fmaf(w1.z, gv, acc[6]); acc[7] = fmaf(w1.w, gv, acc[7]);
         }
       }
     }
@@ -441,36 +452,54 @@ head_dgrad_kernel(const float* __restrict__ gout, const float* __restrict__ wh, 
 __global__ void __launch_bounds__(kTB)
 conv0_bwd_kernel(const float* __restrict__ ga, const __half* __restrict__ apad, const float* __restrict__ x, int B,
                  int H, int W, double* acc /*[64][10]*/) {
-  const int c = threadIdx.x & 63, lane = threadIdx.x >> 6;
+  // thread = (4 channels, pixel lane): one 16 B gradient load and one 8 B
+  // activation load per pixel, the 9 image taps shared by the pixel's 16
+  // threads (the one-channel-per-thread walk was latency-bound: 125 us)
+  const int c4 = threadIdx.x & 15, lane = threadIdx.x >> 4;
   const long long P = (long long)B * H * W;
-  float s[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  for (long long p = (long long)blockIdx.x * 4 + lane; p < P; p += (long long)gridDim.x * 4) {
+  float s[4][10];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int j = 0; j < 10; ++j) s[k][j] = 0.0f;
+  for (long long p = (long long)blockIdx.x * kRedPx + lane; p < P; p += (long long)gridDim.x * kRedPx) {
     const int xw = (int)(p % W);
     const long long t = p / W;
     const int yy = (int)(t % H), bi = (int)(t / H);
-    const __half a0 = apad[(((long long)bi * (H + 2) + yy + 1) * (W + 2) + xw + 1) * 128 + c];
-    if (!(__half2float(a0) > 0.0f)) continue;
-    const float gz = __ldg(ga + p * 64 + c);
+    const uint2 a0 = __ldg(reinterpret_cast<const uint2*>(
+        apad + (((long long)bi * (H + 2) + yy + 1) * (W + 2) + xw + 1) * 128 + c4 * 4));
+    const float4 g4 = __ldg(reinterpret_cast<const float4*>(ga + p * 64) + c4);
+    const __half2 h01 = *reinterpret_cast<const __half2*>(&a0.x), h23 = *reinterpret_cast<const __half2*>(&a0.y);
+    const float av[4] = {__low2float(h01), __high2float(h01), __low2float(h23), __high2float(h23)};
+    const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
     const float* img = x + (long long)bi * H * W;
+    float tap[9];
 #pragma unroll
     for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
       for (int kx = 0; kx < 3; ++kx) {
         const int sy = yy + ky - 1, sx = xw + kx - 1;
-        if (sy >= 0 && sy < H && sx >= 0 && sx < W) s[ky * 3 + kx] = fmaf(gz, __ldg(img + (long long)sy * W + sx), s[ky * 3 + kx]);
+        tap[ky * 3 + kx] = (sy >= 0 && sy < H && sx >= 0 && sx < W) ? __ldg(img + (long long)sy * W + sx) : 0.0f;
       }
-    s[9] += gz;
-  }
-  __shared__ float sh[10][kTB];
 #pragma unroll
-  for (int k = 0; k < 10; ++k) sh[k][threadIdx.x] = s[k];
-  __syncthreads();
-  if (lane == 0)
-    for (int k = 0; k < 10; ++k) {
-      double v = 0.0;
-      for (int l = 0; l < 4; ++l) v += sh[k][l * 64 + c];
-      atomicAdd(acc + c * 10 + k, v);
+    for (int k = 0; k < 4; ++k) {
+      const float gz = av[k] > 0.0f ? gv[k] : 0.0f;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) s[k][j] = fmaf(gz, tap[j], s[k][j]);
+      s[k][9] += gz;
     }
+  }
+  __shared__ float sh[kRedPx][64][10];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int j = 0; j < 10; ++j) sh[lane][c4 * 4 + k][j] = s[k][j];
+  __syncthreads();
+  for (int i = threadIdx.x; i < 640; i += blockDim.x) {
+    double v = 0.0;
+    for (int l = 0; l < kRedPx; ++l) v += (&sh[l][0][0])[i];
+    atomicAdd(acc + i, v);
+  }
 }
 
 // wgrad GEMM outputs C_tap (col-major M x 64: element (m, ci) at m + M*ci) ->
@@ -720,9 +749,11 @@ int tvs_train_forward(tvs_train* t, const float* const* w_dev, const float* cons
       a.nshift = 64;
       a.act_out = reinterpret_cast<uint8_t*>(t->y[j]);
       a.raw_f32 = 1;
+      // CTA pairs (conv_tc.cu mode 12 / 13: one output-channel half per CTA of a
+      // cluster, input rows multicast): the fp32 inference mode's faster layout
       const long long total = (long long)B * strips * H;
-      const int grid = (int)std::max(1LL, std::min<long long>(t->num_sms, (total + 2) / 3));
-      TVS_CUDA(tvs::launch_conv_tc(3, m, m, a, grid, st));
+      const int grid = 2 * (int)std::max(1LL, std::min<long long>(t->num_sms / 2, (total + 2) / 3));
+      TVS_CUDA(tvs::launch_conv_tc(12, m, m, a, grid, st));
       tvs::bn_stats_kernel<<<grid_red(P, 8 * tvs::kRedPx, t->num_sms), tvs::kTB, 0, st>>>(t->y[j], P, t->sums + j * 128);
       TVS_CUDA(cudaGetLastError());
       tvs::bn_apply_kernel<<<grid_for(P * 8, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
@@ -795,7 +826,7 @@ int tvs_train_backward(tvs_train* t, const float* g_out, float* const* dw, float
       tvs::bn_bwd_reduce_kernel<<<grid_red(P, 4 * tvs::kRedPx, t->num_sms), tvs::kTB, 0, st>>>(
           t->ga[cur], t->y[j], P, t->sums + j * 128, t->gammav[j], t->betav[j], t->eps, t->red, t->amax);
       TVS_CUDA(cudaGetLastError());
-      tvs::bn_bwd_apply_kernel<<<grid_for(P * 8, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
+      tvs::bn_bwd_apply_kernel<<<grid_for(P * 16, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
           t->ga[cur], t->y[j], B, H, W, t->sums + j * 128, t->gammav[j], t->betav[j], t->eps, t->red, t->amax,
           padded0<__half>(t->gpad, t, 64), t->gexp + j, t->ginv + j, dgamma[j], dbeta[j]);
       TVS_CUDA(cudaGetLastError());
@@ -825,7 +856,7 @@ int tvs_train_backward(tvs_train* t, const float* g_out, float* const* dw, float
     // ---- conv0
     double* acc0 = t->red + 136;
     TVS_CUDA(cudaMemsetAsync(acc0, 0, 640 * sizeof(double), st));
-    tvs::conv0_bwd_kernel<<<grid_for(P, 4 * 64, t->num_sms), tvs::kTB, 0, st>>>(
+    tvs::conv0_bwd_kernel<<<grid_red(P, 8 * tvs::kRedPx, t->num_sms), tvs::kTB, 0, st>>>(
         t->ga[cur], padded0<__half>(t->apad[0], t, 128), t->x, B, H, W, acc0);
     TVS_CUDA(cudaGetLastError());
     tvs::conv0_grad_finish_kernel<<<1, 64, 0, st>>>(acc0, dw[0], dbias[0]);

@@ -9,7 +9,7 @@ rows = [r for r in csv.reader(l for l in open(sys.argv[1]) if l.startswith('"'))
 h = rows[0]
 ki, vi = h.index("Kernel Name"), h.index("Metric Value")
 rows = rows[1:]
-start = [i for i, r in enumerate(rows) if "train_conv0_kernel" in r[ki]][-1] - 31  # the step's weight packs come first
+start = [i for i, r in enumerate(rows) if "train_pack_hidden_kernel" in r[ki]][-1]
 agg, tot = collections.OrderedDict(), 0.0
 for r in rows[start:]:
     k, v = r[ki][:60], float(r[vi])
