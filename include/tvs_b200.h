@@ -178,6 +178,26 @@ int tvs_train_backward(tvs_train* plan, const float* g_out, float* const* dw, fl
 int tvs_train_set_option(tvs_train* plan, const char* name, int value);
 int tvs_train_destroy(tvs_train* plan);
 
+/* Training losses: replaces compute_loss (tvsurrogate
+ * losses.py:54-129) and its autograd graph inside _epoch_pass (training.py:51-53).
+ * pred, gt: DEVICE (B,K,H,W) fp32; image, residual: DEVICE (B,1,H,W) fp32 (only
+ * read for the sum constraint).  terms: bit 0 = sum constraint (selectors L1 /
+ * L3), bit 1 = gradient Huber (L2 / L3); huber_delta = losses.HUBER_DELTA.
+ * tvs_loss_sums writes
+ *   sums   DEVICE B*K*4 + B*2 doubles: per (b,k) [gt energy, residual energy,
+ *          Huber numerator, Huber denominator], then per b [reconstruction
+ *          error, image energy]
+ *   values DEVICE 8 floats: [0] total [1] mse [2] sum term [3] gradient term
+ *          [4] zero-energy bands skipped [5] zero-gradient bands skipped
+ *          [6] bands with energy (0 -> the reference raises ValueError)
+ * tvs_loss_grad writes grad_pred = *g_total (DEVICE scalar) * d total / d pred
+ * from the same sums.  Both run on the caller's current device. */
+int tvs_loss_sums(const float* pred, const float* gt, const float* image, const float* residual, int B, int K, int H,
+                  int W, int terms, float huber_delta, double* sums, float* values, void* stream);
+int tvs_loss_grad(const float* pred, const float* gt, const float* image, const float* residual, int B, int K, int H,
+                  int W, int terms, float huber_delta, const double* sums, const float* g_total, float* grad_pred,
+                  void* stream);
+
 /* Band scoring statistics (spectv metrics.py:28-237), fp64.
  * gt, pred: DEVICE (planes, H, W) fp32.  stats: DEVICE planes x 8 doubles:
  *   [0] sum (gt - pred)^2           -> PSNR / MSE   (metrics.py:28-37)

@@ -54,6 +54,8 @@ EXPORTS = (
     "tvs_train_backward",
     "tvs_train_set_option",
     "tvs_train_destroy",
+    "tvs_loss_sums",
+    "tvs_loss_grad",
 )
 
 _lock = threading.Lock()
@@ -131,6 +133,10 @@ def load() -> ctypes.CDLL:
         lib.tvs_train_set_option.argtypes = [P, ctypes.c_char_p, ctypes.c_int]
         lib.tvs_train_destroy.restype = i
         lib.tvs_train_destroy.argtypes = [P]
+        lib.tvs_loss_sums.restype = i
+        lib.tvs_loss_sums.argtypes = [P, P, P, P, i, i, i, i, i, ctypes.c_float, P, P, P]
+        lib.tvs_loss_grad.restype = i
+        lib.tvs_loss_grad.argtypes = [P, P, P, P, i, i, i, i, i, ctypes.c_float, P, P, P, P]
         lib.tvs_plan_destroy.restype = i
         lib.tvs_plan_destroy.argtypes = [P]
         _lib = lib

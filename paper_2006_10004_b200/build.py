@@ -20,7 +20,7 @@ LIB = PKG / "libtvsb200.so"
 # diagnostics build (--trace): the layer-stack row timeline compiled in
 # (conv_tc.cu TVS_STACK_TRACE); tools/stack_trace.py loads it via TVS_LIB
 TRACE_LIB = PKG / "libtvsb200_trace.so"
-SOURCES = ["tvs_api.cu", "conv_tc.cu", "conv0_tc.cu", "conv_edge.cu", "metrics.cu", "tvflow.cu", "train.cu", "wgrad_tc.cu"]
+SOURCES = ["tvs_api.cu", "conv_tc.cu", "conv0_tc.cu", "conv_edge.cu", "metrics.cu", "tvflow.cu", "train.cu", "wgrad_tc.cu", "loss.cu"]
 HEADERS = ["common.cuh", "sm100.cuh", "host_util.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

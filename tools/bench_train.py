@@ -4,7 +4,10 @@ backward, Adam step; TrainConfig batch_size 8) through the drop-in's train()
 mode on B200, against the same step of the CPU oracle module (torch autograd,
 all host threads) on the same batch.
 
-    python tools/bench_train.py [--size 128] [--batch 8] [--steps 20] [--cpu-steps 2]
+    python tools/bench_train.py [--size 128] [--batch 8] [--steps 20] [--cpu-steps 2] [--loss fused|torch]
+
+--loss torch runs the GPU arm with the reference's own torch-op loss on CUDA
+tensors instead of the fused drop-in (paper_2006_10004_b200.losses).
 
 Prints one JSON line: steps/s and MP/s (pixels trained per second) for both.
 """
@@ -17,9 +20,10 @@ from pathlib import Path
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-from oracle.train_oracle import compute_loss, train_batch  # noqa: E402
+from oracle.train_oracle import compute_loss as oracle_loss, train_batch  # noqa: E402
 from oracle.tvspecnet_oracle import build_seeded_state, oracle_from_state  # noqa: E402
 from paper_2006_10004_b200 import TVSpecNet  # noqa: E402
+from paper_2006_10004_b200.losses import compute_loss as fused_loss  # noqa: E402
 
 flags = {sys.argv[i]: sys.argv[i + 1] for i in range(1, len(sys.argv) - 1) if sys.argv[i].startswith("--")}
 S = int(flags.get("--size", 128))
@@ -29,7 +33,10 @@ cpu_steps = int(flags.get("--cpu-steps", 2))
 state = build_seeded_state()
 
 
-def run(model, dev, n, warm):
+loss_kind = flags.get("--loss", "fused")
+
+
+def run(model, dev, n, warm, compute_loss):
     opt = torch.optim.Adam(model.parameters(), lr=1e-3)
     img, gt, res = (t.to(dev) for t in train_batch(seed=3, B=B, H=S, W=S))
     loss = None
@@ -50,14 +57,14 @@ def run(model, dev, n, warm):
 
 m = TVSpecNet()
 m.load_state_dict(state)
-t_gpu, loss_gpu = run(m.cuda().train(), "cuda", steps, 3)
+t_gpu, loss_gpu = run(m.cuda().train(), "cuda", steps, 3, fused_loss if loss_kind == "fused" else oracle_loss)
 torch.set_num_threads(os.cpu_count() or 1)
-t_cpu, loss_cpu = run(oracle_from_state(state).train(), "cpu", cpu_steps, 1)
+t_cpu, loss_cpu = run(oracle_from_state(state).train(), "cpu", cpu_steps, 1, oracle_loss)
 px = B * S * S / 1e6
 print(json.dumps({
     "metric": "TVSpecNET training step (forward + compute_loss + backward + Adam)", "unit": "steps/s",
     "value": round(1.0 / t_gpu, 2), "ms_per_step": round(t_gpu * 1e3, 3), "mp_per_s": round(px / t_gpu, 2),
-    "batch": B, "size": [S, S], "steps": steps, "selector": "L", "last_loss": loss_gpu,
+    "batch": B, "size": [S, S], "steps": steps, "selector": "L", "loss": loss_kind, "last_loss": loss_gpu,
     "reference_flow": {"value": round(1.0 / t_cpu, 4), "unit": "steps/s", "ms_per_step": round(t_cpu * 1e3, 1),
                        "mp_per_s": round(px / t_cpu, 4), "steps": cpu_steps, "cores": torch.get_num_threads(),
                        "last_loss": loss_cpu,
