@@ -554,8 +554,12 @@ struct tvs_train {
   void* gpad8 = nullptr;     // head gradient operand [B][H+2][W+2][8] (+ guards)
   float* ga[2] = {nullptr, nullptr};
   double* sums = nullptr;    // (depth-2) x 128 batch sums
-  double* red = nullptr;     // 128 BN-backward sums + 8 head bias + 640 conv0
-  int* amax = nullptr;       // 2 ints (float bits) + 1
+  // backward reductions, zeroed by ONE memset per step (they share an allocation):
+  // red = [8 head bias | 640 conv0 | 128 BN-backward sums per hidden layer] doubles,
+  // amax = [2 head | 2 per hidden layer] ints (float bits)
+  double* red = nullptr;
+  int* amax = nullptr;
+  size_t red_bytes = 0;
   int* gexp = nullptr;
   float* ginv = nullptr;     // 2^-s per layer (device scalars for cuBLAS alpha)
   float* fzero = nullptr;
@@ -691,8 +695,9 @@ int tvs_train_create(int device, int depth, int out_bands, tvs_train** out) {
       tvs::fill_ones_kernel<<<1, 64>>>(t->ones, 64);
       TVS_CUDA(cudaGetLastError());
       TVS_CUDA(cudaMalloc(&t->sums, (size_t)nh * 128 * sizeof(double)));
-      TVS_CUDA(cudaMalloc(&t->red, (128 + 8 + 640) * sizeof(double)));
-      TVS_CUDA(cudaMalloc(&t->amax, 4 * sizeof(int)));
+      t->red_bytes = (size_t)(8 + 640 + 128 * nh) * sizeof(double) + (size_t)(2 + 2 * nh) * sizeof(int);
+      TVS_CUDA(cudaMalloc(&t->red, t->red_bytes));
+      t->amax = reinterpret_cast<int*>(t->red + 8 + 640 + 128 * nh);
       TVS_CUDA(cudaMalloc(&t->gexp, (depth + 1) * sizeof(int)));
       TVS_CUDA(cudaMalloc(&t->ginv, (depth + 1) * sizeof(float)));
       TVS_CUDA(cudaMalloc(&t->fzero, sizeof(float)));
@@ -793,10 +798,13 @@ int tvs_train_backward(tvs_train* t, const float* g_out, float* const* dw, float
     const long long P = (long long)B * H * W;
     const int strips = (W + tvs::kStripPx - 1) / tvs::kStripPx;
     // ---- head: bias grad, fp16 gradient operand, wgrad GEMM, dgrad (CUDA cores)
-    TVS_CUDA(cudaMemsetAsync(t->red, 0, (128 + 8 + 640) * sizeof(double), st));
-    TVS_CUDA(cudaMemsetAsync(t->amax, 0, 4 * sizeof(int), st));
+    TVS_CUDA(cudaMemsetAsync(t->red, 0, t->red_bytes, st));  // every reduction slot of this backward
+    double* red_head = t->red;                // 8 head-bias sums
+    double* acc0 = t->red + 8;                // 640 conv0 sums
+    double* red_bn = t->red + 8 + 640;        // 128 per hidden layer
+    int* amax_bn = t->amax + 2;               // 2 per hidden layer
     tvs::head_bwd_reduce_kernel<<<dim3(grid_for((long long)H * W, tvs::kTB * 4, t->num_sms / K + 1), K), tvs::kTB, 0,
-                                  st>>>(g_out, B, K, (long long)H * W, t->red + 128, t->amax);
+                                  st>>>(g_out, B, K, (long long)H * W, red_head, t->amax);
     TVS_CUDA(cudaGetLastError());
     if (t->wgrad_tc) {
       // bands as channels 0..K-1 of the 64-channel gradient buffer (zero above;
@@ -814,20 +822,20 @@ int tvs_train_backward(tvs_train* t, const float* g_out, float* const* dw, float
       tvs::wgrad_scatter_kernel<<<(K * 64 * 9 + 255) / 256, 256, 0, st>>>(t->c9, 8, K, dw[t->depth - 1]);
       TVS_CUDA(cudaGetLastError());
     }
-    tvs::head_bias_finish_kernel<<<1, 32, 0, st>>>(t->red + 128, K, dbias[t->depth - 1]);
+    tvs::head_bias_finish_kernel<<<1, 32, 0, st>>>(red_head, K, dbias[t->depth - 1]);
     tvs::head_dgrad_kernel<<<grid_for(P * 8, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
         g_out, t->wv[t->depth - 1], B, K, H, W, t->ga[0]);
     TVS_CUDA(cudaGetLastError());
     int cur = 0;
     // ---- hidden layers, top down
     for (int j = nh - 1; j >= 0; --j) {
-      TVS_CUDA(cudaMemsetAsync(t->red, 0, 128 * sizeof(double), st));
-      TVS_CUDA(cudaMemsetAsync(t->amax, 0, 2 * sizeof(int), st));
       tvs::bn_bwd_reduce_kernel<<<grid_red(P, 4 * tvs::kRedPx, t->num_sms), tvs::kTB, 0, st>>>(
-          t->ga[cur], t->y[j], P, t->sums + j * 128, t->gammav[j], t->betav[j], t->eps, t->red, t->amax);
+          t->ga[cur], t->y[j], P, t->sums + j * 128, t->gammav[j], t->betav[j], t->eps, red_bn + j * 128,
+          amax_bn + j * 2);
       TVS_CUDA(cudaGetLastError());
       tvs::bn_bwd_apply_kernel<<<grid_for(P * 16, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
-          t->ga[cur], t->y[j], B, H, W, t->sums + j * 128, t->gammav[j], t->betav[j], t->eps, t->red, t->amax,
+          t->ga[cur], t->y[j], B, H, W, t->sums + j * 128, t->gammav[j], t->betav[j], t->eps, red_bn + j * 128,
+          amax_bn + j * 2,
           padded0<__half>(t->gpad, t, 64), t->gexp + j, t->ginv + j, dgamma[j], dbeta[j]);
       TVS_CUDA(cudaGetLastError());
       // wgrad: dW_j = sum g_y (x) a_j-1 (hi halves), unscaled by alpha = 2^-s
@@ -854,8 +862,6 @@ int tvs_train_backward(tvs_train* t, const float* g_out, float* const* dw, float
       cur ^= 1;
     }
     // ---- conv0
-    double* acc0 = t->red + 136;
-    TVS_CUDA(cudaMemsetAsync(acc0, 0, 640 * sizeof(double), st));
     tvs::conv0_bwd_kernel<<<grid_red(P, 8 * tvs::kRedPx, t->num_sms), tvs::kTB, 0, st>>>(
         t->ga[cur], padded0<__half>(t->apad[0], t, 128), t->x, B, H, W, acc0);
     TVS_CUDA(cudaGetLastError());
@@ -881,7 +887,7 @@ int tvs_train_destroy(tvs_train* t) {
     train_free_ws(t);
     if (t->blas) cublasDestroy(t->blas);
     void* ptrs[] = {t->wsplit, t->wt, t->hpack, t->ones, t->zero_shift, t->sums, t->red,
-                    t->amax, t->gexp, t->ginv, t->fzero, t->c9, t->wpart};
+                    t->gexp, t->ginv, t->fzero, t->c9, t->wpart};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     delete t;
