@@ -463,6 +463,11 @@ def run_ours(args, spec):
         line["fp32_mode_cuda_cores"] = {"value": round(r["value"], 3), "unit": UNIT,
                                         "ms_per_step": round(r["ms"], 3), "steps": r["steps"],
                                         "note": "TVS_FP32_CUDA=1: fp32 FFMA + fp64 combine kernels"}
+    if world == 1 and args.train_steps > 0 and str(args.config) == "2":
+        try:
+            line["train_step"] = train_step_leg(state, args.train_steps)
+        except Exception as e:  # never lose the bench line to the extra leg
+            line["train_step"] = {"error": f"{type(e).__name__}: {e}"[:200]}
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         mp_s, secs = cpu_reference(spec, 1, 0, spec.batch, threads, budget_s=args.cpu_seconds)
@@ -474,6 +479,40 @@ def run_ours(args, spec):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def train_step_leg(state, steps, B=8, S=128):
+    """SURVEY §8(f) row 4 beside the inference line: one _epoch_pass iteration
+    (training.py:45-61: zero_grad, model(img), compute_loss, backward, Adam step,
+    loss read) through the drop-in's train() mode and fused losses, at the
+    reference's batch size 8 on seeded synthetic 128 x 128 crops."""
+    from paper_2006_10004_b200 import TVSpecNet
+    from paper_2006_10004_b200.losses import compute_loss
+
+    m = TVSpecNet()
+    m.load_state_dict(state)
+    m = m.cuda().train()
+    opt = torch.optim.Adam(m.parameters(), lr=1e-3)
+    g = torch.Generator().manual_seed(3)
+    gt = torch.randn(B, 5, S, S, generator=g).cuda()
+    res = (0.1 * torch.randn(B, 1, S, S, generator=g)).cuda()
+    img = gt.sum(1, keepdim=True) + res
+    warm = 3
+    for it in range(warm + steps):
+        if it == warm:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+        opt.zero_grad(set_to_none=True)
+        v = compute_loss(m(img), gt, img, res, "L")
+        v.total.backward()
+        opt.step()
+        loss = float(v.total.detach())
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": round(1.0 / dt, 2), "unit": "steps/s", "ms_per_step": round(dt * 1e3, 3), "batch": B,
+            "size": [S, S], "steps": steps, "selector": "L", "last_loss": round(loss, 6),
+            "note": "forward (batch-stat BN, split tcgen05 convs) + fused loss + backward (tcgen05 dgrad/wgrad) + "
+                    "Adam, wall clock incl. the per-step loss read; tools/bench_train.py times the CPU flow beside it"}
 
 
 def main():
@@ -494,6 +533,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-max-images", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--train-steps", type=int, default=10, help="steps of the training-step leg (0 = skip)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps
