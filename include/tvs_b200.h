@@ -174,7 +174,9 @@ int tvs_train_backward(tvs_train* plan, const float* g_out, float* const* dw, fl
                        float* const* dgamma, float* const* dbeta, void* stream);
 /* Training options (the train-plan counterpart of tvs_plan_set_option):
  *   "wgrad_tc"  1 (default) weight gradients on the tcgen05 kernel (wgrad_tc.cu),
- *               0 one cuBLAS split-K GEMM per filter tap. */
+ *               0 one cuBLAS split-K GEMM per filter tap.
+ *   "head_dgrad_tc" 1 (default) the head's input gradient on the hidden layers'
+ *               tcgen05 dgrad kernel (fp16 operands), 0 the fp32 CUDA-core kernel. */
 int tvs_train_set_option(tvs_train* plan, const char* name, int value);
 int tvs_train_destroy(tvs_train* plan);
 

@@ -196,6 +196,7 @@ cudaError_t launch_pack_hidden_f16(const float* w, const float* scale, uint8_t* 
 cudaError_t launch_pack_hidden_split(const float* w, const float* scale, uint8_t* out, cudaStream_t st, int cin = 64,
                                      int co0 = 0, int ci0 = 0);
 cudaError_t launch_pack_hidden_f16_t(const float* w, uint8_t* out, cudaStream_t st);  // training dgrad pack
+cudaError_t launch_pack_head_f16_t(const float* w, int K, uint8_t* out, cudaStream_t st);  // training head dgrad pack
 // training step: split (forward) + transposed fp16 (dgrad) packs of n hidden layers, one launch per 32 layers
 constexpr int kTrainPackLayers = 32;
 struct TrainPackPtrs { const float* w[kTrainPackLayers]; };

@@ -1336,6 +1336,26 @@ __global__ void pack_hidden_f16_t_kernel(const float* __restrict__ w, uint8_t* _
   if (idx < kC * kC) pack_f16_t_elem(w, out, idx);
 }
 
+// Training head dgrad: the head filter W_h[k][ci][3][3] (k < K bands) as a
+// 64 x 64 transposed pack with zero rows for k >= K, so the head's input
+// gradient runs on the same tcgen05 dgrad kernel as the hidden layers (the
+// gradient operand holds the bands in channels 0..K-1 of a 64-channel buffer)
+__global__ void pack_head_f16_t_kernel(const float* __restrict__ w, int K, uint8_t* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // co*64 + ci, co = band
+  if (idx >= kC * kC) return;
+  const int co = idx / kC, ci = idx % kC;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int ky = t / 3, kx = t % 3;
+    const float v = co < K ? w[idx * 9 + t] : 0.0f;
+    put_b(out, ConvCfg<0>::kWdx, 2 - kx, ky * 64 + ci, co, __float2half_rn(v));
+  }
+}
+cudaError_t launch_pack_head_f16_t(const float* w, int K, uint8_t* out, cudaStream_t st) {
+  pack_head_f16_t_kernel<<<(kC * kC + 127) / 128, 128, 0, st>>>(w, K, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pack_hidden_f16_t(const float* w, uint8_t* out, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(out, 0, ConvCfg<0>::kW, st);
   if (e != cudaSuccess) return e;

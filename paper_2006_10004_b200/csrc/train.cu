@@ -543,6 +543,7 @@ struct tvs_train {
   uint8_t* wsplit = nullptr;
   uint8_t* wt = nullptr;
   uint8_t* hpack = nullptr;
+  uint8_t* wt_head = nullptr;  // head filter as a transposed 64 x 64 dgrad pack (zero rows above out_bands)
   float* ones = nullptr;
   float* zero_shift = nullptr;
   // per-shape workspace
@@ -567,6 +568,7 @@ struct tvs_train {
   // wgrad on tcgen05 (wgrad_tc.cu; option "wgrad_tc", default on): split-K
   // partials and the 2-D tensor maps of the gradient / activation buffers
   int wgrad_tc = 1;
+  int head_dgrad_tc = 1;  // head input gradient on the tcgen05 dgrad kernel (needs wgrad_tc's 64-channel operand)
   float* wpart = nullptr;
   CUtensorMap gmap;
   std::vector<CUtensorMap> amaps;
@@ -689,6 +691,7 @@ int tvs_train_create(int device, int depth, int out_bands, tvs_train** out) {
       TVS_CUDA(cudaMalloc(&t->wsplit, (size_t)nh * tvs::conv_wpack_split_bytes()));
       TVS_CUDA(cudaMalloc(&t->wt, (size_t)nh * tvs::conv_wpack_bytes(false)));
       TVS_CUDA(cudaMalloc(&t->hpack, tvs::conv_wpack_bytes(true)));
+      TVS_CUDA(cudaMalloc(&t->wt_head, tvs::conv_wpack_bytes(false)));
       TVS_CUDA(cudaMalloc(&t->ones, 64 * sizeof(float)));
       TVS_CUDA(cudaMalloc(&t->zero_shift, 64 * sizeof(float)));
       TVS_CUDA(cudaMemset(t->zero_shift, 0, 64 * sizeof(float)));
@@ -739,6 +742,7 @@ int tvs_train_forward(tvs_train* t, const float* const* w_dev, const float* cons
     // this step's weight packs
     TVS_CUDA(tvs::launch_train_pack_hidden(w_dev + 1, nh, t->wsplit, t->wt, st));
     TVS_CUDA(tvs::launch_pack_head_f16(w_dev[t->depth - 1], t->out_bands, t->hpack, st));
+    TVS_CUDA(tvs::launch_pack_head_f16_t(w_dev[t->depth - 1], t->out_bands, t->wt_head, st));
     const long long P = (long long)B * H * W;
     tvs::train_conv0_kernel<<<(unsigned)((P + tvs::kTB - 1) / tvs::kTB), tvs::kTB, 0, st>>>(
         x, w_dev[0], bias_dev[0], B, H, W, padded0<__half>(t->apad[0], t, 128));
@@ -823,9 +827,27 @@ int tvs_train_backward(tvs_train* t, const float* g_out, float* const* dw, float
       TVS_CUDA(cudaGetLastError());
     }
     tvs::head_bias_finish_kernel<<<1, 32, 0, st>>>(red_head, K, dbias[t->depth - 1]);
-    tvs::head_dgrad_kernel<<<grid_for(P * 8, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
-        g_out, t->wv[t->depth - 1], B, K, H, W, t->ga[0]);
-    TVS_CUDA(cudaGetLastError());
+    if (t->wgrad_tc && t->head_dgrad_tc) {
+      // head dgrad on the hidden layers' tcgen05 dgrad kernel: the gradient buffer
+      // holds the scaled fp16 bands in channels 0..K-1 (zero above), the filter
+      // pack has zero rows above K (the CUDA-core kernel below took 109 us, this 22)
+      const CUtensorMap m = make_act_map(interior<__half>(t->gpad, t, 64), B, H, W, tvs::kHaloPx, 64, 1);
+      tvs::ConvArgs a{};
+      a.B = B; a.H = H; a.W = W; a.strips = strips; a.row0 = 0; a.rows = H;
+      a.wpack = t->wt_head;
+      a.shift = t->zero_shift;
+      a.nshift = 64;
+      a.act_out = reinterpret_cast<uint8_t*>(t->ga[0]);
+      a.raw_f32 = 1;
+      a.out_exp = t->gexp + nh;
+      const long long total = (long long)B * strips * H;
+      const int grid = (int)std::max(1LL, std::min<long long>(t->num_sms, (total + 2) / 3));
+      TVS_CUDA(tvs::launch_conv_tc(0, m, m, a, grid, st));
+    } else {
+      tvs::head_dgrad_kernel<<<grid_for(P * 8, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
+          g_out, t->wv[t->depth - 1], B, K, H, W, t->ga[0]);
+      TVS_CUDA(cudaGetLastError());
+    }
     int cur = 0;
     // ---- hidden layers, top down
     for (int j = nh - 1; j >= 0; --j) {
@@ -875,6 +897,7 @@ int tvs_train_set_option(tvs_train* t, const char* name, int value) {
     if (!t || !name) throw TvsError(TVS_E_INVALID, "null argument");
     const std::string k(name);
     if (k == "wgrad_tc") t->wgrad_tc = value != 0;  // 0: the cuBLAS split-K GEMMs (one per tap)
+    else if (k == "head_dgrad_tc") t->head_dgrad_tc = value != 0;  // 0: the fp32 CUDA-core head dgrad
     else throw TvsError(TVS_E_INVALID, "unknown training option: " + k);
   });
 }
@@ -886,7 +909,7 @@ int tvs_train_destroy(tvs_train* t) {
     cudaDeviceSynchronize();
     train_free_ws(t);
     if (t->blas) cublasDestroy(t->blas);
-    void* ptrs[] = {t->wsplit, t->wt, t->hpack, t->ones, t->zero_shift, t->sums, t->red,
+    void* ptrs[] = {t->wsplit, t->wt, t->hpack, t->wt_head, t->ones, t->zero_shift, t->sums, t->red,
                     t->gexp, t->ginv, t->fzero, t->c9, t->wpart};
     for (void* p : ptrs)
       if (p) cudaFree(p);

@@ -145,9 +145,31 @@ def test_wgrad_tcgen05_matches_cublas(shape):
         m.load_state_dict(build_seeded_state())
         m = m.cuda().train()
         m._train_plan(0).set_option("wgrad_tc", tc)
+        m._train_plan(0).set_option("head_dgrad_tc", 0)  # same fp32 head dgrad in both arms
         img, gt, res = (t.cuda() for t in train_batch(seed=7, B=B, H=H, W=W))
         compute_loss(m(img), gt, img, res, "L").total.backward()
         grads[tc] = {n: p.grad.detach().cpu().numpy() for n, p in m.named_parameters()}
     for n, g in grads[1].items():
         assert np.isfinite(g).all(), n
         assert _rel(g, grads[0][n]) <= 1e-4, (n, _rel(g, grads[0][n]))
+
+
+def test_head_dgrad_on_tcgen05_stays_inside_the_fp16_backward_budget(gold):
+    """The head's input gradient on the hidden layers' tcgen05 dgrad kernel
+    (fp16 operands, train option head_dgrad_tc, default) against the fp32
+    CUDA-core kernel: both within the gradient gate of the fp64 step, and the
+    two apart by no more than the fp16-backward budget (9.7e-4
+    emulated for fp16 backward operands)."""
+    worst = {}
+    grads = {}
+    for tc in (1, 0):
+        m = TVSpecNet()
+        m.load_state_dict(build_seeded_state())
+        m = m.cuda().train()
+        m._train_plan(0).set_option("head_dgrad_tc", tc)
+        _step(m, "L3", "cuda")
+        grads[tc] = {n: p.grad.detach().cpu().numpy() for n, p in m.named_parameters()}
+        worst[tc] = max(_rel(g, gold[f"grad64_{n}"]) for n, g in grads[tc].items())
+    print(f"worst gradient rel-L2 vs fp64: tcgen05 head dgrad {worst[1]:.3e}, CUDA-core {worst[0]:.3e}")
+    assert worst[1] <= GRAD_TOL and worst[0] <= GRAD_TOL
+    assert max(_rel(g, grads[0][n]) for n, g in grads[1].items()) <= 5e-3
