@@ -59,14 +59,16 @@ m = TVSpecNet()
 m.load_state_dict(state)
 t_gpu, loss_gpu = run(m.cuda().train(), "cuda", steps, 3, fused_loss if loss_kind == "fused" else oracle_loss)
 torch.set_num_threads(os.cpu_count() or 1)
-t_cpu, loss_cpu = run(oracle_from_state(state).train(), "cpu", cpu_steps, 1, oracle_loss)
 px = B * S * S / 1e6
+ref = None
+if cpu_steps > 0:  # --cpu-steps 0: GPU arm only
+    t_cpu, loss_cpu = run(oracle_from_state(state).train(), "cpu", cpu_steps, 1, oracle_loss)
+    ref = {"value": round(1.0 / t_cpu, 4), "unit": "steps/s", "ms_per_step": round(t_cpu * 1e3, 1),
+           "mp_per_s": round(px / t_cpu, 4), "steps": cpu_steps, "cores": torch.get_num_threads(),
+           "last_loss": loss_cpu, "note": "CPU oracle module (torch autograd fp32), same batch, same loop"}
 print(json.dumps({
     "metric": "TVSpecNET training step (forward + compute_loss + backward + Adam)", "unit": "steps/s",
     "value": round(1.0 / t_gpu, 2), "ms_per_step": round(t_gpu * 1e3, 3), "mp_per_s": round(px / t_gpu, 2),
     "batch": B, "size": [S, S], "steps": steps, "selector": "L", "loss": loss_kind, "last_loss": loss_gpu,
-    "reference_flow": {"value": round(1.0 / t_cpu, 4), "unit": "steps/s", "ms_per_step": round(t_cpu * 1e3, 1),
-                       "mp_per_s": round(px / t_cpu, 4), "steps": cpu_steps, "cores": torch.get_num_threads(),
-                       "last_loss": loss_cpu,
-                       "note": "CPU oracle module (torch autograd fp32), same batch, same loop"},
+    "reference_flow": ref,
 }))
