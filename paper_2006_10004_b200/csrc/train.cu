@@ -14,9 +14,13 @@
 //   * dgrad convs run the fp16 tcgen05 hidden kernel (mode 0, raw fp32
 //     output) on per-layer power-of-two-scaled fp16 gradients and the
 //     transposed, flipped fp16 filters;
-//   * wgrad is a plain GEMM over pixels on zero-bordered fp16 buffers (see
-//     Layout) through cuBLAS, one per tap;
-//   * conv0 and head backward, BatchNorm backward: CUDA cores, fp32/fp64.
+//   * wgrad is a GEMM over pixels on zero-bordered fp16 buffers (see Layout):
+//     one tcgen05 launch per layer with MN-major operands (wgrad_tc.cu); the
+//     first version, one cuBLAS split-K GEMM per tap, stays behind the train
+//     option wgrad_tc = 0 as the A/B reference;
+//   * the head's input gradient runs on the same tcgen05 dgrad kernel (bands
+//     as channels 0..K-1 of the 64-channel gradient operand);
+//   * conv0 backward and BatchNorm backward: CUDA cores, fp32/fp64.
 //
 // Layout.  Activations a_j (j = 0..depth-2) are stored as fp16 hi/lo pairs
 // [B][H+2][W+2][128] with a zero border and `guard` zero pixels before and
