@@ -361,7 +361,10 @@ class TVSpecNet(nn.Module):
         out = torch.empty((B, K, nrows, W), dtype=torch.float32, pin_memory=True)
         cout = torch.empty((B, 1, nrows, W), dtype=torch.float32, pin_memory=True) if closure else None
         idx = dev.index
-        if isinstance(self.host_chunks, (list, tuple)):
+        nb = self._host_row_bands(B, H, W, row0, nrows, closure)
+        if nb > 1:
+            sizes = [B]
+        elif isinstance(self.host_chunks, (list, tuple)):
             w = [float(v) for v in self.host_chunks]
             cuts = [0] + [round(B * sum(w[:i + 1]) / sum(w)) for i in range(len(w))]
             sizes = [cuts[i + 1] - cuts[i] for i in range(len(w)) if cuts[i + 1] > cuts[i]]
@@ -377,7 +380,11 @@ class TVSpecNet(nn.Module):
             sizes = cache[skey]
         # sub-batch forwards report their status at the final plan.sync (one
         # synchronisation instead of one per sub-batch)
-        run = self._single if len(sizes) == 1 else self._pipeline
+        if nb > 1:
+            def run(plan, x_pin, out, cout, sizes, dev, closure, row0, nrows):
+                return self._pipeline_rows(plan, x_pin, out, cout, dev, closure, nb)
+        else:
+            run = self._single if len(sizes) == 1 else self._pipeline
         if self._options.get("check", 1) == 1:
             plan.set_option("check", 2)
             try:
@@ -385,6 +392,93 @@ class TVSpecNet(nn.Module):
             finally:
                 plan.set_option("check", 1)
         return run(plan, x_pin, out, cout, sizes, dev, closure, row0, nrows)
+
+    # single large image from the host: number of row bands of the band pipeline
+    # (None = automatic, 0 / 1 = off)
+    host_row_bands = None
+
+    def _host_row_bands(self, B: int, H: int, W: int, row0: int, nrows: int, closure: bool) -> int:
+        """Row bands for one large host image (config 3's shape): the D2H of a
+        1024 x 1024 result (24 MB, 0.45 ms) is half of its forward, and a batch
+        of one has no other sub-batch to hide it behind.  Two (four for >= 6 MP)
+        bands with a `depth`-row halo (recomputed) flow through the
+        same three streams as sub-batches do."""
+        if B != 1 or row0 != 0 or nrows != H or self.unshuffle != 1:
+            return 1
+        if self.host_row_bands is not None:
+            return max(1, min(int(self.host_row_bands), H))
+        out_bytes = 4 * (self.out_bands + (1 if closure else 0)) * H * W
+        if out_bytes <= (16 << 20) or H < 512:
+            return 1
+        # few, large bands: every band pays a forward's fixed costs (measured:
+        # 1024^2 1.50 ms whole, 1.43 in 2 bands, 1.53 in 4; 2048^2 5.60 / 4.89 /
+        # 4.97; one 2160 x 3840 frame 9.48 in 2, 9.25 in 4, 10.3 in 8)
+        return 4 if H * W >= (6 << 20) else 2
+
+    def _pipeline_rows(self, plan, x_pin, out, cout, dev, closure, nbands):
+        """One image as `nbands` row bands: band i's input rows (with halo) go
+        H2D while band i-1 computes and band i-2's result goes D2H.  Each band
+        is the forward of the halo-extended slice with a valid-row window
+        (shard.row_bands), bitwise equal to the rows of the whole-image
+        forward for in-range inputs (the per-image power-of-two input scale is
+        chosen per band for inputs outside [2^-6, 64])."""
+        from .shard import row_bands
+
+        _, _, H, W = x_pin.shape
+        K = self.out_bands
+        bands = row_bands(H, nbands, self.depth)
+        hmax = max(b.src1 - b.src0 for b in bands)
+        rmax = max(b.rows for b in bands)
+        idx = dev.index
+        with torch.cuda.device(dev):
+            comp = torch.cuda.current_stream(dev)
+            pipes = self.__dict__.setdefault("_row_pipes", {})
+            pk = (hmax, rmax, K, W, closure)
+            pipe = pipes.get(idx)
+            if pipe is None or pipe["key"] != pk:
+                old = pipe
+                pipe = {"key": pk,
+                        "h2d": old["h2d"] if old else torch.cuda.Stream(dev),
+                        "d2h": old["d2h"] if old else torch.cuda.Stream(dev),
+                        "xbuf": [torch.empty((hmax, W), device=dev) for _ in range(2)],
+                        "bbuf": [torch.empty((K, rmax, W), device=dev) for _ in range(2)],
+                        "cbuf": [torch.empty((rmax, W), device=dev) if closure else None for _ in range(2)],
+                        "events": []}
+                pipes[idx] = pipe
+            h2d, d2h = pipe["h2d"], pipe["d2h"]
+            evs = pipe["events"]
+            while len(evs) < 4 + 2 * len(bands):
+                evs.append(torch.cuda.Event())
+            x_free, b_free = evs[0:2], evs[2:4]
+            for ev in x_free + b_free:
+                ev.record(comp)
+            for i, b in enumerate(bands):
+                j, hb = i % 2, b.src1 - b.src0
+                xb = pipe["xbuf"][j].view(-1)[: hb * W].view(hb, W)
+                ob = pipe["bbuf"][j].view(-1)[: K * b.rows * W].view(K, b.rows, W)
+                cb = pipe["cbuf"][j].view(-1)[: b.rows * W].view(b.rows, W) if closure else None
+                h2d.wait_event(x_free[j])
+                with torch.cuda.stream(h2d):
+                    xb.copy_(x_pin[0, 0, b.src0:b.src1], non_blocking=True)
+                landed = evs[4 + 2 * i]
+                landed.record(h2d)
+                comp.wait_event(landed)
+                comp.wait_event(b_free[j])
+                plan.forward(xb.data_ptr(), ob.data_ptr(), cb.data_ptr() if closure else 0, 1, hb, W,
+                             b.valid_row0, b.rows, comp.cuda_stream)
+                done = evs[5 + 2 * i]
+                done.record(comp)
+                x_free[j].record(comp)
+                d2h.wait_event(done)
+                with torch.cuda.stream(d2h):
+                    for k in range(K):  # contiguous row blocks of each band plane
+                        out[0, k, b.out0:b.out1].copy_(ob[k], non_blocking=True)
+                    if closure:
+                        cout[0, 0, b.out0:b.out1].copy_(cb, non_blocking=True)
+                b_free[j].record(d2h)
+            d2h.synchronize()
+            plan.sync(comp.cuda_stream)
+        return out, cout
 
     def _single(self, plan, x_pin, out, cout, sizes, dev, closure, row0, nrows):
         """One sub-batch (batch 1, the reference's predict_bands pattern): H2D,

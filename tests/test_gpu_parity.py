@@ -572,3 +572,26 @@ def test_fp32_cta_pairs_bitwise(seeded_state, shape):
         with torch.no_grad():
             outs.append(m(x))
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("prec", ["fast", "fp32"])
+def test_host_row_band_pipeline_bitwise(prec):
+    """One large host image runs as row bands with `depth`-row halos through
+    the H2D / compute / D2H streams (model._pipeline_rows): bitwise equal to
+    the whole-image forward, closure plane included; automatic for config 3's
+    shape, off for small results and batches."""
+    m = TVSpecNet(precision=prec).eval()
+    m.load_state_dict(build_seeded_state())
+    x = torch.rand(1, 1, 300, 260, generator=torch.Generator().manual_seed(9))
+    m.host_row_bands = 0
+    b0, c0 = m.forward_planes(x, closure=True)
+    for nb in (2, 3, 7):
+        m.host_row_bands = nb
+        b1, c1 = m.forward_planes(x, closure=True)
+        assert torch.equal(b0, b1) and torch.equal(c0, c1), nb
+    m.host_row_bands = None
+    assert m._host_row_bands(1, 1024, 1024, 0, 1024, False) == 2
+    assert m._host_row_bands(1, 2160, 3840, 0, 2160, False) == 4
+    assert m._host_row_bands(1, 256, 256, 0, 256, False) == 1
+    assert m._host_row_bands(2, 1024, 1024, 0, 1024, False) == 1
+    assert m._host_row_bands(1, 1024, 1024, 0, 512, False) == 1
