@@ -1007,16 +1007,34 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           __syncwarp();
           if (lane == 0) mbar_arrive(&slot_empty[slot]);
           if (!Cfg::kStack && a.raw_f32) {  // training dgrad: raw fp32 accumulator, unscaled
-            if (xg < a.W) {
-              const float m = a.out_exp ? pow2i(-__ldg(a.out_exp)) : 1.0f;
-              float* dst = reinterpret_cast<float*>(a.act_out) + (((long long)g.b * a.H + q) * a.W + xg) * 64;
+            // The lane's 64 fp32 channels go out through the warp's 4 KB staging
+            // tile in two halves of 32 channels, transposed so that every store
+            // instruction writes whole 128-byte lines (4 pixels x 32 channels);
+            // per-lane 256 B rows cost 32 partial sectors per instruction and made
+            // this epilogue 2.6x slower per pixel than the inference layer's TMA store.
+            const float m = a.out_exp ? pow2i(-__ldg(a.out_exp)) : 1.0f;
+            float* row = reinterpret_cast<float*>(a.act_out) +
+                         (((long long)g.b * a.H + q) * a.W + g.x0 + quarter * 32) * 64;  // pixel 0 of this warp
 #pragma unroll
-              for (int c4 = 0; c4 < 16; ++c4)
-                *reinterpret_cast<float4*>(dst + c4 * 4) =
-                    make_float4(__uint_as_float(v[c4 >> 2][(c4 & 3) * 4]) * m,
-                                __uint_as_float(v[c4 >> 2][(c4 & 3) * 4 + 1]) * m,
-                                __uint_as_float(v[c4 >> 2][(c4 & 3) * 4 + 2]) * m,
-                                __uint_as_float(v[c4 >> 2][(c4 & 3) * 4 + 3]) * m);
+            for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {  // 16-byte chunk c of the lane's 128-byte half row, XOR-swizzled
+                const int j = hf * 2 + (c >> 2), i0 = (c & 3) * 4;
+                st_shared_v4(stage_out + lane * 128 + ((c ^ (lane & 7)) << 4),
+                             __float_as_uint(__uint_as_float(v[j][i0]) * m),
+                             __float_as_uint(__uint_as_float(v[j][i0 + 1]) * m),
+                             __float_as_uint(__uint_as_float(v[j][i0 + 2]) * m),
+                             __float_as_uint(__uint_as_float(v[j][i0 + 3]) * m));
+              }
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {  // 4 pixels x 128 B per instruction
+                const int pp = i * 4 + (lane >> 3), c = lane & 7;
+                const float4 t = ld_shared_f4(stage_out + pp * 128 + ((c ^ (pp & 7)) << 4));
+                if (g.x0 + quarter * 32 + pp < a.W)
+                  *reinterpret_cast<float4*>(row + (long long)pp * 64 + hf * 32 + c * 4) = t;
+              }
+              __syncwarp();
             }
             continue;
           }
