@@ -176,7 +176,9 @@ int tvs_train_backward(tvs_train* plan, const float* g_out, float* const* dw, fl
  *   "wgrad_tc"  1 (default) weight gradients on the tcgen05 kernel (wgrad_tc.cu),
  *               0 one cuBLAS split-K GEMM per filter tap.
  *   "head_dgrad_tc" 1 (default) the head's input gradient on the hidden layers'
- *               tcgen05 dgrad kernel (fp16 operands), 0 the fp32 CUDA-core kernel. */
+ *               tcgen05 dgrad kernel (fp16 operands), 0 the fp32 CUDA-core kernel.
+ *   "bn_fused"  1 (default) BatchNorm's batch sums come from the forward conv's
+ *               epilogue, 0 from a separate pass over the conv output. */
 int tvs_train_set_option(tvs_train* plan, const char* name, int value);
 int tvs_train_destroy(tvs_train* plan);
 

@@ -132,6 +132,11 @@ struct ConvArgs {
   // `bands` (the first block's partial output)
   const float* acc_in;
   int acc_bands;
+  // training forward (mode 13, raw_f32): per-channel batch sums of the raw
+  // output, [0, 64) sum y and [64, 128) sum y^2 (fp64, zeroed by the host): the
+  // epilogue reduces each row across the warp's 32 pixels and every lane
+  // carries one channel, so BatchNorm's statistics need no pass over y
+  double* bn_sums;
   unsigned long long watchdog_ns;  // layer stack: give up a row-flag wait after this long
   KernelSpan* span;                // null, or accumulate this launch's device duration
   // TVS_CONV_DBG / plan option "debug" (results invalid except kDbgWithholdFlag,

@@ -813,6 +813,7 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
     const uint32_t shift_u = smem_u32(sShift);
     if (!kHead && !Cfg::kSplit && !Cfg::kWide && lane == 0) prefetch_tmap(&tm_out);
     uint32_t seq = 0, gsel = 0;  // gsel = seq % kGroups
+    double bn_s1 = 0.0, bn_s2 = 0.0;  // training forward (mode 13): this lane's channel, sum y and sum y^2
     int grp_key = -1;            // layer stack: (image, layer) whose scaled shift sShiftG[grp] holds
     const uint32_t shift_g = smem_u32(&sShiftG[Cfg::kStack ? grp : 0][0]);
     Iter it(a, Cfg::kVisits, Cfg::kParts);
@@ -933,20 +934,54 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
           const int ndy = (q > 0 ? 1 : 0) + 1 + (q + 1 < a.H ? 1 : 0);
           const float kDb = 1.0f + 0.5f * 0.7213f * 3.0f * 1.1920929e-7f * (float)ndy;
           if (Cfg::kAux && a.raw_f32) {  // training forward: pre-BatchNorm conv output, fp32
-            if (xg < a.W) {
-              float* dst = reinterpret_cast<float*>(a.act_out) + (((long long)g.b * a.H + q) * a.W + xg) * 64 + hh * 32;
+            const bool inside = xg < a.W;
+            float* dst = reinterpret_cast<float*>(a.act_out) + (((long long)g.b * a.H + q) * a.W + xg) * 64 + hh * 32;
 #pragma unroll
-              for (int c4 = 0; c4 < 8; ++c4) {
-                float f[4];
+            for (int c8 = 0; c8 < 4; ++c8) {
+              float f[8];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                  const int ch = c4 * 4 + t;
-                  const float z = fmaf(__uint_as_float(e[ch >> 4][ch & 15]), kDb,
-                                       fmaf(__uint_as_float(o[ch >> 4][ch & 15]), kDb,
-                                            __uint_as_float(c[ch >> 4][ch & 15])));
-                  f[t] = z * (1.0f / kSplitWScale);
+              for (int t = 0; t < 8; ++t) {
+                const int ch = c8 * 8 + t;
+                const float z = fmaf(__uint_as_float(e[ch >> 4][ch & 15]), kDb,
+                                     fmaf(__uint_as_float(o[ch >> 4][ch & 15]), kDb,
+                                          __uint_as_float(c[ch >> 4][ch & 15])));
+                f[t] = z * (1.0f / kSplitWScale);
+              }
+              if (inside) {
+                *reinterpret_cast<float4*>(dst + c8 * 8) = make_float4(f[0], f[1], f[2], f[3]);
+                *reinterpret_cast<float4*>(dst + c8 * 8 + 4) = make_float4(f[4], f[5], f[6], f[7]);
+              }
+              if (Cfg::kPairH && a.bn_sums) {
+                // batch statistics: sum and sum of squares of these 8 channels over
+                // the warp's 32 pixels.  A transposing butterfly (4 + 2 + 1 exchanges
+                // inside groups of 8 lanes, then two across the groups) leaves the
+                // 32-pixel sums of channel 8*c8 + lane % 8 in every lane; the lanes
+                // of group c8 add them to their fp64 accumulator (lane = channel).
+                float s1[8], s2[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                  s1[t] = inside ? f[t] : 0.0f;
+                  s2[t] = s1[t] * s1[t];
                 }
-                *reinterpret_cast<float4*>(dst + c4 * 4) = make_float4(f[0], f[1], f[2], f[3]);
+#pragma unroll
+                for (int off = 4; off >= 1; off >>= 1) {
+                  const bool up = lane & off;
+#pragma unroll
+                  for (int i = 0; i < off; ++i) {
+                    const float k1 = up ? s1[i + off] : s1[i], g1 = up ? s1[i] : s1[i + off];
+                    const float k2 = up ? s2[i + off] : s2[i], g2 = up ? s2[i] : s2[i + off];
+                    s1[i] = k1 + __shfl_xor_sync(0xffffffffu, g1, off);
+                    s2[i] = k2 + __shfl_xor_sync(0xffffffffu, g2, off);
+                  }
+                }
+                s1[0] += __shfl_xor_sync(0xffffffffu, s1[0], 8);
+                s2[0] += __shfl_xor_sync(0xffffffffu, s2[0], 8);
+                s1[0] += __shfl_xor_sync(0xffffffffu, s1[0], 16);
+                s2[0] += __shfl_xor_sync(0xffffffffu, s2[0], 16);
+                if ((lane >> 3) == c8) {
+                  bn_s1 += (double)s1[0];
+                  bn_s2 += (double)s2[0];
+                }
               }
             }
             continue;
@@ -1246,6 +1281,12 @@ conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_consta
       }
     }
     if (!kHead && !Cfg::kSplit && !Cfg::kWide && lane == 0) bulk_wait<0>();
+    if constexpr (Cfg::kAux && Cfg::kPairH) {
+      if (a.raw_f32 && a.bn_sums) {  // lane = channel 32 * half + lane of this CTA's output-channel half
+        atomicAdd(a.bn_sums + pair_rank * 32 + lane, bn_s1);
+        atomicAdd(a.bn_sums + 64 + pair_rank * 32 + lane, bn_s2);
+      }
+    }
   }
 
   tc_fence_before();

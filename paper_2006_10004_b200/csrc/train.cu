@@ -574,6 +574,7 @@ struct tvs_train {
   // wgrad on tcgen05 (wgrad_tc.cu; option "wgrad_tc", default on): split-K
   // partials and the 2-D tensor maps of the gradient / activation buffers
   int wgrad_tc = 1;
+  int bn_fused = 1;       // batch statistics summed in the forward conv's epilogue (0: bn_stats_kernel pass)
   int head_dgrad_tc = 1;  // head input gradient on the tcgen05 dgrad kernel (needs wgrad_tc's 64-channel operand)
   float* wpart = nullptr;
   CUtensorMap gmap;
@@ -768,9 +769,13 @@ int tvs_train_forward(tvs_train* t, const float* const* w_dev, const float* cons
       // cluster, input rows multicast): the fp32 inference mode's faster layout
       const long long total = (long long)B * strips * H;
       const int grid = 2 * (int)std::max(1LL, std::min<long long>(t->num_sms / 2, (total + 2) / 3));
+      if (t->bn_fused) a.bn_sums = t->sums + j * 128;
       TVS_CUDA(tvs::launch_conv_tc(12, m, m, a, grid, st));
-      tvs::bn_stats_kernel<<<grid_red(P, 8 * tvs::kRedPx, t->num_sms), tvs::kTB, 0, st>>>(t->y[j], P, t->sums + j * 128);
-      TVS_CUDA(cudaGetLastError());
+      if (!t->bn_fused) {
+        tvs::bn_stats_kernel<<<grid_red(P, 8 * tvs::kRedPx, t->num_sms), tvs::kTB, 0, st>>>(t->y[j], P,
+                                                                                            t->sums + j * 128);
+        TVS_CUDA(cudaGetLastError());
+      }
       tvs::bn_apply_kernel<<<grid_for(P * 8, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
           t->y[j], B, H, W, t->sums + j * 128, gamma_dev[j], beta_dev[j], eps, padded0<__half>(t->apad[j + 1], t, 128),
           mean_out + j * 64, var_out + j * 64);
@@ -904,6 +909,7 @@ int tvs_train_set_option(tvs_train* t, const char* name, int value) {
     const std::string k(name);
     if (k == "wgrad_tc") t->wgrad_tc = value != 0;  // 0: the cuBLAS split-K GEMMs (one per tap)
     else if (k == "head_dgrad_tc") t->head_dgrad_tc = value != 0;  // 0: the fp32 CUDA-core head dgrad
+    else if (k == "bn_fused") t->bn_fused = value != 0;  // 0: batch statistics by a separate pass over y
     else throw TvsError(TVS_E_INVALID, "unknown training option: " + k);
   });
 }

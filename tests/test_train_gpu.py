@@ -173,3 +173,35 @@ def test_head_dgrad_on_tcgen05_stays_inside_the_fp16_backward_budget(gold):
     print(f"worst gradient rel-L2 vs fp64: tcgen05 head dgrad {worst[1]:.3e}, CUDA-core {worst[0]:.3e}")
     assert worst[1] <= GRAD_TOL and worst[0] <= GRAD_TOL
     assert max(_rel(g, grads[0][n]) for n, g in grads[1].items()) <= 5e-3
+
+
+@pytest.mark.parametrize("shape", [(2, 32, 32), (3, 37, 150), (1, 5, 7), (2, 1, 1)])
+def test_fused_batch_statistics_match_the_separate_pass(shape):
+    """BatchNorm's batch sums from the forward conv's epilogue (train option
+    bn_fused, default) against the separate pass over the conv output: same
+    values summed in a different order (fp32 over a warp's 32 pixels, then
+    fp64), so outputs, running statistics and gradients agree closely."""
+    B, H, W = shape
+    res = {}
+    for fused in (1, 0):
+        m = TVSpecNet()
+        m.load_state_dict(build_seeded_state())
+        m = m.cuda().train()
+        m._train_plan(0).set_option("bn_fused", fused)
+        img, gt, r = (t.cuda() for t in train_batch(seed=8, B=B, H=H, W=W))
+        out = m(img)
+        compute_loss(out, gt, img, r, "L").total.backward()
+        bns = [mod for mod in m.modules() if isinstance(mod, torch.nn.BatchNorm2d)]
+        res[fused] = (out.detach().cpu().numpy(), [bn.running_var.cpu().numpy() for bn in bns],
+                      {n: p.grad.detach().cpu().numpy() for n, p in m.named_parameters()})
+    np.testing.assert_allclose(res[1][1][0], res[0][1][0], rtol=1e-5, atol=1e-7)  # first layer: same input
+    if B * H * W <= 2:
+        # two samples per channel: the normalised values are +-1 whatever the data and the
+        # variance is rounding noise, so later layers amplify last-bit differences
+        assert np.isfinite(res[1][0]).all()
+        return
+    assert _rel(res[1][0], res[0][0]) <= 1e-5  # measured 1.5-2.1e-6
+    for a, b in zip(res[1][1], res[0][1]):
+        np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-6)
+    for n, g in res[1][2].items():
+        assert _rel(g, res[0][2][n]) <= 2e-3, (n, _rel(g, res[0][2][n]))

@@ -5,6 +5,7 @@ mode on B200, against the same step of the CPU oracle module (torch autograd,
 all host threads) on the same batch.
 
     python tools/bench_train.py [--size 128] [--batch 8] [--steps 20] [--cpu-steps 2] [--loss fused|torch]
+                                [--train-opts bn_fused=0,...]
 
 --loss torch runs the GPU arm with the reference's own torch-op loss on CUDA
 tensors instead of the fused drop-in (paper_2006_10004_b200.losses).
@@ -57,6 +58,9 @@ def run(model, dev, n, warm, compute_loss):
 
 m = TVSpecNet()
 m.load_state_dict(state)
+for kv in filter(None, flags.get("--train-opts", "").split(",")):  # e.g. --train-opts bn_fused=0,wgrad_tc=0
+    name, val = kv.split("=")
+    m._train_plan(0).set_option(name, int(val))
 t_gpu, loss_gpu = run(m.cuda().train(), "cuda", steps, 3, fused_loss if loss_kind == "fused" else oracle_loss)
 torch.set_num_threads(os.cpu_count() or 1)
 px = B * S * S / 1e6
