@@ -198,6 +198,9 @@ wgrad_reduce_kernel(const float* __restrict__ part, int nctas, int rows, const f
 size_t wgrad_part_bytes(int num_sms) { return (size_t)num_sms * wg::kPairs * 128 * 64 * sizeof(float); }
 
 // [rows][row_halves] fp16 pixel-major buffer as a 2-D tensor map over its first 64 channels
+// (L2 promotion 128 B: the activation rows are 256 B (hi | lo) of which only the hi
+// half is read; 256 B promotion fetched the lo halves too, 415 instead of 276 MB
+// per layer at 64 x 128^2 in a kernel that runs at HBM speed)
 CUtensorMap make_wgrad_map(const void* base, long long rows, int row_halves, int box_rows) {
   CUtensorMap m;
   cuuint64_t dims[2] = {64, (cuuint64_t)rows};
@@ -206,7 +209,7 @@ CUtensorMap make_wgrad_map(const void* base, long long rows, int row_halves, int
   cuuint32_t estr[2] = {1, 1};
   CUresult r = tvs_host::get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides,
                                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw tvs_host::TvsError(TVS_E_CUDA, "cuTensorMapEncodeTiled (wgrad) failed: " + std::to_string((int)r));
   return m;
