@@ -124,6 +124,7 @@ class TVSpecNet(nn.Module):
         state["_plans"] = {}
         state["_train_plans"] = {}
         state.pop("_wk_cache", None)
+        state.pop("_train_stage", None)
         return state
 
     def _train_plan(self, idx: int):
