@@ -125,6 +125,7 @@ class TVSpecNet(nn.Module):
         state["_train_plans"] = {}
         state.pop("_wk_cache", None)
         state.pop("_train_stage", None)
+        state.pop("_train_layers", None)
         return state
 
     def _train_plan(self, idx: int):

@@ -26,11 +26,16 @@ from . import _native
 
 
 def _layers(model):
-    """(conv0, [(conv_j, bn_j)], head) of the reference body layout."""
-    mods = list(model.body)
-    convs = [m for m in mods if isinstance(m, nn.Conv2d)]
-    bns = [m for m in mods if isinstance(m, nn.BatchNorm2d)]
-    return convs[0], list(zip(convs[1:-1], bns)), convs[-1]
+    """(conv0, [(conv_j, bn_j)], head) of the reference body layout (cached per
+    module list: the walk is ~50 us and a step asks three times)."""
+    mods = tuple(model.body._modules.values())
+    cache = model.__dict__.get("_train_layers")
+    if cache is None or cache[0] != mods:
+        convs = [m for m in mods if isinstance(m, nn.Conv2d)]
+        bns = [m for m in mods if isinstance(m, nn.BatchNorm2d)]
+        cache = (mods, (convs[0], list(zip(convs[1:-1], bns)), convs[-1]))
+        model.__dict__["_train_layers"] = cache
+    return cache[1]
 
 
 def train_params(model) -> list[torch.Tensor]:
