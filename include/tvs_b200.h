@@ -177,6 +177,8 @@ int tvs_train_backward(tvs_train* plan, const float* g_out, float* const* dw, fl
  *               0 one cuBLAS split-K GEMM per filter tap.
  *   "head_dgrad_tc" 1 (default) the head's input gradient on the hidden layers'
  *               tcgen05 dgrad kernel (fp16 operands), 0 the fp32 CUDA-core kernel.
+ *   "bn_bwd_fused" 1 (default) BatchNorm backward's reduction and apply passes in
+ *               one cooperative launch, 0 two kernels.
  *   "bn_fused"  1 (default) BatchNorm's batch sums come from the forward conv's
  *               epilogue, 0 from a separate pass over the conv output. */
 int tvs_train_set_option(tvs_train* plan, const char* name, int value);

@@ -32,6 +32,7 @@
 // exact tap sum.  Pre-BN conv outputs y_j are fp32 [B][H][W][64].
 #include <cublas_v2.h>
 #include <cuda.h>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -208,10 +209,10 @@ bn_apply_kernel(const float* __restrict__ y, int B, int H, int W, const double* 
 // g_z = g_a * [z > 0] with z = gamma*yhat + beta recomputed exactly as the
 // forward did; S1[c] = sum g_z, S2[c] = sum g_z * yhat (fp64), and the
 // amax of |g_z| and |yhat| (as float bits) for the fp16 scale of pass 2.
-__global__ void __launch_bounds__(kTB)
-bn_bwd_reduce_kernel(const float* __restrict__ ga, const float* __restrict__ y, long long P, const double* sums,
-                     const float* __restrict__ gamma, const float* __restrict__ beta, float eps, double* red,
-                     int* amax_bits) {
+__device__ __forceinline__ void
+bn_bwd_reduce_body(const float* __restrict__ ga, const float* __restrict__ y, long long P, const double* sums,
+                   const float* __restrict__ gamma, const float* __restrict__ beta, float eps, double* red,
+                   int* amax_bits) {
   // thread = (4 channels, pixel lane), four pixels in flight (see bn_stats_kernel)
   const int c4 = threadIdx.x & 15, lane = threadIdx.x >> 4;
   float mean[4], rstd[4], sa[4], sb[4];
@@ -274,11 +275,11 @@ bn_bwd_reduce_kernel(const float* __restrict__ ga, const float* __restrict__ y, 
 // into the zero-bordered gradient buffer [B][H+2][W+2][64]; s puts a bound of
 // |g_y| near 2^10 (no overflow in the dgrad conv's fp16 operand, full fp16
 // precision).  Block 0 exports dgamma = S2, dbeta = S1, s and 2^-s.
-__global__ void __launch_bounds__(kTB)
-bn_bwd_apply_kernel(const float* __restrict__ ga, const float* __restrict__ y, int B, int H, int W,
-                    const double* sums, const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
-                    const double* red, const int* amax_bits, __half* __restrict__ gpad, int* gexp, float* ginv,
-                    float* dgamma, float* dbeta) {
+__device__ __forceinline__ void
+bn_bwd_apply_body(const float* __restrict__ ga, const float* __restrict__ y, int B, int H, int W,
+                  const double* sums, const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+                  const double* red, const int* amax_bits, __half* __restrict__ gpad, int* gexp, float* ginv,
+                  float* dgamma, float* dbeta) {
   __shared__ __align__(16) float s_sa[64], s_sb[64], s_k[64], s_m1[64], s_m2[64], s_mean[64], s_rstd[64];
   __shared__ float s_scale;
   const double n = (double)B * H * W;
@@ -347,6 +348,34 @@ bn_bwd_apply_kernel(const float* __restrict__ ga, const float* __restrict__ y, i
     *reinterpret_cast<uint2*>(dst) =
         make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
   }
+}
+
+__global__ void __launch_bounds__(kTB)
+bn_bwd_reduce_kernel(const float* __restrict__ ga, const float* __restrict__ y, long long P, const double* sums,
+                     const float* __restrict__ gamma, const float* __restrict__ beta, float eps, double* red,
+                     int* amax_bits) {
+  bn_bwd_reduce_body(ga, y, P, sums, gamma, beta, eps, red, amax_bits);
+}
+__global__ void __launch_bounds__(kTB)
+bn_bwd_apply_kernel(const float* __restrict__ ga, const float* __restrict__ y, int B, int H, int W,
+                    const double* sums, const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+                    const double* red, const int* amax_bits, __half* __restrict__ gpad, int* gexp, float* ginv,
+                    float* dgamma, float* dbeta) {
+  bn_bwd_apply_body(ga, y, B, H, W, sums, gamma, beta, eps, red, amax_bits, gpad, gexp, ginv, dgamma, dbeta);
+}
+// Both passes in one cooperative launch: the grid-wide barrier replaces the
+// kernel boundary, and the second read of ga and y comes from L2 when the
+// layer fits (33 MB each at 8 x 128^2).  Launched with
+// cudaLaunchCooperativeKernel on a co-resident grid (tvs_train_backward).
+__global__ void __launch_bounds__(kTB)
+bn_bwd_fused_kernel(const float* __restrict__ ga, const float* __restrict__ y, int B, int H, int W,
+                    const double* sums, const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+                    double* red, int* amax_bits, __half* __restrict__ gpad, int* gexp, float* ginv, float* dgamma,
+                    float* dbeta) {
+  bn_bwd_reduce_body(ga, y, (long long)B * H * W, sums, gamma, beta, eps, red, amax_bits);
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+  bn_bwd_apply_body(ga, y, B, H, W, sums, gamma, beta, eps, red, amax_bits, gpad, gexp, ginv, dgamma, dbeta);
 }
 
 // Head backward, pass 1: dbias[k] = sum g_out[k] (fp64) and amax |g_out|.
@@ -574,6 +603,8 @@ struct tvs_train {
   // wgrad on tcgen05 (wgrad_tc.cu; option "wgrad_tc", default on): split-K
   // partials and the 2-D tensor maps of the gradient / activation buffers
   int wgrad_tc = 1;
+  int bn_bwd_fused = 1;   // BatchNorm backward's two passes in one cooperative launch (0: two kernels)
+  int bn_bwd_coop_blocks = 0;  // co-resident blocks of bn_bwd_fused_kernel on this device (0: unknown yet)
   int bn_fused = 1;       // batch statistics summed in the forward conv's epilogue (0: bn_stats_kernel pass)
   int head_dgrad_tc = 1;  // head input gradient on the tcgen05 dgrad kernel (needs wgrad_tc's 64-channel operand)
   float* wpart = nullptr;
@@ -862,7 +893,37 @@ int tvs_train_backward(tvs_train* t, const float* g_out, float* const* dw, float
     int cur = 0;
     // ---- hidden layers, top down
     for (int j = nh - 1; j >= 0; --j) {
-      tvs::bn_bwd_reduce_kernel<<<grid_red(P, 4 * tvs::kRedPx, t->num_sms), tvs::kTB, 0, st>>>(
+      const int red_grid = grid_red(P, 4 * tvs::kRedPx, t->num_sms);
+      if (t->bn_bwd_fused && t->bn_bwd_coop_blocks == 0) {
+        int per_sm = 0;
+        TVS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tvs::bn_bwd_fused_kernel, tvs::kTB, 0));
+        t->bn_bwd_coop_blocks = std::max(1, per_sm * t->num_sms);
+      }
+      // one cooperative launch while ga and y (512 B per pixel) stay in L2 between
+      // the passes; beyond that the apply pass wants its own, larger grid (64 x 128^2:
+      // 13.3 ms fused against 12.4 ms as two kernels)
+      const bool fits_l2 = P * 512 <= (96LL << 20);
+      if (t->bn_bwd_fused && fits_l2 && red_grid <= t->bn_bwd_coop_blocks) {
+        const float* ga_p = t->ga[cur];
+        const float* y_p = t->y[j];
+        int Bv = B, Hv = H, Wv = W;
+        const double* sums_p = t->sums + j * 128;
+        const float* gam = t->gammav[j];
+        const float* bet = t->betav[j];
+        float epsv = t->eps;
+        double* red_p = red_bn + j * 128;
+        int* amax_p = amax_bn + j * 2;
+        __half* gp = padded0<__half>(t->gpad, t, 64);
+        int* gexp_p = t->gexp + j;
+        float* ginv_p = t->ginv + j;
+        float* dg = dgamma[j];
+        float* db = dbeta[j];
+        void* args[] = {&ga_p, &y_p, &Bv, &Hv, &Wv, &sums_p, &gam, &bet, &epsv, &red_p, &amax_p, &gp, &gexp_p,
+                        &ginv_p, &dg, &db};
+        TVS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(tvs::bn_bwd_fused_kernel), dim3(red_grid),
+                                             dim3(tvs::kTB), args, 0, st));
+      } else {
+      tvs::bn_bwd_reduce_kernel<<<red_grid, tvs::kTB, 0, st>>>(
           t->ga[cur], t->y[j], P, t->sums + j * 128, t->gammav[j], t->betav[j], t->eps, red_bn + j * 128,
           amax_bn + j * 2);
       TVS_CUDA(cudaGetLastError());
@@ -871,6 +932,7 @@ int tvs_train_backward(tvs_train* t, const float* g_out, float* const* dw, float
           amax_bn + j * 2,
           padded0<__half>(t->gpad, t, 64), t->gexp + j, t->ginv + j, dgamma[j], dbeta[j]);
       TVS_CUDA(cudaGetLastError());
+      }
       // wgrad: dW_j = sum g_y (x) a_j-1 (hi halves), unscaled by alpha = 2^-s
       if (t->wgrad_tc) {
         wgrad_tc(t, j, 64, t->ginv + j, dw[j + 1], st);
@@ -909,6 +971,7 @@ int tvs_train_set_option(tvs_train* t, const char* name, int value) {
     const std::string k(name);
     if (k == "wgrad_tc") t->wgrad_tc = value != 0;  // 0: the cuBLAS split-K GEMMs (one per tap)
     else if (k == "head_dgrad_tc") t->head_dgrad_tc = value != 0;  // 0: the fp32 CUDA-core head dgrad
+    else if (k == "bn_bwd_fused") t->bn_bwd_fused = value != 0;  // 0: BatchNorm backward as two kernels
     else if (k == "bn_fused") t->bn_fused = value != 0;  // 0: batch statistics by a separate pass over y
     else throw TvsError(TVS_E_INVALID, "unknown training option: " + k);
   });

@@ -205,3 +205,24 @@ def test_fused_batch_statistics_match_the_separate_pass(shape):
         np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-6)
     for n, g in res[1][2].items():
         assert _rel(g, res[0][2][n]) <= 2e-3, (n, _rel(g, res[0][2][n]))
+
+
+@pytest.mark.parametrize("shape", [(2, 32, 32), (3, 37, 150), (1, 5, 7)])
+def test_bn_backward_cooperative_launch_matches_two_kernels(shape):
+    """BatchNorm backward's reduction and apply passes in one cooperative launch
+    (train option bn_bwd_fused, default) against the two-kernel path: the same
+    code on either side of a grid barrier instead of a kernel boundary; only the
+    order of the fp64 atomics differs."""
+    B, H, W = shape
+    grads = {}
+    for fused in (1, 0):
+        m = TVSpecNet()
+        m.load_state_dict(build_seeded_state())
+        m = m.cuda().train()
+        m._train_plan(0).set_option("bn_bwd_fused", fused)
+        img, gt, res = (t.cuda() for t in train_batch(seed=12, B=B, H=H, W=W))
+        compute_loss(m(img), gt, img, res, "L3").total.backward()
+        grads[fused] = {n: p.grad.detach().cpu().numpy() for n, p in m.named_parameters()}
+    for n, g in grads[1].items():
+        assert np.isfinite(g).all(), n
+        assert _rel(g, grads[0][n]) <= 1e-5, (n, _rel(g, grads[0][n]))
