@@ -920,18 +920,26 @@ int tvs_train_backward(tvs_train* t, const float* g_out, float* const* dw, float
         float* db = dbeta[j];
         void* args[] = {&ga_p, &y_p, &Bv, &Hv, &Wv, &sums_p, &gam, &bet, &epsv, &red_p, &amax_p, &gp, &gexp_p,
                         &ginv_p, &dg, &db};
-        TVS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(tvs::bn_bwd_fused_kernel), dim3(red_grid),
-                                             dim3(tvs::kTB), args, 0, st));
-      } else {
-      tvs::bn_bwd_reduce_kernel<<<red_grid, tvs::kTB, 0, st>>>(
-          t->ga[cur], t->y[j], P, t->sums + j * 128, t->gammav[j], t->betav[j], t->eps, red_bn + j * 128,
-          amax_bn + j * 2);
-      TVS_CUDA(cudaGetLastError());
-      tvs::bn_bwd_apply_kernel<<<grid_for(P * 16, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
-          t->ga[cur], t->y[j], B, H, W, t->sums + j * 128, t->gammav[j], t->betav[j], t->eps, red_bn + j * 128,
-          amax_bn + j * 2,
-          padded0<__half>(t->gpad, t, 64), t->gexp + j, t->ginv + j, dgamma[j], dbeta[j]);
-      TVS_CUDA(cudaGetLastError());
+        const cudaError_t ce = cudaLaunchCooperativeKernel(
+            reinterpret_cast<const void*>(tvs::bn_bwd_fused_kernel), dim3(red_grid), dim3(tvs::kTB), args, 0, st);
+        if (ce == cudaErrorCooperativeLaunchTooLarge) {
+          // the driver cannot make the grid co-resident here (MPS SM limits, green
+          // contexts): nothing ran; use the two kernels from now on
+          cudaGetLastError();
+          t->bn_bwd_fused = 0;
+        } else {
+          TVS_CUDA(ce);
+        }
+      }
+      if (!(t->bn_bwd_fused && fits_l2 && red_grid <= t->bn_bwd_coop_blocks)) {
+        tvs::bn_bwd_reduce_kernel<<<red_grid, tvs::kTB, 0, st>>>(
+            t->ga[cur], t->y[j], P, t->sums + j * 128, t->gammav[j], t->betav[j], t->eps, red_bn + j * 128,
+            amax_bn + j * 2);
+        TVS_CUDA(cudaGetLastError());
+        tvs::bn_bwd_apply_kernel<<<grid_for(P * 16, tvs::kTB * 4, t->num_sms), tvs::kTB, 0, st>>>(
+            t->ga[cur], t->y[j], B, H, W, t->sums + j * 128, t->gammav[j], t->betav[j], t->eps, red_bn + j * 128,
+            amax_bn + j * 2, padded0<__half>(t->gpad, t, 64), t->gexp + j, t->ginv + j, dgamma[j], dbeta[j]);
+        TVS_CUDA(cudaGetLastError());
       }
       // wgrad: dW_j = sum g_y (x) a_j-1 (hi halves), unscaled by alpha = 2^-s
       if (t->wgrad_tc) {
