@@ -132,3 +132,22 @@ def test_host_schedule_partitions_batch(B):
     items = big * 2 * 15
     assert items >= 6 * 148 and items >= 0.95 * 148 * -(-items // 148)
     assert sizes[-1] <= 8
+
+
+def test_host_path_planning_is_pure_python():
+    """Sub-batch schedules and the row-band rule of the host-tensor path
+    (model._host_schedule / _host_row_bands) need no device."""
+    m = TVSpecNet()
+    for B in (1, 2, 3, 8, 17, 64, 65, 512):
+        sizes = m._host_schedule(B, 256, 256, 256, False, 148)
+        assert sum(sizes) == B and all(n > 0 for n in sizes), (B, sizes)
+    assert m._host_schedule(64, 256, 256, 256, False, 148) == [4, 39, 17, 4]
+    # one large image: 2 row bands, 4 from 6 MP; never for batches, windows or small results
+    assert m._host_row_bands(1, 1024, 1024, 0, 1024, False) == 2
+    assert m._host_row_bands(1, 2160, 3840, 0, 2160, True) == 4
+    assert m._host_row_bands(1, 256, 256, 0, 256, True) == 1
+    assert m._host_row_bands(4, 1024, 1024, 0, 1024, False) == 1
+    assert m._host_row_bands(1, 1024, 1024, 8, 512, False) == 1
+    m.host_row_bands = 3
+    assert m._host_row_bands(1, 300, 260, 0, 300, False) == 3
+    assert m._host_row_bands(2, 300, 260, 0, 300, False) == 1
