@@ -123,9 +123,10 @@ class TVSpecNet(nn.Module):
         state = self.__dict__.copy()
         state["_plans"] = {}
         state["_train_plans"] = {}
-        state.pop("_wk_cache", None)
-        state.pop("_train_stage", None)
-        state.pop("_train_layers", None)
+        # per-process caches (device buffers, streams, events, module walks) never travel
+        for k in ("_wk_cache", "_train_stage", "_train_layers", "_train_step_id", "_single_bufs", "_host_pipes",
+                  "_row_pipes", "_sched_cache"):
+            state.pop(k, None)
         return state
 
     def _train_plan(self, idx: int):

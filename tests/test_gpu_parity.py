@@ -595,3 +595,21 @@ def test_host_row_band_pipeline_bitwise(prec):
     assert m._host_row_bands(1, 256, 256, 0, 256, False) == 1
     assert m._host_row_bands(2, 1024, 1024, 0, 1024, False) == 1
     assert m._host_row_bands(1, 1024, 1024, 0, 512, False) == 1
+
+
+def test_model_pickles_and_deep_copies_after_host_forwards():
+    """The per-process caches of the host paths (device staging buffers, streams,
+    events) stay out of pickles and deep copies; the copy computes the same."""
+    import copy
+    import pickle
+
+    m = TVSpecNet().eval()
+    m.load_state_dict(build_seeded_state())
+    x1 = torch.rand(1, 1, 40, 130, generator=torch.Generator().manual_seed(2))
+    x8 = torch.rand(8, 1, 24, 40, generator=torch.Generator().manual_seed(3))
+    y1, y8 = m(x1), m(x8)  # single-sub-batch path and sub-batch pipeline
+    m.host_row_bands = 2
+    yb = m(x1)
+    assert torch.equal(yb, y1)
+    for clone in (pickle.loads(pickle.dumps(m)), copy.deepcopy(m)):
+        assert torch.equal(clone(x1), y1) and torch.equal(clone(x8), y8)
