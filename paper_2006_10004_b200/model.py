@@ -262,6 +262,12 @@ class TVSpecNet(nn.Module):
             raise ValueError(f"unshuffle=2 needs an even row window, got {rows}")
         if check_reconstruction and not x.is_cuda:
             raise ValueError("check_reconstruction needs a CUDA input (device-side check sums)")
+        if B == 0:  # an empty batch is a valid forward (the reference returns (0, K, H, W)): nothing to launch
+            bands = x.new_empty((0, self.out_bands, nrows, W))
+            clos = x.new_empty((0, 1, nrows, W)) if (closure or check_reconstruction) else None
+            if check_reconstruction:
+                return bands, clos, x.new_empty((0,), dtype=torch.float64)
+            return bands, clos
         if not x.is_cuda:
             return self._forward_host(plan, x, dev, closure, row0, nrows)
         closure = closure or check_reconstruction

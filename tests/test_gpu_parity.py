@@ -613,3 +613,15 @@ def test_model_pickles_and_deep_copies_after_host_forwards():
     assert torch.equal(yb, y1)
     for clone in (pickle.loads(pickle.dumps(m)), copy.deepcopy(m)):
         assert torch.equal(clone(x1), y1) and torch.equal(clone(x8), y8)
+
+
+def test_empty_batch_returns_empty_planes_like_the_reference():
+    m = TVSpecNet().eval()
+    m.load_state_dict(build_seeded_state())
+    ref = oracle_from_state(build_seeded_state())
+    for x in (torch.zeros(0, 1, 8, 12), torch.zeros(0, 1, 8, 12).cuda()):
+        with torch.no_grad():
+            y = m(x)
+        assert tuple(y.shape) == tuple(ref(torch.zeros(0, 1, 8, 12)).shape) == (0, 5, 8, 12) and y.device == x.device
+        b, c = m.forward_planes(x, closure=True)
+        assert tuple(b.shape) == (0, 5, 8, 12) and tuple(c.shape) == (0, 1, 8, 12)
