@@ -92,3 +92,53 @@ def test_training_step_with_fused_loss_matches_reference_step():
         g, ref = p.grad.detach().cpu().numpy(), gold[f"grad64_{n}"]
         worst = max(worst, float(np.linalg.norm(g - ref) / max(np.linalg.norm(ref), 1e-30)))
     assert worst <= 2e-2, worst
+
+
+# ---- the reference's own loss tests (pkg/trainer/tests/test_losses.py), run
+# ---- against the drop-in with the reference's CPU-tensor calling convention
+def _ref_case(b=2, k=3, size=8, seed=0):  # test_losses.py:8-13
+    gen = torch.Generator().manual_seed(seed)
+    gt = torch.randn(b, k, size, size, generator=gen)
+    res = torch.randn(b, 1, size, size, generator=gen)
+    img = gt.sum(dim=1, keepdim=True) + res
+    return gt, res, img
+
+
+def test_reference_perfect_prediction_is_zero():  # test_losses.py:15-20
+    gt, res, img = _ref_case()
+    for selector in SELECTORS:
+        value = compute_loss(gt.clone(), gt, img, res, selector)
+        assert float(value.total) == pytest.approx(0.0, abs=1e-10)
+        assert value.skipped_bands == 0
+
+
+def test_reference_zero_prediction_is_unit_loss():  # test_losses.py:23-32
+    gt, res, img = _ref_case()
+    assert float(compute_loss(torch.zeros_like(gt), gt, img, res, "L").total) == 1.0
+    value = compute_loss(torch.zeros_like(gt), gt, img, res, "L2")
+    assert float(value.gradient_huber) == pytest.approx(1.0, rel=1e-6)
+
+
+def test_reference_scale_invariance_and_selector_composition():  # test_losses.py:35-55
+    gt, res, img = _ref_case()
+    pred = gt + 0.1 * torch.randn_like(gt)
+    a = compute_loss(pred, gt, img, res, "L")
+    b = compute_loss(3.0 * pred, 3.0 * gt, img, res, "L")
+    assert float(a.mse) == pytest.approx(float(b.mse), rel=1e-5)
+    pred = gt + 0.05 * torch.randn_like(gt)
+    parts = {s: compute_loss(pred, gt, img, res, s) for s in SELECTORS}
+    assert float(parts["L1"].total) == pytest.approx(float(parts["L"].mse) + float(parts["L1"].sum_constraint), rel=1e-6)
+    assert float(parts["L3"].total) == pytest.approx(
+        float(parts["L"].mse) + float(parts["L3"].sum_constraint) + float(parts["L3"].gradient_huber), rel=1e-6)
+
+
+def test_reference_band_sum_skips_and_gradients():  # test_losses.py:58-97
+    gt, res, img = _ref_case()
+    assert float(compute_loss(gt.clone(), gt, img, res, "L1").sum_constraint) == pytest.approx(0.0, abs=1e-10)
+    gt0 = gt.clone()
+    gt0[0, 1] = 0.0
+    value = compute_loss(gt0 + 0.1, gt0, img, res, "L")
+    assert value.skipped_bands == 1 and torch.isfinite(value.total)
+    pred = (gt + 0.1 * torch.randn_like(gt)).requires_grad_(True)
+    compute_loss(pred, gt, img, res, "L3").total.backward()
+    assert pred.grad is not None and torch.isfinite(pred.grad).all()
